@@ -1,0 +1,187 @@
+/*
+ * srtt_b200.h — C-ABI of the B200-native Sub-R Tucker / H-Tucker engine.
+ *
+ * This is the drop-in boundary for the reference's hot path (srtt, the C++
+ * library of arxiv 2603.21379). The reference exposes C++ templates only and
+ * no FFI; every entry point below replaces one reference function and keeps
+ * its argument meaning, validation order, error messages and output layout:
+ * tensors are flat with the FIRST index fastest (reference tensor.hpp:17-20),
+ * matrices column-major (common.hpp:21-24), indices int64 (Eigen::Index).
+ * Plain pointers and sizes only; no torch or CUDA types in the signatures.
+ *
+ * Error behaviour: every function returns a status code. The reference
+ * throws std::invalid_argument / std::out_of_range / JobError; the matching
+ * codes are SRTT_ERR_INVALID_ARGUMENT / SRTT_ERR_OUT_OF_RANGE, with the
+ * reference's message text in srtt_last_error() (thread-local). The C++
+ * wrapper (srtt_b200.hpp) rethrows the std exception.
+ *
+ * Pointer location: `*_on_device` = 0 means host memory (the library copies
+ * host<->device inside the call; pinned host buffers make this fast),
+ * 1 means CUDA device memory on the handle's device.
+ */
+#ifndef SRTT_B200_H
+#define SRTT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SRTT_OK 0
+#define SRTT_ERR_INVALID_ARGUMENT 1 /* std::invalid_argument in the reference */
+#define SRTT_ERR_OUT_OF_RANGE 2     /* std::out_of_range */
+#define SRTT_ERR_CUDA 3
+#define SRTT_ERR_NCCL 4
+#define SRTT_ERR_OUT_OF_MEMORY 5
+#define SRTT_ERR_INTERNAL 6
+#define SRTT_ERR_JOB 7 /* JobError(job): message starts with "job <index>: " */
+
+/* Stage names of the reference's StageTimings (parallel.hpp:30-40) plus the
+ * host<->device copies of this implementation. */
+#define SRTT_STAGE_SAMPLING 0
+#define SRTT_STAGE_EXTRACT 1 /* fused into SKETCH on the GPU: always 0 */
+#define SRTT_STAGE_SKETCH 2
+#define SRTT_STAGE_SVD 3
+#define SRTT_STAGE_TRANSFER 4
+#define SRTT_STAGE_TTM 5
+#define SRTT_STAGE_GATHER 6
+#define SRTT_STAGE_SERIAL_TAIL 7
+#define SRTT_STAGE_FACTOR_WALL 8
+#define SRTT_STAGE_H2D 9
+#define SRTT_STAGE_D2H 10
+#define SRTT_NUM_STAGES 11
+
+typedef struct srtt_handle srtt_handle;
+
+typedef struct srtt_options {
+  int32_t device;     /* CUDA device ordinal */
+  int32_t use_graphs; /* capture/replay the launch sequence in CUDA graphs */
+  int32_t reserved[6];
+} srtt_options;
+
+/* ExecPolicy (parallel.hpp:23-28). `workers` and `slice_mode` are accepted
+ * for API parity (the GPU runs every mode / node concurrently and the core
+ * pass over all SMs); index_partitions and emulate_serial_root keep their
+ * reference meaning. slice_mode = -1 means auto. */
+typedef struct srtt_exec_policy {
+  int64_t workers;
+  int64_t slice_mode;
+  int64_t index_partitions;
+  int32_t emulate_serial_root;
+  int32_t reserved;
+} srtt_exec_policy;
+
+/* SubsampleReport (tucker.hpp:129-134) / HtSubsampleReport
+ * (htucker.hpp:196-201). Arrays are caller-allocated (d entries for Tucker,
+ * num_nodes for H-Tucker) and may be NULL. Warnings are written
+ * newline-separated into `warnings` (may be NULL). */
+typedef struct srtt_report {
+  int64_t* sample_counts;
+  int64_t* achieved_ranks;
+  char* warnings;
+  int64_t warnings_capacity;
+  int64_t num_warnings;
+  double stage_seconds[SRTT_NUM_STAGES];
+  int32_t flags; /* bit0: a Box-Muller u1 == 0 draw was met (p = 2^-53) */
+  int32_t reserved;
+} srtt_report;
+
+/* Dimension tree (dimension_tree.hpp:9-17), heap/BFS node order, root = 0.
+ * Node i holds modes[mode_begin[i] .. mode_begin[i+1]) ascending. */
+typedef struct srtt_tree {
+  int32_t num_nodes;
+  const int32_t* mode_begin; /* num_nodes + 1 */
+  const int32_t* modes;
+  const int32_t* left;  /* -1 for leaves */
+  const int32_t* right; /* -1 for leaves */
+} srtt_tree;
+
+/* ---- handle ------------------------------------------------------------ */
+int srtt_create(const srtt_options* opts, srtt_handle** out);
+int srtt_destroy(srtt_handle* h);
+const char* srtt_last_error(void);
+int srtt_version(void);
+/* Number of kernel launches issued by the last decomposition call. */
+int64_t srtt_last_launch_count(srtt_handle* h);
+
+/* ---- host-side sampling (bit-exact with the reference) ------------------ */
+/* RngStream(seed, stream_id) + sample_indices / sample_indices_partitioned
+ * (rng.hpp:30-62, sampling.hpp:14-66). `draws_out` (nullable) receives the
+ * number of u64 draws the parent stream consumed (0 when partitioned). */
+int srtt_sample_indices(uint64_t seed, uint64_t stream_id, int64_t m, int64_t s, int64_t partitions,
+                        int64_t* idx_out, uint64_t* draws_out);
+/* `n` normals of stream (seed, stream_id) starting after `draw_offset` u64
+ * draws, normal index t0 on (the device generator, for parity tests). */
+int srtt_stream_normals(srtt_handle* h, uint64_t seed, uint64_t stream_id, uint64_t draw_offset,
+                        uint64_t t0, int64_t n, double* out);
+/* DimensionTree::balanced (dimension_tree.hpp:36-64). Arrays sized
+ * 2*order-1 (mode_begin: 2*order, modes: order*(depth+1) <= order*order). */
+int srtt_tree_balanced(int32_t order, int32_t* num_nodes, int32_t* mode_begin, int32_t* modes,
+                       int32_t* left, int32_t* right, int32_t* parent, int32_t* level);
+
+/* ---- the two hot-path entry points -------------------------------------- */
+/* sub_r_hosvd (tucker.hpp:177-242). core_out: prod(ranks) doubles (first
+ * index fastest); factors_out[k]: dims[k] x ranks[k] column-major. */
+int srtt_sub_r_hosvd(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d,
+                     const int64_t* dims, const int64_t* ranks, int64_t oversampling,
+                     const int64_t* samples, uint64_t seed, const srtt_exec_policy* exec,
+                     double* core_out, double* const* factors_out, int32_t out_on_device,
+                     srtt_report* rep);
+
+/* sub_r_rtl_ht (htucker.hpp:210-341). ranks / samples have one entry per
+ * node (root entry of ranks must be 1). leaf_factors_out is indexed by MODE
+ * (dims[m] x r_leaf); transfers_out by NODE id: r_S x r_l x r_r (root:
+ * 1 x r_l x r_r), NULL entries for leaves. */
+int srtt_sub_r_rtl_ht(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d,
+                      const int64_t* dims, const srtt_tree* tree, const int64_t* ranks,
+                      const int64_t* samples, int64_t oversampling, uint64_t seed,
+                      const srtt_exec_policy* exec, double* const* leaf_factors_out,
+                      double* const* transfers_out, int32_t out_on_device, srtt_report* rep);
+
+/* ---- component entry points (the reference's test-facing functions) ----- */
+/* extract_group_fibers (unfolding.hpp:57-111); a single mode gives
+ * extract_fibers (unfolding.hpp:32-52). y_out: n_S x ncols column-major. */
+int srtt_extract_fibers(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d,
+                        const int64_t* dims, int32_t nmodes, const int32_t* modes, int64_t ncols,
+                        const int64_t* cols, double* y_out, int32_t out_on_device);
+
+/* K1 alone: Z = Y * Omega for one target, Omega drawn from stream
+ * (seed, stream_id) after `draw_offset` draws (or given explicitly as
+ * omega, ncols x c column-major, nullable). z_out: n_S x c. */
+int srtt_sketch(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d, const int64_t* dims,
+                int32_t nmodes, const int32_t* modes, int64_t ncols, const int64_t* cols, int32_t c,
+                uint64_t seed, uint64_t stream_id, uint64_t draw_offset, const double* omega,
+                double* z_out, int32_t out_on_device);
+
+/* K2 alone: range_basis_of_sketch (sketch.hpp:74-93). z: n x c host or
+ * device; q_out: n x rank; sv_out (nullable): min(n, c) singular values.
+ * Padding continues stream (seed, stream_id) at normal index
+ * normal_base after draw_offset draws. */
+int srtt_range_basis_of_sketch(srtt_handle* h, const double* z, int32_t z_on_device, int64_t n,
+                               int32_t c, int32_t rank, uint64_t seed, uint64_t stream_id,
+                               uint64_t draw_offset, int64_t normal_base, double* q_out,
+                               int64_t* numerical_rank, double* sv_out, int32_t out_on_device);
+
+/* K3 alone: core = X x_0 U_0^T ... x_{d-1} U_{d-1}^T (core_from_factors,
+ * tucker.hpp:43-50; sliced_core, parallel.hpp:355-445). factors[k]:
+ * dims[k] x ranks[k] column-major (host or device per factors_on_device). */
+int srtt_multi_ttm_core(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d,
+                        const int64_t* dims, const int64_t* ranks, const double* const* factors,
+                        int32_t factors_on_device, double* core_out, int32_t out_on_device);
+
+/* K4: transfer_tensor (htucker.hpp:44-63). b_out: rs x rl x rr. */
+int srtt_transfer_tensor(srtt_handle* h, const double* u_node, const double* u_left,
+                         const double* u_right, int64_t nl, int64_t nr, int32_t rs, int32_t rl,
+                         int32_t rr, int32_t on_device, double* b_out);
+
+/* K5: root_transfer (htucker.hpp:67-85). b_out: 1 x rl x rr. */
+int srtt_root_transfer(srtt_handle* h, const double* x, int32_t x_on_device, int64_t nl,
+                       int64_t nr, const double* u_left, int32_t rl, const double* u_right,
+                       int32_t rr, int32_t factors_on_device, double* b_out,
+                       int32_t out_on_device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SRTT_B200_H */

@@ -1,0 +1,1474 @@
+// Host runtime of the B200 engine: handle (device, streams, events,
+// grow-only workspace arena, pinned parameter staging), planners (TSQR tree
+// per sketch target; core-pass work decomposition) and the C-ABI entry
+// points of include/srtt_b200.h. Validation order and messages follow the
+// reference (tucker.hpp:184-197, htucker.hpp:217-233, sketch.hpp:77-78,
+// unfolding.hpp:46-47/86-87) so callers see the same errors.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "host_rng.hpp"
+#include "srtt_b200.h"
+#include "srtt_params.h"
+
+// ---- kernel launchers (k_*.cu) ---------------------------------------------
+size_t srtt_sketch_smem_bytes(int cmax);
+cudaError_t srtt_launch_sketch(const SketchTarget*, int, int64_t, int, cudaStream_t);
+size_t srtt_basis_top_smem(int m, int c, int r);
+size_t srtt_basis_level_smem(int mb, int c);
+cudaError_t srtt_launch_basis_top(const BasisTarget*, int, size_t, cudaStream_t);
+cudaError_t srtt_launch_tsqr_factor(const BasisTarget*, int, int, int, size_t, cudaStream_t);
+cudaError_t srtt_launch_tsqr_apply(const BasisTarget*, int, int, int, size_t, cudaStream_t);
+cudaError_t srtt_launch_pad(const BasisTarget*, int, double*, int64_t, cudaStream_t);
+int srtt_core_threads();
+size_t srtt_core_smem_bytes(const CoreParams& P);
+int srtt_core_occupancy(const CoreParams& P);
+cudaError_t srtt_launch_core(const CUtensorMap*, const CoreParams&, int, cudaStream_t);
+cudaError_t srtt_launch_prep(const double*, int64_t, int, int, int, int, double*, cudaStream_t);
+cudaError_t srtt_launch_transpose(const double*, int64_t, int, double*, cudaStream_t);
+cudaError_t srtt_launch_ttm(const TtmParams&, cudaStream_t);
+
+typedef struct TransferTarget {
+  const double* us;
+  const double* ul;
+  const double* ur;
+  double* b;
+  int64_t nl, nr;
+  int32_t rs, rl, rr;
+  int32_t cta_begin;
+} TransferTarget;
+typedef struct GatherParams {
+  const double* x;
+  const int64_t* cols;
+  double* y;
+  int64_t rows, w;
+  int32_t nrow_modes, ncol_modes;
+  int64_t row_dim[SRTT_MAX_ORDER], row_stride[SRTT_MAX_ORDER];
+  int64_t col_dim[SRTT_MAX_ORDER], col_stride[SRTT_MAX_ORDER];
+} GatherParams;
+cudaError_t srtt_launch_transfer(const TransferTarget*, int, int, int, int, cudaStream_t);
+cudaError_t srtt_launch_gather(const GatherParams&, cudaStream_t);
+
+namespace {
+
+// ---- errors -----------------------------------------------------------------
+thread_local std::string g_last_error;
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+[[noreturn]] void invalid(const std::string& msg) { fail(SRTT_ERR_INVALID_ARGUMENT, msg); }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  fail(e == cudaErrorMemoryAllocation ? SRTT_ERR_OUT_OF_MEMORY : SRTT_ERR_CUDA,
+       std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return SRTT_OK;
+  } catch (const Error& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return SRTT_ERR_INVALID_ARGUMENT;
+  } catch (const std::out_of_range& e) {
+    g_last_error = e.what();
+    return SRTT_ERR_OUT_OF_RANGE;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host out of memory";
+    return SRTT_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SRTT_ERR_INTERNAL;
+  }
+}
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// ---- buffers ----------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  bool ensure(size_t bytes) {  // returns true when reallocated
+    if (bytes <= cap) return false;
+    size_t want = std::max(bytes, cap + cap / 2);
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      e = cudaMalloc(&p, bytes);
+      want = bytes;
+    }
+    CK(e);
+    cap = want;
+    return true;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    const size_t want = std::max(bytes, cap * 2);
+    CK(cudaMallocHost(&p, want));
+    cap = want;
+  }
+  ~HostBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+// Two-pass layout helper: take() records aligned offsets; resolve after the
+// backing buffer is large enough.
+struct Layout {
+  size_t off = 0;
+  size_t take(size_t bytes, size_t align = 256) {
+    off = (off + align - 1) / align * align;
+    const size_t o = off;
+    off += bytes;
+    return o;
+  }
+};
+
+// ---- tensor map encoder (driver entry point; no -lcuda needed) ------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encoder() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) fail(SRTT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+void encode_tmap(CUtensorMap* map, const double* x, int64_t n0, int64_t Q, int W) {
+  cuuint64_t gdim[2] = {(cuuint64_t)n0, (cuuint64_t)Q};
+  cuuint64_t gstride[1] = {(cuuint64_t)n0 * sizeof(double)};
+  cuuint32_t box[2] = {16, (cuuint32_t)W};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(x), gdim,
+                             gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(SRTT_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
+int64_t prod(const std::vector<int64_t>& v, size_t lo = 0, size_t hi = SIZE_MAX) {
+  int64_t p = 1;
+  for (size_t i = lo; i < std::min(hi, v.size()); ++i) p *= v[i];
+  return p;
+}
+
+}  // namespace
+
+// ---- handle -----------------------------------------------------------------
+struct srtt_handle {
+  int device = 0;
+  int sms = 148;
+  int use_graphs = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[8] = {};
+  DevBuf xbuf;     // device copy of host inputs
+  DevBuf ws;       // workspace arena
+  DevBuf dparams;  // device copy of the parameter blob
+  HostBuf hparams; // pinned parameter blob
+  HostBuf hinfo;   // pinned read-back (ranks, flags)
+  DevBuf ones;
+  int64_t launches = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Parameter blob: host pinned staging, uploaded with one copy.
+struct Blob {
+  Layout lay;
+  std::vector<std::pair<size_t, std::vector<unsigned char>>> items;
+  size_t add(const void* src, size_t bytes) {
+    const size_t o = lay.take(bytes, 64);
+    items.emplace_back(o, std::vector<unsigned char>((const unsigned char*)src,
+                                                       (const unsigned char*)src + bytes));
+    return o;
+  }
+  size_t reserve(size_t bytes) { return lay.take(bytes, 64); }
+};
+
+// ---- basis (K2) planning ------------------------------------------------------
+constexpr size_t kSmemBudget = 200 * 1024;
+
+int top_max_rows(int c, int r) {
+  int lo = 1, hi = 1 << 20;
+  if (srtt_basis_top_smem(1, c, r) > kSmemBudget) return 0;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (srtt_basis_top_smem(mid, c, r) <= kSmemBudget) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+int level_block_rows(int c) {
+  int m = 1024;
+  while (m > 2 * c && srtt_basis_level_smem(m, c) > kSmemBudget) m -= 32;
+  return m;
+}
+
+struct BasisPlan {
+  int64_t n;
+  int c, r;
+  int nlevels;
+  int64_t lv_n[SRTT_MAX_QR_LEVELS + 1];
+  int lv_nblk[SRTT_MAX_QR_LEVELS + 1];
+  int lv_blk[SRTT_MAX_QR_LEVELS + 1];
+};
+
+BasisPlan plan_basis(int64_t n, int c, int r) {
+  BasisPlan b{};
+  b.n = n;
+  b.c = c;
+  b.r = r;
+  const int tmax = top_max_rows(c, r);
+  const int blk = level_block_rows(c);
+  if (tmax < c) invalid("range_basis_of_sketch: sketch too wide for the B200 basis kernel");
+  int64_t nl = n;
+  int l = 0;
+  while (nl > tmax) {
+    if (l >= SRTT_MAX_QR_LEVELS) invalid("range_basis_of_sketch: sketch too tall");
+    const int nblk = (int)((nl + blk - 1) / blk);
+    const int64_t nn = (int64_t)nblk * c;
+    if (nn >= nl) invalid("range_basis_of_sketch: TSQR cannot shrink this sketch");
+    b.lv_n[l] = nl;
+    b.lv_nblk[l] = nblk;
+    b.lv_blk[l] = blk;
+    nl = nn;
+    ++l;
+  }
+  b.lv_n[l] = nl;
+  b.lv_nblk[l] = 1;
+  b.lv_blk[l] = (int)nl;
+  b.nlevels = l;
+  return b;
+}
+
+struct BasisBuffers {  // offsets into the workspace
+  size_t a[SRTT_MAX_QR_LEVELS + 1], tau[SRTT_MAX_QR_LEVELS + 1], y[SRTT_MAX_QR_LEVELS + 1];
+  size_t info, sv, pad;
+};
+
+// z (level-0 matrix) and u (final basis) are supplied by the caller.
+BasisBuffers layout_basis(Layout& L, const BasisPlan& p) {
+  BasisBuffers B{};
+  for (int l = 0; l <= p.nlevels; ++l) {
+    B.a[l] = l == 0 ? SIZE_MAX : L.take(sizeof(double) * p.lv_n[l] * p.c);
+    B.tau[l] = L.take(sizeof(double) * (size_t)p.lv_nblk[l] * p.c);
+    B.y[l] = l == 0 ? SIZE_MAX : L.take(sizeof(double) * p.lv_n[l] * p.r);
+  }
+  B.info = L.take(4 * sizeof(int32_t));
+  B.sv = L.take(sizeof(double) * p.c);
+  B.pad = 0;
+  return B;
+}
+
+BasisTarget fill_basis(const BasisPlan& p, const BasisBuffers& B, char* ws, double* z, double* u,
+                       uint64_t state0, uint64_t draw_offset, int64_t normal_base) {
+  BasisTarget T{};
+  T.u = u;
+  T.sv = reinterpret_cast<double*>(ws + B.sv);
+  T.info = reinterpret_cast<int32_t*>(ws + B.info);
+  T.n = p.n;
+  T.c = p.c;
+  T.r = p.r;
+  T.nlevels = p.nlevels;
+  for (int l = 0; l <= p.nlevels; ++l) {
+    QrLevel& q = T.lv[l];
+    q.a = l == 0 ? z : reinterpret_cast<double*>(ws + B.a[l]);
+    q.tau = reinterpret_cast<double*>(ws + B.tau[l]);
+    q.y = l == 0 ? u : reinterpret_cast<double*>(ws + B.y[l]);
+    q.n = p.lv_n[l];
+    q.nblk = p.lv_nblk[l];
+    q.blk_rows = p.lv_blk[l];
+  }
+  for (int l = 0; l < p.nlevels; ++l) T.lv[l].r_out = T.lv[l + 1].a;
+  T.state0 = state0;
+  T.draw_offset = draw_offset;
+  T.normal_base = normal_base;
+  return T;
+}
+
+// Grouped K2 launch sequence over many targets (device array dT).
+int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const BasisTarget* dT,
+                       double* pad_scratch, int64_t pad_stride) {
+  // Targets' cta_begin per level were filled by the caller (assign_basis_ctas).
+  int launches = 0;
+  int maxlev = 0;
+  for (auto& t : targets) maxlev = std::max(maxlev, t.nlevels);
+  const int nt = (int)targets.size();
+  for (int l = 0; l < maxlev; ++l) {
+    int nctas = 0;
+    size_t smem = 0;
+    for (auto& t : targets)
+      if (t.nlevels > l) {
+        nctas += t.lv[l].nblk;
+        smem = std::max(smem, srtt_basis_level_smem(t.lv[l].blk_rows, t.c));
+      }
+    CK(srtt_launch_tsqr_factor(dT, nt, l, nctas, smem, h->stream));
+    ++launches;
+  }
+  size_t smem = 0;
+  for (auto& t : targets) smem = std::max(smem, srtt_basis_top_smem((int)t.lv[t.nlevels].n, t.c, t.r));
+  CK(srtt_launch_basis_top(dT, nt, smem, h->stream));
+  ++launches;
+  for (int l = maxlev - 1; l >= 0; --l) {
+    int nctas = 0;
+    size_t sm = 0;
+    for (auto& t : targets)
+      if (t.nlevels > l) {
+        nctas += t.lv[l].nblk;
+        sm = std::max(sm, srtt_basis_level_smem(t.lv[l].blk_rows, t.c));
+      }
+    CK(srtt_launch_tsqr_apply(dT, nt, l, nctas, sm, h->stream));
+    ++launches;
+  }
+  if (maxlev > 0) {
+    CK(srtt_launch_pad(dT, nt, pad_scratch, pad_stride, h->stream));
+    ++launches;
+  }
+  return launches;
+}
+
+void assign_basis_ctas(std::vector<BasisTarget>& targets) {
+  for (int l = 0; l < SRTT_MAX_QR_LEVELS; ++l) {
+    int c = 0;
+    for (auto& t : targets) {
+      t.cta_begin[l] = c;
+      if (t.nlevels > l) c += t.lv[l].nblk;
+    }
+  }
+}
+
+// ---- core (K3) planning --------------------------------------------------------
+struct CorePlan {
+  CoreParams P{};
+  int grid = 0;
+  std::vector<int64_t> dims;   // modes of the (possibly reshaped) tensor
+  std::vector<int64_t> ranks;
+  int64_t part_doubles = 0;
+  size_t ufrag_doubles = 0;
+};
+
+CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>& ranks, int sms,
+                   int force_m = 0, int force_S = 0) {
+  const int d = (int)dims.size();
+  CorePlan cp;
+  cp.dims = dims;
+  cp.ranks = ranks;
+  CoreParams& P = cp.P;
+  const int64_t n0 = dims[0];
+  const int64_t N = prod(dims);
+  const int64_t Q = N / n0;
+  P.n0 = n0;
+  P.Q = Q;
+  P.r0 = (int)ranks[0];
+  P.NT = (P.r0 + 7) / 8;
+  if (P.NT > 8) invalid("core: rank of mode 0 above 64 is not supported by the B200 core kernel");
+  P.RB = n0 <= 256 ? (int)((n0 + 15) / 16 * 16) : (P.NT > 4 ? 128 : 256);
+  P.nrb = (int)((n0 + P.RB - 1) / P.RB);
+  P.W = 64;
+  P.use_tma = (n0 % 2 == 0) ? 1 : 0;
+
+  struct Cand {
+    int m;
+    int S;
+    int64_t SL, G, GS, items;
+    int A, acc_total;
+    double cost;
+  };
+  Cand best{};
+  best.cost = 1e300;
+  int64_t Am = P.r0;
+  int acc_total = 0;
+  for (int m = 2; m <= d; ++m) {
+    Am *= ranks[m - 1];
+    acc_total += (int)Am;
+    if (acc_total > 12288) break;
+    if (force_m && m != force_m) continue;
+    const int64_t GS = prod(dims, 1, m);
+    const int64_t G = Q / GS;
+    const int64_t target_items = 8LL * sms;
+    int64_t S = force_S ? force_S : std::max<int64_t>(1, (target_items + P.nrb * G - 1) / (P.nrb * G));
+    S = std::min<int64_t>(S, (GS + P.W - 1) / P.W);
+    int64_t SL = ((GS + S - 1) / S + P.W - 1) / P.W * P.W;
+    S = (GS + SL - 1) / SL;
+    const int64_t items = P.nrb * G * S;
+    const int64_t last = GS - (S - 1) * SL;
+    const int64_t loaded = (S - 1) * SL + (last + P.W - 1) / P.W * P.W;
+    const double waste = (double)(loaded - GS) * G * n0 * 8.0;
+    const double out = (double)items * Am * 8.0;
+    const int grid = (int)std::min<int64_t>(items, sms);
+    const int64_t rounds = (items + grid - 1) / grid;
+    const double eff = (double)items / ((double)rounds * grid);
+    const double cost = (double)N * 8.0 / eff + waste + 2.0 * out;
+    if (cost < best.cost) best = Cand{m, (int)S, SL, G, GS, items, (int)Am, acc_total, cost};
+  }
+  if (best.m == 0) invalid("core: no feasible fold depth");
+  P.m = best.m;
+  P.S = best.S;
+  P.SL = best.SL;
+  P.G = best.G;
+  P.GS = best.GS;
+  P.nitems = best.items;
+  P.A = best.A;
+  for (int k = 1; k < best.m; ++k) {
+    P.fdim[k - 1] = dims[k];
+    P.frank[k - 1] = (int)ranks[k];
+  }
+  int off = 0;
+  int64_t Al = P.r0;
+  for (int l = 2; l <= best.m; ++l) {
+    Al *= ranks[l - 1];
+    P.acc_off[l] = off;
+    off += (int)Al;
+  }
+  P.acc_total = off;
+  cp.part_doubles = best.items * best.A;
+  cp.ufrag_doubles = (size_t)P.nrb * P.RB * P.NT * 8;
+  return cp;
+}
+
+// Launches the full core pass for factors already on the device.
+// x: device tensor (dims), u[k]: device n_k x r_k column-major, out: device core.
+int launch_core_pass(srtt_handle* h, CorePlan& cp, const double* x, const std::vector<const double*>& u,
+                     double* out, char* ws, size_t off_ufrag, const std::vector<size_t>& off_fu,
+                     size_t off_part, size_t off_tmp0, size_t off_tmp1) {
+  int launches = 0;
+  CoreParams& P = cp.P;
+  const int d = (int)cp.dims.size();
+  P.x = x;
+  P.ufrag = reinterpret_cast<double*>(ws + off_ufrag);
+  P.part = reinterpret_cast<double*>(ws + off_part);
+  CK(srtt_launch_prep(u[0], P.n0, P.r0, P.RB, P.NT, P.nrb, const_cast<double*>(P.ufrag), h->stream));
+  ++launches;
+  for (int k = 1; k < P.m; ++k) {
+    double* ut = reinterpret_cast<double*>(ws + off_fu[k]);
+    CK(srtt_launch_transpose(u[k], cp.dims[k], (int)cp.ranks[k], ut, h->stream));
+    ++launches;
+    P.fu[k - 1] = ut;
+  }
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  if (P.use_tma) encode_tmap(&tmap, x, P.n0, P.Q, P.W);
+  const int occ = std::max(1, srtt_core_occupancy(P));
+  cp.grid = (int)std::min<int64_t>(P.nitems, (int64_t)occ * h->sms);
+  CK(srtt_launch_core(&tmap, P, cp.grid, h->stream));
+  ++launches;
+  // tail: fixed-order reduction of the item partials + TTMs of modes m..d-1
+  const int nparts = P.nrb * P.S;
+  if (P.m == d) {
+    TtmParams T{};
+    T.in = P.part;
+    T.u = reinterpret_cast<const double*>(h->ones.p);
+    T.out = out;
+    T.g = P.A;
+    T.n = 1;
+    T.post = 1;
+    T.rr = 1;
+    T.transpose = 1;
+    T.nparts = nparts;
+    T.part_stride = (int64_t)P.G * P.A;
+    CK(srtt_launch_ttm(T, h->stream));
+    ++launches;
+  } else {
+    const double* in = P.part;
+    int64_t g = P.A;
+    int np = nparts;
+    for (int k = P.m; k < d; ++k) {
+      const int64_t post = prod(cp.dims, k + 1);
+      TtmParams T{};
+      T.in = in;
+      T.u = u[k];
+      T.g = g;
+      T.n = cp.dims[k];
+      T.post = post;
+      T.rr = cp.ranks[k];
+      T.transpose = 1;
+      T.nparts = np;
+      T.part_stride = (int64_t)P.G * P.A;
+      T.out = (k == d - 1) ? out : reinterpret_cast<double*>(ws + (((k - P.m) % 2) ? off_tmp1 : off_tmp0));
+      CK(srtt_launch_ttm(T, h->stream));
+      ++launches;
+      in = T.out;
+      g *= cp.ranks[k];
+      np = 1;
+    }
+  }
+  return launches;
+}
+
+// Workspace needs of the core pass.
+void layout_core(Layout& L, const CorePlan& cp, size_t& off_ufrag, std::vector<size_t>& off_fu,
+                 size_t& off_part, size_t& off_tmp0, size_t& off_tmp1) {
+  const int d = (int)cp.dims.size();
+  off_ufrag = L.take(sizeof(double) * cp.ufrag_doubles);
+  off_fu.assign(d, 0);
+  for (int k = 1; k < cp.P.m; ++k) off_fu[k] = L.take(sizeof(double) * cp.dims[k] * cp.ranks[k]);
+  off_part = L.take(sizeof(double) * cp.part_doubles);
+  // largest intermediate of the tail
+  int64_t g = cp.P.A, big = 1;
+  for (int k = cp.P.m; k < d; ++k) {
+    g *= cp.ranks[k];
+    big = std::max<int64_t>(big, g * prod(cp.dims, k + 1));
+  }
+  off_tmp0 = L.take(sizeof(double) * big);
+  off_tmp1 = L.take(sizeof(double) * big);
+}
+
+// ---- sketch target construction ---------------------------------------------
+SketchTarget make_sketch_target(const double* x, const std::vector<int64_t>& dims,
+                                const std::vector<int>& modes, int64_t w, int c) {
+  SketchTarget T{};
+  T.x = x;
+  const int d = (int)dims.size();
+  std::vector<int64_t> stride(d);
+  int64_t g = 1;
+  for (int k = 0; k < d; ++k) {
+    stride[k] = g;
+    g *= dims[k];
+  }
+  std::vector<bool> in(d, false);
+  for (int m : modes) in[m] = true;
+  T.rows = 1;
+  for (int k = 0; k < d; ++k) {
+    if (in[k]) {
+      T.row_dim[T.nrow_modes] = dims[k];
+      T.row_stride[T.nrow_modes] = stride[k];
+      T.nrow_modes++;
+      T.rows *= dims[k];
+    } else {
+      T.col_dim[T.ncol_modes] = dims[k];
+      T.col_stride[T.ncol_modes] = stride[k];
+      T.ncol_modes++;
+    }
+  }
+  T.w = w;
+  T.c = c;
+  T.row_tile = (int)std::min<int64_t>(T.rows, 64);
+  return T;
+}
+
+// ---- report helpers ------------------------------------------------------------
+void write_warnings(srtt_report* rep, const std::vector<std::string>& w) {
+  if (!rep) return;
+  rep->num_warnings = (int64_t)w.size();
+  if (!rep->warnings || rep->warnings_capacity <= 0) return;
+  std::string all;
+  for (auto& s : w) all += s + "\n";
+  const size_t n = std::min<size_t>(all.size(), (size_t)rep->warnings_capacity - 1);
+  std::memcpy(rep->warnings, all.data(), n);
+  rep->warnings[n] = 0;
+}
+
+void copy_out(srtt_handle* h, void* dst, const void* src, size_t bytes, int on_device) {
+  CK(cudaMemcpyAsync(dst, src, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                     h->stream));
+}
+
+// Returns a device pointer for `x` (copying host data into h->xbuf).
+const double* stage_input(srtt_handle* h, const double* x, int on_device, int64_t count) {
+  if (on_device) return x;
+  h->xbuf.ensure(sizeof(double) * count);
+  CK(cudaMemcpyAsync(h->xbuf.p, x, sizeof(double) * count, cudaMemcpyHostToDevice, h->stream));
+  return reinterpret_cast<const double*>(h->xbuf.p);
+}
+
+struct Timer {
+  srtt_handle* h;
+  int n = 0;
+  void mark() { CK(cudaEventRecord(h->ev[n++], h->stream)); }
+  double between(int a, int b) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, h->ev[a], h->ev[b]));
+    return ms * 1e-3;
+  }
+};
+
+// ==================================================================================
+// Sub-R-HOSVD
+// ==================================================================================
+void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d, const int64_t* dims_p,
+                     const int64_t* ranks_p, int64_t p, const int64_t* samples_p, uint64_t seed,
+                     const srtt_exec_policy* exec, double* core_out, double* const* factors_out,
+                     int out_on_device, srtt_report* rep) {
+  if (d < 1 || d > SRTT_MAX_ORDER) invalid("sub_r_hosvd: unsupported order");
+  std::vector<int64_t> dims(dims_p, dims_p + d), ranks(ranks_p, ranks_p + d), samples(samples_p, samples_p + d);
+  for (int k = 0; k < d; ++k)
+    if (dims[k] < 1) invalid("Shape: dimensions must be >= 1");
+  const int64_t N = prod(dims);
+  // validation order and messages: tucker.hpp:184-197 (validate_ranks first)
+  for (int k = 0; k < d; ++k)
+    if (ranks[k] < 1 || ranks[k] > dims[k])
+      invalid("sub_r_hosvd: rank out of range in mode " + std::to_string(k));
+  for (int k = 0; k < d; ++k) {
+    if (samples[k] < ranks[k] + p)
+      invalid("sub_r_hosvd: samples below rank + oversampling in mode " + std::to_string(k));
+    if (samples[k] > N / dims[k])
+      invalid("sub_r_hosvd: more samples than fibers in mode " + std::to_string(k));
+  }
+  for (int k = 0; k < d; ++k)
+    if (ranks[k] + p > SRTT_MAX_SKETCH_COLS)
+      invalid("sub_r_hosvd: rank + oversampling above 64 is not supported by the B200 basis kernel");
+  std::vector<std::string> warnings;
+  if (p < 4) warnings.push_back("oversampling below the recommended minimum of 4");
+  const int64_t partitions = exec ? exec->index_partitions : 1;
+
+  DeviceGuard guard(h->device);
+  h->launches = 0;
+  Timer tm{h};
+  tm.mark();  // 0
+  const double* x = stage_input(h, x_in, x_on_device, N);
+  tm.mark();  // 1 (after H2D)
+
+  // --- host sampling: one stream per mode (tucker.hpp:145), JobError(k) on failure
+  const double ts0 = now_s();
+  std::vector<std::vector<int64_t>> cols(d);
+  std::vector<uint64_t> draws(d), state0(d);
+  for (int k = 0; k < d; ++k) {
+    srtt_host::Stream rng(seed, (uint64_t)k);
+    try {
+      if (partitions > 1)
+        srtt_host::sample_indices_partitioned(N / dims[k], samples[k], partitions, rng, cols[k]);
+      else
+        srtt_host::sample_indices(N / dims[k], samples[k], rng, cols[k]);
+    } catch (const std::exception& e) {
+      fail(SRTT_ERR_JOB, "job " + std::to_string(k) + ": " + e.what());
+    }
+    draws[k] = rng.draws;
+    state0[k] = srtt_host::stream_state0(seed, (uint64_t)k);
+  }
+  const double t_sampling = now_s() - ts0;
+
+  // --- workspace layout
+  Layout L;
+  std::vector<size_t> off_z(d), off_u(d);
+  std::vector<BasisPlan> bp(d);
+  std::vector<BasisBuffers> bb(d);
+  int cmax = 0;
+  for (int k = 0; k < d; ++k) {
+    const int c = (int)(ranks[k] + p);
+    cmax = std::max(cmax, c);
+    off_z[k] = L.take(sizeof(double) * dims[k] * c);
+    off_u[k] = L.take(sizeof(double) * dims[k] * ranks[k]);
+    bp[k] = plan_basis(dims[k], c, (int)ranks[k]);
+    bb[k] = layout_basis(L, bp[k]);
+  }
+  const size_t off_flags = L.take(sizeof(int32_t) * 4);
+  const size_t off_core = L.take(sizeof(double) * prod(ranks));
+  int64_t max_n = 0;
+  for (int k = 0; k < d; ++k) max_n = std::max(max_n, dims[k]);
+  const size_t off_pad = L.take(sizeof(double) * max_n * d);
+  CorePlan cp;
+  size_t off_ufrag = 0, off_part = 0, off_tmp0 = 0, off_tmp1 = 0;
+  std::vector<size_t> off_fu;
+  if (d >= 2) {
+    cp = plan_core(dims, ranks, h->sms);
+    layout_core(L, cp, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+  } else {
+    off_tmp0 = L.take(sizeof(double));
+  }
+  h->ws.ensure(L.off);
+  char* ws = reinterpret_cast<char*>(h->ws.p);
+
+  // --- parameter blob
+  Blob blob;
+  std::vector<size_t> off_cols(d);
+  for (int k = 0; k < d; ++k) off_cols[k] = blob.add(cols[k].data(), sizeof(int64_t) * cols[k].size());
+  const size_t off_sk = blob.reserve(sizeof(SketchTarget) * d);
+  const size_t off_bt = blob.reserve(sizeof(BasisTarget) * d);
+  h->dparams.ensure(blob.lay.off);
+  h->hparams.ensure(blob.lay.off);
+  char* dp = reinterpret_cast<char*>(h->dparams.p);
+  char* hp = reinterpret_cast<char*>(h->hparams.p);
+  for (auto& it : blob.items) std::memcpy(hp + it.first, it.second.data(), it.second.size());
+  std::vector<SketchTarget> sk(d);
+  std::vector<BasisTarget> bt(d);
+  int64_t ctas = 0;
+  int32_t* d_flags = reinterpret_cast<int32_t*>(ws + off_flags);
+  for (int k = 0; k < d; ++k) {
+    const int c = (int)(ranks[k] + p);
+    sk[k] = make_sketch_target(x, dims, {k}, samples[k], c);
+    sk[k].cols = reinterpret_cast<const int64_t*>(dp + off_cols[k]);
+    sk[k].z = reinterpret_cast<double*>(ws + off_z[k]);
+    sk[k].state0 = state0[k];
+    sk[k].draw_offset = draws[k];
+    sk[k].cta_begin = ctas;
+    sk[k].flags = d_flags;
+    ctas += (sk[k].rows + sk[k].row_tile - 1) / sk[k].row_tile;
+    bt[k] = fill_basis(bp[k], bb[k], ws, sk[k].z, reinterpret_cast<double*>(ws + off_u[k]), state0[k],
+                       draws[k], samples[k] * c);
+  }
+  assign_basis_ctas(bt);
+  std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * d);
+  std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * d);
+  CK(cudaMemsetAsync(d_flags, 0, sizeof(int32_t) * 4, h->stream));
+  CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
+  tm.mark();  // 2
+
+  // --- K1: grouped gather + sketch over all modes
+  CK(srtt_launch_sketch(reinterpret_cast<const SketchTarget*>(dp + off_sk), d, ctas, cmax, h->stream));
+  h->launches++;
+  tm.mark();  // 3
+  // --- K2: basis of every sketch
+  h->launches += launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt),
+                                    reinterpret_cast<double*>(ws + off_pad), max_n);
+  tm.mark();  // 4
+  // --- K3: core pass
+  std::vector<const double*> uptr(d);
+  for (int k = 0; k < d; ++k) uptr[k] = reinterpret_cast<const double*>(ws + off_u[k]);
+  double* d_core = reinterpret_cast<double*>(ws + off_core);
+  if (d >= 2) {
+    h->launches += launch_core_pass(h, cp, x, uptr, d_core, ws, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+  } else {
+    TtmParams T{};
+    T.in = x;
+    T.u = uptr[0];
+    T.out = d_core;
+    T.g = 1;
+    T.n = dims[0];
+    T.post = 1;
+    T.rr = ranks[0];
+    T.transpose = 1;
+    T.nparts = 1;
+    CK(srtt_launch_ttm(T, h->stream));
+    h->launches++;
+  }
+  tm.mark();  // 5
+  // --- outputs + report read-back
+  copy_out(h, core_out, d_core, sizeof(double) * prod(ranks), out_on_device);
+  for (int k = 0; k < d; ++k) copy_out(h, factors_out[k], uptr[k], sizeof(double) * dims[k] * ranks[k], out_on_device);
+  h->hinfo.ensure(sizeof(int32_t) * 4 * (d + 1));
+  int32_t* hi = reinterpret_cast<int32_t*>(h->hinfo.p);
+  for (int k = 0; k < d; ++k)
+    CK(cudaMemcpyAsync(hi + 4 * k, bt[k].info, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(hi + 4 * d, d_flags, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, h->stream));
+  tm.mark();  // 6
+  CK(cudaStreamSynchronize(h->stream));
+  CK(cudaGetLastError());
+
+  for (int k = 0; k < d; ++k) {
+    const int q = hi[4 * k];
+    if (rep && rep->achieved_ranks) rep->achieved_ranks[k] = q;
+    if (q < ranks[k])
+      warnings.push_back("mode " + std::to_string(k) + ": sketch revealed rank " + std::to_string(q) +
+                         " < target " + std::to_string(ranks[k]) + "; basis padded");
+  }
+  if (rep) {
+    if (rep->sample_counts)
+      for (int k = 0; k < d; ++k) rep->sample_counts[k] = samples[k];
+    std::memset(rep->stage_seconds, 0, sizeof(rep->stage_seconds));
+    rep->stage_seconds[SRTT_STAGE_SAMPLING] = t_sampling;
+    rep->stage_seconds[SRTT_STAGE_H2D] = tm.between(0, 1);
+    rep->stage_seconds[SRTT_STAGE_SKETCH] = tm.between(2, 3);
+    rep->stage_seconds[SRTT_STAGE_SVD] = tm.between(3, 4);
+    rep->stage_seconds[SRTT_STAGE_TTM] = tm.between(4, 5);
+    rep->stage_seconds[SRTT_STAGE_FACTOR_WALL] = t_sampling + tm.between(2, 4);
+    rep->stage_seconds[SRTT_STAGE_D2H] = tm.between(5, 6);
+    rep->flags = hi[4 * d];
+    write_warnings(rep, warnings);
+  }
+}
+
+}  // namespace
+
+// ==================================================================================
+// C-ABI
+// ==================================================================================
+extern "C" {
+
+const char* srtt_last_error(void) { return g_last_error.c_str(); }
+int srtt_version(void) { return 100; }
+
+int srtt_create(const srtt_options* opts, srtt_handle** out) {
+  return guarded([&] {
+    if (!out) invalid("srtt_create: null output");
+    auto h = std::make_unique<srtt_handle>();
+    h->device = opts ? opts->device : 0;
+    h->use_graphs = opts ? opts->use_graphs : 0;
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (h->device < 0 || h->device >= ndev) invalid("srtt_create: no such CUDA device");
+    DeviceGuard g(h->device);
+    CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->device));
+    int major = 0;
+    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, h->device));
+    if (major != 10) fail(SRTT_ERR_CUDA, "srtt: this build targets sm_100a (B200) only");
+    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    for (auto& e : h->ev) CK(cudaEventCreate(&e));
+    h->ones.ensure(sizeof(double));
+    const double one = 1.0;
+    CK(cudaMemcpy(h->ones.p, &one, sizeof(double), cudaMemcpyHostToDevice));
+    *out = h.release();
+  });
+}
+
+int srtt_destroy(srtt_handle* h) {
+  return guarded([&] {
+    if (!h) return;
+    {
+      DeviceGuard g(h->device);
+      cudaStreamSynchronize(h->stream);
+      for (auto& e : h->ev) cudaEventDestroy(e);
+      cudaStreamDestroy(h->stream);
+    }
+    delete h;
+  });
+}
+
+int64_t srtt_last_launch_count(srtt_handle* h) { return h ? h->launches : -1; }
+
+int srtt_sample_indices(uint64_t seed, uint64_t stream_id, int64_t m, int64_t s, int64_t partitions,
+                        int64_t* idx_out, uint64_t* draws_out) {
+  return guarded([&] {
+    srtt_host::Stream rng(seed, stream_id);
+    std::vector<int64_t> out;
+    if (partitions > 1 || partitions < 1)
+      srtt_host::sample_indices_partitioned(m, s, partitions, rng, out);
+    else
+      srtt_host::sample_indices(m, s, rng, out);
+    std::memcpy(idx_out, out.data(), sizeof(int64_t) * out.size());
+    if (draws_out) *draws_out = rng.draws;
+  });
+}
+
+int srtt_tree_balanced(int32_t order, int32_t* num_nodes, int32_t* mode_begin, int32_t* modes,
+                       int32_t* left, int32_t* right, int32_t* parent, int32_t* level) {
+  return guarded([&] {
+    if (order < 2) invalid("DimensionTree: order must be >= 2");
+    struct N {
+      std::vector<int32_t> m;
+      int32_t l = -1, r = -1, p = -1, lv = 0;
+    };
+    std::vector<N> nodes;
+    N root;
+    for (int k = 0; k < order; ++k) root.m.push_back(k);
+    nodes.push_back(root);
+    std::vector<int> queue{0};
+    for (size_t qi = 0; qi < queue.size(); ++qi) {
+      const int id = queue[qi];
+      if (nodes[id].m.size() == 1) continue;
+      const size_t half = (nodes[id].m.size() + 1) / 2;
+      N a, b;
+      a.m.assign(nodes[id].m.begin(), nodes[id].m.begin() + half);
+      b.m.assign(nodes[id].m.begin() + half, nodes[id].m.end());
+      a.p = b.p = id;
+      a.lv = b.lv = nodes[id].lv + 1;
+      const int li = (int)nodes.size();
+      nodes.push_back(a);
+      const int ri = (int)nodes.size();
+      nodes.push_back(b);
+      nodes[id].l = li;
+      nodes[id].r = ri;
+      queue.push_back(li);
+      queue.push_back(ri);
+    }
+    *num_nodes = (int32_t)nodes.size();
+    int32_t pos = 0;
+    for (size_t i = 0; i < nodes.size(); ++i) {
+      mode_begin[i] = pos;
+      for (int32_t m : nodes[i].m) modes[pos++] = m;
+      left[i] = nodes[i].l;
+      right[i] = nodes[i].r;
+      if (parent) parent[i] = nodes[i].p;
+      if (level) level[i] = nodes[i].lv;
+    }
+    mode_begin[nodes.size()] = pos;
+  });
+}
+
+int srtt_sub_r_hosvd(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d, const int64_t* dims,
+                     const int64_t* ranks, int64_t oversampling, const int64_t* samples, uint64_t seed,
+                     const srtt_exec_policy* exec, double* core_out, double* const* factors_out,
+                     int32_t out_on_device, srtt_report* rep) {
+  return guarded([&] {
+    if (!h) invalid("srtt: null handle");
+    run_sub_r_hosvd(h, x, x_on_device, d, dims, ranks, oversampling, samples, seed, exec, core_out,
+                    factors_out, out_on_device, rep);
+  });
+}
+
+}  // extern "C"
+
+cudaError_t srtt_launch_normals(uint64_t, uint64_t, uint64_t, int64_t, double*, cudaStream_t);
+
+namespace {
+
+// ==================================================================================
+// Dimension tree (dimension_tree.hpp:27-152) as seen through srtt_tree
+// ==================================================================================
+struct Tree {
+  int n = 0;
+  std::vector<std::vector<int>> modes;
+  std::vector<int> left, right, parent, level;
+  bool leaf(int i) const { return left[i] < 0; }
+};
+
+Tree read_tree(const srtt_tree* t, int d) {
+  if (!t || t->num_nodes < 1) invalid("DimensionTree: empty");
+  Tree T;
+  T.n = t->num_nodes;
+  T.modes.resize(T.n);
+  T.left.assign(t->left, t->left + T.n);
+  T.right.assign(t->right, t->right + T.n);
+  T.parent.assign(T.n, -1);
+  T.level.assign(T.n, 0);
+  for (int i = 0; i < T.n; ++i) {
+    for (int k = t->mode_begin[i]; k < t->mode_begin[i + 1]; ++k) T.modes[i].push_back(t->modes[k]);
+    std::sort(T.modes[i].begin(), T.modes[i].end());
+  }
+  const int order = (int)T.modes[0].size();
+  if (order < 2) invalid("DimensionTree: order must be >= 2");
+  for (int k = 0; k < order; ++k)
+    if (T.modes[0][k] != k) invalid("DimensionTree: root must hold modes 0..d-1");
+  int leaves = 0;
+  for (int i = 0; i < T.n; ++i) {
+    if ((T.left[i] < 0) != (T.right[i] < 0)) invalid("DimensionTree: node must have zero or two children");
+    if (T.leaf(i)) {
+      if (T.modes[i].size() != 1) invalid("DimensionTree: leaves must hold a single mode");
+      ++leaves;
+      continue;
+    }
+    if (T.left[i] >= T.n || T.right[i] >= T.n) invalid("DimensionTree: child index out of range");
+    const auto& l = T.modes[T.left[i]];
+    const auto& r = T.modes[T.right[i]];
+    if (l.size() + r.size() != T.modes[i].size()) invalid("DimensionTree: children do not partition the node");
+    if (l.back() >= r.front()) invalid("DimensionTree: left child modes must precede right child modes");
+    std::vector<int> merged = l;
+    merged.insert(merged.end(), r.begin(), r.end());
+    if (merged != T.modes[i]) invalid("DimensionTree: children do not partition the node");
+    T.parent[T.left[i]] = i;
+    T.parent[T.right[i]] = i;
+  }
+  if (leaves != order) invalid("DimensionTree: expected one leaf per mode");
+  if (order != d) invalid("sub_r_rtl_ht: tree and tensor order mismatch");
+  return T;
+}
+
+// ==================================================================================
+// Sub-R-RtL-HT
+// ==================================================================================
+void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d, const int64_t* dims_p,
+                      const srtt_tree* tree_p, const int64_t* ranks_p, const int64_t* samples_p, int64_t p,
+                      uint64_t seed, const srtt_exec_policy* exec, double* const* leaf_out,
+                      double* const* transfers_out, int out_on_device, srtt_report* rep) {
+  if (d < 2 || d > SRTT_MAX_ORDER) invalid("sub_r_rtl_ht: unsupported order");
+  std::vector<int64_t> dims(dims_p, dims_p + d);
+  for (int k = 0; k < d; ++k)
+    if (dims[k] < 1) invalid("Shape: dimensions must be >= 1");
+  const Tree tr = read_tree(tree_p, d);
+  const int nn = tr.n;
+  std::vector<int64_t> ranks(ranks_p, ranks_p + nn), samples(samples_p, samples_p + nn);
+  const int64_t N = prod(dims);
+  auto node_rows = [&](int i) {
+    int64_t r = 1;
+    for (int m : tr.modes[i]) r *= dims[m];
+    return r;
+  };
+  // validate_node_ranks (htucker.hpp:109-121), then the sample budgets (:223-233)
+  if (ranks[0] != 1) invalid("sub_r_rtl_ht: root rank must be 1");
+  for (int i = 1; i < nn; ++i) {
+    const int64_t mx = std::min(node_rows(i), N / node_rows(i));
+    if (ranks[i] < 1 || ranks[i] > mx) invalid("sub_r_rtl_ht: rank out of range at node " + std::to_string(i));
+  }
+  for (int i = 1; i < nn; ++i) {
+    if (samples[i] < ranks[i] + p)
+      invalid("sub_r_rtl_ht: samples below rank + oversampling at node " + std::to_string(i));
+    if (samples[i] > N / node_rows(i))
+      invalid("sub_r_rtl_ht: more samples than fibers at node " + std::to_string(i));
+  }
+  for (int i = 1; i < nn; ++i)
+    if (ranks[i] + p > SRTT_MAX_SKETCH_COLS)
+      invalid("sub_r_rtl_ht: rank + oversampling above 64 is not supported by the B200 basis kernel");
+  std::vector<std::string> warnings;
+  if (p < 4) warnings.push_back("oversampling below the recommended minimum of 4");
+  const int64_t partitions = exec ? exec->index_partitions : 1;
+
+  DeviceGuard guard(h->device);
+  h->launches = 0;
+  Timer tm{h};
+  tm.mark();  // 0
+  const double* x = stage_input(h, x_in, x_on_device, N);
+  tm.mark();  // 1
+
+  const int nt = nn - 1;  // one basis target per non-root node (ids 1..nn-1)
+  const double ts0 = now_s();
+  std::vector<std::vector<int64_t>> cols(nt);
+  std::vector<uint64_t> draws(nt), state0(nt);
+  for (int t = 0; t < nt; ++t) {
+    const int id = t + 1;
+    srtt_host::Stream rng(seed, (uint64_t)id);
+    const int64_t m = N / node_rows(id);
+    try {
+      if (partitions > 1)
+        srtt_host::sample_indices_partitioned(m, samples[id], partitions, rng, cols[t]);
+      else
+        srtt_host::sample_indices(m, samples[id], rng, cols[t]);
+    } catch (const std::exception& e) {
+      fail(SRTT_ERR_JOB, "job " + std::to_string(t) + ": " + e.what());
+    }
+    draws[t] = rng.draws;
+    state0[t] = srtt_host::stream_state0(seed, (uint64_t)id);
+  }
+  const double t_sampling = now_s() - ts0;
+
+  Layout L;
+  std::vector<size_t> off_z(nt), off_u(nt);
+  std::vector<BasisPlan> bp(nt);
+  std::vector<BasisBuffers> bb(nt);
+  int cmax = 0;
+  int64_t max_n = 0;
+  for (int t = 0; t < nt; ++t) {
+    const int id = t + 1;
+    const int c = (int)(ranks[id] + p);
+    const int64_t rows = node_rows(id);
+    cmax = std::max(cmax, c);
+    max_n = std::max(max_n, rows);
+    off_z[t] = L.take(sizeof(double) * rows * c);
+    off_u[t] = L.take(sizeof(double) * rows * ranks[id]);
+    bp[t] = plan_basis(rows, c, (int)ranks[id]);
+    bb[t] = layout_basis(L, bp[t]);
+  }
+  const size_t off_pad = L.take(sizeof(double) * max_n * nt);
+  const size_t off_flags = L.take(sizeof(int32_t) * 4);
+  // transfers of internal non-root nodes, and the root
+  std::vector<int> internal;
+  for (int i = 1; i < nn; ++i)
+    if (!tr.leaf(i)) internal.push_back(i);
+  std::vector<size_t> off_b(nn, 0);
+  for (int i : internal)
+    off_b[i] = L.take(sizeof(double) * ranks[i] * ranks[tr.left[i]] * ranks[tr.right[i]]);
+  const int rl0 = (int)ranks[tr.left[0]], rr0 = (int)ranks[tr.right[0]];
+  off_b[0] = L.take(sizeof(double) * rl0 * rr0);
+  const std::vector<int64_t> rdims = {node_rows(tr.left[0]), node_rows(tr.right[0])};
+  const std::vector<int64_t> rranks = {rl0, rr0};
+  CorePlan cp = plan_core(rdims, rranks, h->sms);
+  size_t off_ufrag = 0, off_part = 0, off_tmp0 = 0, off_tmp1 = 0;
+  std::vector<size_t> off_fu;
+  layout_core(L, cp, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+  h->ws.ensure(L.off);
+  char* ws = reinterpret_cast<char*>(h->ws.p);
+
+  Blob blob;
+  std::vector<size_t> off_cols(nt);
+  for (int t = 0; t < nt; ++t) off_cols[t] = blob.add(cols[t].data(), sizeof(int64_t) * cols[t].size());
+  const size_t off_sk = blob.reserve(sizeof(SketchTarget) * nt);
+  const size_t off_bt = blob.reserve(sizeof(BasisTarget) * nt);
+  const size_t off_tt = blob.reserve(sizeof(TransferTarget) * std::max<size_t>(1, internal.size()));
+  h->dparams.ensure(blob.lay.off);
+  h->hparams.ensure(blob.lay.off);
+  char* dp = reinterpret_cast<char*>(h->dparams.p);
+  char* hp = reinterpret_cast<char*>(h->hparams.p);
+  for (auto& it : blob.items) std::memcpy(hp + it.first, it.second.data(), it.second.size());
+  std::vector<SketchTarget> sk(nt);
+  std::vector<BasisTarget> bt(nt);
+  int32_t* d_flags = reinterpret_cast<int32_t*>(ws + off_flags);
+  int64_t ctas = 0;
+  auto ubasis = [&](int id) { return reinterpret_cast<double*>(ws + off_u[id - 1]); };
+  for (int t = 0; t < nt; ++t) {
+    const int id = t + 1;
+    const int c = (int)(ranks[id] + p);
+    sk[t] = make_sketch_target(x, dims, tr.modes[id], samples[id], c);
+    sk[t].cols = reinterpret_cast<const int64_t*>(dp + off_cols[t]);
+    sk[t].z = reinterpret_cast<double*>(ws + off_z[t]);
+    sk[t].state0 = state0[t];
+    sk[t].draw_offset = draws[t];
+    sk[t].cta_begin = ctas;
+    sk[t].flags = d_flags;
+    ctas += (sk[t].rows + sk[t].row_tile - 1) / sk[t].row_tile;
+    bt[t] = fill_basis(bp[t], bb[t], ws, sk[t].z, ubasis(id), state0[t], draws[t], samples[id] * c);
+  }
+  assign_basis_ctas(bt);
+  std::vector<TransferTarget> tt;
+  int tctas = 0, max_rl = 1, max_rr = 1;
+  for (int i : internal) {
+    TransferTarget T{};
+    T.us = ubasis(i);
+    T.ul = ubasis(tr.left[i]);
+    T.ur = ubasis(tr.right[i]);
+    T.b = reinterpret_cast<double*>(ws + off_b[i]);
+    T.nl = node_rows(tr.left[i]);
+    T.nr = node_rows(tr.right[i]);
+    T.rs = (int)ranks[i];
+    T.rl = (int)ranks[tr.left[i]];
+    T.rr = (int)ranks[tr.right[i]];
+    T.cta_begin = tctas;
+    tctas += T.rs;
+    max_rl = std::max(max_rl, T.rl);
+    max_rr = std::max(max_rr, T.rr);
+    tt.push_back(T);
+  }
+  std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * nt);
+  std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * nt);
+  if (!tt.empty()) std::memcpy(hp + off_tt, tt.data(), sizeof(TransferTarget) * tt.size());
+  CK(cudaMemsetAsync(d_flags, 0, sizeof(int32_t) * 4, h->stream));
+  CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
+  tm.mark();  // 2
+  CK(srtt_launch_sketch(reinterpret_cast<const SketchTarget*>(dp + off_sk), nt, ctas, cmax, h->stream));
+  h->launches++;
+  tm.mark();  // 3
+  h->launches += launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt),
+                                    reinterpret_cast<double*>(ws + off_pad), max_n);
+  tm.mark();  // 4
+  if (!tt.empty()) {
+    CK(srtt_launch_transfer(reinterpret_cast<const TransferTarget*>(dp + off_tt), (int)tt.size(), tctas, max_rl,
+                            max_rr, h->stream));
+    h->launches++;
+  }
+  tm.mark();  // 5
+  // root transfer: the K3 engine on M = X viewed as n_l x n_r (htucker.hpp:67-85)
+  std::vector<const double*> ur = {ubasis(tr.left[0]), ubasis(tr.right[0])};
+  double* d_root = reinterpret_cast<double*>(ws + off_b[0]);
+  h->launches += launch_core_pass(h, cp, x, ur, d_root, ws, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+  tm.mark();  // 6
+  for (int i = 1; i < nn; ++i)
+    if (tr.leaf(i)) {
+      const int mode = tr.modes[i][0];
+      copy_out(h, leaf_out[mode], ubasis(i), sizeof(double) * dims[mode] * ranks[i], out_on_device);
+    }
+  if (transfers_out) {
+    for (int i : internal)
+      if (transfers_out[i])
+        copy_out(h, transfers_out[i], ws + off_b[i],
+                 sizeof(double) * ranks[i] * ranks[tr.left[i]] * ranks[tr.right[i]], out_on_device);
+    if (transfers_out[0]) copy_out(h, transfers_out[0], d_root, sizeof(double) * rl0 * rr0, out_on_device);
+  }
+  h->hinfo.ensure(sizeof(int32_t) * 4 * (nt + 1));
+  int32_t* hi = reinterpret_cast<int32_t*>(h->hinfo.p);
+  for (int t = 0; t < nt; ++t)
+    CK(cudaMemcpyAsync(hi + 4 * t, bt[t].info, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(hi + 4 * nt, d_flags, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, h->stream));
+  tm.mark();  // 7
+  CK(cudaStreamSynchronize(h->stream));
+  CK(cudaGetLastError());
+  for (int t = 0; t < nt; ++t) {
+    const int id = t + 1;
+    const int q = hi[4 * t];
+    if (rep && rep->achieved_ranks) rep->achieved_ranks[id] = q;
+    if (q < ranks[id])
+      warnings.push_back("node " + std::to_string(id) + ": sketch revealed rank " + std::to_string(q) +
+                         " < target; basis padded");
+  }
+  if (rep) {
+    if (rep->achieved_ranks) rep->achieved_ranks[0] = 1;
+    if (rep->sample_counts)
+      for (int i = 0; i < nn; ++i) rep->sample_counts[i] = samples[i];
+    std::memset(rep->stage_seconds, 0, sizeof(rep->stage_seconds));
+    rep->stage_seconds[SRTT_STAGE_SAMPLING] = t_sampling;
+    rep->stage_seconds[SRTT_STAGE_H2D] = tm.between(0, 1);
+    rep->stage_seconds[SRTT_STAGE_SKETCH] = tm.between(2, 3);
+    rep->stage_seconds[SRTT_STAGE_SVD] = tm.between(3, 4);
+    rep->stage_seconds[SRTT_STAGE_TRANSFER] = tm.between(4, 5);
+    rep->stage_seconds[SRTT_STAGE_SERIAL_TAIL] = tm.between(5, 6);
+    rep->stage_seconds[SRTT_STAGE_FACTOR_WALL] = t_sampling + tm.between(2, 4);
+    rep->stage_seconds[SRTT_STAGE_D2H] = tm.between(6, 7);
+    rep->flags = hi[4 * nt];
+    write_warnings(rep, warnings);
+  }
+}
+
+// ---- helpers for component entry points ------------------------------------
+struct Scratch {  // device copies of small host inputs for component calls
+  srtt_handle* h;
+  std::vector<std::pair<const void*, size_t>> pending;
+};
+
+const double* to_device(srtt_handle* h, DevBuf& buf, const double* src, int64_t count, int on_device) {
+  if (on_device) return src;
+  buf.ensure(sizeof(double) * std::max<int64_t>(count, 1));
+  CK(cudaMemcpyAsync(buf.p, src, sizeof(double) * count, cudaMemcpyHostToDevice, h->stream));
+  return reinterpret_cast<const double*>(buf.p);
+}
+
+struct CompBufs {
+  DevBuf a, b, c, d, e, idx;
+};
+
+void validate_modes(int d, const int64_t* dims, int nmodes, const int32_t* modes, const char* what) {
+  if (nmodes < 1) invalid("ModeSet: must be non-empty");
+  std::vector<int> m(modes, modes + nmodes);
+  std::sort(m.begin(), m.end());
+  if (std::adjacent_find(m.begin(), m.end()) != m.end()) invalid("ModeSet: modes must be distinct");
+  if (m.front() < 0) invalid("ModeSet: modes must be >= 0");
+  if (m.back() >= d) invalid("ModeSet: mode out of range for order " + std::to_string(d));
+  if (nmodes >= d && nmodes > 1) invalid(std::string(what) + ": mode set must be a proper subset");
+  for (int k = 0; k < d; ++k)
+    if (dims[k] < 1) invalid("Shape: dimensions must be >= 1");
+}
+
+}  // namespace
+
+extern "C" {
+
+int srtt_sub_r_rtl_ht(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d, const int64_t* dims,
+                      const srtt_tree* tree, const int64_t* ranks, const int64_t* samples, int64_t oversampling,
+                      uint64_t seed, const srtt_exec_policy* exec, double* const* leaf_factors_out,
+                      double* const* transfers_out, int32_t out_on_device, srtt_report* rep) {
+  return guarded([&] {
+    if (!h) invalid("srtt: null handle");
+    run_sub_r_rtl_ht(h, x, x_on_device, d, dims, tree, ranks, samples, oversampling, seed, exec, leaf_factors_out,
+                     transfers_out, out_on_device, rep);
+  });
+}
+
+int srtt_stream_normals(srtt_handle* h, uint64_t seed, uint64_t stream_id, uint64_t draw_offset, uint64_t t0,
+                        int64_t n, double* out) {
+  return guarded([&] {
+    DeviceGuard g(h->device);
+    CompBufs B;
+    B.a.ensure(sizeof(double) * std::max<int64_t>(n, 1));
+    CK(srtt_launch_normals(srtt_host::stream_state0(seed, stream_id), draw_offset, t0, n,
+                           reinterpret_cast<double*>(B.a.p), h->stream));
+    CK(cudaMemcpyAsync(out, B.a.p, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int srtt_extract_fibers(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d, const int64_t* dims,
+                        int32_t nmodes, const int32_t* modes, int64_t ncols, const int64_t* cols, double* y_out,
+                        int32_t out_on_device) {
+  return guarded([&] {
+    const char* what = nmodes == 1 ? "extract_fibers" : "extract_group_fibers";
+    validate_modes(d, dims, nmodes, modes, what);
+    std::vector<int64_t> dv(dims, dims + d);
+    const int64_t N = prod(dv);
+    std::vector<int> mv(modes, modes + nmodes);
+    SketchTarget T = make_sketch_target(nullptr, dv, mv, ncols, 1);
+    const int64_t total_cols = N / T.rows;
+    for (int64_t j = 0; j < ncols; ++j)
+      if (cols[j] < 0 || cols[j] >= total_cols)
+        throw std::out_of_range(std::string(what) + ": column index out of range");
+    DeviceGuard g(h->device);
+    CompBufs B;
+    const double* dx = to_device(h, B.a, x, N, x_on_device);
+    B.idx.ensure(sizeof(int64_t) * std::max<int64_t>(ncols, 1));
+    CK(cudaMemcpyAsync(B.idx.p, cols, sizeof(int64_t) * ncols, cudaMemcpyHostToDevice, h->stream));
+    double* dy = y_out;
+    if (!out_on_device) {
+      B.b.ensure(sizeof(double) * std::max<int64_t>(T.rows * ncols, 1));
+      dy = reinterpret_cast<double*>(B.b.p);
+    }
+    GatherParams P{};
+    P.x = dx;
+    P.cols = reinterpret_cast<const int64_t*>(B.idx.p);
+    P.y = dy;
+    P.rows = T.rows;
+    P.w = ncols;
+    P.nrow_modes = T.nrow_modes;
+    P.ncol_modes = T.ncol_modes;
+    std::memcpy(P.row_dim, T.row_dim, sizeof(P.row_dim));
+    std::memcpy(P.row_stride, T.row_stride, sizeof(P.row_stride));
+    std::memcpy(P.col_dim, T.col_dim, sizeof(P.col_dim));
+    std::memcpy(P.col_stride, T.col_stride, sizeof(P.col_stride));
+    if (T.rows * ncols > 0) CK(srtt_launch_gather(P, h->stream));
+    if (!out_on_device)
+      CK(cudaMemcpyAsync(y_out, dy, sizeof(double) * T.rows * ncols, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int srtt_sketch(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d, const int64_t* dims,
+                int32_t nmodes, const int32_t* modes, int64_t ncols, const int64_t* cols, int32_t c, uint64_t seed,
+                uint64_t stream_id, uint64_t draw_offset, const double* omega, double* z_out,
+                int32_t out_on_device) {
+  return guarded([&] {
+    validate_modes(d, dims, nmodes, modes, "extract_group_fibers");
+    if (c < 1 || c > SRTT_MAX_SKETCH_COLS) invalid("sketch: columns out of range");
+    std::vector<int64_t> dv(dims, dims + d);
+    const int64_t N = prod(dv);
+    std::vector<int> mv(modes, modes + nmodes);
+    DeviceGuard g(h->device);
+    CompBufs B;
+    const double* dx = to_device(h, B.a, x, N, x_on_device);
+    SketchTarget T = make_sketch_target(dx, dv, mv, ncols, c);
+    for (int64_t j = 0; j < ncols; ++j)
+      if (cols[j] < 0 || cols[j] >= N / T.rows) throw std::out_of_range("extract_fibers: column index out of range");
+    B.idx.ensure(sizeof(int64_t) * std::max<int64_t>(ncols, 1));
+    CK(cudaMemcpyAsync(B.idx.p, cols, sizeof(int64_t) * ncols, cudaMemcpyHostToDevice, h->stream));
+    T.cols = reinterpret_cast<const int64_t*>(B.idx.p);
+    if (omega) T.omega = to_device(h, B.c, omega, ncols * c, 0);
+    B.b.ensure(sizeof(double) * T.rows * c);
+    T.z = reinterpret_cast<double*>(B.b.p);
+    T.state0 = srtt_host::stream_state0(seed, stream_id);
+    T.draw_offset = draw_offset;
+    B.e.ensure(sizeof(int32_t) * 4 + sizeof(SketchTarget));
+    T.flags = reinterpret_cast<int32_t*>(B.e.p);
+    CK(cudaMemsetAsync(T.flags, 0, sizeof(int32_t) * 4, h->stream));
+    T.cta_begin = 0;
+    SketchTarget* dT = reinterpret_cast<SketchTarget*>(reinterpret_cast<char*>(B.e.p) + 64);
+    B.d.ensure(sizeof(SketchTarget));
+    dT = reinterpret_cast<SketchTarget*>(B.d.p);
+    CK(cudaMemcpyAsync(dT, &T, sizeof(T), cudaMemcpyHostToDevice, h->stream));
+    const int64_t ctas = (T.rows + T.row_tile - 1) / T.row_tile;
+    CK(srtt_launch_sketch(dT, 1, ctas, c, h->stream));
+    copy_out(h, z_out, T.z, sizeof(double) * T.rows * c, out_on_device);
+    CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int srtt_range_basis_of_sketch(srtt_handle* h, const double* z, int32_t z_on_device, int64_t n, int32_t c,
+                               int32_t rank, uint64_t seed, uint64_t stream_id, uint64_t draw_offset,
+                               int64_t normal_base, double* q_out, int64_t* numerical_rank, double* sv_out,
+                               int32_t out_on_device) {
+  return guarded([&] {
+    if (rank < 1 || rank > c) invalid("range_basis_of_sketch: rank out of range");
+    if (c > SRTT_MAX_SKETCH_COLS) invalid("range_basis_of_sketch: more than 64 sketch columns unsupported");
+    if (n < 1) invalid("range_basis_of_sketch: empty sketch");
+    DeviceGuard g(h->device);
+    CompBufs B;
+    // the basis overwrites its input: always work on a private copy
+    B.a.ensure(sizeof(double) * n * c);
+    CK(cudaMemcpyAsync(B.a.p, z, sizeof(double) * n * c,
+                       z_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
+    BasisPlan bp = plan_basis(n, c, rank);
+    Layout L;
+    BasisBuffers bb = layout_basis(L, bp);
+    const size_t off_u = L.take(sizeof(double) * n * rank);
+    const size_t off_pad = L.take(sizeof(double) * n);
+    const size_t off_t = L.take(sizeof(BasisTarget));
+    B.b.ensure(L.off);
+    char* ws = reinterpret_cast<char*>(B.b.p);
+    std::vector<BasisTarget> bt = {fill_basis(bp, bb, ws, reinterpret_cast<double*>(B.a.p),
+                                              reinterpret_cast<double*>(ws + off_u),
+                                              srtt_host::stream_state0(seed, stream_id), draw_offset, normal_base)};
+    assign_basis_ctas(bt);
+    CK(cudaMemcpyAsync(ws + off_t, bt.data(), sizeof(BasisTarget), cudaMemcpyHostToDevice, h->stream));
+    launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(ws + off_t), reinterpret_cast<double*>(ws + off_pad),
+                       n);
+    copy_out(h, q_out, ws + off_u, sizeof(double) * n * rank, out_on_device);
+    int32_t info[4];
+    CK(cudaMemcpyAsync(info, bt[0].info, sizeof(info), cudaMemcpyDeviceToHost, h->stream));
+    std::vector<double> sv(std::min<int64_t>(n, c));
+    CK(cudaMemcpyAsync(sv.data(), bt[0].sv, sizeof(double) * sv.size(), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (numerical_rank) *numerical_rank = info[0];
+    if (sv_out) std::memcpy(sv_out, sv.data(), sizeof(double) * sv.size());
+  });
+}
+
+int srtt_multi_ttm_core(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d, const int64_t* dims,
+                        const int64_t* ranks, const double* const* factors, int32_t factors_on_device,
+                        double* core_out, int32_t out_on_device) {
+  return guarded([&] {
+    if (d < 2 || d > SRTT_MAX_ORDER) invalid("multi_ttm_core: order must be in [2, 16]");
+    std::vector<int64_t> dv(dims, dims + d), rv(ranks, ranks + d);
+    for (int k = 0; k < d; ++k)
+      if (dv[k] < 1 || rv[k] < 1 || rv[k] > dv[k]) invalid("sliced_core: factor rows mismatch in mode " + std::to_string(k));
+    DeviceGuard g(h->device);
+    const int64_t N = prod(dv);
+    CompBufs B;
+    const double* dx = to_device(h, B.a, x, N, x_on_device);
+    std::vector<DevBuf> ub(d);
+    std::vector<const double*> u(d);
+    for (int k = 0; k < d; ++k) u[k] = to_device(h, ub[k], factors[k], dv[k] * rv[k], factors_on_device);
+    CorePlan cp = plan_core(dv, rv, h->sms);
+    Layout L;
+    size_t off_ufrag, off_part, off_tmp0, off_tmp1;
+    std::vector<size_t> off_fu;
+    layout_core(L, cp, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+    const size_t off_core = L.take(sizeof(double) * prod(rv));
+    B.b.ensure(L.off);
+    char* ws = reinterpret_cast<char*>(B.b.p);
+    launch_core_pass(h, cp, dx, u, reinterpret_cast<double*>(ws + off_core), ws, off_ufrag, off_fu, off_part,
+                     off_tmp0, off_tmp1);
+    copy_out(h, core_out, ws + off_core, sizeof(double) * prod(rv), out_on_device);
+    CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int srtt_transfer_tensor(srtt_handle* h, const double* u_node, const double* u_left, const double* u_right,
+                         int64_t nl, int64_t nr, int32_t rs, int32_t rl, int32_t rr, int32_t on_device,
+                         double* b_out) {
+  return guarded([&] {
+    if (nl < 1 || nr < 1 || rs < 1 || rl < 1 || rr < 1) invalid("transfer_tensor: empty operand");
+    DeviceGuard g(h->device);
+    CompBufs B;
+    TransferTarget T{};
+    T.us = to_device(h, B.a, u_node, nl * nr * rs, on_device);
+    T.ul = to_device(h, B.b, u_left, nl * rl, on_device);
+    T.ur = to_device(h, B.c, u_right, nr * rr, on_device);
+    B.d.ensure(sizeof(double) * rs * rl * rr + 256 + sizeof(TransferTarget));
+    T.b = reinterpret_cast<double*>(B.d.p);
+    T.nl = nl;
+    T.nr = nr;
+    T.rs = rs;
+    T.rl = rl;
+    T.rr = rr;
+    T.cta_begin = 0;
+    char* tp = reinterpret_cast<char*>(B.d.p) + ((sizeof(double) * rs * rl * rr + 255) / 256 * 256);
+    CK(cudaMemcpyAsync(tp, &T, sizeof(T), cudaMemcpyHostToDevice, h->stream));
+    CK(srtt_launch_transfer(reinterpret_cast<const TransferTarget*>(tp), 1, rs, rl, rr, h->stream));
+    copy_out(h, b_out, T.b, sizeof(double) * rs * rl * rr, on_device);
+    CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int srtt_root_transfer(srtt_handle* h, const double* x, int32_t x_on_device, int64_t nl, int64_t nr,
+                       const double* u_left, int32_t rl, const double* u_right, int32_t rr,
+                       int32_t factors_on_device, double* b_out, int32_t out_on_device) {
+  return guarded([&] {
+    if (nl < 1 || nr < 1) invalid("root_transfer: child rows do not factor the tensor size");
+    const int64_t dims2[2] = {nl, nr};
+    const int64_t ranks2[2] = {rl, rr};
+    const double* f[2] = {u_left, u_right};
+    // identical to the 2-mode core: B(0, j, k) = (U_l^T M U_r)(j, k)
+    const int rc = srtt_multi_ttm_core(h, x, x_on_device, 2, dims2, ranks2, f, factors_on_device, b_out,
+                                       out_on_device);
+    if (rc != SRTT_OK) throw Error{rc, g_last_error};
+  });
+}
+
+}  // extern "C"

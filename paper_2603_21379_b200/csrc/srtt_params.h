@@ -1,0 +1,118 @@
+// Plain-C parameter blocks shared by the host planner (host.cu) and the
+// sm_100a kernels. Everything is POD so a whole array of targets travels to
+// the device in one cudaMemcpyAsync and the launch sequence can be captured
+// once in a CUDA graph and replayed with new seeds.
+#pragma once
+#include <stdint.h>
+
+#define SRTT_MAX_ORDER 16
+#define SRTT_MAX_SKETCH_COLS 64  // r + p limit of the basis kernels
+
+// ---------------------------------------------------------------------------
+// K1: fused fiber gather + in-kernel Gaussian sketch, Z = Y * Omega.
+// One "target" is a Tucker mode (tucker.hpp:141-168) or an H-Tucker node
+// (htucker.hpp:263-287). Y is never materialised: each sampled fibre element
+// is loaded into a register and immediately multiplied into Z.
+// ---------------------------------------------------------------------------
+typedef struct SketchTarget {
+  const double* x;        // tensor data (first index fastest)
+  const int64_t* cols;    // w sampled columns of the (mode-set) unfolding
+  const double* omega;    // optional explicit Omega (w x c, column-major); NULL = generate
+  double* z;              // out: rows x c, column-major (ld = rows)
+  int64_t rows;           // n_S
+  int64_t w;              // fibres sampled
+  int32_t c;              // r + p
+  int32_t nrow_modes;     // modes of S (ascending): row digit decode
+  int32_t ncol_modes;     // complement modes (ascending): column digit decode
+  int32_t row_tile;       // rows handled per CTA
+  int64_t row_dim[SRTT_MAX_ORDER];
+  int64_t row_stride[SRTT_MAX_ORDER];
+  int64_t col_dim[SRTT_MAX_ORDER];
+  int64_t col_stride[SRTT_MAX_ORDER];
+  uint64_t state0;        // RngStream(seed, id) initial state (rng.hpp:30-36)
+  uint64_t draw_offset;   // u64 draws consumed by the sampling step
+  int64_t cta_begin;      // first CTA index of this target in the grouped grid
+  int32_t* flags;         // device status word (bit 0: Box-Muller u1 == 0 met)
+} SketchTarget;
+
+// ---------------------------------------------------------------------------
+// K2: basis of a sketch (sketch.hpp:74-93): Householder TSQR of Z, one-sided
+// Jacobi SVD of the small triangular factor, rank decision at
+// tol = max(rows, cols) * eps * sigma_1, U = Q * V[:, :q], Gaussian padding
+// from the same stream.
+// ---------------------------------------------------------------------------
+typedef struct QrLevel {
+  double* a;       // level matrix (n_l x c, ld = n_l); overwritten with reflectors
+  double* tau;     // nblk x c
+  double* r_out;   // stacked R of the next level (nblk*c x c, ld = nblk*c) (NULL at top)
+  double* y;       // back-application buffer for this level (n_l x r, ld = n_l)
+  int64_t n;       // rows at this level
+  int32_t nblk;    // row blocks at this level
+  int32_t blk_rows;
+} QrLevel;
+
+#define SRTT_MAX_QR_LEVELS 6
+
+typedef struct BasisTarget {
+  double* u;              // out: n x r column-major (ld = n)
+  double* sv;             // out: min(n, c) singular values, descending (may be NULL)
+  int32_t* info;          // out: [0] achieved (numerical) rank q, [1] nrank, [2] flags
+  int64_t n;              // sketch rows
+  int32_t c;              // sketch columns (r + p)
+  int32_t r;              // target rank
+  int32_t nlevels;        // TSQR levels below the top (0 => single block)
+  int32_t cta_begin[SRTT_MAX_QR_LEVELS];  // CTA offsets for grouped level launches
+  QrLevel lv[SRTT_MAX_QR_LEVELS + 1];     // lv[0] = Z itself ... lv[nlevels] = top
+  uint64_t state0;        // stream of the target (padding continues it)
+  uint64_t draw_offset;   // draws consumed by sampling
+  int64_t normal_base;    // normals already consumed by Omega (w * c)
+} BasisTarget;
+
+// ---------------------------------------------------------------------------
+// K3/K5: fused multi-TTM streaming engine. X is viewed as M (n0 x Q),
+// column-major. Stage 1 (mode 0, the only stride-1 mode) runs on FP64 tensor
+// cores (DMMA.8x8x4 via mma.sync) over TMA-loaded, 128B-swizzled boxes of
+// 16 rows x W columns; stages 2..m fold the t1 tiles into nested
+// accumulators in shared memory. Each work item writes one partial of
+// R_m = X x_0 U_0^T ... x_{m-1} U_{m-1}^T for one level-m group.
+// ---------------------------------------------------------------------------
+typedef struct CoreParams {
+  const double* x;
+  const double* ufrag;     // U0 in B-fragment order: [nrb][RB/4][NT][32]
+  const double* fu[SRTT_MAX_ORDER];  // fold factors U_1..U_{m-1}, ROW-major (n_k x r_k)
+  double* part;            // out: [nrb][S][G][A]
+  int64_t n0;              // rows (mode 0 extent, or n_left for the root pass)
+  int64_t Q;               // columns
+  int64_t fdim[SRTT_MAX_ORDER];  // n_1..n_{m-1}
+  int32_t frank[SRTT_MAX_ORDER]; // r_1..r_{m-1}
+  int64_t GS;              // columns per level-m group
+  int64_t G;               // number of groups
+  int64_t SL;              // columns per split (multiple of W)
+  int64_t nitems;          // nrb * G * S
+  int32_t S;               // splits per group
+  int32_t m;               // fold depth (>= 2)
+  int32_t r0;              // rank of mode 0
+  int32_t NT;              // N-tiles (ceil(r0 / 8))
+  int32_t RB;              // rows per row block (multiple of 16, <= 256)
+  int32_t nrb;             // row blocks
+  int32_t W;               // columns per TMA box
+  int32_t A;               // prod_{k<m} r_k (output entries per item)
+  int32_t use_tma;         // 1: cp.async.bulk.tensor loads; 0: warp-copy path (odd n0)
+  int32_t acc_off[SRTT_MAX_ORDER + 1];  // smem offsets (doubles) of acc_2..acc_m
+  int32_t acc_total;       // doubles of all accumulators
+} CoreParams;
+
+// Generic small TTM used by the tail of the core pass and by reconstruct:
+// out(g, b, post) = sum_i in(g, i, post) * U(i, b)   (U given as n x r).
+// When nparts > 1 the input is a sum of nparts partial tensors spaced by
+// part_stride (fixed summation order: deterministic).
+typedef struct TtmParams {
+  const double* in;
+  const double* u;       // column-major n x rr (ld = n); transpose flag picks U vs U^T
+  double* out;
+  int64_t g, n, post;    // input viewed as g x n x post
+  int64_t rr;            // output extent along the mode
+  int32_t transpose;     // 1: contract with U^T (u is n x rr) ; 0: with U (u is rr x n)
+  int32_t nparts;
+  int64_t part_stride;
+} TtmParams;

@@ -1,0 +1,566 @@
+"""Python mirror of the reference's hot-path API over the C-ABI.
+
+Names, argument meaning, validation and error behaviour follow the
+reference's C++ API (proj/include/srtt/*.hpp); every compute call goes
+through ``libsrtt_b200.so`` (hand-written sm_100a kernels).  There is no
+CPU fallback: if the shared library is missing or no B200 is visible, the
+calls raise.
+
+Layout conventions (reference tensor.hpp:17-20, common.hpp:21-24): tensors
+are flat with the FIRST index fastest -- a numpy array ``x`` of shape dims is
+passed as ``np.ravel(x, order="F")``; factors are column-major ``n x r``.
+
+Reference exceptions map to Python ones:
+  std::invalid_argument -> InvalidArgument (ValueError)
+  std::out_of_range     -> OutOfRange (IndexError)
+  JobError(job)         -> JobError (RuntimeError, ``.job`` holds the index)
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import load_library
+
+# ---------------------------------------------------------------------------
+# errors
+# ---------------------------------------------------------------------------
+SRTT_OK = 0
+SRTT_ERR_INVALID_ARGUMENT = 1
+SRTT_ERR_OUT_OF_RANGE = 2
+SRTT_ERR_CUDA = 3
+SRTT_ERR_NCCL = 4
+SRTT_ERR_OUT_OF_MEMORY = 5
+SRTT_ERR_INTERNAL = 6
+SRTT_ERR_JOB = 7
+
+STAGES = ["sampling", "extract", "sketch", "svd", "transfer", "ttm", "gather", "serial_tail",
+          "factor_wall", "h2d", "d2h"]
+
+
+class SrttError(RuntimeError):
+    pass
+
+
+class InvalidArgument(ValueError):
+    pass
+
+
+class OutOfRange(IndexError):
+    pass
+
+
+class JobError(RuntimeError):
+    """parallel.hpp:79-129: first failing job's index + message."""
+
+    def __init__(self, msg):
+        super().__init__(msg)
+        try:
+            self.job = int(msg.split(":", 1)[0].split()[1])
+        except Exception:  # pragma: no cover
+            self.job = -1
+
+
+class CudaError(SrttError):
+    pass
+
+
+def _check(rc):
+    if rc == SRTT_OK:
+        return
+    msg = _L().srtt_last_error().decode()
+    if rc == SRTT_ERR_INVALID_ARGUMENT:
+        raise InvalidArgument(msg)
+    if rc == SRTT_ERR_OUT_OF_RANGE:
+        raise OutOfRange(msg)
+    if rc == SRTT_ERR_JOB:
+        raise JobError(msg)
+    if rc in (SRTT_ERR_CUDA, SRTT_ERR_OUT_OF_MEMORY):
+        raise CudaError(msg)
+    raise SrttError(f"srtt error {rc}: {msg}")
+
+
+# ---------------------------------------------------------------------------
+# C structs
+# ---------------------------------------------------------------------------
+class _Options(C.Structure):
+    _fields_ = [("device", C.c_int32), ("use_graphs", C.c_int32), ("reserved", C.c_int32 * 6)]
+
+
+class _Exec(C.Structure):
+    _fields_ = [("workers", C.c_int64), ("slice_mode", C.c_int64), ("index_partitions", C.c_int64),
+                ("emulate_serial_root", C.c_int32), ("reserved", C.c_int32)]
+
+
+class _Report(C.Structure):
+    _fields_ = [("sample_counts", C.POINTER(C.c_int64)), ("achieved_ranks", C.POINTER(C.c_int64)),
+                ("warnings", C.c_char_p), ("warnings_capacity", C.c_int64), ("num_warnings", C.c_int64),
+                ("stage_seconds", C.c_double * len(STAGES)), ("flags", C.c_int32), ("reserved", C.c_int32)]
+
+
+class _Tree(C.Structure):
+    _fields_ = [("num_nodes", C.c_int32), ("mode_begin", C.POINTER(C.c_int32)), ("modes", C.POINTER(C.c_int32)),
+                ("left", C.POINTER(C.c_int32)), ("right", C.POINTER(C.c_int32))]
+
+
+_LIB = None
+
+
+def _L():
+    global _LIB
+    if _LIB is None:
+        lib = load_library()
+        vp = C.c_void_p
+        i32, i64, u64 = C.c_int32, C.c_int64, C.c_uint64
+        lib.srtt_last_error.restype = C.c_char_p
+        lib.srtt_create.argtypes = [C.POINTER(_Options), C.POINTER(vp)]
+        lib.srtt_destroy.argtypes = [vp]
+        lib.srtt_last_launch_count.argtypes = [vp]
+        lib.srtt_last_launch_count.restype = i64
+        lib.srtt_sample_indices.argtypes = [u64, u64, i64, i64, i64, vp, vp]
+        lib.srtt_stream_normals.argtypes = [vp, u64, u64, u64, u64, i64, vp]
+        lib.srtt_tree_balanced.argtypes = [i32] + [vp] * 7
+        lib.srtt_sub_r_hosvd.argtypes = [vp, vp, i32, i32, vp, vp, i64, vp, u64, vp, vp, vp, i32, vp]
+        lib.srtt_sub_r_rtl_ht.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, i64, u64, vp, vp, vp, i32, vp]
+        lib.srtt_extract_fibers.argtypes = [vp, vp, i32, i32, vp, i32, vp, i64, vp, vp, i32]
+        lib.srtt_sketch.argtypes = [vp, vp, i32, i32, vp, i32, vp, i64, vp, i32, u64, u64, u64, vp, vp, i32]
+        lib.srtt_range_basis_of_sketch.argtypes = [vp, vp, i32, i64, i32, i32, u64, u64, u64, i64, vp, vp, vp,
+                                                   i32]
+        lib.srtt_multi_ttm_core.argtypes = [vp, vp, i32, i32, vp, vp, vp, i32, vp, i32]
+        lib.srtt_transfer_tensor.argtypes = [vp, vp, vp, vp, i64, i64, i32, i32, i32, i32, vp]
+        lib.srtt_root_transfer.argtypes = [vp, vp, i32, i64, i64, vp, i32, vp, i32, i32, vp, i32]
+        _LIB = lib
+    return _LIB
+
+
+def _ptr(a):
+    """(pointer, on_device) of a numpy array or a CUDA torch tensor."""
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data, 0
+    if hasattr(a, "data_ptr") and getattr(a, "is_cuda", False):
+        return a.data_ptr(), 1
+    raise TypeError(f"unsupported buffer type {type(a)}")
+
+
+def _i64(v):
+    return np.ascontiguousarray(np.asarray(v, dtype=np.int64))
+
+
+def _flat_f64(x):
+    if isinstance(x, np.ndarray):
+        return np.ascontiguousarray(np.ravel(x, order="F"), dtype=np.float64)
+    if hasattr(x, "is_cuda") and x.is_cuda:
+        import torch
+
+        if x.dtype != torch.float64 or not x.is_contiguous():
+            raise TypeError("device tensors must be contiguous float64 (first index fastest)")
+        return x
+    return np.ascontiguousarray(np.ravel(np.asarray(x, dtype=np.float64), order="F"))
+
+
+# ---------------------------------------------------------------------------
+# handle
+# ---------------------------------------------------------------------------
+class Handle:
+    """Owns a device, a stream, the workspace arena and pinned staging."""
+
+    def __init__(self, device: int = 0, use_graphs: bool = False):
+        self._h = C.c_void_p()
+        opts = _Options(device=device, use_graphs=int(use_graphs))
+        _check(_L().srtt_create(C.byref(opts), C.byref(self._h)))
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value and _LIB is not None:
+            _LIB.srtt_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        self.close()
+
+    @property
+    def last_launch_count(self) -> int:
+        return int(_L().srtt_last_launch_count(self._h))
+
+
+_DEFAULT = {}
+
+
+def default_handle(device: int = 0) -> Handle:
+    if device not in _DEFAULT:
+        _DEFAULT[device] = Handle(device)
+    return _DEFAULT[device]
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped types
+# ---------------------------------------------------------------------------
+@dataclass
+class ExecPolicy:
+    """parallel.hpp:23-28."""
+    workers: int = 1
+    slice_mode: int | None = None
+    index_partitions: int = 1
+    emulate_serial_root: bool = False
+
+    def _c(self):
+        return _Exec(self.workers, -1 if self.slice_mode is None else self.slice_mode, self.index_partitions,
+                     int(self.emulate_serial_root), 0)
+
+
+@dataclass
+class SubsampleReport:
+    """tucker.hpp:129-134 / htucker.hpp:196-201, plus device stage times."""
+    sample_counts: list = field(default_factory=list)
+    achieved_ranks: list = field(default_factory=list)
+    warnings: list = field(default_factory=list)
+    timings: dict = field(default_factory=dict)
+    flags: int = 0
+    launches: int = 0
+
+
+HtSubsampleReport = SubsampleReport
+
+
+@dataclass
+class TuckerDecomposition:
+    core: object      # numpy nd-array of shape ranks (or a flat device tensor)
+    factors: list     # U_k, n_k x r_k
+
+
+@dataclass
+class HTuckerDecomposition:
+    tree: "DimensionTree"
+    leaf_factors: list
+    transfers: list
+
+
+class TreeNode:
+    def __init__(self, modes, left, right, parent, level):
+        self.modes = [int(m) for m in modes]
+        self.left, self.right, self.parent, self.level = left, right, parent, level
+
+    def is_leaf(self):
+        return self.left < 0
+
+
+class DimensionTree:
+    """dimension_tree.hpp:27-152 (balanced() is computed by the library)."""
+
+    def __init__(self, nodes):
+        self.nodes = nodes
+
+    @staticmethod
+    def balanced(order: int) -> "DimensionTree":
+        n = max(2 * order - 1, 1)
+        nn = C.c_int32()
+        mb = np.zeros(n + 1, np.int32)
+        modes = np.zeros(max(order * order, 1), np.int32)
+        left, right, parent, level = (np.zeros(n, np.int32) for _ in range(4))
+        _check(_L().srtt_tree_balanced(order, C.byref(nn), mb.ctypes.data, modes.ctypes.data, left.ctypes.data,
+                                       right.ctypes.data, parent.ctypes.data, level.ctypes.data))
+        nodes = [TreeNode(modes[mb[i]:mb[i + 1]], int(left[i]), int(right[i]), int(parent[i]), int(level[i]))
+                 for i in range(nn.value)]
+        return DimensionTree(nodes)
+
+    @property
+    def num_nodes(self):
+        return len(self.nodes)
+
+    @property
+    def order(self):
+        return len(self.nodes[0].modes)
+
+    def node(self, i):
+        return self.nodes[i]
+
+    def leaves(self):
+        return [i for i, n in enumerate(self.nodes) if n.is_leaf()]
+
+    def depth(self):
+        return max(n.level for n in self.nodes)
+
+    def internal_nodes_bottom_up(self):
+        out = []
+        for lvl in range(self.depth(), 0, -1):
+            out += [i for i in range(1, self.num_nodes) if not self.nodes[i].is_leaf() and self.nodes[i].level == lvl]
+        return out
+
+    def node_rows(self, i, dims):
+        return int(np.prod([dims[m] for m in self.nodes[i].modes]))
+
+    def node_cols(self, i, dims):
+        return int(np.prod(dims)) // self.node_rows(i, dims)
+
+    def _c(self):
+        mb, modes = [0], []
+        for n in self.nodes:
+            modes += [int(m) for m in n.modes]
+            mb.append(len(modes))
+        self._keep = [np.asarray(mb, np.int32), np.asarray(modes or [0], np.int32),
+                      np.asarray([n.left for n in self.nodes], np.int32),
+                      np.asarray([n.right for n in self.nodes], np.int32)]
+        P = C.POINTER(C.c_int32)
+        return _Tree(len(self.nodes), *(k.ctypes.data_as(P) for k in self._keep))
+
+
+def uniform_node_ranks(tree, rank):
+    """dimension_tree.hpp:159-163."""
+    out = [rank] * tree.num_nodes
+    out[0] = 1
+    return out
+
+
+def node_sample_counts(tree, dims, alpha):
+    """dimension_tree.hpp:174-183."""
+    import math
+
+    out = [1] * tree.num_nodes
+    for i in range(1, tree.num_nodes):
+        out[i] = min(int(math.ceil(alpha * tree.node_rows(i, dims))), tree.node_cols(i, dims))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# sampling (host, bit-exact)
+# ---------------------------------------------------------------------------
+def sample_indices(m: int, s: int, seed: int, stream_id: int, partitions: int = 1):
+    """RngStream(seed, stream_id) + sample_indices[_partitioned]; returns
+    (indices, u64 draws consumed by the parent stream)."""
+    out = np.zeros(max(int(s), 1), np.int64)
+    draws = C.c_uint64()
+    _check(_L().srtt_sample_indices(seed & (2**64 - 1), stream_id & (2**64 - 1), m, s, partitions,
+                                    out.ctypes.data, C.byref(draws)))
+    return out[:s], int(draws.value)
+
+
+def stream_normals(seed, stream_id, draw_offset, t0, n, handle=None):
+    """Device generator of the stream's normals (K1's Omega source)."""
+    h = handle or default_handle()
+    out = np.zeros(n)
+    _check(_L().srtt_stream_normals(h._h, seed, stream_id, draw_offset, t0, n, out.ctypes.data))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# decompositions
+# ---------------------------------------------------------------------------
+def _report_from(crep, n, ach, samp, report, handle):
+    if report is None:
+        return
+    report.sample_counts = [int(v) for v in samp[:n]]
+    report.achieved_ranks = [int(v) for v in ach[:n]]
+    txt = crep.warnings.decode() if crep.warnings else ""
+    report.warnings = [w for w in txt.split("\n") if w]
+    report.timings = {name: float(crep.stage_seconds[i]) for i, name in enumerate(STAGES)}
+    report.flags = int(crep.flags)
+    report.launches = handle.last_launch_count
+
+
+def _alloc_out(shape_list, device_out, like):
+    if device_out:
+        import torch
+
+        dev = like.device if hasattr(like, "device") else torch.device("cuda")
+        return [torch.empty(int(np.prod(s)), dtype=torch.float64, device=dev) for s in shape_list]
+    return [np.zeros(int(np.prod(s))) for s in shape_list]
+
+
+def sub_r_hosvd(x, target, oversampling, samples, seed, exec_policy=None, report=None, *, dims=None,
+                handle=None, device_out=False):
+    """tucker.hpp:177-242.  ``x``: numpy nd-array (dims taken from its shape)
+    or a flat float64 array / CUDA tensor together with ``dims``."""
+    h = handle or default_handle()
+    if dims is None:
+        dims = list(np.shape(x))
+    d = len(dims)
+    xf = _flat_f64(x)
+    xp, xdev = _ptr(xf)
+    dims_a, ranks_a, samp_a = _i64(dims), _i64(target), _i64(samples)
+    if len(ranks_a) != d:
+        raise InvalidArgument("sub_r_hosvd: rank vector order mismatch")
+    if len(samp_a) != len(ranks_a):
+        raise InvalidArgument("sub_r_hosvd: samples vector order mismatch")
+    outs = _alloc_out([ranks_a] + [(dims[k], target[k]) for k in range(d)], device_out, xf)
+    fptrs = (C.c_void_p * d)(*[_ptr(o)[0] for o in outs[1:]])
+    ach, sc = np.zeros(d, np.int64), np.zeros(d, np.int64)
+    wbuf = C.create_string_buffer(8192)
+    crep = _Report(sc.ctypes.data_as(C.POINTER(C.c_int64)), ach.ctypes.data_as(C.POINTER(C.c_int64)),
+                   C.cast(wbuf, C.c_char_p), 8192, 0)
+    ex = exec_policy._c() if exec_policy is not None else None
+    _check(_L().srtt_sub_r_hosvd(h._h, xp, xdev, d, dims_a.ctypes.data, ranks_a.ctypes.data, int(oversampling),
+                                 samp_a.ctypes.data, int(seed) & (2**64 - 1),
+                                 C.byref(ex) if ex is not None else None, _ptr(outs[0])[0], fptrs,
+                                 int(device_out), C.byref(crep)))
+    _report_from(crep, d, ach, sc, report, h)
+    if device_out:
+        return TuckerDecomposition(core=outs[0], factors=outs[1:])
+    core = outs[0].reshape(tuple(int(r) for r in target), order="F")
+    factors = [outs[k + 1].reshape((dims[k], target[k]), order="F") for k in range(d)]
+    return TuckerDecomposition(core=core, factors=factors)
+
+
+def sub_r_rtl_ht(x, tree, ranks, samples, oversampling, seed, exec_policy=None, report=None, *, dims=None,
+                 handle=None, device_out=False):
+    """htucker.hpp:210-341."""
+    h = handle or default_handle()
+    if dims is None:
+        dims = list(np.shape(x))
+    d = len(dims)
+    xf = _flat_f64(x)
+    xp, xdev = _ptr(xf)
+    if tree.order != d:
+        raise InvalidArgument("sub_r_rtl_ht: tree and tensor order mismatch")
+    nn = tree.num_nodes
+    if len(ranks) != nn:
+        raise InvalidArgument("sub_r_rtl_ht: rank vector must have one entry per node")
+    if len(samples) != nn:
+        raise InvalidArgument("sub_r_rtl_ht: samples vector must have one entry per node")
+    ranks_a, samp_a, dims_a = _i64(ranks), _i64(samples), _i64(dims)
+    leaf_shape = [None] * d
+    for i in tree.leaves():
+        m = tree.node(i).modes[0]
+        leaf_shape[m] = (dims[m], ranks[i])
+    tshape = {}
+    for i in range(nn):
+        n = tree.node(i)
+        if not n.is_leaf():
+            tshape[i] = (1 if i == 0 else ranks[i], ranks[n.left], ranks[n.right])
+    leaf = _alloc_out(leaf_shape, device_out, xf)
+    trs = {i: _alloc_out([s], device_out, xf)[0] for i, s in tshape.items()}
+    lp = (C.c_void_p * d)(*[_ptr(o)[0] for o in leaf])
+    tp = (C.c_void_p * nn)(*[_ptr(trs[i])[0] if i in trs else None for i in range(nn)])
+    ach, sc = np.zeros(nn, np.int64), np.zeros(nn, np.int64)
+    wbuf = C.create_string_buffer(8192)
+    crep = _Report(sc.ctypes.data_as(C.POINTER(C.c_int64)), ach.ctypes.data_as(C.POINTER(C.c_int64)),
+                   C.cast(wbuf, C.c_char_p), 8192, 0)
+    ct = tree._c()
+    ex = exec_policy._c() if exec_policy is not None else None
+    _check(_L().srtt_sub_r_rtl_ht(h._h, xp, xdev, d, dims_a.ctypes.data, C.byref(ct), ranks_a.ctypes.data,
+                                  samp_a.ctypes.data, int(oversampling), int(seed) & (2**64 - 1),
+                                  C.byref(ex) if ex is not None else None, lp, tp, int(device_out),
+                                  C.byref(crep)))
+    _report_from(crep, nn, ach, sc, report, h)
+    if device_out:
+        return HTuckerDecomposition(tree, leaf, [trs.get(i) for i in range(nn)])
+    leaf_np = [leaf[m].reshape(leaf_shape[m], order="F") for m in range(d)]
+    tr_np = [trs[i].reshape(tshape[i], order="F") if i in trs else None for i in range(nn)]
+    return HTuckerDecomposition(tree, leaf_np, tr_np)
+
+
+# ---------------------------------------------------------------------------
+# components (reference test-facing functions)
+# ---------------------------------------------------------------------------
+def extract_group_fibers(x, modes, cols, *, handle=None):
+    """unfolding.hpp:57-111 (a single mode == extract_fibers)."""
+    h = handle or default_handle()
+    dims = list(x.shape)
+    xf = _flat_f64(x)
+    modes_a = np.ascontiguousarray(np.asarray(modes, np.int32))
+    cols_a = _i64(cols)
+    rows = int(np.prod([dims[m] for m in modes])) if len(modes) else 0
+    y = np.zeros(max(rows * len(cols_a), 1))
+    dims_a = _i64(dims)  # keep alive across the call
+    _check(_L().srtt_extract_fibers(h._h, xf.ctypes.data, 0, len(dims), dims_a.ctypes.data, len(modes_a),
+                                    modes_a.ctypes.data, len(cols_a), cols_a.ctypes.data, y.ctypes.data, 0))
+    return y[:rows * len(cols_a)].reshape((rows, len(cols_a)), order="F")
+
+
+def extract_fibers(x, mode, cols, *, handle=None):
+    """unfolding.hpp:32-52."""
+    return extract_group_fibers(x, [mode], cols, handle=handle)
+
+
+def sketch(x, modes, cols, c, seed, stream_id, draw_offset, omega=None, *, handle=None):
+    """K1 alone: Z = Y(cols) * Omega, Omega from stream (seed, stream_id)."""
+    h = handle or default_handle()
+    dims = list(x.shape)
+    xf = _flat_f64(x)
+    modes_a = np.ascontiguousarray(np.asarray(modes, np.int32))
+    cols_a = _i64(cols)
+    rows = int(np.prod([dims[m] for m in modes]))
+    z = np.zeros(rows * c)
+    om = None if omega is None else np.ascontiguousarray(np.ravel(omega, order="F"), dtype=np.float64)
+    dims_a = _i64(dims)
+    _check(_L().srtt_sketch(h._h, xf.ctypes.data, 0, len(dims), dims_a.ctypes.data, len(modes_a),
+                            modes_a.ctypes.data, len(cols_a), cols_a.ctypes.data, c, seed, stream_id, draw_offset,
+                            om.ctypes.data if om is not None else None, z.ctypes.data, 0))
+    return z.reshape((rows, c), order="F")
+
+
+@dataclass
+class RangeBasis:
+    q: np.ndarray
+    numerical_rank: int
+    singular_values: np.ndarray
+
+
+def range_basis_of_sketch(z, rank, seed=0, stream_id=0, draw_offset=0, normal_base=0, *, handle=None):
+    """sketch.hpp:74-93 (padding continues stream (seed, stream_id))."""
+    h = handle or default_handle()
+    z = np.asarray(z, dtype=np.float64)
+    n, c = z.shape
+    zf = np.ascontiguousarray(np.ravel(z, order="F"))
+    q = np.zeros(n * max(rank, 1))
+    nr = C.c_int64()
+    sv = np.zeros(min(n, c))
+    _check(_L().srtt_range_basis_of_sketch(h._h, zf.ctypes.data, 0, n, c, rank, seed, stream_id, draw_offset,
+                                           normal_base, q.ctypes.data, C.byref(nr), sv.ctypes.data, 0))
+    return RangeBasis(q.reshape((n, rank), order="F"), int(nr.value), sv)
+
+
+def multi_ttm_core(x, factors, *, handle=None):
+    """core_from_factors (tucker.hpp:43-50) / sliced_core (parallel.hpp:355-445)."""
+    h = handle or default_handle()
+    dims = list(x.shape)
+    ranks = [f.shape[1] for f in factors]
+    xf = _flat_f64(x)
+    fs = [np.ascontiguousarray(np.ravel(f, order="F"), dtype=np.float64) for f in factors]
+    fp = (C.c_void_p * len(fs))(*[f.ctypes.data for f in fs])
+    out = np.zeros(int(np.prod(ranks)))
+    dims_a, ranks_a = _i64(dims), _i64(ranks)
+    _check(_L().srtt_multi_ttm_core(h._h, xf.ctypes.data, 0, len(dims), dims_a.ctypes.data,
+                                    ranks_a.ctypes.data, fp, 0, out.ctypes.data, 0))
+    return out.reshape(tuple(ranks), order="F")
+
+
+core_from_factors = multi_ttm_core
+
+
+def sliced_core(x, factors, policy=None, *, handle=None):
+    """parallel.hpp:355-445: same numbers for every policy on the GPU."""
+    if policy is not None and policy.slice_mode is not None and not 0 <= policy.slice_mode < x.ndim:
+        raise InvalidArgument("sliced_core: slice mode out of range")
+    return multi_ttm_core(x, factors, handle=handle)
+
+
+def transfer_tensor(u_node, u_left, u_right, *, handle=None):
+    """htucker.hpp:44-63."""
+    h = handle or default_handle()
+    nl, rl = u_left.shape
+    nr, rr = u_right.shape
+    if u_node.shape[0] != nl * nr:
+        raise InvalidArgument("transfer_tensor: node rows must equal product of child rows")
+    rs = u_node.shape[1]
+    a, b, c = (np.ascontiguousarray(np.ravel(m, order="F"), dtype=np.float64) for m in (u_node, u_left, u_right))
+    out = np.zeros(rs * rl * rr)
+    _check(_L().srtt_transfer_tensor(h._h, a.ctypes.data, b.ctypes.data, c.ctypes.data, nl, nr, rs, rl, rr, 0,
+                                     out.ctypes.data))
+    return out.reshape((rs, rl, rr), order="F")
+
+
+def root_transfer(x, u_left, u_right, *, handle=None):
+    """htucker.hpp:67-85."""
+    h = handle or default_handle()
+    nl, rl = u_left.shape
+    nr, rr = u_right.shape
+    if nl * nr != x.size:
+        raise InvalidArgument("root_transfer: child rows do not factor the tensor size")
+    xf = _flat_f64(x)
+    a, b = (np.ascontiguousarray(np.ravel(m, order="F"), dtype=np.float64) for m in (u_left, u_right))
+    out = np.zeros(rl * rr)
+    _check(_L().srtt_root_transfer(h._h, xf.ctypes.data, 0, nl, nr, a.ctypes.data, rl, b.ctypes.data, rr, 0,
+                                   out.ctypes.data, 0))
+    return out.reshape((1, rl, rr), order="F")
