@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Headline benchmark: fp64 tensor entries decomposed per second.
+
+One "step" = one full Sub-R-HOSVD (or Sub-R-RtL-HT for c4) of the config's
+synthetic tensor: host index sampling + K1 sketch + K2 basis + K3 core pass,
+X resident in HBM (``value``); ``e2e`` times the same call through the C-ABI
+with X in pinned HOST memory (H2D of X and D2H of the factors/core inside
+the timed region).  Default workload: BASELINE.json configs[1] (order-5
+Tucker 40^5, 1.02e8 entries, 819 MB > L2, so no L2 flush is needed).
+
+``--impl reference`` times the CPU restatement of the reference (oracle/,
+numpy + OpenBLAS on all host cores; the reference itself needs Eigen, absent
+in this image) on the same config.
+
+Multi-GPU (torchrun): each rank decomposes its own replica (seed = rank),
+weak scaling, no data-path collective; time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tensor entries decomposed/sec (fp64)"
+UNIT = "entries/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while running."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + ",".join(self.FIELDS),
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no_samples"], "samples": 0}
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+
+        sm = [num(s[0]) for s in self.samples if num(s[0]) is not None]
+        mx = [num(s[1]) for s in self.samples if num(s[1]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def _dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------------------
+# one decomposition through the product API
+# ---------------------------------------------------------------------------
+def _run_product(P, cfg, x, dims, seed, handle, device_out=True, report=None):
+    if cfg.kind == "tucker":
+        return P.sub_r_hosvd(x, [cfg.rank] * cfg.order, cfg.p, cfg.samples(), seed, report=report, dims=dims,
+                             handle=handle, device_out=device_out)
+    tree = P.DimensionTree.balanced(cfg.order)
+    ranks = P.uniform_node_ranks(tree, cfg.rank)
+    samples = [1] + [min(4 * (cfg.rank + cfg.p), tree.node_cols(i, dims)) for i in range(1, tree.num_nodes)]
+    return P.sub_r_rtl_ht(x, tree, ranks, samples, cfg.p, seed, report=report, dims=dims, handle=handle,
+                          device_out=device_out)
+
+
+def _run_oracle(O, cfg, X, seed):
+    if cfg.kind == "tucker":
+        return O.sub_r_hosvd(X, [cfg.rank] * cfg.order, cfg.p, cfg.samples(), seed)
+    tree = O.DimensionTree.balanced(cfg.order)
+    ranks = O.uniform_node_ranks(tree, cfg.rank)
+    samples = [1] + [min(4 * (cfg.rank + cfg.p), tree.node_cols(i, X.shape)) for i in range(1, tree.num_nodes)]
+    return O.sub_r_rtl_ht(X, tree, ranks, samples, cfg.p, seed)
+
+
+def cpu_baseline(cfg, x_host_flat, seed, budget_s=20.0, max_runs=5):
+    """Oracle port on the host cores, bounded to ~budget_s of CPU work."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import srtt_oracle as O
+
+    X = O.as_tensor(x_host_flat, cfg.dims)
+    _run_oracle(O, cfg, X, seed)  # warm-up (BLAS threads, page faults)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_runs and (time.perf_counter() - t_start) < budget_s:
+        t0 = time.perf_counter()
+        _run_oracle(O, cfg, X, seed)
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    return {"value": cfg.entries / med, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"full {cfg.name} decomposition (N={cfg.entries}), median of {len(times)} runs, numpy+OpenBLAS "
+                      f"restatement in oracle/ (reference needs Eigen, absent)",
+            "seconds_per_step": med}
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return
+    from paper_2603_21379_b200 import synth
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import srtt_oracle as O
+
+    cfg = synth.CONFIGS[args.config]
+    x = synth.make_tensor(cfg, seed=0, backend="numpy")
+    X = O.as_tensor(x, cfg.dims)
+    for _ in range(args.warmup):
+        _run_oracle(O, cfg, X, 0)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _run_oracle(O, cfg, X, 0)
+    el = time.perf_counter() - t0
+    value = cfg.entries * args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config_dict(cfg),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"full {cfg.name} decomposition per step (numpy+OpenBLAS restatement of the "
+                                       f"reference in oracle/; the reference needs Eigen, absent in this image)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _config_dict(cfg):
+    return {"workload": cfg.name, "description": cfg.description, "dims": list(cfg.dims), "rank": cfg.rank,
+            "oversampling": cfg.p, "samples_per_target": 4 * (cfg.rank + cfg.p), "entries": cfg.entries,
+            "bytes": cfg.entries * 8, "l2": "inputs larger than L2 (126 MB); no flush" if cfg.entries * 8 > 126e6
+            else "input smaller than L2: L2 flushed between steps"}
+
+
+# ---------------------------------------------------------------------------
+# product arm
+# ---------------------------------------------------------------------------
+def run_product(args):
+    import torch
+
+    rank, world, local = _dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2603_21379_b200 as P
+    from paper_2603_21379_b200 import synth
+
+    cfg = synth.CONFIGS[args.config]
+    dims = list(cfg.dims)
+    x = synth.make_tensor(cfg, seed=rank, backend="torch", device=f"cuda:{local}")
+    torch.cuda.synchronize()
+    h = P.Handle(local)
+    stream = torch.cuda.current_stream()
+    h.set_stream(stream.cuda_stream)
+    small = cfg.entries * 8 < 256e6
+    flush = torch.empty(int(256e6 // 8), dtype=torch.float64, device=dev) if small else None
+
+    rep = P.SubsampleReport()
+    for _ in range(args.warmup):
+        _run_product(P, cfg, x, dims, 0, h, report=rep)
+    torch.cuda.synchronize()
+    launches_per_step = rep.launches
+
+    def timed_loop(n):
+        core_t = []
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        total = 0.0
+        for _ in range(n):
+            if flush is not None:
+                flush.fill_(1.0)
+            ev0.record(stream)
+            r = P.SubsampleReport()
+            _run_product(P, cfg, x, dims, 0, h, report=r)
+            ev1.record(stream)
+            ev1.synchronize()
+            total += ev0.elapsed_time(ev1) / 1e3
+            core_t.append(r.kernel_seconds.get("core", 0.0))
+        return total, core_t
+
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    elapsed, core_t = timed_loop(args.steps)
+    torch.cuda.synchronize()
+    # keep the same workload running until the clock sampler has >= 3 samples
+    t_extra = time.perf_counter()
+    while len(sampler.samples) < 3 and time.perf_counter() - t_extra < 10:
+        timed_loop(max(1, args.steps // 4))
+    sampler.stop()
+    clocks = sampler.summary()
+    el = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(el, op=torch.distributed.ReduceOp.MAX)
+    elapsed = float(el.item())
+    value = world * cfg.entries * args.steps / elapsed
+
+    # e2e: through the C-ABI with X in pinned host memory, outputs to host
+    x_host = x.cpu().pin_memory()
+    xh = x_host.numpy()
+    for _ in range(max(1, min(args.warmup, 2))):
+        _run_product(P, cfg, xh, dims, 0, h, device_out=False)
+    e2e_steps = max(1, min(args.steps, 20))
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(e2e_steps):
+        _run_product(P, cfg, xh, dims, 0, h, device_out=False)
+    ev1.record(stream)
+    ev1.synchronize()
+    e2e_el = torch.tensor([ev0.elapsed_time(ev1) / 1e3], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(e2e_el, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = world * cfg.entries * e2e_steps / float(e2e_el.item())
+    samples_total = sum(4 * (cfg.rank + cfg.p) for _ in range(cfg.order))
+    if cfg.kind == "tucker":
+        d2h = 8 * (cfg.rank ** cfg.order + sum(n * cfg.rank for n in dims))
+    else:
+        d2h = 8 * (sum(n * cfg.rank for n in dims) + (cfg.order - 2) * cfg.rank ** 3 + cfg.rank ** 2)
+    h2d = 8 * cfg.entries + 8 * samples_total
+
+    peaks, peak_kind = _peaks()
+    core_med = statistics.median(core_t) if core_t else 0.0
+    alg_bytes = 8.0 * cfg.entries
+    achieved = alg_bytes / core_med / 1e9 if core_med > 0 else None
+    roofline = {"bound": "hbm", "kernel": "core_kernel (K3/K5 streaming multi-TTM)",
+                "achieved": achieved, "peak": peaks["hbm_gbs"], "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
+                "traffic": _traffic_from_profiles(cfg.name),
+                "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": core_med * 1e3,
+                "kernel_share_of_step": core_med / (elapsed / args.steps)}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(_config_dict(cfg), parallelism=f"replicas x{world}" if world > 1 else "single GPU"),
+            "clocks": clocks, "gpu_launches": launches_per_step * args.steps,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "steps": e2e_steps},
+            "roofline": roofline}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, x_host.numpy(), 0)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def _traffic_from_profiles(cfg_name):
+    """dram bytes per core-kernel launch from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", f"ncu_core_{cfg_name}.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_product(args)
+
+
+if __name__ == "__main__":
+    main()

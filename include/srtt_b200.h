@@ -85,6 +85,11 @@ typedef struct srtt_report {
   double stage_seconds[SRTT_NUM_STAGES];
   int32_t flags; /* bit0: a Box-Muller u1 == 0 draw was met (p = 2^-53) */
   int32_t reserved;
+  /* device time of the dominant kernels of the call (CUDA events around the
+   * launch): [0] K1 sketch, [1] K2 basis (all launches), [2] K3/K5 core
+   * streaming kernel only, [3] K4 transfers */
+  double kernel_seconds[4];
+  int64_t launches; /* kernels launched by the call */
 } srtt_report;
 
 /* Dimension tree (dimension_tree.hpp:9-17), heap/BFS node order, root = 0.
@@ -104,6 +109,10 @@ const char* srtt_last_error(void);
 int srtt_version(void);
 /* Number of kernel launches issued by the last decomposition call. */
 int64_t srtt_last_launch_count(srtt_handle* h);
+/* Run all work of this handle on an external cudaStream_t (passed as void*;
+ * NULL restores the handle's own stream). Lets a caller time calls with
+ * its own CUDA events. */
+int srtt_set_stream(srtt_handle* h, void* stream);
 
 /* ---- host-side sampling (bit-exact with the reference) ------------------ */
 /* RngStream(seed, stream_id) + sample_indices / sample_indices_partitioned

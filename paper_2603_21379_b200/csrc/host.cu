@@ -34,6 +34,7 @@ cudaError_t srtt_launch_pad(const BasisTarget*, int, double*, int64_t, cudaStrea
 int srtt_core_threads();
 size_t srtt_core_smem_bytes(const CoreParams& P);
 int srtt_core_occupancy(const CoreParams& P);
+int srtt_core_max_stages(const CoreParams& P, size_t budget);
 cudaError_t srtt_launch_core(const CUtensorMap*, const CoreParams&, int, cudaStream_t);
 cudaError_t srtt_launch_prep(const double*, int64_t, int, int, int, int, double*, cudaStream_t);
 cudaError_t srtt_launch_transpose(const double*, int64_t, int, double*, cudaStream_t);
@@ -205,7 +206,9 @@ struct srtt_handle {
   int sms = 148;
   int use_graphs = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
   cudaEvent_t ev[8] = {};
+  cudaEvent_t kev[8] = {};  // per-kernel pairs: [2i] start, [2i+1] end
   DevBuf xbuf;     // device copy of host inputs
   DevBuf ws;       // workspace arena
   DevBuf dparams;  // device copy of the parameter blob
@@ -403,6 +406,8 @@ struct CorePlan {
   size_t ufrag_doubles = 0;
 };
 
+int pad_tiles(int64_t r) { return r <= 8 ? 1 : (r <= 16 ? 2 : (r <= 32 ? 4 : 0)); }
+
 CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>& ranks, int sms,
                    int force_m = 0, int force_S = 0) {
   const int d = (int)dims.size();
@@ -416,48 +421,59 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
   P.n0 = n0;
   P.Q = Q;
   P.r0 = (int)ranks[0];
-  P.NT = (P.r0 + 7) / 8;
-  if (P.NT > 8) invalid("core: rank of mode 0 above 64 is not supported by the B200 core kernel");
-  P.RB = n0 <= 256 ? (int)((n0 + 15) / 16 * 16) : (P.NT > 4 ? 128 : 256);
+  P.NT = pad_tiles(ranks[0]);
+  P.NT1 = pad_tiles(ranks[1]);
+  if (!P.NT || !P.NT1) invalid("core: ranks above 32 in modes 0 and 1 are not supported by the B200 core kernel");
+  P.RB = n0 <= 256 ? (int)((n0 + 15) / 16 * 16) : 256;
   P.nrb = (int)((n0 + P.RB - 1) / P.RB);
-  P.W = 64;
   P.use_tma = (n0 % 2 == 0) ? 1 : 0;
+  P.fdim[0] = dims[1];
+  P.frank[0] = (int)ranks[1];
 
   struct Cand {
-    int m;
-    int S;
-    int64_t SL, G, GS, items;
-    int A, acc_total;
-    double cost;
-  };
-  Cand best{};
-  best.cost = 1e300;
-  int64_t Am = P.r0;
-  int acc_total = 0;
-  for (int m = 2; m <= d; ++m) {
-    Am *= ranks[m - 1];
-    acc_total += (int)Am;
-    if (acc_total > 12288) break;
+    int m = 0, S = 0, ns = 0;
+    int64_t SL = 0, G = 0, GS = 0, items = 0;
+    int A = 0;
+    double cost = 1e300;
+  } best;
+  const double tp_bytes = 16.0 * P.RB * 8.0;
+  for (int m = 2; m <= std::min(3, d); ++m) {
     if (force_m && m != force_m) continue;
+    CoreParams T = P;
+    T.m = m;
+    T.A = (int)(ranks[0] * ranks[1] * (m == 3 ? ranks[2] : 1));
+    const int ns = srtt_core_max_stages(T, kSmemBudget + 20 * 1024);
+    if (ns < 3) continue;
     const int64_t GS = prod(dims, 1, m);
     const int64_t G = Q / GS;
-    const int64_t target_items = 8LL * sms;
-    int64_t S = force_S ? force_S : std::max<int64_t>(1, (target_items + P.nrb * G - 1) / (P.nrb * G));
-    S = std::min<int64_t>(S, (GS + P.W - 1) / P.W);
-    int64_t SL = ((GS + S - 1) / S + P.W - 1) / P.W * P.W;
-    S = (GS + SL - 1) / SL;
-    const int64_t items = P.nrb * G * S;
-    const int64_t last = GS - (S - 1) * SL;
-    const int64_t loaded = (S - 1) * SL + (last + P.W - 1) / P.W * P.W;
-    const double waste = (double)(loaded - GS) * G * n0 * 8.0;
-    const double out = (double)items * Am * 8.0;
-    const int grid = (int)std::min<int64_t>(items, sms);
-    const int64_t rounds = (items + grid - 1) / grid;
-    const double eff = (double)items / ((double)rounds * grid);
-    const double cost = (double)N * 8.0 / eff + waste + 2.0 * out;
-    if (cost < best.cost) best = Cand{m, (int)S, SL, G, GS, items, (int)Am, acc_total, cost};
+    const int64_t max_s = (GS + 15) / 16;
+    for (int64_t S = 1; S <= max_s; S = S < 8 ? S + 1 : S * 2) {
+      if (force_S && S != force_S) continue;
+      const int64_t SL = ((GS + S - 1) / S + 15) / 16 * 16;
+      const int64_t Se = (GS + SL - 1) / SL;
+      const int64_t items = P.nrb * G * Se;
+      const int64_t ntp = SL / 16;
+      const int64_t grid = std::min<int64_t>(items, sms);
+      const int64_t rounds = (items + grid - 1) / grid;
+      const double item_units = (double)((ntp + 7) / 8) + 0.5;  // +0.5: per-item barrier/reduction
+      const double stream = (double)rounds * grid * 8.0 * item_units * tp_bytes;
+      const double out = 2.0 * (double)items * T.A * 8.0;
+      const double cost = stream + out;
+      if (cost < best.cost) {
+        best.m = m;
+        best.S = (int)Se;
+        best.ns = ns;
+        best.SL = SL;
+        best.G = G;
+        best.GS = GS;
+        best.items = items;
+        best.A = T.A;
+        best.cost = cost;
+      }
+      if (S >= max_s) break;
+    }
   }
-  if (best.m == 0) invalid("core: no feasible fold depth");
+  if (best.m == 0) invalid("core: no feasible work decomposition");
   P.m = best.m;
   P.S = best.S;
   P.SL = best.SL;
@@ -465,18 +481,11 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
   P.GS = best.GS;
   P.nitems = best.items;
   P.A = best.A;
-  for (int k = 1; k < best.m; ++k) {
-    P.fdim[k - 1] = dims[k];
-    P.frank[k - 1] = (int)ranks[k];
+  P.nstages = best.ns;
+  if (best.m == 3) {
+    P.fdim[1] = dims[2];
+    P.frank[1] = (int)ranks[2];
   }
-  int off = 0;
-  int64_t Al = P.r0;
-  for (int l = 2; l <= best.m; ++l) {
-    Al *= ranks[l - 1];
-    P.acc_off[l] = off;
-    off += (int)Al;
-  }
-  P.acc_total = off;
   cp.part_doubles = best.items * best.A;
   cp.ufrag_doubles = (size_t)P.nrb * P.RB * P.NT * 8;
   return cp;
@@ -501,12 +510,14 @@ int launch_core_pass(srtt_handle* h, CorePlan& cp, const double* x, const std::v
     ++launches;
     P.fu[k - 1] = ut;
   }
+  if (P.m == 2) P.fu[1] = nullptr;
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
-  if (P.use_tma) encode_tmap(&tmap, x, P.n0, P.Q, P.W);
-  const int occ = std::max(1, srtt_core_occupancy(P));
-  cp.grid = (int)std::min<int64_t>(P.nitems, (int64_t)occ * h->sms);
+  if (P.use_tma) encode_tmap(&tmap, x, P.n0, P.Q, 16);
+  cp.grid = (int)std::min<int64_t>(P.nitems, (int64_t)h->sms);
+  CK(cudaEventRecord(h->kev[4], h->stream));
   CK(srtt_launch_core(&tmap, P, cp.grid, h->stream));
+  CK(cudaEventRecord(h->kev[5], h->stream));
   ++launches;
   // tail: fixed-order reduction of the item partials + TTMs of modes m..d-1
   const int nparts = P.nrb * P.S;
@@ -637,6 +648,12 @@ struct Timer {
     return ms * 1e-3;
   }
 };
+
+double kernel_pair(srtt_handle* h, int i) {
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, h->kev[2 * i], h->kev[2 * i + 1]));
+  return ms * 1e-3;
+}
 
 // ==================================================================================
 // Sub-R-HOSVD
@@ -819,6 +836,11 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     rep->stage_seconds[SRTT_STAGE_FACTOR_WALL] = t_sampling + tm.between(2, 4);
     rep->stage_seconds[SRTT_STAGE_D2H] = tm.between(5, 6);
     rep->flags = hi[4 * d];
+    rep->kernel_seconds[0] = tm.between(2, 3);
+    rep->kernel_seconds[1] = tm.between(3, 4);
+    rep->kernel_seconds[2] = d >= 2 ? kernel_pair(h, 2) : 0.0;
+    rep->kernel_seconds[3] = 0.0;
+    rep->launches = h->launches;
     write_warnings(rep, warnings);
   }
 }
@@ -847,8 +869,10 @@ int srtt_create(const srtt_options* opts, srtt_handle** out) {
     int major = 0;
     CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, h->device));
     if (major != 10) fail(SRTT_ERR_CUDA, "srtt: this build targets sm_100a (B200) only");
-    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+    h->stream = h->own_stream;
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
+    for (auto& e : h->kev) CK(cudaEventCreate(&e));
     h->ones.ensure(sizeof(double));
     const double one = 1.0;
     CK(cudaMemcpy(h->ones.p, &one, sizeof(double), cudaMemcpyHostToDevice));
@@ -863,13 +887,21 @@ int srtt_destroy(srtt_handle* h) {
       DeviceGuard g(h->device);
       cudaStreamSynchronize(h->stream);
       for (auto& e : h->ev) cudaEventDestroy(e);
-      cudaStreamDestroy(h->stream);
+      for (auto& e : h->kev) cudaEventDestroy(e);
+      cudaStreamDestroy(h->own_stream);
     }
     delete h;
   });
 }
 
 int64_t srtt_last_launch_count(srtt_handle* h) { return h ? h->launches : -1; }
+
+int srtt_set_stream(srtt_handle* h, void* stream) {
+  return guarded([&] {
+    if (!h) invalid("srtt: null handle");
+    h->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : h->own_stream;
+  });
+}
 
 int srtt_sample_indices(uint64_t seed, uint64_t stream_id, int64_t m, int64_t s, int64_t partitions,
                         int64_t* idx_out, uint64_t* draws_out) {
@@ -1216,6 +1248,11 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     rep->stage_seconds[SRTT_STAGE_FACTOR_WALL] = t_sampling + tm.between(2, 4);
     rep->stage_seconds[SRTT_STAGE_D2H] = tm.between(6, 7);
     rep->flags = hi[4 * nt];
+    rep->kernel_seconds[0] = tm.between(2, 3);
+    rep->kernel_seconds[1] = tm.between(3, 4);
+    rep->kernel_seconds[2] = kernel_pair(h, 2);
+    rep->kernel_seconds[3] = tm.between(4, 5);
+    rep->launches = h->launches;
     write_warnings(rep, warnings);
   }
 }

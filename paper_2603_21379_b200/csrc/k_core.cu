@@ -5,20 +5,28 @@
 //   sliced_core (slab reduction + tail TTM)  parallel.hpp:355-445
 //   root_transfer  (U_l^T M U_r)             htucker.hpp:67-85
 //
-// X is viewed as M = n0 x Q (column-major; mode 0 is the only stride-1
-// mode, its fibres are M's columns). Work items are (row block, level-m
-// group, split) triples; each persistent CTA streams its items' boxes of
-// 16 rows x W columns through an 8-stage TMA ring (cp.async.bulk.tensor,
-// 128-byte swizzle, mbarrier complete_tx) fed by one producer warp.
-// Stage 1 (t1 = U0^T X_box, the only FLOP-heavy step: 2 r0 flop/entry) runs
-// on the FP64 tensor cores: each compute warp owns 8-column M-tiles (even /
-// odd column interleave so the swizzled A-fragment loads are conflict free)
-// and issues mma.sync.m8n8k4.f64 against U0 B-fragments resident in shared
-// memory. The t1 tile then folds into nested shared-memory accumulators
-// acc_l (modes 1..m-1) with flush-on-index-change, which is linear and
-// therefore correct for any item boundary. X is read from HBM exactly once.
-// Item results are written to fixed slots and reduced in a fixed order by
-// the tail, so the core is bitwise reproducible run to run.
+// X is viewed as M = n0 x Q (column-major; mode 0 is the only stride-1 mode
+// and its fibres are M's columns). A work item is one contiguous column
+// range of one row block inside one level-m group (m = 2 or 3); the CTA's
+// 8 warps split the item into contiguous runs of 16-column "tile pairs".
+//
+// Each warp is its own producer and consumer: lane 0 keeps a private ring
+// of NS TMA boxes (16 rows x 16 columns, 128-byte swizzle,
+// cp.async.bulk.tensor + mbarrier complete_tx) NS boxes ahead of the
+// consumer, across item boundaries. Per box, stage 1 computes
+//   T(ranks0 x 16 cols) += U0^T(ranks0 x 16 rows) X(16 rows x 16 cols)
+// on the FP64 tensor cores (mma.sync.m8n8k4.f64 = DMMA.8x8x4): A = U0
+// fragments resident in shared memory, B = X fragments read conflict-free
+// from the swizzled box (even/odd column interleave). When a tile pair's
+// rows are done, stage 2 folds mode 1 with a second DMMA,
+//   R2(ranks0 x ranks1) += T(ranks0 x 16 cols) U1[i1(col), :],
+// whose A operand is the stage-1 accumulator itself: the column <-> k-slot
+// map is chosen so each thread already holds its A values (no shuffles).
+// Columns of other level-2 groups or beyond the item are masked through the
+// B operand. For m = 3 a finished level-2 group is flushed into a
+// warp-private acc3 (r0 r1 r2) with U2[i2, :]. At the end of an item the
+// 8 warp partials are summed in a fixed order into the item's output slot,
+// so the core is bitwise reproducible run to run. X is read exactly once.
 #include <cuda.h>
 
 #include "srtt_device.cuh"
@@ -28,11 +36,9 @@ namespace {
 
 using namespace srtt_dev;
 
-constexpr int kComputeWarps = 8;
-constexpr int kComputeThreads = kComputeWarps * 32;
-constexpr int kThreads = kComputeThreads + 32;  // + producer warp
-constexpr int kStages = 8;
-constexpr int kFoldScratch = 1024;  // doubles
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kBoxDoubles = 16 * 16;  // 16 rows x 16 columns, 2 KB
 
 struct Item {
   int rho;
@@ -41,260 +47,255 @@ struct Item {
   int64_t c_lo, c_hi;
 };
 
+// rho-major ordering: consecutive items of a CTA (stride gridDim) share the
+// row block, so U0's fragments are reloaded rarely.
 __device__ __forceinline__ Item decode_item(const CoreParams& P, int64_t it) {
   Item I;
-  I.rho = (int)(it % P.nrb);
-  const int64_t rest = it / P.nrb;
-  I.sigma = (int)(rest % P.S);
+  const int64_t per_rho = P.G * P.S;
+  I.rho = (int)(it / per_rho);
+  const int64_t rest = it - (int64_t)I.rho * per_rho;
   I.p = rest / P.S;
+  I.sigma = (int)(rest - I.p * P.S);
   I.c_lo = I.p * P.GS + (int64_t)I.sigma * P.SL;
-  I.c_hi = min(I.c_lo + P.SL, (I.p + 1) * P.GS);
+  I.c_hi = min64(I.c_lo + P.SL, (I.p + 1) * P.GS);
   return I;
 }
 
 __device__ __forceinline__ int boxes_of(const CoreParams& P, int rho) {
-  const int64_t rows = srtt_dev::min64(P.RB, P.n0 - (int64_t)rho * P.RB);
+  const int64_t rows = min64(P.RB, P.n0 - (int64_t)rho * P.RB);
   return (int)((rows + 15) / 16);
 }
 
-// Level-l fold: acc2[a0 + r0*a1] += sum_{j in run} T1[a0][j] * U1[i1(j)][a1].
-__device__ void fold_level2(const CoreParams& P, const double* T1, int W, int j0, int len, int64_t i1_0,
-                            double* acc2, double* scratch) {
-  const int tid = threadIdx.x;
-  const int r0 = P.r0, r1 = P.frank[0];
-  const double* __restrict__ U1 = P.fu[0];
-  const int nb = (r1 + 3) / 4;
-  const int units = r0 * nb;
-  const int JG = units >= kComputeThreads ? 1 : min(kComputeThreads / units, max(len, 1));
-  if (JG == 1) {
-    // every (a0, a1) pair has a single owner: accumulate in place
-    for (int unit = tid; unit < units; unit += kComputeThreads) {
-      const int a0 = unit % r0, a1b = (unit / r0) * 4;
-      double s[4] = {0, 0, 0, 0};
-      for (int jj = 0; jj < len; ++jj) {
-        const double t = T1[a0 * W + j0 + jj];
-        const double* ur = U1 + (i1_0 + jj) * r1 + a1b;
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (a1b + e < r1) s[e] += t * ur[e];
+__device__ __forceinline__ void warp_range(const Item& I, int warp, int* lo, int* hi) {
+  const int ntp = (int)((I.c_hi - I.c_lo + 15) / 16);
+  *lo = (ntp * warp) / kWarps;
+  *hi = (ntp * (warp + 1)) / kWarps;
+}
+
+// Producer-side walk over this warp's (item, tile pair, box) sequence.
+struct WarpIter {
+  int64_t item;
+  int tp, tp_end, b, nbox, rho;
+  int64_t c_lo;
+  bool valid;
+
+  __device__ void seek(const CoreParams& P, int warp) {
+    while (item < P.nitems) {
+      const Item I = decode_item(P, item);
+      int lo, hi;
+      warp_range(I, warp, &lo, &hi);
+      if (lo < hi) {
+        tp = lo;
+        tp_end = hi;
+        b = 0;
+        nbox = boxes_of(P, I.rho);
+        rho = I.rho;
+        c_lo = I.c_lo;
+        valid = true;
+        return;
       }
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (a1b + e < r1) acc2[a0 + r0 * (a1b + e)] += s[e];
+      item += gridDim.x;
     }
-    named_sync(1, kComputeThreads);
-    return;
+    valid = false;
   }
-  // partial sums into scratch[(jg*units + unit)*4 + e]  (JG*units <= 256)
-  for (int u = tid; u < units * JG; u += kComputeThreads) {
-    const int unit = u % units, jg = u / units;
-    const int a0 = unit % r0, a1b = (unit / r0) * 4;
-    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-    for (int jj = jg; jj < len; jj += JG) {
-      const double t = T1[a0 * W + j0 + jj];
-      const double* ur = U1 + (i1_0 + jj) * r1 + a1b;
-      s0 += t * ur[0];
-      if (a1b + 1 < r1) s1 += t * ur[1];
-      if (a1b + 2 < r1) s2 += t * ur[2];
-      if (a1b + 3 < r1) s3 += t * ur[3];
-    }
-    double* o = scratch + ((size_t)jg * units + unit) * 4;
-    o[0] = s0; o[1] = s1; o[2] = s2; o[3] = s3;
+  __device__ void next(const CoreParams& P, int warp) {
+    if (++b < nbox) return;
+    b = 0;
+    if (++tp < tp_end) return;
+    item += gridDim.x;
+    seek(P, warp);
   }
-  named_sync(1, kComputeThreads);
-  for (int idx = tid; idx < r0 * r1; idx += kComputeThreads) {
-    const int a0 = idx % r0, a1 = idx / r0;
-    const int unit = a0 + r0 * (a1 / 4), e = a1 % 4;
-    double s = 0.0;
-    for (int jg = 0; jg < JG; ++jg) s += scratch[((size_t)jg * units + unit) * 4 + e];
-    acc2[idx] += s;
-  }
-  named_sync(1, kComputeThreads);
+};
+
+__device__ __forceinline__ double swz(const double* st, int col, int row) {
+  return st[col * 16 + ((((row >> 1) ^ (col & 7)) << 1) | (row & 1))];
 }
 
-// acc_{l+1}[a + A_l * b] += acc_l[a] * U_l[i][b]; acc_l = 0.
-__device__ void flush_level(const CoreParams& P, double* accs, int l, int64_t i) {
-  const int tid = threadIdx.x;
-  double* src = accs + P.acc_off[l];
-  double* dst = accs + P.acc_off[l + 1];
-  int Al = P.r0;
-  for (int k = 0; k < l - 1; ++k) Al *= P.frank[k];
-  const int rl = P.frank[l - 1];
-  const double* __restrict__ Ul = P.fu[l - 1] + i * rl;
-  for (int idx = tid; idx < Al * rl; idx += kComputeThreads) {
-    const int a = idx % Al, b = idx / Al;
-    dst[idx] += src[a] * Ul[b];
-  }
-  named_sync(1, kComputeThreads);
-  for (int idx = tid; idx < Al; idx += kComputeThreads) src[idx] = 0.0;
-  named_sync(1, kComputeThreads);
-}
-
-__device__ void fold_chunk(const CoreParams& P, const double* T1, int W, int64_t q0, int nvalid,
-                           bool last_chunk_of_item, double* accs, double* scratch) {
-  const int64_t n1 = P.fdim[0];
-  int j = 0;
-  while (j < nvalid) {
-    const int64_t q = q0 + j;
-    const int64_t i1 = q % n1;
-    const int len = (int)srtt_dev::min64(n1 - i1, nvalid - j);
-    fold_level2(P, T1, W, j, len, i1, accs + P.acc_off[2], scratch);
-    j += len;
-    const int64_t qlast = q + len - 1;
-    const bool item_end = last_chunk_of_item && j == nvalid;
-    // cascade flushes: level l (2..m-1) completes when digits 1..l-1 of
-    // qlast are at their maxima, or at the end of the item.
-    int64_t rem = qlast;
-    bool complete = (rem % n1 == n1 - 1) || item_end;
-    rem /= n1;
-    for (int l = 2; l < P.m && complete; ++l) {
-      const int64_t nl = P.fdim[l - 1];
-      const int64_t il = rem % nl;
-      flush_level(P, accs, l, il);
-      complete = (il == nl - 1) || item_end;
-      rem /= nl;
-    }
-  }
-}
-
-template <int NT, int MT>
+template <int MT, int NT1, bool M3>
 __global__ void __launch_bounds__(kThreads, 1)
     core_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CoreParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  const int W = P.W;
-  const int stage_doubles = 16 * W;
-  // carve (stage buffers first: 1024-byte aligned for the 128B swizzle)
-  uintptr_t base = (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023);
-  double* stages = reinterpret_cast<double*>(base);
-  double* ufrag = stages + (size_t)kStages * stage_doubles;
-  double* T1 = ufrag + (size_t)P.RB * NT * 8;
-  double* accs = T1 + (size_t)P.r0 * W;
-  double* scratch = accs + P.acc_total;
-  uint64_t* full = reinterpret_cast<uint64_t*>(scratch + kFoldScratch);
-  uint64_t* empty = full + kStages;
+  const int NS = P.nstages;
+  const uintptr_t base = (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023);
+  double* rings = reinterpret_cast<double*>(base);
+  double* ufrag = rings + (size_t)kWarps * NS * kBoxDoubles;
+  double* slots = ufrag + (size_t)(P.RB / 4) * MT * 32;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + (size_t)kWarps * P.A);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], P.use_tma ? 1 : 32);
-      mbar_init(&empty[s], kComputeWarps);
-    }
+  const int g = lane >> 2, tq = lane & 3;
+  double* ring = rings + (size_t)warp * NS * kBoxDoubles;
+  uint64_t* bar = bars + warp * NS;
+  double* slot = slots + (size_t)warp * P.A;
+
+  const int r0 = P.r0, r1 = P.frank[0];
+  const int64_t n1 = P.fdim[0];
+  const double* __restrict__ U1 = P.fu[0];
+
+  if (lane == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == kComputeWarps) {
-    // ------------------------- producer warp -------------------------
-    if (P.use_tma && lane == 0) prefetch_tmap(&tmap);
-    uint32_t it = 0;
-    for (int64_t item = blockIdx.x; item < P.nitems; item += gridDim.x) {
-      const Item I = decode_item(P, item);
-      const int nbox = boxes_of(P, I.rho);
-      for (int64_t c0 = I.c_lo; c0 < I.c_hi; c0 += W) {
-        for (int b = 0; b < nbox; ++b, ++it) {
-          const int s = it % kStages;
-          const uint32_t ph = (it / kStages) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          double* dst = stages + (size_t)s * stage_doubles;
-          const int64_t row0 = (int64_t)I.rho * P.RB + 16 * b;
-          if (P.use_tma) {
-            if (lane == 0) {
-              mbar_arrive_expect_tx(&full[s], (uint32_t)(stage_doubles * sizeof(double)));
-              tma_load_2d(dst, &tmap, &full[s], (int32_t)row0, (int32_t)c0);
-            }
-          } else {
-            // warp copy into the same 128B-swizzled layout (odd n0)
-            for (int e = lane; e < stage_doubles; e += 32) {
-              const int jj = e >> 4, ii = e & 15;
-              const int64_t row = row0 + ii, col = c0 + jj;
-              const double v = (row < P.n0 && col < P.Q) ? P.x[col * P.n0 + row] : 0.0;
-              dst[jj * 16 + ((((ii >> 1) ^ (jj & 7)) << 1) | (ii & 1))] = v;
-            }
-            mbar_arrive(&full[s]);
-          }
-        }
-      }
+  WarpIter pit;
+  pit.item = blockIdx.x;
+  pit.seek(P, warp);
+  if (P.use_tma && lane == 0) {
+    prefetch_tmap(&tmap);
+    for (int s = 0; s < NS && pit.valid; ++s) {
+      mbar_arrive_expect_tx(&bar[s], kBoxDoubles * sizeof(double));
+      tma_load_2d(ring + s * kBoxDoubles, &tmap, &bar[s], pit.rho * P.RB + 16 * pit.b,
+                  (int32_t)(pit.c_lo + 16 * pit.tp));
+      pit.next(P, warp);
     }
-    return;
   }
 
-  // --------------------------- compute warps ---------------------------
-  const int tid = threadIdx.x;  // 0..kComputeThreads-1
-  const int g = lane >> 2, tq = lane & 3;
-  uint32_t it = 0;
+  uint32_t consumed = 0;
   int cur_rho = -1;
   for (int64_t item = blockIdx.x; item < P.nitems; item += gridDim.x) {
     const Item I = decode_item(P, item);
-    const int nbox = boxes_of(P, I.rho);
     if (I.rho != cur_rho) {
-      named_sync(1, kComputeThreads);
-      const double* src = P.ufrag + (size_t)I.rho * P.RB * NT * 8;
-      for (int e = tid; e < P.RB * NT * 8; e += kComputeThreads) ufrag[e] = src[e];
+      __syncthreads();
+      const double* src = P.ufrag + (size_t)I.rho * (P.RB / 4) * MT * 32;
+      for (int e = threadIdx.x; e < (P.RB / 4) * MT * 32; e += kThreads) ufrag[e] = src[e];
       cur_rho = I.rho;
+      __syncthreads();
     }
-    for (int e = tid; e < P.acc_total; e += kComputeThreads) accs[e] = 0.0;
-    named_sync(1, kComputeThreads);
+    const int nbox = boxes_of(P, I.rho);
+    if (M3)
+      for (int e = lane; e < P.A; e += 32) slot[e] = 0.0;
+    __syncwarp();
+    double r2[MT][NT1][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT1; ++nt) r2[mt][nt][0] = r2[mt][nt][1] = 0.0;
+    int64_t cur_g2 = -1;  // level-2 group held in r2 (M3 only)
 
-    for (int64_t c0 = I.c_lo; c0 < I.c_hi; c0 += W) {
-      double d[MT][NT][2];
+    // flush r2 (group grp) into the warp-private acc3
+    auto flush = [&](int64_t grp) {
+      const int r2n = P.frank[1];
+      const int64_t i2 = grp % P.fdim[1];
+      const double* __restrict__ U2 = P.fu[1] + i2 * r2n;
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) d[mt][nt][0] = d[mt][nt][1] = 0.0;
-      int colg[MT];
+        for (int nt = 0; nt < NT1; ++nt)
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const int tau = warp * MT + mt;
-        colg[mt] = 16 * (tau >> 1) + 2 * g + (tau & 1);
-      }
-      for (int b = 0; b < nbox; ++b, ++it) {
-        const int s = it % kStages;
-        const uint32_t ph = (it / kStages) & 1;
-        mbar_wait(&full[s], ph);
-        const double* st = stages + (size_t)s * stage_doubles;
-        const double* uf = ufrag + (size_t)b * 4 * NT * 32;
+          for (int v = 0; v < 2; ++v) {
+            const int a0 = g + 8 * mt, a1 = 2 * tq + v + 8 * nt;
+            if (a0 < r0 && a1 < r1) {
+              const double val = r2[mt][nt][v];
+              double* dst = slot + a0 + r0 * a1;
+              for (int a2 = 0; a2 < r2n; ++a2) dst[(size_t)r0 * r1 * a2] += val * __ldg(U2 + a2);
+            }
+            r2[mt][nt][v] = 0.0;
+          }
+      __syncwarp();
+    };
+
+    int tp_lo, tp_hi;
+    warp_range(I, warp, &tp_lo, &tp_hi);
+    for (int tp = tp_lo; tp < tp_hi; ++tp) {
+      const int64_t c0 = I.c_lo + 16 * tp;
+      double t[2][MT][2];
+#pragma unroll
+      for (int par = 0; par < 2; ++par)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) t[par][mt][0] = t[par][mt][1] = 0.0;
+      for (int b = 0; b < nbox; ++b, ++consumed) {
+        const int s = consumed % NS;
+        double* st = ring + s * kBoxDoubles;
+        if (P.use_tma) {
+          mbar_wait(&bar[s], (consumed / NS) & 1);
+        } else {
+          const int64_t row0 = (int64_t)I.rho * P.RB + 16 * b;
+          for (int e = lane; e < kBoxDoubles; e += 32) {
+            const int jj = e >> 4, ii = e & 15;
+            const int64_t row = row0 + ii, col = c0 + jj;
+            const double v = (row < P.n0 && col < P.Q) ? P.x[col * P.n0 + row] : 0.0;
+            st[jj * 16 + ((((ii >> 1) ^ (jj & 7)) << 1) | (ii & 1))] = v;
+          }
+          __syncwarp();
+        }
+        const double* uf = ufrag + (size_t)b * 4 * MT * 32;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
-          const int ii = 4 * ks + tq;
-          double a[MT];
+          const int row = 4 * ks + tq;
+          const double x0 = swz(st, 2 * g, row);      // even columns
+          const double x1 = swz(st, 2 * g + 1, row);  // odd columns
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
-            const int jj = colg[mt];
-            a[mt] = st[jj * 16 + ((((ii >> 1) ^ (jj & 7)) << 1) | (ii & 1))];
-          }
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            const double bf = uf[(ks * NT + nt) * 32 + lane];
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) dmma_8x8x4(d[mt][nt][0], d[mt][nt][1], a[mt], bf);
+            const double a = uf[(ks * MT + mt) * 32 + lane];
+            dmma_8x8x4(t[0][mt][0], t[0][mt][1], a, x0);
+            dmma_8x8x4(t[1][mt][0], t[1][mt][1], a, x1);
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        if (P.use_tma && lane == 0 && pit.valid) {
+          mbar_arrive_expect_tx(&bar[s], kBoxDoubles * sizeof(double));
+          tma_load_2d(st, &tmap, &bar[s], pit.rho * P.RB + 16 * pit.b, (int32_t)(pit.c_lo + 16 * pit.tp));
+          pit.next(P, warp);
+        }
       }
-      // t1 tile -> shared memory T1[a][col]
+      // ---- stage 2: fold mode 1 (thread holds T[g+8mt][col], col = c0 + 4tq + 2s + par)
+      const int64_t clast = min64(c0 + 15, I.c_hi - 1);
+      const int64_t g_first = c0 / n1, g_last = clast / n1;
+      for (int64_t grp = g_first; grp <= g_last; ++grp) {
+        if (M3) {
+          if (cur_g2 >= 0 && grp != cur_g2) flush(cur_g2);
+          cur_g2 = grp;
+        }
+        const int64_t gbase = grp * n1;
+#pragma unroll
+        for (int par = 0; par < 2; ++par)
+#pragma unroll
+          for (int s2 = 0; s2 < 2; ++s2) {
+            const int64_t col = c0 + 4 * tq + 2 * s2 + par;
+            const bool ok = col < I.c_hi && col >= gbase && col < gbase + n1;
+            const double* urow = U1 + (col - gbase) * r1;
+            double bv[NT1];
+#pragma unroll
+            for (int nt = 0; nt < NT1; ++nt) {
+              const int a1 = g + 8 * nt;
+              bv[nt] = (ok && a1 < r1) ? __ldg(urow + a1) : 0.0;
+            }
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+              for (int nt = 0; nt < NT1; ++nt)
+                dmma_8x8x4(r2[mt][nt][0], r2[mt][nt][1], t[par][mt][s2], bv[nt]);
+          }
+      }
+    }
+    // ---- item end: warp partial -> slot, fixed-order CTA reduction
+    if (M3) {
+      if (cur_g2 >= 0) flush(cur_g2);
+    } else {
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
+        for (int nt = 0; nt < NT1; ++nt)
 #pragma unroll
           for (int v = 0; v < 2; ++v) {
-            const int a = 8 * nt + 2 * tq + v;
-            if (a < P.r0) T1[a * W + colg[mt]] = d[mt][nt][v];
+            const int a0 = g + 8 * mt, a1 = 2 * tq + v + 8 * nt;
+            if (a0 < r0 && a1 < r1) slot[a0 + r0 * a1] = r2[mt][nt][v];
           }
-      named_sync(1, kComputeThreads);
-      const int nvalid = (int)srtt_dev::min64(W, I.c_hi - c0);
-      fold_chunk(P, T1, W, c0, nvalid, c0 + W >= I.c_hi, accs, scratch);
     }
-    // item result -> fixed slot
+    __syncthreads();
     double* out = P.part + (((int64_t)I.rho * P.S + I.sigma) * P.G + I.p) * P.A;
-    const double* accm = accs + P.acc_off[P.m];
-    for (int e = tid; e < P.A; e += kComputeThreads) out[e] = accm[e];
-    named_sync(1, kComputeThreads);
+    for (int e = threadIdx.x; e < P.A; e += kThreads) {
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) sum += slots[(size_t)w * P.A + e];
+      out[e] = sum;
+    }
+    __syncthreads();
   }
 }
 
-// U0 -> B-fragment order; fold factors -> row-major.
+// U0 -> fragment order [rho][kstep][mt][lane] = U0[rho*RB + 4 kstep + lane%4][8 mt + lane/4].
 __global__ void prep_kernel(const double* __restrict__ u0, int64_t n0, int r0, int RB, int NT, int nrb,
                             double* __restrict__ ufrag) {
   const int64_t total = (int64_t)nrb * RB * NT * 8;
@@ -343,62 +344,60 @@ __global__ void ttm_kernel(const TtmParams T) {
   }
 }
 
+template <int MT, int NT1, bool M3>
+cudaError_t launch_t(const CUtensorMap* tmap, const CoreParams& P, int grid, size_t smem, cudaStream_t s) {
+  cudaError_t e =
+      cudaFuncSetAttribute(core_kernel<MT, NT1, M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  core_kernel<MT, NT1, M3><<<grid, kThreads, smem, s>>>(*tmap, P);
+  return cudaGetLastError();
+}
+
+template <int MT, int NT1>
+cudaError_t launch_m(const CUtensorMap* tmap, const CoreParams& P, int grid, size_t smem, cudaStream_t s) {
+  return P.m == 3 ? launch_t<MT, NT1, true>(tmap, P, grid, smem, s)
+                  : launch_t<MT, NT1, false>(tmap, P, grid, smem, s);
+}
+
+template <int MT>
+cudaError_t launch_n(const CUtensorMap* tmap, const CoreParams& P, int grid, size_t smem, cudaStream_t s) {
+  switch (P.NT1) {
+    case 1: return launch_m<MT, 1>(tmap, P, grid, smem, s);
+    case 2: return launch_m<MT, 2>(tmap, P, grid, smem, s);
+    case 4: return launch_m<MT, 4>(tmap, P, grid, smem, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 }  // namespace
 
 int srtt_core_threads() { return kThreads; }
 
+// Shared memory of the core kernel for a given stage count.
 size_t srtt_core_smem_bytes(const CoreParams& P) {
-  const size_t doubles = (size_t)kStages * 16 * P.W + (size_t)P.RB * P.NT * 8 + (size_t)P.r0 * P.W +
-                         P.acc_total + kFoldScratch;
-  return 1024 + doubles * sizeof(double) + 2 * kStages * sizeof(uint64_t);
+  const size_t doubles = (size_t)kWarps * P.nstages * kBoxDoubles + (size_t)(P.RB / 4) * P.NT * 32 +
+                         (size_t)kWarps * P.A;
+  return 1024 + doubles * sizeof(double) + (size_t)kWarps * P.nstages * sizeof(uint64_t);
 }
 
-template <int NT, int MT>
-static cudaError_t launch_core_t(const CUtensorMap* tmap, const CoreParams& P, int grid, cudaStream_t s) {
-  const size_t smem = srtt_core_smem_bytes(P);
-  cudaError_t e = cudaFuncSetAttribute(core_kernel<NT, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
-  core_kernel<NT, MT><<<grid, kThreads, smem, s>>>(*tmap, P);
-  return cudaGetLastError();
-}
-
-int srtt_core_occupancy(const CoreParams& P) {
-  const size_t smem = srtt_core_smem_bytes(P);
-  int nb = 0;
-#define OCC(NTV)                                                                                    \
-  case NTV:                                                                                         \
-    cudaFuncSetAttribute(core_kernel<NTV, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, core_kernel<NTV, 1>, kThreads, smem);        \
-    break;
-  switch (P.NT) {
-    OCC(1) OCC(2) OCC(3) OCC(4) OCC(5) OCC(6) OCC(7) OCC(8)
-    default: break;
+int srtt_core_max_stages(const CoreParams& P, size_t budget) {
+  CoreParams Q = P;
+  int best = 0;
+  for (int ns = 2; ns <= 16; ++ns) {
+    Q.nstages = ns;
+    if (srtt_core_smem_bytes(Q) <= budget) best = ns;
   }
-#undef OCC
-  return nb;
+  return best;
 }
+
+int srtt_core_occupancy(const CoreParams&) { return 1; }
 
 cudaError_t srtt_launch_core(const CUtensorMap* tmap, const CoreParams& P, int grid, cudaStream_t s) {
-  const int MT = P.W / (8 * kComputeWarps);
-  if (MT == 1) {
-    switch (P.NT) {
-      case 1: return launch_core_t<1, 1>(tmap, P, grid, s);
-      case 2: return launch_core_t<2, 1>(tmap, P, grid, s);
-      case 3: return launch_core_t<3, 1>(tmap, P, grid, s);
-      case 4: return launch_core_t<4, 1>(tmap, P, grid, s);
-      case 5: return launch_core_t<5, 1>(tmap, P, grid, s);
-      case 6: return launch_core_t<6, 1>(tmap, P, grid, s);
-      case 7: return launch_core_t<7, 1>(tmap, P, grid, s);
-      case 8: return launch_core_t<8, 1>(tmap, P, grid, s);
-    }
-  } else if (MT == 2) {
-    switch (P.NT) {
-      case 1: return launch_core_t<1, 2>(tmap, P, grid, s);
-      case 2: return launch_core_t<2, 2>(tmap, P, grid, s);
-      case 3: return launch_core_t<3, 2>(tmap, P, grid, s);
-      case 4: return launch_core_t<4, 2>(tmap, P, grid, s);
-    }
+  const size_t smem = srtt_core_smem_bytes(P);
+  switch (P.NT) {
+    case 1: return launch_n<1>(tmap, P, grid, smem, s);
+    case 2: return launch_n<2>(tmap, P, grid, smem, s);
+    case 4: return launch_n<4>(tmap, P, grid, smem, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -411,14 +410,14 @@ cudaError_t srtt_launch_prep(const double* u0, int64_t n0, int r0, int RB, int N
 
 cudaError_t srtt_launch_transpose(const double* u, int64_t n, int r, double* ut, cudaStream_t s) {
   const int64_t total = n * r;
-  const int blocks = (int)srtt_dev::min64(1024, (total + 255) / 256);
+  const int blocks = (int)min64(1024, (total + 255) / 256);
   transpose_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(u, n, r, ut);
   return cudaGetLastError();
 }
 
 cudaError_t srtt_launch_ttm(const TtmParams& T, cudaStream_t s) {
   const int64_t total = T.g * T.rr * T.post;
-  const int blocks = (int)srtt_dev::min64(148 * 16, (total + 255) / 256);
+  const int blocks = (int)min64(148 * 16, (total + 255) / 256);
   ttm_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(T);
   return cudaGetLastError();
 }

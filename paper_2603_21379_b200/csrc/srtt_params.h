@@ -69,37 +69,35 @@ typedef struct BasisTarget {
 } BasisTarget;
 
 // ---------------------------------------------------------------------------
-// K3/K5: fused multi-TTM streaming engine. X is viewed as M (n0 x Q),
-// column-major. Stage 1 (mode 0, the only stride-1 mode) runs on FP64 tensor
-// cores (DMMA.8x8x4 via mma.sync) over TMA-loaded, 128B-swizzled boxes of
-// 16 rows x W columns; stages 2..m fold the t1 tiles into nested
-// accumulators in shared memory. Each work item writes one partial of
-// R_m = X x_0 U_0^T ... x_{m-1} U_{m-1}^T for one level-m group.
+// K3/K5: fused multi-TTM streaming engine (see k_core.cu). X is viewed as
+// M (n0 x Q), column-major; a work item is one column range of one row
+// block inside one level-m group (m = 2 or 3). Each item writes
+// R_m = X x_0 U_0^T ... x_{m-1} U_{m-1}^T restricted to its columns into a
+// fixed output slot part[rho][sigma][p][A].
 // ---------------------------------------------------------------------------
 typedef struct CoreParams {
   const double* x;
-  const double* ufrag;     // U0 in B-fragment order: [nrb][RB/4][NT][32]
-  const double* fu[SRTT_MAX_ORDER];  // fold factors U_1..U_{m-1}, ROW-major (n_k x r_k)
+  const double* ufrag;     // U0 in fragment order: [nrb][RB/4][NT][32]
+  const double* fu[2];     // U_1, U_2 ROW-major (n_k x r_k)
   double* part;            // out: [nrb][S][G][A]
   int64_t n0;              // rows (mode 0 extent, or n_left for the root pass)
   int64_t Q;               // columns
-  int64_t fdim[SRTT_MAX_ORDER];  // n_1..n_{m-1}
-  int32_t frank[SRTT_MAX_ORDER]; // r_1..r_{m-1}
+  int64_t fdim[2];         // n_1, n_2
+  int32_t frank[2];        // r_1, r_2
   int64_t GS;              // columns per level-m group
   int64_t G;               // number of groups
-  int64_t SL;              // columns per split (multiple of W)
+  int64_t SL;              // columns per split (multiple of 16)
   int64_t nitems;          // nrb * G * S
   int32_t S;               // splits per group
-  int32_t m;               // fold depth (>= 2)
+  int32_t m;               // fold depth (2 or 3)
   int32_t r0;              // rank of mode 0
-  int32_t NT;              // N-tiles (ceil(r0 / 8))
+  int32_t NT;              // 8-rank tiles of mode 0 (1, 2 or 4)
+  int32_t NT1;             // 8-rank tiles of mode 1 (1, 2 or 4)
   int32_t RB;              // rows per row block (multiple of 16, <= 256)
   int32_t nrb;             // row blocks
-  int32_t W;               // columns per TMA box
   int32_t A;               // prod_{k<m} r_k (output entries per item)
   int32_t use_tma;         // 1: cp.async.bulk.tensor loads; 0: warp-copy path (odd n0)
-  int32_t acc_off[SRTT_MAX_ORDER + 1];  // smem offsets (doubles) of acc_2..acc_m
-  int32_t acc_total;       // doubles of all accumulators
+  int32_t nstages;         // per-warp TMA ring depth
 } CoreParams;
 
 // Generic small TTM used by the tail of the core pass and by reconstruct:

@@ -97,7 +97,8 @@ class _Exec(C.Structure):
 class _Report(C.Structure):
     _fields_ = [("sample_counts", C.POINTER(C.c_int64)), ("achieved_ranks", C.POINTER(C.c_int64)),
                 ("warnings", C.c_char_p), ("warnings_capacity", C.c_int64), ("num_warnings", C.c_int64),
-                ("stage_seconds", C.c_double * len(STAGES)), ("flags", C.c_int32), ("reserved", C.c_int32)]
+                ("stage_seconds", C.c_double * len(STAGES)), ("flags", C.c_int32), ("reserved", C.c_int32),
+                ("kernel_seconds", C.c_double * 4), ("launches", C.c_int64)]
 
 
 class _Tree(C.Structure):
@@ -119,6 +120,7 @@ def _L():
         lib.srtt_destroy.argtypes = [vp]
         lib.srtt_last_launch_count.argtypes = [vp]
         lib.srtt_last_launch_count.restype = i64
+        lib.srtt_set_stream.argtypes = [vp, vp]
         lib.srtt_sample_indices.argtypes = [u64, u64, i64, i64, i64, vp, vp]
         lib.srtt_stream_normals.argtypes = [vp, u64, u64, u64, u64, i64, vp]
         lib.srtt_tree_balanced.argtypes = [i32] + [vp] * 7
@@ -180,6 +182,11 @@ class Handle:
     def __del__(self):
         self.close()
 
+    def set_stream(self, stream_ptr):
+        """Run on an external cudaStream_t (int handle, e.g. torch's
+        ``torch.cuda.current_stream().cuda_stream``); None = own stream."""
+        _check(_L().srtt_set_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
     @property
     def last_launch_count(self) -> int:
         return int(_L().srtt_last_launch_count(self._h))
@@ -219,6 +226,7 @@ class SubsampleReport:
     timings: dict = field(default_factory=dict)
     flags: int = 0
     launches: int = 0
+    kernel_seconds: dict = field(default_factory=dict)
 
 
 HtSubsampleReport = SubsampleReport
@@ -356,7 +364,9 @@ def _report_from(crep, n, ach, samp, report, handle):
     report.warnings = [w for w in txt.split("\n") if w]
     report.timings = {name: float(crep.stage_seconds[i]) for i, name in enumerate(STAGES)}
     report.flags = int(crep.flags)
-    report.launches = handle.last_launch_count
+    report.launches = int(crep.launches)
+    report.kernel_seconds = {"sketch": float(crep.kernel_seconds[0]), "basis": float(crep.kernel_seconds[1]),
+                             "core": float(crep.kernel_seconds[2]), "transfer": float(crep.kernel_seconds[3])}
 
 
 def _alloc_out(shape_list, device_out, like):
