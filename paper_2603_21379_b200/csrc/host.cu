@@ -27,9 +27,11 @@ size_t srtt_sketch_smem_bytes(int cmax);
 cudaError_t srtt_launch_sketch(const SketchTarget*, int, int64_t, int, cudaStream_t);
 size_t srtt_basis_top_smem(int m, int c, int r);
 size_t srtt_basis_level_smem(int mb, int c);
-cudaError_t srtt_launch_basis_top(const BasisTarget*, int, size_t, cudaStream_t);
-cudaError_t srtt_launch_tsqr_factor(const BasisTarget*, int, int, int, size_t, cudaStream_t);
-cudaError_t srtt_launch_tsqr_apply(const BasisTarget*, int, int, int, size_t, cudaStream_t);
+cudaError_t srtt_launch_basis_top(const BasisTarget*, const int*, int, size_t, cudaStream_t);
+size_t srtt_basis_small_smem(int m, int c, int r);
+cudaError_t srtt_launch_basis_small(const BasisTarget*, const int*, int, size_t, cudaStream_t);
+cudaError_t srtt_launch_tsqr_factor(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
+cudaError_t srtt_launch_tsqr_apply(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_pad(const BasisTarget*, int, double*, int64_t, cudaStream_t);
 int srtt_core_threads();
 size_t srtt_core_smem_bytes(const CoreParams& P);
@@ -38,6 +40,8 @@ int srtt_core_max_stages(const CoreParams& P, size_t budget);
 cudaError_t srtt_launch_core(const CUtensorMap*, const CoreParams&, int, cudaStream_t);
 cudaError_t srtt_launch_prep(const double*, int64_t, int, int, int, int, double*, cudaStream_t);
 cudaError_t srtt_launch_transpose(const double*, int64_t, int, double*, cudaStream_t);
+cudaError_t srtt_launch_prep_all(const double*, int64_t, int, int, int, int, double*, int, const double* const*,
+                                 double* const*, const int64_t*, const int*, cudaStream_t);
 cudaError_t srtt_launch_ttm(const TtmParams&, cudaStream_t);
 
 typedef struct TransferTarget {
@@ -201,6 +205,8 @@ int64_t prod(const std::vector<int64_t>& v, size_t lo = 0, size_t hi = SIZE_MAX)
 }  // namespace
 
 // ---- handle -----------------------------------------------------------------
+constexpr int kInfoInts = 4096;  // 4 ints per target + flags
+
 struct srtt_handle {
   int device = 0;
   int sms = 148;
@@ -213,7 +219,8 @@ struct srtt_handle {
   DevBuf ws;       // workspace arena
   DevBuf dparams;  // device copy of the parameter blob
   HostBuf hparams; // pinned parameter blob
-  HostBuf hinfo;   // pinned read-back (ranks, flags)
+  int32_t* hinfo = nullptr;   // mapped pinned: per-target info + flags, written by kernels
+  int32_t* dinfo = nullptr;   // device alias of hinfo
   DevBuf ones;
   int64_t launches = 0;
 };
@@ -320,11 +327,11 @@ BasisBuffers layout_basis(Layout& L, const BasisPlan& p) {
 }
 
 BasisTarget fill_basis(const BasisPlan& p, const BasisBuffers& B, char* ws, double* z, double* u,
-                       uint64_t state0, uint64_t draw_offset, int64_t normal_base) {
+                       uint64_t state0, uint64_t draw_offset, int64_t normal_base, int32_t* info = nullptr) {
   BasisTarget T{};
   T.u = u;
   T.sv = reinterpret_cast<double*>(ws + B.sv);
-  T.info = reinterpret_cast<int32_t*>(ws + B.info);
+  T.info = info ? info : reinterpret_cast<int32_t*>(ws + B.info);
   T.n = p.n;
   T.c = p.c;
   T.r = p.r;
@@ -345,14 +352,50 @@ BasisTarget fill_basis(const BasisPlan& p, const BasisBuffers& B, char* ws, doub
   return T;
 }
 
+// Which targets take the one-warp small path (single block, fits 96 KB).
+bool basis_is_small(const BasisTarget& t) {
+  return t.nlevels == 0 && t.n <= 1024 && srtt_basis_small_smem((int)t.n, t.c, t.r) <= 96 * 1024;
+}
+
+struct BasisLists {
+  std::vector<int> small, big;
+  size_t off_small = 0, off_big = 0;  // blob offsets
+  size_t off_map[SRTT_MAX_QR_LEVELS] = {};  // per TSQR level: CTA -> (target, block)
+};
+
+BasisLists make_basis_lists(const std::vector<BasisTarget>& targets, Blob& blob) {
+  BasisLists L;
+  for (int i = 0; i < (int)targets.size(); ++i) (basis_is_small(targets[i]) ? L.small : L.big).push_back(i);
+  for (int l = 0; l < SRTT_MAX_QR_LEVELS; ++l) {
+    std::vector<int2> map;
+    for (int i = 0; i < (int)targets.size(); ++i)
+      if (targets[i].nlevels > l)
+        for (int b = 0; b < targets[i].lv[l].nblk; ++b) map.push_back(make_int2(i, b));
+    if (map.empty()) break;
+    L.off_map[l] = blob.add(map.data(), sizeof(int2) * map.size());
+  }
+  const int zero = 0;
+  L.off_small = blob.add(L.small.empty() ? &zero : L.small.data(), sizeof(int) * std::max<size_t>(1, L.small.size()));
+  L.off_big = blob.add(L.big.empty() ? &zero : L.big.data(), sizeof(int) * std::max<size_t>(1, L.big.size()));
+  return L;
+}
+
 // Grouped K2 launch sequence over many targets (device array dT).
 int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const BasisTarget* dT,
-                       double* pad_scratch, int64_t pad_stride) {
-  // Targets' cta_begin per level were filled by the caller (assign_basis_ctas).
+                       const BasisLists& lists, const char* dblob, double* pad_scratch, int64_t pad_stride) {
   int launches = 0;
   int maxlev = 0;
   for (auto& t : targets) maxlev = std::max(maxlev, t.nlevels);
   const int nt = (int)targets.size();
+  if (!lists.small.empty()) {
+    size_t smem = 0;
+    for (int i : lists.small)
+      smem = std::max(smem, srtt_basis_small_smem((int)targets[i].n, targets[i].c, targets[i].r));
+    CK(srtt_launch_basis_small(dT, reinterpret_cast<const int*>(dblob + lists.off_small), (int)lists.small.size(),
+                               smem, h->stream));
+    ++launches;
+  }
+  if (lists.big.empty()) return launches;
   for (int l = 0; l < maxlev; ++l) {
     int nctas = 0;
     size_t smem = 0;
@@ -361,12 +404,15 @@ int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const 
         nctas += t.lv[l].nblk;
         smem = std::max(smem, srtt_basis_level_smem(t.lv[l].blk_rows, t.c));
       }
-    CK(srtt_launch_tsqr_factor(dT, nt, l, nctas, smem, h->stream));
+    CK(srtt_launch_tsqr_factor(dT, reinterpret_cast<const int2*>(dblob + lists.off_map[l]), l, nctas, smem,
+                               h->stream));
     ++launches;
   }
   size_t smem = 0;
-  for (auto& t : targets) smem = std::max(smem, srtt_basis_top_smem((int)t.lv[t.nlevels].n, t.c, t.r));
-  CK(srtt_launch_basis_top(dT, nt, smem, h->stream));
+  for (int i : lists.big)
+    smem = std::max(smem, srtt_basis_top_smem((int)targets[i].lv[targets[i].nlevels].n, targets[i].c, targets[i].r));
+  CK(srtt_launch_basis_top(dT, reinterpret_cast<const int*>(dblob + lists.off_big), (int)lists.big.size(), smem,
+                           h->stream));
   ++launches;
   for (int l = maxlev - 1; l >= 0; --l) {
     int nctas = 0;
@@ -376,7 +422,8 @@ int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const 
         nctas += t.lv[l].nblk;
         sm = std::max(sm, srtt_basis_level_smem(t.lv[l].blk_rows, t.c));
       }
-    CK(srtt_launch_tsqr_apply(dT, nt, l, nctas, sm, h->stream));
+    CK(srtt_launch_tsqr_apply(dT, reinterpret_cast<const int2*>(dblob + lists.off_map[l]), l, nctas, sm,
+                              h->stream));
     ++launches;
   }
   if (maxlev > 0) {
@@ -431,7 +478,7 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
   P.frank[0] = (int)ranks[1];
 
   struct Cand {
-    int m = 0, S = 0, ns = 0;
+    int m = 0, S = 0, ns = 0, tpb = 1;
     int64_t SL = 0, G = 0, GS = 0, items = 0;
     int A = 0;
     double cost = 1e300;
@@ -442,20 +489,31 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
     CoreParams T = P;
     T.m = m;
     T.A = (int)(ranks[0] * ranks[1] * (m == 3 ? ranks[2] : 1));
-    const int ns = srtt_core_max_stages(T, kSmemBudget + 20 * 1024);
-    if (ns < 3) continue;
+    // widest box that still leaves a ring of >= 4 boxes per warp
+    int tpb = 0, ns = 0;
+    for (int tb : {4, 2, 1}) {
+      T.tpb = tb;
+      const int n = srtt_core_max_stages(T, kSmemBudget + 20 * 1024);
+      if (n >= 4 || (tb == 1 && n >= 2)) {
+        tpb = tb;
+        ns = n;
+        break;
+      }
+    }
+    if (!tpb) continue;
+    const int64_t bc = 16 * tpb;
     const int64_t GS = prod(dims, 1, m);
     const int64_t G = Q / GS;
-    const int64_t max_s = (GS + 15) / 16;
+    const int64_t max_s = (GS + bc - 1) / bc;
     for (int64_t S = 1; S <= max_s; S = S < 8 ? S + 1 : S * 2) {
       if (force_S && S != force_S) continue;
-      const int64_t SL = ((GS + S - 1) / S + 15) / 16 * 16;
+      const int64_t SL = ((GS + S - 1) / S + bc - 1) / bc * bc;
       const int64_t Se = (GS + SL - 1) / SL;
       const int64_t items = P.nrb * G * Se;
-      const int64_t ntp = SL / 16;
+      const int64_t ntg = SL / bc;
       const int64_t grid = std::min<int64_t>(items, sms);
       const int64_t rounds = (items + grid - 1) / grid;
-      const double item_units = (double)((ntp + 7) / 8) + 0.5;  // +0.5: per-item barrier/reduction
+      const double item_units = (double)((ntg + 7) / 8) * tpb + 0.5;  // +0.5: item-end barrier/reduction
       const double stream = (double)rounds * grid * 8.0 * item_units * tp_bytes;
       const double out = 2.0 * (double)items * T.A * 8.0;
       const double cost = stream + out;
@@ -463,6 +521,7 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
         best.m = m;
         best.S = (int)Se;
         best.ns = ns;
+        best.tpb = tpb;
         best.SL = SL;
         best.G = G;
         best.GS = GS;
@@ -482,6 +541,7 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
   P.nitems = best.items;
   P.A = best.A;
   P.nstages = best.ns;
+  P.tpb = best.tpb;
   if (best.m == 3) {
     P.fdim[1] = dims[2];
     P.frank[1] = (int)ranks[2];
@@ -502,18 +562,26 @@ int launch_core_pass(srtt_handle* h, CorePlan& cp, const double* x, const std::v
   P.x = x;
   P.ufrag = reinterpret_cast<double*>(ws + off_ufrag);
   P.part = reinterpret_cast<double*>(ws + off_part);
-  CK(srtt_launch_prep(u[0], P.n0, P.r0, P.RB, P.NT, P.nrb, const_cast<double*>(P.ufrag), h->stream));
-  ++launches;
-  for (int k = 1; k < P.m; ++k) {
-    double* ut = reinterpret_cast<double*>(ws + off_fu[k]);
-    CK(srtt_launch_transpose(u[k], cp.dims[k], (int)cp.ranks[k], ut, h->stream));
+  {
+    const double* us[2] = {nullptr, nullptr};
+    double* uts[2] = {nullptr, nullptr};
+    int64_t ns[2] = {0, 0};
+    int rs[2] = {0, 0};
+    for (int k = 1; k < P.m; ++k) {
+      us[k - 1] = u[k];
+      uts[k - 1] = reinterpret_cast<double*>(ws + off_fu[k]);
+      ns[k - 1] = cp.dims[k];
+      rs[k - 1] = (int)cp.ranks[k];
+      P.fu[k - 1] = uts[k - 1];
+    }
+    CK(srtt_launch_prep_all(u[0], P.n0, P.r0, P.RB, P.NT, P.nrb, const_cast<double*>(P.ufrag), P.m - 1, us, uts,
+                            ns, rs, h->stream));
     ++launches;
-    P.fu[k - 1] = ut;
   }
   if (P.m == 2) P.fu[1] = nullptr;
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
-  if (P.use_tma) encode_tmap(&tmap, x, P.n0, P.Q, 16);
+  if (P.use_tma) encode_tmap(&tmap, x, P.n0, P.Q, 16 * P.tpb);
   cp.grid = (int)std::min<int64_t>(P.nitems, (int64_t)h->sms);
   CK(cudaEventRecord(h->kev[4], h->stream));
   CK(srtt_launch_core(&tmap, P, cp.grid, h->stream));
@@ -720,11 +788,10 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     const int c = (int)(ranks[k] + p);
     cmax = std::max(cmax, c);
     off_z[k] = L.take(sizeof(double) * dims[k] * c);
-    off_u[k] = L.take(sizeof(double) * dims[k] * ranks[k]);
+    off_u[k] = out_on_device ? 0 : L.take(sizeof(double) * dims[k] * ranks[k]);
     bp[k] = plan_basis(dims[k], c, (int)ranks[k]);
     bb[k] = layout_basis(L, bp[k]);
   }
-  const size_t off_flags = L.take(sizeof(int32_t) * 4);
   const size_t off_core = L.take(sizeof(double) * prod(ranks));
   int64_t max_n = 0;
   for (int k = 0; k < d; ++k) max_n = std::max(max_n, dims[k]);
@@ -735,27 +802,29 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   if (d >= 2) {
     cp = plan_core(dims, ranks, h->sms);
     layout_core(L, cp, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
-  } else {
-    off_tmp0 = L.take(sizeof(double));
   }
   h->ws.ensure(L.off);
   char* ws = reinterpret_cast<char*>(h->ws.p);
+  std::vector<double*> uptr(d);
+  for (int k = 0; k < d; ++k)
+    uptr[k] = out_on_device ? factors_out[k] : reinterpret_cast<double*>(ws + off_u[k]);
+  double* d_core = out_on_device ? core_out : reinterpret_cast<double*>(ws + off_core);
 
-  // --- parameter blob
+  // --- parameter blob (indices, target descriptors, basis lists): one H2D copy
+  if (4 * (d + 1) > kInfoInts) invalid("sub_r_hosvd: too many modes");
+  int32_t* hi = h->hinfo;
+  std::memset(hi, 0, sizeof(int32_t) * 4 * (d + 1));
+  int32_t* d_flags = h->dinfo + 4 * d;
   Blob blob;
   std::vector<size_t> off_cols(d);
   for (int k = 0; k < d; ++k) off_cols[k] = blob.add(cols[k].data(), sizeof(int64_t) * cols[k].size());
   const size_t off_sk = blob.reserve(sizeof(SketchTarget) * d);
   const size_t off_bt = blob.reserve(sizeof(BasisTarget) * d);
-  h->dparams.ensure(blob.lay.off);
-  h->hparams.ensure(blob.lay.off);
-  char* dp = reinterpret_cast<char*>(h->dparams.p);
-  char* hp = reinterpret_cast<char*>(h->hparams.p);
-  for (auto& it : blob.items) std::memcpy(hp + it.first, it.second.data(), it.second.size());
   std::vector<SketchTarget> sk(d);
   std::vector<BasisTarget> bt(d);
   int64_t ctas = 0;
-  int32_t* d_flags = reinterpret_cast<int32_t*>(ws + off_flags);
+  h->dparams.ensure(blob.lay.off + 4096);
+  char* dp = reinterpret_cast<char*>(h->dparams.p);
   for (int k = 0; k < d; ++k) {
     const int c = (int)(ranks[k] + p);
     sk[k] = make_sketch_target(x, dims, {k}, samples[k], c);
@@ -766,13 +835,17 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     sk[k].cta_begin = ctas;
     sk[k].flags = d_flags;
     ctas += (sk[k].rows + sk[k].row_tile - 1) / sk[k].row_tile;
-    bt[k] = fill_basis(bp[k], bb[k], ws, sk[k].z, reinterpret_cast<double*>(ws + off_u[k]), state0[k],
-                       draws[k], samples[k] * c);
+    bt[k] = fill_basis(bp[k], bb[k], ws, sk[k].z, uptr[k], state0[k], draws[k], samples[k] * c, h->dinfo + 4 * k);
   }
   assign_basis_ctas(bt);
+  const BasisLists lists = make_basis_lists(bt, blob);
+  h->dparams.ensure(blob.lay.off);
+  h->hparams.ensure(blob.lay.off);
+  dp = reinterpret_cast<char*>(h->dparams.p);
+  char* hp = reinterpret_cast<char*>(h->hparams.p);
+  for (auto& it : blob.items) std::memcpy(hp + it.first, it.second.data(), it.second.size());
   std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * d);
   std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * d);
-  CK(cudaMemsetAsync(d_flags, 0, sizeof(int32_t) * 4, h->stream));
   CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
   tm.mark();  // 2
 
@@ -781,19 +854,17 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   h->launches++;
   tm.mark();  // 3
   // --- K2: basis of every sketch
-  h->launches += launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt),
+  h->launches += launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt), lists, dp,
                                     reinterpret_cast<double*>(ws + off_pad), max_n);
   tm.mark();  // 4
   // --- K3: core pass
-  std::vector<const double*> uptr(d);
-  for (int k = 0; k < d; ++k) uptr[k] = reinterpret_cast<const double*>(ws + off_u[k]);
-  double* d_core = reinterpret_cast<double*>(ws + off_core);
+  std::vector<const double*> ucp(uptr.begin(), uptr.end());
   if (d >= 2) {
-    h->launches += launch_core_pass(h, cp, x, uptr, d_core, ws, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+    h->launches += launch_core_pass(h, cp, x, ucp, d_core, ws, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
   } else {
     TtmParams T{};
     T.in = x;
-    T.u = uptr[0];
+    T.u = ucp[0];
     T.out = d_core;
     T.g = 1;
     T.n = dims[0];
@@ -805,14 +876,11 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     h->launches++;
   }
   tm.mark();  // 5
-  // --- outputs + report read-back
-  copy_out(h, core_out, d_core, sizeof(double) * prod(ranks), out_on_device);
-  for (int k = 0; k < d; ++k) copy_out(h, factors_out[k], uptr[k], sizeof(double) * dims[k] * ranks[k], out_on_device);
-  h->hinfo.ensure(sizeof(int32_t) * 4 * (d + 1));
-  int32_t* hi = reinterpret_cast<int32_t*>(h->hinfo.p);
-  for (int k = 0; k < d; ++k)
-    CK(cudaMemcpyAsync(hi + 4 * k, bt[k].info, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaMemcpyAsync(hi + 4 * d, d_flags, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, h->stream));
+  // --- outputs (host destinations only; device outputs were written in place)
+  if (!out_on_device) {
+    copy_out(h, core_out, d_core, sizeof(double) * prod(ranks), 0);
+    for (int k = 0; k < d; ++k) copy_out(h, factors_out[k], uptr[k], sizeof(double) * dims[k] * ranks[k], 0);
+  }
   tm.mark();  // 6
   CK(cudaStreamSynchronize(h->stream));
   CK(cudaGetLastError());
@@ -836,6 +904,8 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     rep->stage_seconds[SRTT_STAGE_FACTOR_WALL] = t_sampling + tm.between(2, 4);
     rep->stage_seconds[SRTT_STAGE_D2H] = tm.between(5, 6);
     rep->flags = hi[4 * d];
+    rep->reserved = 0;  // max Jacobi sweeps over the targets
+    for (int k = 0; k < d; ++k) rep->reserved = std::max(rep->reserved, hi[4 * k + 2]);
     rep->kernel_seconds[0] = tm.between(2, 3);
     rep->kernel_seconds[1] = tm.between(3, 4);
     rep->kernel_seconds[2] = d >= 2 ? kernel_pair(h, 2) : 0.0;
@@ -873,6 +943,8 @@ int srtt_create(const srtt_options* opts, srtt_handle** out) {
     h->stream = h->own_stream;
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
     for (auto& e : h->kev) CK(cudaEventCreate(&e));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->hinfo), kInfoInts * sizeof(int32_t), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dinfo), h->hinfo, 0));
     h->ones.ensure(sizeof(double));
     const double one = 1.0;
     CK(cudaMemcpy(h->ones.p, &one, sizeof(double), cudaMemcpyHostToDevice));
@@ -889,6 +961,7 @@ int srtt_destroy(srtt_handle* h) {
       for (auto& e : h->ev) cudaEventDestroy(e);
       for (auto& e : h->kev) cudaEventDestroy(e);
       cudaStreamDestroy(h->own_stream);
+      if (h->hinfo) cudaFreeHost(h->hinfo);
     }
     delete h;
   });
@@ -1115,7 +1188,10 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     bb[t] = layout_basis(L, bp[t]);
   }
   const size_t off_pad = L.take(sizeof(double) * max_n * nt);
-  const size_t off_flags = L.take(sizeof(int32_t) * 4);
+  if (4 * (nt + 1) > kInfoInts) invalid("sub_r_rtl_ht: too many tree nodes");
+  int32_t* hi = h->hinfo;
+  std::memset(hi, 0, sizeof(int32_t) * 4 * (nt + 1));
+  int32_t* d_flags = h->dinfo + 4 * nt;
   // transfers of internal non-root nodes, and the root
   std::vector<int> internal;
   for (int i = 1; i < nn; ++i)
@@ -1140,16 +1216,15 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   const size_t off_sk = blob.reserve(sizeof(SketchTarget) * nt);
   const size_t off_bt = blob.reserve(sizeof(BasisTarget) * nt);
   const size_t off_tt = blob.reserve(sizeof(TransferTarget) * std::max<size_t>(1, internal.size()));
-  h->dparams.ensure(blob.lay.off);
-  h->hparams.ensure(blob.lay.off);
+  h->dparams.ensure(blob.lay.off + 4096);
   char* dp = reinterpret_cast<char*>(h->dparams.p);
-  char* hp = reinterpret_cast<char*>(h->hparams.p);
-  for (auto& it : blob.items) std::memcpy(hp + it.first, it.second.data(), it.second.size());
   std::vector<SketchTarget> sk(nt);
   std::vector<BasisTarget> bt(nt);
-  int32_t* d_flags = reinterpret_cast<int32_t*>(ws + off_flags);
   int64_t ctas = 0;
-  auto ubasis = [&](int id) { return reinterpret_cast<double*>(ws + off_u[id - 1]); };
+  auto ubasis = [&](int id) {
+    if (out_on_device && tr.leaf(id)) return leaf_out[tr.modes[id][0]];
+    return reinterpret_cast<double*>(ws + off_u[id - 1]);
+  };
   for (int t = 0; t < nt; ++t) {
     const int id = t + 1;
     const int c = (int)(ranks[id] + p);
@@ -1161,9 +1236,15 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     sk[t].cta_begin = ctas;
     sk[t].flags = d_flags;
     ctas += (sk[t].rows + sk[t].row_tile - 1) / sk[t].row_tile;
-    bt[t] = fill_basis(bp[t], bb[t], ws, sk[t].z, ubasis(id), state0[t], draws[t], samples[id] * c);
+    bt[t] = fill_basis(bp[t], bb[t], ws, sk[t].z, ubasis(id), state0[t], draws[t], samples[id] * c,
+                       h->dinfo + 4 * t);
   }
   assign_basis_ctas(bt);
+  const BasisLists lists = make_basis_lists(bt, blob);
+  h->dparams.ensure(blob.lay.off);
+  h->hparams.ensure(blob.lay.off);
+  char* hp = reinterpret_cast<char*>(h->hparams.p);
+  for (auto& it : blob.items) std::memcpy(hp + it.first, it.second.data(), it.second.size());
   std::vector<TransferTarget> tt;
   int tctas = 0, max_rl = 1, max_rr = 1;
   for (int i : internal) {
@@ -1171,7 +1252,8 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     T.us = ubasis(i);
     T.ul = ubasis(tr.left[i]);
     T.ur = ubasis(tr.right[i]);
-    T.b = reinterpret_cast<double*>(ws + off_b[i]);
+    T.b = (out_on_device && transfers_out && transfers_out[i]) ? transfers_out[i]
+                                                               : reinterpret_cast<double*>(ws + off_b[i]);
     T.nl = node_rows(tr.left[i]);
     T.nr = node_rows(tr.right[i]);
     T.rs = (int)ranks[i];
@@ -1186,13 +1268,12 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * nt);
   std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * nt);
   if (!tt.empty()) std::memcpy(hp + off_tt, tt.data(), sizeof(TransferTarget) * tt.size());
-  CK(cudaMemsetAsync(d_flags, 0, sizeof(int32_t) * 4, h->stream));
   CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
   tm.mark();  // 2
   CK(srtt_launch_sketch(reinterpret_cast<const SketchTarget*>(dp + off_sk), nt, ctas, cmax, h->stream));
   h->launches++;
   tm.mark();  // 3
-  h->launches += launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt),
+  h->launches += launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt), lists, dp,
                                     reinterpret_cast<double*>(ws + off_pad), max_n);
   tm.mark();  // 4
   if (!tt.empty()) {
@@ -1203,26 +1284,24 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   tm.mark();  // 5
   // root transfer: the K3 engine on M = X viewed as n_l x n_r (htucker.hpp:67-85)
   std::vector<const double*> ur = {ubasis(tr.left[0]), ubasis(tr.right[0])};
-  double* d_root = reinterpret_cast<double*>(ws + off_b[0]);
+  double* d_root = (out_on_device && transfers_out && transfers_out[0]) ? transfers_out[0]
+                                                                       : reinterpret_cast<double*>(ws + off_b[0]);
   h->launches += launch_core_pass(h, cp, x, ur, d_root, ws, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
   tm.mark();  // 6
-  for (int i = 1; i < nn; ++i)
-    if (tr.leaf(i)) {
-      const int mode = tr.modes[i][0];
-      copy_out(h, leaf_out[mode], ubasis(i), sizeof(double) * dims[mode] * ranks[i], out_on_device);
+  if (!out_on_device) {
+    for (int i = 1; i < nn; ++i)
+      if (tr.leaf(i)) {
+        const int mode = tr.modes[i][0];
+        copy_out(h, leaf_out[mode], ubasis(i), sizeof(double) * dims[mode] * ranks[i], 0);
+      }
+    if (transfers_out) {
+      for (int i : internal)
+        if (transfers_out[i])
+          copy_out(h, transfers_out[i], ws + off_b[i],
+                   sizeof(double) * ranks[i] * ranks[tr.left[i]] * ranks[tr.right[i]], 0);
+      if (transfers_out[0]) copy_out(h, transfers_out[0], d_root, sizeof(double) * rl0 * rr0, 0);
     }
-  if (transfers_out) {
-    for (int i : internal)
-      if (transfers_out[i])
-        copy_out(h, transfers_out[i], ws + off_b[i],
-                 sizeof(double) * ranks[i] * ranks[tr.left[i]] * ranks[tr.right[i]], out_on_device);
-    if (transfers_out[0]) copy_out(h, transfers_out[0], d_root, sizeof(double) * rl0 * rr0, out_on_device);
   }
-  h->hinfo.ensure(sizeof(int32_t) * 4 * (nt + 1));
-  int32_t* hi = reinterpret_cast<int32_t*>(h->hinfo.p);
-  for (int t = 0; t < nt; ++t)
-    CK(cudaMemcpyAsync(hi + 4 * t, bt[t].info, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaMemcpyAsync(hi + 4 * nt, d_flags, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, h->stream));
   tm.mark();  // 7
   CK(cudaStreamSynchronize(h->stream));
   CK(cudaGetLastError());
@@ -1248,6 +1327,8 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     rep->stage_seconds[SRTT_STAGE_FACTOR_WALL] = t_sampling + tm.between(2, 4);
     rep->stage_seconds[SRTT_STAGE_D2H] = tm.between(6, 7);
     rep->flags = hi[4 * nt];
+    rep->reserved = 0;
+    for (int t = 0; t < nt; ++t) rep->reserved = std::max(rep->reserved, hi[4 * t + 2]);
     rep->kernel_seconds[0] = tm.between(2, 3);
     rep->kernel_seconds[1] = tm.between(3, 4);
     rep->kernel_seconds[2] = kernel_pair(h, 2);
@@ -1422,9 +1503,16 @@ int srtt_range_basis_of_sketch(srtt_handle* h, const double* z, int32_t z_on_dev
                                               reinterpret_cast<double*>(ws + off_u),
                                               srtt_host::stream_state0(seed, stream_id), draw_offset, normal_base)};
     assign_basis_ctas(bt);
+    Blob blob;
+    const BasisLists lists = make_basis_lists(bt, blob);
+    std::vector<unsigned char> hb(blob.lay.off);
+    for (auto& it : blob.items) std::memcpy(hb.data() + it.first, it.second.data(), it.second.size());
+    B.c.ensure(hb.size() + 64);
+    CK(cudaMemcpyAsync(B.c.p, hb.data(), hb.size(), cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(ws + off_t, bt.data(), sizeof(BasisTarget), cudaMemcpyHostToDevice, h->stream));
-    launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(ws + off_t), reinterpret_cast<double*>(ws + off_pad),
-                       n);
+    launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(ws + off_t), lists,
+                       reinterpret_cast<const char*>(B.c.p), reinterpret_cast<double*>(ws + off_pad), n);
+    CK(cudaStreamSynchronize(h->stream));
     copy_out(h, q_out, ws + off_u, sizeof(double) * n * rank, out_on_device);
     int32_t info[4];
     CK(cudaMemcpyAsync(info, bt[0].info, sizeof(info), cudaMemcpyDeviceToHost, h->stream));

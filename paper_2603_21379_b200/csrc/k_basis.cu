@@ -122,61 +122,112 @@ __device__ __forceinline__ void rr_pair(int pr, int rd, int kk, int* p, int* q) 
   }
 }
 
-// One-sided Jacobi on the rows of B (k x cc, row-major, ld = cc); rotations
-// accumulated into V (k x k, column-major, starts as I). On exit the rows of
-// B are mutually orthogonal and B_in = V * B_out.
-__device__ void jacobi_rows(double* B, int k, int cc, double* V, int* flag) {
+
+// Stage a target descriptor into shared memory (one cooperative copy)
+// so the kernels never re-read its fields from global memory.
+__device__ __forceinline__ void stage_target(BasisTarget* dst, const BasisTarget* src) {
+  const int* s = reinterpret_cast<const int*>(src);
+  int* d = reinterpret_cast<int*>(dst);
+  for (int i = threadIdx.x; i < (int)(sizeof(BasisTarget) / sizeof(int)); i += blockDim.x) d[i] = s[i];
+}
+
+// Round-robin schedule for kk players (kk even, <= 64): pairs[rd * kk/2 + pr]
+// = (p | q << 8) with p < q; entries with q >= k are dummies.
+__device__ void build_pairs(unsigned short* pairs, int kk) {
+  const int np = kk - 1;
+  for (int e = threadIdx.x; e < np * (kk / 2); e += blockDim.x) {
+    const int rd = e / (kk / 2), pr = e % (kk / 2);
+    int p, q;
+    if (pr == 0) { p = rd % np; q = kk - 1; }
+    else { p = (rd + pr) % np; q = (rd - pr + np) % np; }
+    if (p > q) { const int t = p; p = q; q = t; }
+    pairs[e] = (unsigned short)(p | (q << 8));
+  }
+}
+
+// Jacobi rotation zeroing apq: t = sign(d) 2 apq / (|d| + sqrt(d^2 + 4 apq^2)),
+// d = aqq - app (Rutishauser's tan(theta), one sqrt + one division).
+__device__ __forceinline__ void jacobi_rotation(double app, double aqq, double apq, double* cs, double* sn) {
+  const double dd = aqq - app;
+  const double ta = 2.0 * apq;
+  const double t = copysign(1.0, dd) * ta / (fabs(dd) + sqrt(dd * dd + ta * ta));
+  const double c = rsqrt(1.0 + t * t);
+  *cs = c;
+  *sn = c * t;
+}
+
+// One-sided Jacobi on the rows of B (k x c, row-major, ld = ldb) with
+// rotations accumulated into V (k x k, column-major, ld = ldv; starts as I).
+// Round-robin pairs are spread over 4-lane groups (8 pairs per warp, all
+// warps of the block): a pair's three dot products reduce with two
+// shuffles, so a round costs a few hundred cycles instead of a serial
+// dot-product chain. Returns the number of sweeps.
+__device__ int jacobi_rows_g4(double* B, int ldb, int k, int c, double* V, int ldv,
+                              const unsigned short* pairs) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int grp = lane >> 2, gl = lane & 3;
   const int kk = (k + 1) & ~1;
-  const double tol = 2.0 * DBL_EPSILON;
-  if (k < 2) return;
-  for (int sweep = 0; sweep < 80; ++sweep) {
-    __syncthreads();
-    if (threadIdx.x == 0) *flag = 0;
-    __syncthreads();
+  const int npairs = kk / 2;
+  const int slots = nwarps * 8;
+  const double tol2 = 4.0 * DBL_EPSILON * DBL_EPSILON;
+  if (k < 2) return 0;
+  int sweep = 0;
+  for (; sweep < 80; ++sweep) {
+    int rotated = 0;
     for (int rd = 0; rd < kk - 1; ++rd) {
-      for (int pr = warp; pr < kk / 2; pr += kWarps) {
-        int p, q;
-        rr_pair(pr, rd, kk, &p, &q);
-        if (p >= k || q >= k) continue;
-        if (p > q) { const int tmp = p; p = q; q = tmp; }
-        double* bp = B + (size_t)p * cc;
-        double* bq = B + (size_t)q * cc;
-        double app = 0.0, aqq = 0.0, apq = 0.0;
-        for (int j = lane; j < cc; j += 32) {
-          const double x = bp[j], y = bq[j];
-          app += x * x;
-          aqq += y * y;
-          apq += x * y;
+      const unsigned short* pr_rd = pairs + rd * npairs;
+      for (int b0 = 0; b0 < npairs; b0 += slots) {
+        const int pr = b0 + warp * 8 + grp;
+        int p = 0, q = 0;
+        bool valid = pr < npairs;
+        if (valid) {
+          const unsigned short e = pr_rd[pr];
+          p = e & 0xff;
+          q = e >> 8;
+          valid = q < k;
         }
-        app = warp_sum(app);
-        aqq = warp_sum(aqq);
-        apq = warp_sum(apq);
-        if (apq != 0.0 && fabs(apq) > tol * sqrt(app) * sqrt(aqq)) {
-          const double zeta = (aqq - app) / (2.0 * apq);
-          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double cs = 1.0 / sqrt(1.0 + t * t);
-          const double sn = cs * t;
-          for (int j = lane; j < cc; j += 32) {
+        double* bp = B + (size_t)p * ldb;
+        double* bq = B + (size_t)q * ldb;
+        double app = 0.0, aqq = 0.0, apq = 0.0;
+        if (valid)
+          for (int j = gl; j < c; j += 4) {
+            const double x = bp[j], y = bq[j];
+            app += x * x;
+            aqq += y * y;
+            apq += x * y;
+          }
+        app += __shfl_xor_sync(0xffffffffu, app, 1);
+        aqq += __shfl_xor_sync(0xffffffffu, aqq, 1);
+        apq += __shfl_xor_sync(0xffffffffu, apq, 1);
+        app += __shfl_xor_sync(0xffffffffu, app, 2);
+        aqq += __shfl_xor_sync(0xffffffffu, aqq, 2);
+        apq += __shfl_xor_sync(0xffffffffu, apq, 2);
+        if (valid && apq != 0.0 && apq * apq > tol2 * app * aqq) {
+          double cs, sn;
+          jacobi_rotation(app, aqq, apq, &cs, &sn);
+          for (int j = gl; j < c; j += 4) {
             const double x = bp[j], y = bq[j];
             bp[j] = cs * x - sn * y;
             bq[j] = sn * x + cs * y;
           }
-          double* vp = V + (size_t)p * k;
-          double* vq = V + (size_t)q * k;
-          for (int i = lane; i < k; i += 32) {
+          double* vp = V + (size_t)p * ldv;
+          double* vq = V + (size_t)q * ldv;
+          for (int i = gl; i < k; i += 4) {
             const double x = vp[i], y = vq[i];
             vp[i] = cs * x - sn * y;
             vq[i] = sn * x + cs * y;
           }
-          if (lane == 0) *flag = 1;
+          rotated = 1;
         }
       }
-      __syncthreads();
+      if (nwarps > 1) __syncthreads(); else __syncwarp();
     }
-    if (*flag == 0) break;
+    const int any = nwarps > 1 ? __syncthreads_or(rotated) : __any_sync(0xffffffffu, rotated);
+    if (!any) break;
   }
-  __syncthreads();
+  if (nwarps > 1) __syncthreads(); else __syncwarp();
+  return sweep;
 }
 
 // Classical Gram-Schmidt padding (sketch.hpp:48-65) of columns q..r-1 of Y
@@ -258,9 +309,13 @@ __device__ TopSmem carve_top(unsigned char* raw, int m, int c, int r) {
 }
 
 // Top of the TSQR tree (or the whole basis for single-block targets).
-__global__ void __launch_bounds__(kThreads) basis_top_kernel(const BasisTarget* __restrict__ targets) {
+__global__ void __launch_bounds__(kThreads) basis_top_kernel(const BasisTarget* __restrict__ targets,
+                                                            const int* __restrict__ list) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const BasisTarget& T = targets[blockIdx.x];
+  __shared__ BasisTarget T;
+  __shared__ unsigned short pairs[64 * 32];
+  stage_target(&T, &targets[list[blockIdx.x]]);
+  __syncthreads();
   const int top = T.nlevels;
   const QrLevel L = T.lv[top];
   const int m = (int)L.n;
@@ -281,7 +336,9 @@ __global__ void __launch_bounds__(kThreads) basis_top_kernel(const BasisTarget* 
   }
   for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) s.V[idx] = (idx % k == idx / k) ? 1.0 : 0.0;
   __syncthreads();
-  jacobi_rows(s.B, k, c, s.V, s.flag);
+  build_pairs(pairs, (k + 1) & ~1);
+  __syncthreads();
+  const int sweeps = jacobi_rows_g4(s.B, c, k, c, s.V, k, pairs);
   // Singular values = row norms; sort descending (ties by index).
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = warp; i < k; i += kWarps) {
@@ -306,6 +363,7 @@ __global__ void __launch_bounds__(kThreads) basis_top_kernel(const BasisTarget* 
   if (threadIdx.x == 0) {
     T.info[0] = q;
     T.info[1] = nrank;
+    T.info[2] = sweeps;
   }
   if (T.sv)
     for (int i = threadIdx.x; i < k; i += blockDim.x) T.sv[i] = s.sig[s.perm[i]];
@@ -331,26 +389,17 @@ __global__ void __launch_bounds__(kThreads) basis_top_kernel(const BasisTarget* 
   }
 }
 
-__device__ int find_target(const BasisTarget* targets, int ntargets, int level) {
-  // linear scan: targets without this level own no CTAs
-  for (int t = 0; t < ntargets; ++t) {
-    const BasisTarget& T = targets[t];
-    if (T.nlevels > level && (int)blockIdx.x >= T.cta_begin[level] &&
-        (int)blockIdx.x < T.cta_begin[level] + T.lv[level].nblk)
-      return t;
-  }
-  return 0;
-}
-
 // One TSQR level below the top: factor each row block, stack its R.
 __global__ void __launch_bounds__(kThreads) tsqr_factor_kernel(const BasisTarget* __restrict__ targets,
-                                                               int ntargets, int level) {
+                                                               const int2* __restrict__ map, int level) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int t = find_target(targets, ntargets, level);
-  const BasisTarget& T = targets[t];
+  __shared__ BasisTarget T;
+  const int2 tb = map[blockIdx.x];  // (target, block)
+  stage_target(&T, &targets[tb.x]);
+  __syncthreads();
   const QrLevel L = T.lv[level];
   const QrLevel P = T.lv[level + 1];
-  const int b = blockIdx.x - T.cta_begin[level];
+  const int b = tb.y;
   const int c = T.c;
   const int64_t r0 = (int64_t)b * L.blk_rows;
   const int mb = (int)srtt_dev::min64(L.blk_rows, L.n - r0);
@@ -380,13 +429,15 @@ __global__ void __launch_bounds__(kThreads) tsqr_factor_kernel(const BasisTarget
 // Back-application through one TSQR level: rows of the parent's Y belonging
 // to block b, padded with zeros to the block height, times the block's Q.
 __global__ void __launch_bounds__(kThreads) tsqr_apply_kernel(const BasisTarget* __restrict__ targets,
-                                                              int ntargets, int level) {
+                                                              const int2* __restrict__ map, int level) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int t = find_target(targets, ntargets, level);
-  const BasisTarget& T = targets[t];
+  __shared__ BasisTarget T;
+  const int2 tb = map[blockIdx.x];
+  stage_target(&T, &targets[tb.x]);
+  __syncthreads();
   const QrLevel L = T.lv[level];
   const QrLevel P = T.lv[level + 1];
-  const int b = blockIdx.x - T.cta_begin[level];
+  const int b = tb.y;
   const int c = T.c;
   const int q = T.info[0];
   const int64_t r0 = (int64_t)b * L.blk_rows;
@@ -419,12 +470,242 @@ __global__ void __launch_bounds__(kThreads) pad_kernel(const BasisTarget* __rest
                                                        double* scratch, int64_t scratch_stride) {
   __shared__ double dots[SRTT_MAX_SKETCH_COLS];
   __shared__ double red[32];
-  const BasisTarget& T = targets[blockIdx.x];
+  __shared__ BasisTarget T;
+  stage_target(&T, &targets[blockIdx.x]);
+  __syncthreads();
   if (T.nlevels == 0) return;
   const int q = T.info[0];
   if (q >= T.r) return;
   pad_columns(T.u, T.n, T.n, q, T.r, T.state0, T.draw_offset, (uint64_t)T.normal_base,
               scratch + (int64_t)blockIdx.x * scratch_stride, dots, red);
+}
+
+// ===========================================================================
+// Small-sketch path: one WARP per target, no block barriers. Used when the
+// whole n x c sketch fits in shared memory (the common case: Tucker modes,
+// H-Tucker level-2 nodes and leaves). Same algorithm as the block path:
+// Householder QR (lanes own columns), one-sided Jacobi on the rows of R
+// (lanes own round-robin pairs), rank decision, U = Q V(:, perm[:q]),
+// Gram-Schmidt padding from the same stream.
+// ===========================================================================
+struct SmallSmem {
+  double* A;   // m x c, ld = lda (odd)
+  double* B;   // k x c rows, ld = ldb (odd)
+  double* V;   // k x k, ld = ldv (odd)
+  double* Y;   // m x r, ld = lda
+  double* tau;
+  double* sig;
+  double* dots;
+  double* v;
+  int* perm;
+  int lda, ldb, ldv;
+};
+
+__host__ __device__ inline int odd_ld(int n) { return n | 1; }
+
+__device__ SmallSmem carve_small(unsigned char* raw, int m, int c, int r) {
+  const int k = min(m, c);
+  SmallSmem s;
+  s.lda = odd_ld(m);
+  s.ldb = odd_ld(c);
+  s.ldv = odd_ld(k);
+  double* p = reinterpret_cast<double*>(raw);
+  s.A = p; p += (size_t)s.lda * c;
+  s.B = p; p += (size_t)s.ldb * k;
+  s.V = p; p += (size_t)s.ldv * k;
+  s.Y = p; p += (size_t)s.lda * r;
+  s.tau = p; p += c;
+  s.sig = p; p += k;
+  s.dots = p; p += r;
+  s.v = p; p += m;
+  s.perm = reinterpret_cast<int*>(p);
+  return s;
+}
+
+__device__ __forceinline__ double dot4(const double* a, const double* b, int lo, int hi) {
+  double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+  int i = lo;
+  for (; i + 3 < hi; i += 4) {
+    s0 += a[i] * b[i];
+    s1 += a[i + 1] * b[i + 1];
+    s2 += a[i + 2] * b[i + 2];
+    s3 += a[i + 3] * b[i + 3];
+  }
+  for (; i < hi; ++i) s0 += a[i] * b[i];
+  return (s0 + s1) + (s2 + s3);
+}
+
+__global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __restrict__ targets,
+                                                         const int* __restrict__ list) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ BasisTarget T;
+  __shared__ unsigned short pairs[64 * 32];
+  stage_target(&T, &targets[list[blockIdx.x]]);
+  __syncwarp();
+  const int lane = threadIdx.x;
+  const int m = (int)T.n, c = T.c, r = T.r;
+  const int k = min(m, c);
+  SmallSmem s = carve_small(smem_raw, m, c, r);
+  const double* z = T.lv[0].a;
+  for (int idx = lane; idx < m * c; idx += 32) {
+    const int i = idx % m, j = idx / m;
+    s.A[(size_t)j * s.lda + i] = z[idx];
+  }
+  __syncwarp();
+  // ---- Householder QR, lanes own the trailing columns
+  for (int j = 0; j < k; ++j) {
+    double* col = s.A + (size_t)j * s.lda;
+    double part = 0.0;
+    for (int i = j + 1 + lane; i < m; i += 32) part += col[i] * col[i];
+    const double ss = warp_sum(part);
+    const double alpha = col[j];
+    double t = 0.0, scal = 0.0, beta = alpha;
+    if (ss != 0.0) {
+      const double nrm = sqrt(alpha * alpha + ss);
+      beta = -copysign(nrm, alpha);
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (t != 0.0)
+      for (int i = j + 1 + lane; i < m; i += 32) col[i] *= scal;
+    __syncwarp();
+    if (lane == 0) {
+      col[j] = beta;
+      s.tau[j] = t;
+    }
+    if (t != 0.0) {
+      const int grp = lane >> 2, gl = lane & 3;
+      for (int jb = j + 1; jb < c; jb += 8) {
+        const int jj = jb + grp;
+        double* cj = s.A + (size_t)min(jj, c - 1) * s.lda;
+        double w = 0.0;
+        if (jj < c)
+          for (int i = j + 1 + gl; i < m; i += 4) w += col[i] * cj[i];
+        w += __shfl_xor_sync(0xffffffffu, w, 1);
+        w += __shfl_xor_sync(0xffffffffu, w, 2);
+        if (jj < c) {
+          const double tw = t * (w + cj[j]);
+          __syncwarp(0xffffffffu);
+          if (gl == 0) cj[j] -= tw;
+          for (int i = j + 1 + gl; i < m; i += 4) cj[i] -= tw * col[i];
+        } else {
+          __syncwarp(0xffffffffu);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // ---- R rows -> B, V = I
+  for (int idx = lane; idx < k * c; idx += 32) {
+    const int i = idx / c, j = idx % c;
+    s.B[(size_t)i * s.ldb + j] = (j >= i) ? s.A[(size_t)j * s.lda + i] : 0.0;
+  }
+  for (int idx = lane; idx < k * k; idx += 32) {
+    const int i = idx % k, j = idx / k;
+    s.V[(size_t)j * s.ldv + i] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncwarp();
+  // ---- one-sided Jacobi on rows (4-lane groups own pairs)
+  build_pairs(pairs, (k + 1) & ~1);
+  __syncwarp();
+  const int sweeps = jacobi_rows_g4(s.B, s.ldb, k, c, s.V, s.ldv, pairs);
+  // ---- singular values, ordering, rank decision
+  for (int i = lane; i < k; i += 32) {
+    const double* bi = s.B + (size_t)i * s.ldb;
+    s.sig[i] = sqrt(dot4(bi, bi, 0, c));
+  }
+  __syncwarp();
+  for (int i = lane; i < k; i += 32) {
+    int rank = 0;
+    for (int j = 0; j < k; ++j) rank += (s.sig[j] > s.sig[i]) || (s.sig[j] == s.sig[i] && j < i);
+    s.perm[rank] = i;
+  }
+  __syncwarp();
+  const double smax = s.sig[s.perm[0]];
+  const double tol_rank = (double)max(m, c) * DBL_EPSILON * smax;
+  int nrank = 0;
+  for (int i = 0; i < k; ++i) nrank += s.sig[i] > tol_rank;
+  const int q = min(nrank, r);
+  if (lane == 0) {
+    T.info[0] = q;
+    T.info[1] = nrank;
+    T.info[2] = sweeps;
+  }
+  if (T.sv)
+    for (int i = lane; i < k; i += 32) T.sv[i] = s.sig[s.perm[i]];
+  // ---- Y = Q [V(:, perm[:q]); 0], 4-lane groups own output columns
+  {
+    const int grp = lane >> 2, gl = lane & 3;
+    for (int cb = 0; cb < q; cb += 8) {
+      const int col = cb + grp;
+      const bool act = col < q;
+      double* y = s.Y + (size_t)min(col, q - 1) * s.lda;
+      if (act) {
+        const double* vc = s.V + (size_t)s.perm[col] * s.ldv;
+        for (int i = gl; i < m; i += 4) y[i] = i < k ? vc[i] : 0.0;
+      }
+      __syncwarp();
+      for (int j = k - 1; j >= 0; --j) {
+        const double t = s.tau[j];
+        if (t == 0.0) continue;
+        const double* vj = s.A + (size_t)j * s.lda;
+        double w = 0.0;
+        if (act)
+          for (int i = j + 1 + gl; i < m; i += 4) w += vj[i] * y[i];
+        w += __shfl_xor_sync(0xffffffffu, w, 1);
+        w += __shfl_xor_sync(0xffffffffu, w, 2);
+        if (act) {
+          const double tw = t * (w + y[j]);
+          __syncwarp(0xffffffffu);
+          if (gl == 0) y[j] -= tw;
+          for (int i = j + 1 + gl; i < m; i += 4) y[i] -= tw * vj[i];
+        } else {
+          __syncwarp(0xffffffffu);
+        }
+        __syncwarp();
+      }
+    }
+  }
+  __syncwarp();
+  // ---- Gaussian padding (sketch.hpp:48-65), same stream as Omega
+  uint64_t tn = (uint64_t)T.normal_base;
+  for (int j = q; j < r; ++j) {
+    for (int attempt = 0; attempt < 1000; ++attempt) {
+      for (int i = lane; i < m; i += 32)
+        s.v[i] = srtt_dev::normal_at(T.state0, T.draw_offset, tn + (uint64_t)i, nullptr);
+      tn += (uint64_t)m;
+      __syncwarp();
+      for (int round = 0; round < 2 && j > 0; ++round) {
+        for (int jj = 0; jj < j; ++jj) {
+          const double* yc = s.Y + (size_t)jj * s.lda;
+          double part = 0.0;
+          for (int i = lane; i < m; i += 32) part += yc[i] * s.v[i];
+          const double d = warp_sum(part);
+          if (lane == 0) s.dots[jj] = d;
+        }
+        __syncwarp();
+        for (int i = lane; i < m; i += 32) {
+          double acc = 0.0;
+          for (int jj = 0; jj < j; ++jj) acc += s.Y[(size_t)jj * s.lda + i] * s.dots[jj];
+          s.v[i] -= acc;
+        }
+        __syncwarp();
+      }
+      double part = 0.0;
+      for (int i = lane; i < m; i += 32) part += s.v[i] * s.v[i];
+      const double nrm = sqrt(warp_sum(part));
+      if (nrm > 1e-8) {
+        for (int i = lane; i < m; i += 32) s.Y[(size_t)j * s.lda + i] = s.v[i] / nrm;
+        __syncwarp();
+        break;
+      }
+      __syncwarp();
+    }
+  }
+  for (int idx = lane; idx < m * r; idx += 32) {
+    const int i = idx % m, col = idx / m;
+    T.u[idx] = s.Y[(size_t)col * s.lda + i];
+  }
 }
 
 }  // namespace
@@ -441,27 +722,42 @@ size_t srtt_basis_level_smem(int mb, int c) {
 
 int srtt_basis_threads() { return kThreads; }
 
-cudaError_t srtt_launch_basis_top(const BasisTarget* d_targets, int ntargets, size_t smem,
+size_t srtt_basis_small_smem(int m, int c, int r) {
+  const int k = m < c ? m : c;
+  const size_t doubles = (size_t)odd_ld(m) * c + (size_t)odd_ld(c) * k + (size_t)odd_ld(k) * k +
+                         (size_t)odd_ld(m) * r + c + k + r + m + 2;
+  return doubles * sizeof(double) + sizeof(int) * (size_t)(k + 2);
+}
+
+cudaError_t srtt_launch_basis_small(const BasisTarget* d_targets, const int* d_list, int n, size_t smem,
+                                    cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  cudaFuncSetAttribute(basis_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  basis_small_kernel<<<n, 32, smem, stream>>>(d_targets, d_list);
+  return cudaGetLastError();
+}
+
+cudaError_t srtt_launch_basis_top(const BasisTarget* d_targets, const int* d_list, int ntargets, size_t smem,
                                   cudaStream_t stream) {
   if (ntargets <= 0) return cudaSuccess;
   cudaFuncSetAttribute(basis_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  basis_top_kernel<<<ntargets, kThreads, smem, stream>>>(d_targets);
+  basis_top_kernel<<<ntargets, kThreads, smem, stream>>>(d_targets, d_list);
   return cudaGetLastError();
 }
 
-cudaError_t srtt_launch_tsqr_factor(const BasisTarget* d_targets, int ntargets, int level, int nctas,
+cudaError_t srtt_launch_tsqr_factor(const BasisTarget* d_targets, const int2* d_map, int level, int nctas,
                                     size_t smem, cudaStream_t stream) {
   if (nctas <= 0) return cudaSuccess;
   cudaFuncSetAttribute(tsqr_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  tsqr_factor_kernel<<<nctas, kThreads, smem, stream>>>(d_targets, ntargets, level);
+  tsqr_factor_kernel<<<nctas, kThreads, smem, stream>>>(d_targets, d_map, level);
   return cudaGetLastError();
 }
 
-cudaError_t srtt_launch_tsqr_apply(const BasisTarget* d_targets, int ntargets, int level, int nctas,
+cudaError_t srtt_launch_tsqr_apply(const BasisTarget* d_targets, const int2* d_map, int level, int nctas,
                                    size_t smem, cudaStream_t stream) {
   if (nctas <= 0) return cudaSuccess;
   cudaFuncSetAttribute(tsqr_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  tsqr_apply_kernel<<<nctas, kThreads, smem, stream>>>(d_targets, ntargets, level);
+  tsqr_apply_kernel<<<nctas, kThreads, smem, stream>>>(d_targets, d_map, level);
   return cudaGetLastError();
 }
 

@@ -38,7 +38,6 @@ using namespace srtt_dev;
 
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
-constexpr int kBoxDoubles = 16 * 16;  // 16 rows x 16 columns, 2 KB
 
 struct Item {
   int rho;
@@ -66,27 +65,27 @@ __device__ __forceinline__ int boxes_of(const CoreParams& P, int rho) {
   return (int)((rows + 15) / 16);
 }
 
-__device__ __forceinline__ void warp_range(const Item& I, int warp, int* lo, int* hi) {
-  const int ntp = (int)((I.c_hi - I.c_lo + 15) / 16);
-  *lo = (ntp * warp) / kWarps;
-  *hi = (ntp * (warp + 1)) / kWarps;
+__device__ __forceinline__ void warp_range(const Item& I, int bc, int warp, int* lo, int* hi) {
+  const int ntg = (int)((I.c_hi - I.c_lo + bc - 1) / bc);
+  *lo = (ntg * warp) / kWarps;
+  *hi = (ntg * (warp + 1)) / kWarps;
 }
 
-// Producer-side walk over this warp's (item, tile pair, box) sequence.
+// Producer-side walk over this warp's (item, tile group, box) sequence.
 struct WarpIter {
   int64_t item;
-  int tp, tp_end, b, nbox, rho;
+  int tg, tg_end, b, nbox, rho;
   int64_t c_lo;
   bool valid;
 
-  __device__ void seek(const CoreParams& P, int warp) {
+  __device__ void seek(const CoreParams& P, int bc, int warp) {
     while (item < P.nitems) {
       const Item I = decode_item(P, item);
       int lo, hi;
-      warp_range(I, warp, &lo, &hi);
+      warp_range(I, bc, warp, &lo, &hi);
       if (lo < hi) {
-        tp = lo;
-        tp_end = hi;
+        tg = lo;
+        tg_end = hi;
         b = 0;
         nbox = boxes_of(P, I.rho);
         rho = I.rho;
@@ -98,12 +97,12 @@ struct WarpIter {
     }
     valid = false;
   }
-  __device__ void next(const CoreParams& P, int warp) {
+  __device__ __forceinline__ void next(const CoreParams& P, int bc, int warp) {
     if (++b < nbox) return;
     b = 0;
-    if (++tp < tp_end) return;
+    if (++tg < tg_end) return;
     item += gridDim.x;
-    seek(P, warp);
+    seek(P, bc, warp);
   }
 };
 
@@ -111,25 +110,30 @@ __device__ __forceinline__ double swz(const double* st, int col, int row) {
   return st[col * 16 + ((((row >> 1) ^ (col & 7)) << 1) | (row & 1))];
 }
 
-template <int MT, int NT1, bool M3>
+// MT: 8-rank tiles of mode 0; NT1: of mode 1; M3: fold depth 3;
+// TPB: 16-column tile pairs per TMA box (box = 16 rows x 16*TPB columns).
+template <int MT, int NT1, bool M3, int TPB>
 __global__ void __launch_bounds__(kThreads, 1)
     core_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CoreParams P) {
+  constexpr int BC = 16 * TPB;
+  constexpr int BOX = 16 * BC;
+  constexpr int KP = MT == 1 ? 2 : 1;  // split-K accumulators for DMMA ILP
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int NS = P.nstages;
   const uintptr_t base = (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023);
   double* rings = reinterpret_cast<double*>(base);
-  double* ufrag = rings + (size_t)kWarps * NS * kBoxDoubles;
+  double* ufrag = rings + (size_t)kWarps * NS * BOX;
   double* slots = ufrag + (size_t)(P.RB / 4) * MT * 32;
   uint64_t* bars = reinterpret_cast<uint64_t*>(slots + (size_t)kWarps * P.A);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
-  double* ring = rings + (size_t)warp * NS * kBoxDoubles;
+  double* ring = rings + (size_t)warp * NS * BOX;
   uint64_t* bar = bars + warp * NS;
   double* slot = slots + (size_t)warp * P.A;
 
   const int r0 = P.r0, r1 = P.frank[0];
-  const int64_t n1 = P.fdim[0];
+  const int n1 = (int)P.fdim[0];
   const double* __restrict__ U1 = P.fu[0];
 
   if (lane == 0) {
@@ -140,18 +144,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   WarpIter pit;
   pit.item = blockIdx.x;
-  pit.seek(P, warp);
+  pit.seek(P, BC, warp);
   if (P.use_tma && lane == 0) {
     prefetch_tmap(&tmap);
     for (int s = 0; s < NS && pit.valid; ++s) {
-      mbar_arrive_expect_tx(&bar[s], kBoxDoubles * sizeof(double));
-      tma_load_2d(ring + s * kBoxDoubles, &tmap, &bar[s], pit.rho * P.RB + 16 * pit.b,
-                  (int32_t)(pit.c_lo + 16 * pit.tp));
-      pit.next(P, warp);
+      mbar_arrive_expect_tx(&bar[s], BOX * sizeof(double));
+      tma_load_2d(ring + s * BOX, &tmap, &bar[s], pit.rho * P.RB + 16 * pit.b, (int32_t)(pit.c_lo + BC * pit.tg));
+      pit.next(P, BC, warp);
     }
   }
 
-  uint32_t consumed = 0;
+  int stage = 0;
+  uint32_t phase = 0;
   int cur_rho = -1;
   for (int64_t item = blockIdx.x; item < P.nitems; item += gridDim.x) {
     const Item I = decode_item(P, item);
@@ -173,7 +177,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int nt = 0; nt < NT1; ++nt) r2[mt][nt][0] = r2[mt][nt][1] = 0.0;
     int64_t cur_g2 = -1;  // level-2 group held in r2 (M3 only)
 
-    // flush r2 (group grp) into the warp-private acc3
     auto flush = [&](int64_t grp) {
       const int r2n = P.frank[1];
       const int64_t i2 = grp % P.fdim[1];
@@ -195,23 +198,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
     };
 
-    int tp_lo, tp_hi;
-    warp_range(I, warp, &tp_lo, &tp_hi);
-    for (int tp = tp_lo; tp < tp_hi; ++tp) {
-      const int64_t c0 = I.c_lo + 16 * tp;
-      double t[2][MT][2];
+    int tg_lo, tg_hi;
+    warp_range(I, BC, warp, &tg_lo, &tg_hi);
+    for (int tg = tg_lo; tg < tg_hi; ++tg) {
+      const int64_t c0 = I.c_lo + (int64_t)BC * tg;
+      double t[TPB][2][MT][KP][2];
 #pragma unroll
-      for (int par = 0; par < 2; ++par)
+      for (int h = 0; h < TPB; ++h)
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) t[par][mt][0] = t[par][mt][1] = 0.0;
-      for (int b = 0; b < nbox; ++b, ++consumed) {
-        const int s = consumed % NS;
-        double* st = ring + s * kBoxDoubles;
+        for (int par = 0; par < 2; ++par)
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int kp = 0; kp < KP; ++kp) t[h][par][mt][kp][0] = t[h][par][mt][kp][1] = 0.0;
+      for (int b = 0; b < nbox; ++b) {
+        double* st = ring + stage * BOX;
         if (P.use_tma) {
-          mbar_wait(&bar[s], (consumed / NS) & 1);
+          mbar_wait(&bar[stage], phase);
         } else {
           const int64_t row0 = (int64_t)I.rho * P.RB + 16 * b;
-          for (int e = lane; e < kBoxDoubles; e += 32) {
+          for (int e = lane; e < BOX; e += 32) {
             const int jj = e >> 4, ii = e & 15;
             const int64_t row = row0 + ii, col = c0 + jj;
             const double v = (row < P.n0 && col < P.Q) ? P.x[col * P.n0 + row] : 0.0;
@@ -223,50 +229,101 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
           const int row = 4 * ks + tq;
-          const double x0 = swz(st, 2 * g, row);      // even columns
-          const double x1 = swz(st, 2 * g + 1, row);  // odd columns
+          double a[MT];
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            const double a = uf[(ks * MT + mt) * 32 + lane];
-            dmma_8x8x4(t[0][mt][0], t[0][mt][1], a, x0);
-            dmma_8x8x4(t[1][mt][0], t[1][mt][1], a, x1);
+          for (int mt = 0; mt < MT; ++mt) a[mt] = uf[(ks * MT + mt) * 32 + lane];
+#pragma unroll
+          for (int h = 0; h < TPB; ++h) {
+            const double x0 = swz(st, 16 * h + 2 * g, row);
+            const double x1 = swz(st, 16 * h + 2 * g + 1, row);
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+              double* d0 = t[h][0][mt][ks % KP];
+              double* d1 = t[h][1][mt][ks % KP];
+              dmma_8x8x4(d0[0], d0[1], a[mt], x0);
+              dmma_8x8x4(d1[0], d1[1], a[mt], x1);
+            }
           }
         }
         __syncwarp();
         if (P.use_tma && lane == 0 && pit.valid) {
-          mbar_arrive_expect_tx(&bar[s], kBoxDoubles * sizeof(double));
-          tma_load_2d(st, &tmap, &bar[s], pit.rho * P.RB + 16 * pit.b, (int32_t)(pit.c_lo + 16 * pit.tp));
-          pit.next(P, warp);
+          mbar_arrive_expect_tx(&bar[stage], BOX * sizeof(double));
+          tma_load_2d(st, &tmap, &bar[stage], pit.rho * P.RB + 16 * pit.b, (int32_t)(pit.c_lo + BC * pit.tg));
+          pit.next(P, BC, warp);
+        }
+        if (++stage == NS) {
+          stage = 0;
+          phase ^= 1;
         }
       }
-      // ---- stage 2: fold mode 1 (thread holds T[g+8mt][col], col = c0 + 4tq + 2s + par)
-      const int64_t clast = min64(c0 + 15, I.c_hi - 1);
-      const int64_t g_first = c0 / n1, g_last = clast / n1;
-      for (int64_t grp = g_first; grp <= g_last; ++grp) {
-        if (M3) {
-          if (cur_g2 >= 0 && grp != cur_g2) flush(cur_g2);
-          cur_g2 = grp;
-        }
-        const int64_t gbase = grp * n1;
+      if (KP == 2) {
 #pragma unroll
-        for (int par = 0; par < 2; ++par)
+        for (int h = 0; h < TPB; ++h)
 #pragma unroll
-          for (int s2 = 0; s2 < 2; ++s2) {
-            const int64_t col = c0 + 4 * tq + 2 * s2 + par;
-            const bool ok = col < I.c_hi && col >= gbase && col < gbase + n1;
-            const double* urow = U1 + (col - gbase) * r1;
-            double bv[NT1];
+          for (int par = 0; par < 2; ++par)
 #pragma unroll
-            for (int nt = 0; nt < NT1; ++nt) {
-              const int a1 = g + 8 * nt;
-              bv[nt] = (ok && a1 < r1) ? __ldg(urow + a1) : 0.0;
+            for (int mt = 0; mt < MT; ++mt) {
+              t[h][par][mt][0][0] += t[h][par][mt][KP - 1][0];
+              t[h][par][mt][0][1] += t[h][par][mt][KP - 1][1];
             }
+      }
+      // ---- stage 2: fold mode 1; thread holds T[g+8mt][col], col = c0h + 4tq + 2s + par
 #pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-              for (int nt = 0; nt < NT1; ++nt)
-                dmma_8x8x4(r2[mt][nt][0], r2[mt][nt][1], t[par][mt][s2], bv[nt]);
+      for (int h = 0; h < TPB; ++h) {
+        const int64_t c0h = c0 + 16 * h;
+        if (c0h >= I.c_hi) break;
+        const int64_t g_first = c0h / n1;
+        const int off0 = (int)(c0h - g_first * n1);
+        const bool fast = (c0h + 16 <= I.c_hi) && (off0 + 16 <= n1);
+        if (fast) {
+          if (M3) {
+            if (cur_g2 >= 0 && g_first != cur_g2) flush(cur_g2);
+            cur_g2 = g_first;
           }
+#pragma unroll
+          for (int par = 0; par < 2; ++par)
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+              const double* urow = U1 + (off0 + 4 * tq + 2 * s2 + par) * r1;
+              double bv[NT1];
+#pragma unroll
+              for (int nt = 0; nt < NT1; ++nt) bv[nt] = (g + 8 * nt < r1) ? __ldg(urow + g + 8 * nt) : 0.0;
+#pragma unroll
+              for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < NT1; ++nt)
+                  dmma_8x8x4(r2[mt][nt][0], r2[mt][nt][1], t[h][par][mt][0][s2], bv[nt]);
+            }
+        } else {
+          const int64_t clast = min64(c0h + 15, I.c_hi - 1);
+          const int64_t g_last = clast / n1;
+          for (int64_t grp = g_first; grp <= g_last; ++grp) {
+            if (M3) {
+              if (cur_g2 >= 0 && grp != cur_g2) flush(cur_g2);
+              cur_g2 = grp;
+            }
+            const int64_t gbase = grp * n1;
+#pragma unroll
+            for (int par = 0; par < 2; ++par)
+#pragma unroll
+              for (int s2 = 0; s2 < 2; ++s2) {
+                const int64_t col = c0h + 4 * tq + 2 * s2 + par;
+                const bool ok = col < I.c_hi && col >= gbase && col < gbase + n1;
+                const double* urow = U1 + (col - gbase) * r1;
+                double bv[NT1];
+#pragma unroll
+                for (int nt = 0; nt < NT1; ++nt) {
+                  const int a1 = g + 8 * nt;
+                  bv[nt] = (ok && a1 < r1) ? __ldg(urow + a1) : 0.0;
+                }
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                  for (int nt = 0; nt < NT1; ++nt)
+                    dmma_8x8x4(r2[mt][nt][0], r2[mt][nt][1], t[h][par][mt][0][s2], bv[nt]);
+              }
+          }
+        }
       }
     }
     // ---- item end: warp partial -> slot, fixed-order CTA reduction
@@ -323,7 +380,9 @@ __global__ void transpose_kernel(const double* __restrict__ u, int64_t n, int r,
 }
 
 // out(gi, b, pi) = sum_i in(gi, i, pi) * coef(i, b), summed over nparts
-// partial inputs in a fixed order.
+// partial inputs in a fixed order. Four independent accumulators keep
+// several loads in flight per thread (the tail is latency-, not
+// bandwidth-bound).
 __global__ void ttm_kernel(const TtmParams T) {
   const int64_t total = T.g * T.rr * T.post;
   for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
@@ -332,31 +391,99 @@ __global__ void ttm_kernel(const TtmParams T) {
     const int64_t rest = o / T.g;
     const int64_t b = rest % T.rr;
     const int64_t pi = rest / T.rr;
-    double s = 0.0;
-    for (int64_t i = 0; i < T.n; ++i) {
-      const int64_t idx = gi + T.g * (i + T.n * pi);
-      double v = T.in[idx];
-      for (int pp = 1; pp < T.nparts; ++pp) v += T.in[idx + pp * T.part_stride];
-      const double cf = T.transpose ? T.u[i + T.n * b] : T.u[b + T.rr * i];
-      s += v * cf;
+    const double* in = T.in + gi + T.g * T.n * pi;
+    const int64_t cs = T.transpose ? 1 : T.rr;  // coef stride along i
+    const double* cf = T.transpose ? T.u + T.n * b : T.u + b;
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    int64_t i = 0;
+    if (T.nparts == 1) {
+      for (; i + 3 < T.n; i += 4) {
+        s0 += in[T.g * i] * cf[cs * i];
+        s1 += in[T.g * (i + 1)] * cf[cs * (i + 1)];
+        s2 += in[T.g * (i + 2)] * cf[cs * (i + 2)];
+        s3 += in[T.g * (i + 3)] * cf[cs * (i + 3)];
+      }
+      for (; i < T.n; ++i) s0 += in[T.g * i] * cf[cs * i];
+    } else {
+      for (; i < T.n; ++i) {
+        const double* pp = in + T.g * i;
+        double v0 = pp[0], v1 = 0, v2 = 0, v3 = 0;
+        int q = 1;
+        for (; q + 2 < T.nparts; q += 3) {
+          v1 += pp[q * T.part_stride];
+          v2 += pp[(q + 1) * T.part_stride];
+          v3 += pp[(q + 2) * T.part_stride];
+        }
+        for (; q < T.nparts; ++q) v1 += pp[q * T.part_stride];
+        s0 += ((v0 + v1) + (v2 + v3)) * cf[cs * i];
+      }
     }
-    T.out[o] = s;
+    T.out[o] = (s0 + s1) + (s2 + s3);
   }
 }
 
-template <int MT, int NT1, bool M3>
+// All factor reformatting of a core pass in one launch: blockIdx.y = 0
+// builds U0's fragments, 1..2 transpose U1, U2 to row-major.
+struct PrepJobs {
+  const double* u0;
+  double* ufrag;
+  int64_t n0;
+  int r0, RB, NT, nrb;
+  const double* u[2];
+  double* ut[2];
+  int64_t n[2];
+  int r[2];
+  int njobs;
+};
+
+__global__ void prep_all_kernel(const PrepJobs J) {
+  if (blockIdx.y == 0) {
+    const int64_t total = (int64_t)J.nrb * J.RB * J.NT * 8;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const int lane = (int)(e % 32);
+      int64_t rest = e / 32;
+      const int nt = (int)(rest % J.NT);
+      rest /= J.NT;
+      const int64_t kstep = rest % (J.RB / 4);
+      const int64_t rho = rest / (J.RB / 4);
+      const int64_t row = rho * J.RB + 4 * kstep + (lane & 3);
+      const int col = 8 * nt + (lane >> 2);
+      J.ufrag[e] = (row < J.n0 && col < J.r0) ? J.u0[row + J.n0 * col] : 0.0;
+    }
+  } else if ((int)blockIdx.y <= J.njobs) {
+    const int j = blockIdx.y - 1;
+    const int64_t n = J.n[j];
+    const int r = J.r[j];
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * r;
+         e += (int64_t)gridDim.x * blockDim.x)
+      J.ut[j][e] = J.u[j][(e / r) + n * (e % r)];
+  }
+}
+
+template <int MT, int NT1, bool M3, int TPB>
 cudaError_t launch_t(const CUtensorMap* tmap, const CoreParams& P, int grid, size_t smem, cudaStream_t s) {
-  cudaError_t e =
-      cudaFuncSetAttribute(core_kernel<MT, NT1, M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(core_kernel<MT, NT1, M3, TPB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  core_kernel<MT, NT1, M3><<<grid, kThreads, smem, s>>>(*tmap, P);
+  core_kernel<MT, NT1, M3, TPB><<<grid, kThreads, smem, s>>>(*tmap, P);
   return cudaGetLastError();
+}
+
+template <int MT, int NT1, bool M3>
+cudaError_t launch_b(const CUtensorMap* tmap, const CoreParams& P, int grid, size_t smem, cudaStream_t s) {
+  switch (P.tpb) {
+    case 1: return launch_t<MT, NT1, M3, 1>(tmap, P, grid, smem, s);
+    case 2: return launch_t<MT, NT1, M3, 2>(tmap, P, grid, smem, s);
+    case 4: return launch_t<MT, NT1, M3, 4>(tmap, P, grid, smem, s);
+  }
+  return cudaErrorInvalidValue;
 }
 
 template <int MT, int NT1>
 cudaError_t launch_m(const CUtensorMap* tmap, const CoreParams& P, int grid, size_t smem, cudaStream_t s) {
-  return P.m == 3 ? launch_t<MT, NT1, true>(tmap, P, grid, smem, s)
-                  : launch_t<MT, NT1, false>(tmap, P, grid, smem, s);
+  return P.m == 3 ? launch_b<MT, NT1, true>(tmap, P, grid, smem, s)
+                  : launch_b<MT, NT1, false>(tmap, P, grid, smem, s);
 }
 
 template <int MT>
@@ -375,7 +502,7 @@ int srtt_core_threads() { return kThreads; }
 
 // Shared memory of the core kernel for a given stage count.
 size_t srtt_core_smem_bytes(const CoreParams& P) {
-  const size_t doubles = (size_t)kWarps * P.nstages * kBoxDoubles + (size_t)(P.RB / 4) * P.NT * 32 +
+  const size_t doubles = (size_t)kWarps * P.nstages * 256 * P.tpb + (size_t)(P.RB / 4) * P.NT * 32 +
                          (size_t)kWarps * P.A;
   return 1024 + doubles * sizeof(double) + (size_t)kWarps * P.nstages * sizeof(uint64_t);
 }
@@ -405,6 +532,30 @@ cudaError_t srtt_launch_core(const CUtensorMap* tmap, const CoreParams& P, int g
 cudaError_t srtt_launch_prep(const double* u0, int64_t n0, int r0, int RB, int NT, int nrb, double* ufrag,
                              cudaStream_t s) {
   prep_kernel<<<64, 256, 0, s>>>(u0, n0, r0, RB, NT, nrb, ufrag);
+  return cudaGetLastError();
+}
+
+cudaError_t srtt_launch_prep_all(const double* u0, int64_t n0, int r0, int RB, int NT, int nrb, double* ufrag,
+                                 int njobs, const double* const* u, double* const* ut, const int64_t* n,
+                                 const int* r, cudaStream_t s) {
+  PrepJobs J{};
+  J.u0 = u0;
+  J.ufrag = ufrag;
+  J.n0 = n0;
+  J.r0 = r0;
+  J.RB = RB;
+  J.NT = NT;
+  J.nrb = nrb;
+  J.njobs = njobs;
+  for (int j = 0; j < njobs; ++j) {
+    J.u[j] = u[j];
+    J.ut[j] = ut[j];
+    J.n[j] = n[j];
+    J.r[j] = r[j];
+  }
+  const int64_t total = (int64_t)nrb * RB * NT * 8;
+  const int bx = (int)min64(256, (total + 255) / 256);
+  prep_all_kernel<<<dim3(bx > 0 ? bx : 1, 1 + njobs), 256, 0, s>>>(J);
   return cudaGetLastError();
 }
 

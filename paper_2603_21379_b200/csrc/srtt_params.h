@@ -98,6 +98,7 @@ typedef struct CoreParams {
   int32_t A;               // prod_{k<m} r_k (output entries per item)
   int32_t use_tma;         // 1: cp.async.bulk.tensor loads; 0: warp-copy path (odd n0)
   int32_t nstages;         // per-warp TMA ring depth
+  int32_t tpb;             // 16-column tile pairs per TMA box (1, 2 or 4)
 } CoreParams;
 
 // Generic small TTM used by the tail of the core pass and by reconstruct:

@@ -365,6 +365,7 @@ def _report_from(crep, n, ach, samp, report, handle):
     report.timings = {name: float(crep.stage_seconds[i]) for i, name in enumerate(STAGES)}
     report.flags = int(crep.flags)
     report.launches = int(crep.launches)
+    report.jacobi_sweeps = int(crep.reserved)
     report.kernel_seconds = {"sketch": float(crep.kernel_seconds[0]), "basis": float(crep.kernel_seconds[1]),
                              "core": float(crep.kernel_seconds[2]), "transfer": float(crep.kernel_seconds[3])}
 
