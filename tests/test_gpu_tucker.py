@@ -1,0 +1,117 @@
+"""Sub-R-HOSVD on the B200 vs the CPU oracle and the reference's own
+property tests (test_tucker.cpp), through the C-ABI."""
+import numpy as np
+import pytest
+
+import paper_2603_21379_b200 as P
+import srtt_oracle as O
+from parity import aligned_core_error, projector_gap, tucker_rel_error
+from planted import planted_tucker, random_tensor
+
+pytestmark = pytest.mark.gpu
+
+
+def median(v):
+    return sorted(v)[len(v) // 2]
+
+
+@pytest.mark.parametrize("dims,r,p,s,seed", [((15,) * 4, 5, 4, 75, 0), ((128, 128, 128), 8, 5, 52, 0),
+                                             ((40,) * 4, 6, 5, 44, 3), ((20, 30, 25), 4, 4, 30, 11),
+                                             ((9, 9, 9), 4, 5, 81, 21)])
+def test_matches_oracle(handle, dims, r, p, s, seed):
+    x, _, _ = planted_tucker(dims, (r,) * len(dims), 9)
+    x = x + 1e-9 * np.random.default_rng(1).standard_normal(x.shape)
+    rep = P.SubsampleReport()
+    t = P.sub_r_hosvd(x, [r] * len(dims), p, [s] * len(dims), seed, report=rep, handle=handle)
+    orep = O.SubsampleReport()
+    to = O.sub_r_hosvd(x, [r] * len(dims), p, [s] * len(dims), seed, report=orep)
+    assert rep.achieved_ranks == orep.achieved_ranks
+    assert rep.sample_counts == [s] * len(dims)
+    for ug, uc in zip(t.factors, to.factors):
+        assert projector_gap(ug, uc) <= 1e-10
+        assert O.orthonormality_defect(ug) <= 1e-12
+    assert aligned_core_error(t.core, t.factors, to.core, to.factors) <= 1e-10
+    eg, ec = tucker_rel_error(x, t.core, t.factors), O.rel_error(x, O.reconstruct(to))
+    assert abs(eg - ec) <= 1e-10 * max(ec, 1.0)
+
+
+def test_recovers_planted_from_few_fibers(handle):
+    """test_tucker.cpp:105-118."""
+    x, _, _ = planted_tucker((15,) * 4, (5,) * 4, 9)
+    errs = []
+    for seed in range(9):
+        rep = P.SubsampleReport()
+        t = P.sub_r_hosvd(x, [5] * 4, 4, [75] * 4, seed, report=rep, handle=handle)
+        assert rep.achieved_ranks == [5] * 4
+        errs.append(tucker_rel_error(x, t.core, t.factors))
+    assert median(errs) <= 1e-8
+
+
+def test_validation_messages_match_reference(handle):
+    """test_tucker.cpp:130-136 (tucker.hpp:184-197 order and wording)."""
+    x = random_tensor((6, 6, 6), 77)
+    with pytest.raises(P.InvalidArgument, match="samples below rank \\+ oversampling in mode 0"):
+        P.sub_r_hosvd(x, [2] * 3, 4, [5] * 3, 1, handle=handle)
+    with pytest.raises(P.InvalidArgument, match="more samples than fibers in mode 0"):
+        P.sub_r_hosvd(x, [2] * 3, 4, [37] * 3, 1, handle=handle)
+    with pytest.raises(P.InvalidArgument, match="rank out of range in mode 1"):
+        P.sub_r_hosvd(x, [2, 7, 2], 4, [30] * 3, 1, handle=handle)
+    with pytest.raises(P.JobError) as e:  # partitioned sampling failure inside mode job 0
+        P.sub_r_hosvd(x, [2] * 3, 4, [7] * 3, 1, P.ExecPolicy(index_partitions=8), handle=handle)
+    assert e.value.job == 0
+
+
+def test_deterministic_in_the_seed(handle):
+    """test_tucker.cpp:138-163: bitwise identical reruns; partitioned too."""
+    x, _, _ = planted_tucker((10, 10, 10), (3,) * 3, 15)
+    a = P.sub_r_hosvd(x, [3] * 3, 4, [20] * 3, 42, handle=handle)
+    b = P.sub_r_hosvd(x, [3] * 3, 4, [20] * 3, 42, handle=handle)
+    assert all(np.array_equal(u, v) for u, v in zip(a.factors, b.factors)) and np.array_equal(a.core, b.core)
+    pa = P.sub_r_hosvd(x, [3] * 3, 4, [21] * 3, 5, P.ExecPolicy(workers=1, index_partitions=3), handle=handle)
+    pb = P.sub_r_hosvd(x, [3] * 3, 4, [21] * 3, 5, P.ExecPolicy(workers=3, index_partitions=3), handle=handle)
+    assert all(np.array_equal(u, v) for u, v in zip(pa.factors, pb.factors))
+    assert tucker_rel_error(x, pa.core, pa.factors) <= 1e-9
+    po = O.sub_r_hosvd(x, [3] * 3, 4, [21] * 3, 5, O.ExecPolicy(workers=1, index_partitions=3))
+    assert max(projector_gap(u, v) for u, v in zip(pa.factors, po.factors)) <= 1e-10
+
+
+def test_pads_when_rank_exceeds_data_rank(handle):
+    """test_tucker.cpp:165-177, with the padded columns equal to the oracle's."""
+    x, _, _ = planted_tucker((8, 8, 8), (2, 2, 2), 19)
+    rep = P.SubsampleReport()
+    t = P.sub_r_hosvd(x, [4] * 3, 4, [30] * 3, 5, report=rep, handle=handle)
+    assert rep.achieved_ranks == [2, 2, 2] and len(rep.warnings) == 3
+    assert "sketch revealed rank 2 < target 4; basis padded" in rep.warnings[0]
+    assert max(O.orthonormality_defect(u) for u in t.factors) <= 1e-10
+    assert tucker_rel_error(x, t.core, t.factors) <= 1e-9
+    to = O.sub_r_hosvd(x, [4] * 3, 4, [30] * 3, 5)
+    assert max(projector_gap(u, v) for u, v in zip(t.factors, to.factors)) <= 1e-10
+
+
+def test_projection_identity(handle):
+    """test_tucker.cpp:179-198."""
+    x = random_tensor((8, 8, 8), 83)
+    t = P.sub_r_hosvd(x, [3, 4, 5], 2, [30] * 3, 3, handle=handle)
+    via_core = tucker_rel_error(x, t.core, t.factors)
+    via_proj = O.rel_error(x, O.multi_ttm(x, [(k, u @ u.T) for k, u in enumerate(t.factors)]))
+    assert via_core == pytest.approx(via_proj, rel=1e-12)
+
+
+def test_low_oversampling_warning_and_order1(handle):
+    x = random_tensor((30,), 3)
+    rep = P.SubsampleReport()
+    t = P.sub_r_hosvd(x, [1], 0, [1], 3, report=rep, handle=handle)
+    assert rep.warnings[0] == "oversampling below the recommended minimum of 4"
+    to = O.sub_r_hosvd(x, [1], 0, [1], 3)
+    assert np.allclose(np.abs(t.factors[0]), np.abs(to.factors[0]), atol=1e-14)
+
+
+def test_device_resident_inputs_and_outputs(handle):
+    torch = pytest.importorskip("torch")
+    x, _, _ = planted_tucker((20, 20, 20), (3,) * 3, 4)
+    xd = torch.from_numpy(np.ravel(x, order="F").copy()).cuda()
+    td = P.sub_r_hosvd(xd, [3] * 3, 4, [28] * 3, 1, dims=[20, 20, 20], handle=handle, device_out=True)
+    th = P.sub_r_hosvd(x, [3] * 3, 4, [28] * 3, 1, handle=handle)
+    assert np.array_equal(td.core.cpu().numpy(), np.ravel(th.core, order="F"))
+    for k in range(3):
+        assert np.array_equal(td.factors[k].cpu().numpy(), np.ravel(th.factors[k], order="F"))
