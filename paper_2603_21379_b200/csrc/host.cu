@@ -40,8 +40,8 @@ int srtt_core_max_stages(const CoreParams& P, size_t budget);
 cudaError_t srtt_launch_core(const CUtensorMap*, const CoreParams&, int, cudaStream_t);
 cudaError_t srtt_launch_prep(const double*, int64_t, int, int, int, int, double*, cudaStream_t);
 cudaError_t srtt_launch_transpose(const double*, int64_t, int, double*, cudaStream_t);
-cudaError_t srtt_launch_prep_all(const double*, int64_t, int, int, int, int, double*, int, const double* const*,
-                                 double* const*, const int64_t*, const int*, cudaStream_t);
+cudaError_t srtt_launch_prep_all(const CoreParams&, CoreItem*, const double*, int64_t, int, int, int, int, double*,
+                                 int, const double* const*, double* const*, const int64_t*, const int*, cudaStream_t);
 cudaError_t srtt_launch_ttm(const TtmParams&, cudaStream_t);
 
 typedef struct TransferTarget {
@@ -253,6 +253,7 @@ struct Blob {
 
 // ---- basis (K2) planning ------------------------------------------------------
 constexpr size_t kSmemBudget = 200 * 1024;
+constexpr size_t kCoreSmem = 232448 - 256;  // opt-in max dynamic smem per block on sm_100
 
 int top_max_rows(int c, int r) {
   int lo = 1, hi = 1 << 20;
@@ -451,6 +452,7 @@ struct CorePlan {
   std::vector<int64_t> ranks;
   int64_t part_doubles = 0;
   size_t ufrag_doubles = 0;
+  size_t off_items = 0;
 };
 
 int pad_tiles(int64_t r) { return r <= 8 ? 1 : (r <= 16 ? 2 : (r <= 32 ? 4 : 0)); }
@@ -478,7 +480,7 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
   P.frank[0] = (int)ranks[1];
 
   struct Cand {
-    int m = 0, S = 0, ns = 0, tpb = 1;
+    int m = 0, S = 0, ns = 0, tpb = 1, warps = 8;
     int64_t SL = 0, G = 0, GS = 0, items = 0;
     int A = 0;
     double cost = 1e300;
@@ -489,15 +491,30 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
     CoreParams T = P;
     T.m = m;
     T.A = (int)(ranks[0] * ranks[1] * (m == 3 ? ranks[2] : 1));
-    // widest box that still leaves a ring of >= 4 boxes per warp
+    // 16 warps when the rank tiles are small (register budget 128/thread);
+    // widest box that still leaves a ring of >= 3 boxes per warp
+    T.warps = (P.NT * P.NT1 <= 4) ? 16 : 8;
     int tpb = 0, ns = 0;
-    for (int tb : {4, 2, 1}) {
+    for (int tb : {2, 1}) {
+      if (tb == 2 && (P.NT > 2 || P.NT1 > 2)) continue;
       T.tpb = tb;
-      const int n = srtt_core_max_stages(T, kSmemBudget + 20 * 1024);
-      if (n >= 4 || (tb == 1 && n >= 2)) {
+      const int n = srtt_core_max_stages(T, kCoreSmem);
+      if (n >= 3 || (tb == 1 && n >= 2)) {
         tpb = tb;
         ns = n;
         break;
+      }
+    }
+    if (!tpb && T.warps == 16) {  // fall back to 8 warps
+      T.warps = 8;
+      for (int tb : {2, 1}) {
+        T.tpb = tb;
+        const int n = srtt_core_max_stages(T, kCoreSmem);
+        if (n >= 3 || (tb == 1 && n >= 2)) {
+          tpb = tb;
+          ns = n;
+          break;
+        }
       }
     }
     if (!tpb) continue;
@@ -513,8 +530,9 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
       const int64_t ntg = SL / bc;
       const int64_t grid = std::min<int64_t>(items, sms);
       const int64_t rounds = (items + grid - 1) / grid;
-      const double item_units = (double)((ntg + 7) / 8) * tpb + 0.5;  // +0.5: item-end barrier/reduction
-      const double stream = (double)rounds * grid * 8.0 * item_units * tp_bytes;
+      const int W = T.warps;
+      const double item_units = (double)((ntg + W - 1) / W) * tpb + 0.5;  // +0.5: item-end barrier/reduction
+      const double stream = (double)rounds * grid * W * item_units * tp_bytes;
       const double out = 2.0 * (double)items * T.A * 8.0;
       const double cost = stream + out;
       if (cost < best.cost) {
@@ -522,6 +540,7 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
         best.S = (int)Se;
         best.ns = ns;
         best.tpb = tpb;
+        best.warps = T.warps;
         best.SL = SL;
         best.G = G;
         best.GS = GS;
@@ -542,6 +561,7 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
   P.A = best.A;
   P.nstages = best.ns;
   P.tpb = best.tpb;
+  P.warps = best.warps;
   if (best.m == 3) {
     P.fdim[1] = dims[2];
     P.frank[1] = (int)ranks[2];
@@ -556,6 +576,7 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
 int launch_core_pass(srtt_handle* h, CorePlan& cp, const double* x, const std::vector<const double*>& u,
                      double* out, char* ws, size_t off_ufrag, const std::vector<size_t>& off_fu,
                      size_t off_part, size_t off_tmp0, size_t off_tmp1) {
+  const size_t off_items = cp.off_items;
   int launches = 0;
   CoreParams& P = cp.P;
   const int d = (int)cp.dims.size();
@@ -574,8 +595,10 @@ int launch_core_pass(srtt_handle* h, CorePlan& cp, const double* x, const std::v
       rs[k - 1] = (int)cp.ranks[k];
       P.fu[k - 1] = uts[k - 1];
     }
-    CK(srtt_launch_prep_all(u[0], P.n0, P.r0, P.RB, P.NT, P.nrb, const_cast<double*>(P.ufrag), P.m - 1, us, uts,
-                            ns, rs, h->stream));
+    CoreItem* items = reinterpret_cast<CoreItem*>(ws + off_items);
+    P.items = items;
+    CK(srtt_launch_prep_all(P, items, u[0], P.n0, P.r0, P.RB, P.NT, P.nrb, const_cast<double*>(P.ufrag), P.m - 1,
+                            us, uts, ns, rs, h->stream));
     ++launches;
   }
   if (P.m == 2) P.fu[1] = nullptr;
@@ -631,9 +654,10 @@ int launch_core_pass(srtt_handle* h, CorePlan& cp, const double* x, const std::v
 }
 
 // Workspace needs of the core pass.
-void layout_core(Layout& L, const CorePlan& cp, size_t& off_ufrag, std::vector<size_t>& off_fu,
+void layout_core(Layout& L, CorePlan& cp, size_t& off_ufrag, std::vector<size_t>& off_fu,
                  size_t& off_part, size_t& off_tmp0, size_t& off_tmp1) {
   const int d = (int)cp.dims.size();
+  cp.off_items = L.take(sizeof(CoreItem) * (size_t)cp.P.nitems);
   off_ufrag = L.take(sizeof(double) * cp.ufrag_doubles);
   off_fu.assign(d, 0);
   for (int k = 1; k < cp.P.m; ++k) off_fu[k] = L.take(sizeof(double) * cp.dims[k] * cp.ranks[k]);

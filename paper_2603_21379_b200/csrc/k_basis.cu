@@ -110,18 +110,6 @@ __device__ void apply_q_warp(const double* A, int m, int k, int lda, const doubl
   }
 }
 
-// Circle-method round-robin: round `rd` of kk-1 rounds, pair `pr` of kk/2.
-__device__ __forceinline__ void rr_pair(int pr, int rd, int kk, int* p, int* q) {
-  const int np = kk - 1;
-  if (pr == 0) {
-    *p = rd % np;
-    *q = kk - 1;
-  } else {
-    *p = (rd + pr) % np;
-    *q = (rd - pr + np) % np;
-  }
-}
-
 
 // Stage a target descriptor into shared memory (one cooperative copy)
 // so the kernels never re-read its fields from global memory.

@@ -36,42 +36,21 @@ namespace {
 
 using namespace srtt_dev;
 
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
-
-struct Item {
-  int rho;
-  int sigma;
-  int64_t p;
-  int64_t c_lo, c_hi;
-};
-
-// rho-major ordering: consecutive items of a CTA (stride gridDim) share the
-// row block, so U0's fragments are reloaded rarely.
-__device__ __forceinline__ Item decode_item(const CoreParams& P, int64_t it) {
-  Item I;
-  const int64_t per_rho = P.G * P.S;
-  I.rho = (int)(it / per_rho);
-  const int64_t rest = it - (int64_t)I.rho * per_rho;
-  I.p = rest / P.S;
-  I.sigma = (int)(rest - I.p * P.S);
-  I.c_lo = I.p * P.GS + (int64_t)I.sigma * P.SL;
-  I.c_hi = min64(I.c_lo + P.SL, (I.p + 1) * P.GS);
-  return I;
-}
 
 __device__ __forceinline__ int boxes_of(const CoreParams& P, int rho) {
   const int64_t rows = min64(P.RB, P.n0 - (int64_t)rho * P.RB);
   return (int)((rows + 15) / 16);
 }
 
-__device__ __forceinline__ void warp_range(const Item& I, int bc, int warp, int* lo, int* hi) {
-  const int ntg = (int)((I.c_hi - I.c_lo + bc - 1) / bc);
-  *lo = (ntg * warp) / kWarps;
-  *hi = (ntg * (warp + 1)) / kWarps;
+template <int WARPS>
+__device__ __forceinline__ void warp_range(int len, int bc, int warp, int* lo, int* hi) {
+  const int ntg = (len + bc - 1) / bc;
+  *lo = (ntg * warp) / WARPS;
+  *hi = (ntg * (warp + 1)) / WARPS;
 }
 
 // Producer-side walk over this warp's (item, tile group, box) sequence.
+template <int WARPS>
 struct WarpIter {
   int64_t item;
   int tg, tg_end, b, nbox, rho;
@@ -80,9 +59,9 @@ struct WarpIter {
 
   __device__ void seek(const CoreParams& P, int bc, int warp) {
     while (item < P.nitems) {
-      const Item I = decode_item(P, item);
+      const CoreItem I = P.items[item];
       int lo, hi;
-      warp_range(I, bc, warp, &lo, &hi);
+      warp_range<WARPS>(I.len, bc, warp, &lo, &hi);
       if (lo < hi) {
         tg = lo;
         tg_end = hi;
@@ -106,25 +85,25 @@ struct WarpIter {
   }
 };
 
-__device__ __forceinline__ double swz(const double* st, int col, int row) {
-  return st[col * 16 + ((((row >> 1) ^ (col & 7)) << 1) | (row & 1))];
-}
-
 // MT: 8-rank tiles of mode 0; NT1: of mode 1; M3: fold depth 3;
-// TPB: 16-column tile pairs per TMA box (box = 16 rows x 16*TPB columns).
-template <int MT, int NT1, bool M3, int TPB>
-__global__ void __launch_bounds__(kThreads, 1)
+// TPB: 16-column tile pairs per TMA box (box = 16 rows x 16*TPB columns);
+// WARPS: warps per CTA (each its own producer/consumer).
+template <int MT, int NT1, bool M3, int TPB, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1)
     core_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CoreParams P) {
   constexpr int BC = 16 * TPB;
   constexpr int BOX = 16 * BC;
   constexpr int KP = MT == 1 ? 2 : 1;  // split-K accumulators for DMMA ILP
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int NS = P.nstages;
-  const uintptr_t base = (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023);
-  double* rings = reinterpret_cast<double*>(base);
-  double* ufrag = rings + (size_t)kWarps * NS * BOX;
+  // 1024-byte alignment for the 128B swizzle, computed on the shared-window
+  // address so every pointer below stays in the shared state space (LDS/STS,
+  // not generic LD/ST).
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  double* rings = reinterpret_cast<double*>(smem_raw + pad);
+  double* ufrag = rings + (size_t)WARPS * NS * BOX;
   double* slots = ufrag + (size_t)(P.RB / 4) * MT * 32;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + (size_t)kWarps * P.A);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + (size_t)WARPS * P.A);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
@@ -136,13 +115,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n1 = (int)P.fdim[0];
   const double* __restrict__ U1 = P.fu[0];
 
+  // per-lane swizzled offsets of the B fragments: column 2g+par, row 4ks+tq
+  int boff[2][4];
+#pragma unroll
+  for (int par = 0; par < 2; ++par)
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int col = 2 * g + par, row = 4 * ks + tq;
+      boff[par][ks] = col * 16 + ((((row >> 1) ^ (col & 7)) << 1) | (row & 1));
+    }
+
   if (lane == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
 
-  WarpIter pit;
+  WarpIter<WARPS> pit;
   pit.item = blockIdx.x;
   pit.seek(P, BC, warp);
   if (P.use_tma && lane == 0) {
@@ -158,15 +147,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t phase = 0;
   int cur_rho = -1;
   for (int64_t item = blockIdx.x; item < P.nitems; item += gridDim.x) {
-    const Item I = decode_item(P, item);
+    const CoreItem I = P.items[item];
     if (I.rho != cur_rho) {
       __syncthreads();
       const double* src = P.ufrag + (size_t)I.rho * (P.RB / 4) * MT * 32;
-      for (int e = threadIdx.x; e < (P.RB / 4) * MT * 32; e += kThreads) ufrag[e] = src[e];
+      for (int e = threadIdx.x; e < (P.RB / 4) * MT * 32; e += WARPS * 32) ufrag[e] = src[e];
       cur_rho = I.rho;
       __syncthreads();
     }
     const int nbox = boxes_of(P, I.rho);
+    const int len = I.len;
     if (M3)
       for (int e = lane; e < P.A; e += 32) slot[e] = 0.0;
     __syncwarp();
@@ -199,7 +189,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
 
     int tg_lo, tg_hi;
-    warp_range(I, BC, warp, &tg_lo, &tg_hi);
+    warp_range<WARPS>(len, BC, warp, &tg_lo, &tg_hi);
+    // level-2 group tracking of this warp's first column (32-bit)
+    int64_t grp = I.grp0;
+    int off = I.off0 + BC * tg_lo;
+    if (off >= n1) {
+      grp += off / n1;
+      off %= n1;
+    }
     for (int tg = tg_lo; tg < tg_hi; ++tg) {
       const int64_t c0 = I.c_lo + (int64_t)BC * tg;
       double t[TPB][2][MT][KP][2];
@@ -211,7 +208,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
             for (int kp = 0; kp < KP; ++kp) t[h][par][mt][kp][0] = t[h][par][mt][kp][1] = 0.0;
-      for (int b = 0; b < nbox; ++b) {
+      const double* uf = ufrag + lane;
+      for (int b = 0; b < nbox; ++b, uf += 4 * MT * 32) {
         double* st = ring + stage * BOX;
         if (P.use_tma) {
           mbar_wait(&bar[stage], phase);
@@ -225,17 +223,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           __syncwarp();
         }
-        const double* uf = ufrag + (size_t)b * 4 * MT * 32;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
-          const int row = 4 * ks + tq;
           double a[MT];
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) a[mt] = uf[(ks * MT + mt) * 32 + lane];
+          for (int mt = 0; mt < MT; ++mt) a[mt] = uf[(ks * MT + mt) * 32];
 #pragma unroll
           for (int h = 0; h < TPB; ++h) {
-            const double x0 = swz(st, 16 * h + 2 * g, row);
-            const double x1 = swz(st, 16 * h + 2 * g + 1, row);
+            const double x0 = st[h * 256 + boff[0][ks]];
+            const double x1 = st[h * 256 + boff[1][ks]];
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
               double* d0 = t[h][0][mt][ks % KP];
@@ -270,24 +266,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---- stage 2: fold mode 1; thread holds T[g+8mt][col], col = c0h + 4tq + 2s + par
 #pragma unroll
       for (int h = 0; h < TPB; ++h) {
-        const int64_t c0h = c0 + 16 * h;
-        if (c0h >= I.c_hi) break;
-        const int64_t g_first = c0h / n1;
-        const int off0 = (int)(c0h - g_first * n1);
-        const bool fast = (c0h + 16 <= I.c_hi) && (off0 + 16 <= n1);
-        if (fast) {
+        const int rel = BC * tg + 16 * h;  // column offset inside the item
+        if (rel >= len) break;
+        if (off + 16 <= n1 && rel + 16 <= len) {
           if (M3) {
-            if (cur_g2 >= 0 && g_first != cur_g2) flush(cur_g2);
-            cur_g2 = g_first;
+            if (cur_g2 >= 0 && grp != cur_g2) flush(cur_g2);
+            cur_g2 = grp;
           }
+          const double* urow = U1 + (off + 4 * tq) * r1 + g;
 #pragma unroll
           for (int par = 0; par < 2; ++par)
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
-              const double* urow = U1 + (off0 + 4 * tq + 2 * s2 + par) * r1;
               double bv[NT1];
 #pragma unroll
-              for (int nt = 0; nt < NT1; ++nt) bv[nt] = (g + 8 * nt < r1) ? __ldg(urow + g + 8 * nt) : 0.0;
+              for (int nt = 0; nt < NT1; ++nt)
+                bv[nt] = (g + 8 * nt < r1) ? __ldg(urow + (2 * s2 + par) * r1 + 8 * nt) : 0.0;
 #pragma unroll
               for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -295,34 +289,46 @@ __global__ void __launch_bounds__(kThreads, 1)
                   dmma_8x8x4(r2[mt][nt][0], r2[mt][nt][1], t[h][par][mt][0][s2], bv[nt]);
             }
         } else {
-          const int64_t clast = min64(c0h + 15, I.c_hi - 1);
-          const int64_t g_last = clast / n1;
-          for (int64_t grp = g_first; grp <= g_last; ++grp) {
+          // straddles a level-2 group boundary or the item end: per group
+          // segment [lo, hi) of the 16 columns, mask the others in B
+          int64_t gg = grp;
+          int oo = off;
+          const int lim = min(16, len - rel);
+          for (int lo = 0; lo < lim;) {
+            const int hi = min(lim, lo + n1 - oo);
             if (M3) {
-              if (cur_g2 >= 0 && grp != cur_g2) flush(cur_g2);
-              cur_g2 = grp;
+              if (cur_g2 >= 0 && gg != cur_g2) flush(cur_g2);
+              cur_g2 = gg;
             }
-            const int64_t gbase = grp * n1;
+            const double* ubase = U1 + (oo - lo) * r1 + g;
 #pragma unroll
             for (int par = 0; par < 2; ++par)
 #pragma unroll
               for (int s2 = 0; s2 < 2; ++s2) {
-                const int64_t col = c0h + 4 * tq + 2 * s2 + par;
-                const bool ok = col < I.c_hi && col >= gbase && col < gbase + n1;
-                const double* urow = U1 + (col - gbase) * r1;
+                const int j = 4 * tq + 2 * s2 + par;
+                const bool ok = j >= lo && j < hi;
                 double bv[NT1];
 #pragma unroll
-                for (int nt = 0; nt < NT1; ++nt) {
-                  const int a1 = g + 8 * nt;
-                  bv[nt] = (ok && a1 < r1) ? __ldg(urow + a1) : 0.0;
-                }
+                for (int nt = 0; nt < NT1; ++nt)
+                  bv[nt] = (ok && g + 8 * nt < r1) ? __ldg(ubase + j * r1 + 8 * nt) : 0.0;
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
                   for (int nt = 0; nt < NT1; ++nt)
                     dmma_8x8x4(r2[mt][nt][0], r2[mt][nt][1], t[h][par][mt][0][s2], bv[nt]);
               }
+            oo += hi - lo;
+            lo = hi;
+            if (oo >= n1) {
+              oo -= n1;
+              ++gg;
+            }
           }
+        }
+        off += 16;
+        while (off >= n1) {
+          off -= n1;
+          ++grp;
         }
       }
     }
@@ -341,11 +347,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
     }
     __syncthreads();
-    double* out = P.part + (((int64_t)I.rho * P.S + I.sigma) * P.G + I.p) * P.A;
-    for (int e = threadIdx.x; e < P.A; e += kThreads) {
+    double* out = P.part + I.out_off;
+    for (int e = threadIdx.x; e < P.A; e += WARPS * 32) {
       double sum = 0.0;
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) sum += slots[(size_t)w * P.A + e];
+      for (int w = 0; w < WARPS; ++w) sum += slots[(size_t)w * P.A + e];
       out[e] = sum;
     }
     __syncthreads();
@@ -425,6 +431,9 @@ __global__ void ttm_kernel(const TtmParams T) {
 // All factor reformatting of a core pass in one launch: blockIdx.y = 0
 // builds U0's fragments, 1..2 transpose U1, U2 to row-major.
 struct PrepJobs {
+  CoreItem* items;
+  int64_t nitems, G, GS, SL, n1;
+  int S, A;
   const double* u0;
   double* ufrag;
   int64_t n0;
@@ -437,7 +446,27 @@ struct PrepJobs {
 };
 
 __global__ void prep_all_kernel(const PrepJobs J) {
-  if (blockIdx.y == 0) {
+  if ((int)blockIdx.y == J.njobs + 1) {
+    // item table, rho-major: consecutive items of a CTA share the row block
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < J.nitems;
+         it += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t per_rho = J.G * J.S;
+      const int rho = (int)(it / per_rho);
+      const int64_t rest = it - (int64_t)rho * per_rho;
+      const int64_t p = rest / J.S;
+      const int sigma = (int)(rest - p * J.S);
+      CoreItem I;
+      I.c_lo = p * J.GS + (int64_t)sigma * J.SL;
+      const int64_t c_hi = min64(I.c_lo + J.SL, (p + 1) * J.GS);
+      I.len = (int)(c_hi - I.c_lo);
+      I.rho = rho;
+      I.out_off = (((int64_t)rho * J.S + sigma) * J.G + p) * J.A;
+      I.grp0 = I.c_lo / J.n1;
+      I.off0 = (int)(I.c_lo - I.grp0 * J.n1);
+      I.pad = 0;
+      J.items[it] = I;
+    }
+  } else if (blockIdx.y == 0) {
     const int64_t total = (int64_t)J.nrb * J.RB * J.NT * 8;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
@@ -461,21 +490,26 @@ __global__ void prep_all_kernel(const PrepJobs J) {
   }
 }
 
-template <int MT, int NT1, bool M3, int TPB>
-cudaError_t launch_t(const CUtensorMap* tmap, const CoreParams& P, int grid, size_t smem, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(core_kernel<MT, NT1, M3, TPB>,
+template <int MT, int NT1, bool M3, int TPB, int WARPS>
+cudaError_t launch_w(const CUtensorMap* tmap, const CoreParams& P, int grid, size_t smem, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(core_kernel<MT, NT1, M3, TPB, WARPS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  core_kernel<MT, NT1, M3, TPB><<<grid, kThreads, smem, s>>>(*tmap, P);
+  core_kernel<MT, NT1, M3, TPB, WARPS><<<grid, WARPS * 32, smem, s>>>(*tmap, P);
   return cudaGetLastError();
+}
+
+template <int MT, int NT1, bool M3, int TPB>
+cudaError_t launch_t(const CUtensorMap* tmap, const CoreParams& P, int grid, size_t smem, cudaStream_t s) {
+  if (MT * NT1 <= 4 && P.warps == 16) return launch_w<MT, NT1, M3, TPB, (MT * NT1 <= 4 ? 16 : 8)>(tmap, P, grid, smem, s);
+  return launch_w<MT, NT1, M3, TPB, 8>(tmap, P, grid, smem, s);
 }
 
 template <int MT, int NT1, bool M3>
 cudaError_t launch_b(const CUtensorMap* tmap, const CoreParams& P, int grid, size_t smem, cudaStream_t s) {
   switch (P.tpb) {
     case 1: return launch_t<MT, NT1, M3, 1>(tmap, P, grid, smem, s);
-    case 2: return launch_t<MT, NT1, M3, 2>(tmap, P, grid, smem, s);
-    case 4: return launch_t<MT, NT1, M3, 4>(tmap, P, grid, smem, s);
+    case 2: return launch_t<MT, NT1, M3, (MT <= 2 && NT1 <= 2 ? 2 : 1)>(tmap, P, grid, smem, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -498,13 +532,13 @@ cudaError_t launch_n(const CUtensorMap* tmap, const CoreParams& P, int grid, siz
 
 }  // namespace
 
-int srtt_core_threads() { return kThreads; }
+int srtt_core_threads() { return 256; }
 
 // Shared memory of the core kernel for a given stage count.
 size_t srtt_core_smem_bytes(const CoreParams& P) {
-  const size_t doubles = (size_t)kWarps * P.nstages * 256 * P.tpb + (size_t)(P.RB / 4) * P.NT * 32 +
-                         (size_t)kWarps * P.A;
-  return 1024 + doubles * sizeof(double) + (size_t)kWarps * P.nstages * sizeof(uint64_t);
+  const size_t w = P.warps;
+  const size_t doubles = w * P.nstages * 256 * P.tpb + (size_t)(P.RB / 4) * P.NT * 32 + w * P.A;
+  return 1024 + doubles * sizeof(double) + w * P.nstages * sizeof(uint64_t);
 }
 
 int srtt_core_max_stages(const CoreParams& P, size_t budget) {
@@ -535,10 +569,18 @@ cudaError_t srtt_launch_prep(const double* u0, int64_t n0, int r0, int RB, int N
   return cudaGetLastError();
 }
 
-cudaError_t srtt_launch_prep_all(const double* u0, int64_t n0, int r0, int RB, int NT, int nrb, double* ufrag,
-                                 int njobs, const double* const* u, double* const* ut, const int64_t* n,
-                                 const int* r, cudaStream_t s) {
+cudaError_t srtt_launch_prep_all(const CoreParams& P, CoreItem* items, const double* u0, int64_t n0, int r0,
+                                 int RB, int NT, int nrb, double* ufrag, int njobs, const double* const* u,
+                                 double* const* ut, const int64_t* n, const int* r, cudaStream_t s) {
   PrepJobs J{};
+  J.items = items;
+  J.nitems = P.nitems;
+  J.G = P.G;
+  J.GS = P.GS;
+  J.SL = P.SL;
+  J.n1 = P.fdim[0];
+  J.S = P.S;
+  J.A = P.A;
   J.u0 = u0;
   J.ufrag = ufrag;
   J.n0 = n0;
@@ -555,7 +597,7 @@ cudaError_t srtt_launch_prep_all(const double* u0, int64_t n0, int r0, int RB, i
   }
   const int64_t total = (int64_t)nrb * RB * NT * 8;
   const int bx = (int)min64(256, (total + 255) / 256);
-  prep_all_kernel<<<dim3(bx > 0 ? bx : 1, 1 + njobs), 256, 0, s>>>(J);
+  prep_all_kernel<<<dim3(bx > 0 ? bx : 1, 2 + njobs), 256, 0, s>>>(J);
   return cudaGetLastError();
 }
 

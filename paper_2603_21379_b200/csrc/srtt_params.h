@@ -75,8 +75,20 @@ typedef struct BasisTarget {
 // R_m = X x_0 U_0^T ... x_{m-1} U_{m-1}^T restricted to its columns into a
 // fixed output slot part[rho][sigma][p][A].
 // ---------------------------------------------------------------------------
+// One work item of the core pass, built on the device by the prep kernel.
+typedef struct CoreItem {
+  int64_t c_lo;      // first column (of M = n0 x Q)
+  int64_t out_off;   // output slot offset (doubles) in part[]
+  int64_t grp0;      // level-2 group of c_lo
+  int32_t len;       // columns
+  int32_t rho;       // row block
+  int32_t off0;      // offset of c_lo inside its level-2 group
+  int32_t pad;
+} CoreItem;
+
 typedef struct CoreParams {
   const double* x;
+  const CoreItem* items;   // nitems descriptors (device)
   const double* ufrag;     // U0 in fragment order: [nrb][RB/4][NT][32]
   const double* fu[2];     // U_1, U_2 ROW-major (n_k x r_k)
   double* part;            // out: [nrb][S][G][A]
@@ -98,7 +110,8 @@ typedef struct CoreParams {
   int32_t A;               // prod_{k<m} r_k (output entries per item)
   int32_t use_tma;         // 1: cp.async.bulk.tensor loads; 0: warp-copy path (odd n0)
   int32_t nstages;         // per-warp TMA ring depth
-  int32_t tpb;             // 16-column tile pairs per TMA box (1, 2 or 4)
+  int32_t tpb;             // 16-column tile pairs per TMA box (1 or 2)
+  int32_t warps;           // warps per CTA (8 or 16)
 } CoreParams;
 
 // Generic small TTM used by the tail of the core pass and by reconstruct:
