@@ -85,6 +85,17 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 #define CK(x) cuda_check((x), #x)
 
+// During stream capture an event must be recorded as an "external" node to
+// exist (and time) in the replayed graph; outside capture, a plain record.
+void record_event(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(s, &st));
+  if (st == cudaStreamCaptureStatusActive)
+    CK(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
+  else
+    CK(cudaEventRecord(e, s));
+}
+
 template <class F>
 int guarded(F&& f) {
   try {
@@ -223,6 +234,15 @@ struct srtt_handle {
   int32_t* dinfo = nullptr;   // device alias of hinfo
   DevBuf ones;
   int64_t launches = 0;
+  struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;
+  };
+  std::map<std::string, Graph> graphs;
+  ~srtt_handle() {
+    for (auto& g : graphs)
+      if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+  }
 };
 
 namespace {
@@ -606,9 +626,9 @@ int launch_core_pass(srtt_handle* h, CorePlan& cp, const double* x, const std::v
   std::memset(&tmap, 0, sizeof(tmap));
   if (P.use_tma) encode_tmap(&tmap, x, P.n0, P.Q, 16 * P.tpb);
   cp.grid = (int)std::min<int64_t>(P.nitems, (int64_t)h->sms);
-  CK(cudaEventRecord(h->kev[4], h->stream));
+  record_event(h->kev[4], h->stream);
   CK(srtt_launch_core(&tmap, P, cp.grid, h->stream));
-  CK(cudaEventRecord(h->kev[5], h->stream));
+  record_event(h->kev[5], h->stream);
   ++launches;
   // tail: fixed-order reduction of the item partials + TTMs of modes m..d-1
   const int nparts = P.nrb * P.S;
@@ -733,13 +753,54 @@ const double* stage_input(srtt_handle* h, const double* x, int on_device, int64_
 struct Timer {
   srtt_handle* h;
   int n = 0;
-  void mark() { CK(cudaEventRecord(h->ev[n++], h->stream)); }
+  void mark() { record_event(h->ev[n++], h->stream); }
   double between(int a, int b) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, h->ev[a], h->ev[b]));
     return ms * 1e-3;
   }
 };
+
+// Issues the device work of one decomposition: directly, or (use_graphs)
+// captured once per signature into a CUDA graph and replayed. The key holds
+// every pointer the work bakes in (workspace, parameter blob, input,
+// outputs, stream), so buffer growth simply creates a new graph.
+template <class F>
+void run_enqueue(srtt_handle* h, const std::string& key, F&& enqueue) {
+  if (!h->use_graphs) {
+    enqueue();
+    return;
+  }
+  auto it = h->graphs.find(key);
+  if (it == h->graphs.end()) {
+    if (h->graphs.size() > 64) {
+      for (auto& g : h->graphs) cudaGraphExecDestroy(g.second.exec);
+      h->graphs.clear();
+    }
+    CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
+    const int64_t before = h->launches;
+    try {
+      enqueue();
+    } catch (...) {
+      cudaGraph_t g;
+      cudaStreamEndCapture(h->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    cudaGraph_t g;
+    CK(cudaStreamEndCapture(h->stream, &g));
+    srtt_handle::Graph entry;
+    CK(cudaGraphInstantiate(&entry.exec, g, 0));
+    cudaGraphDestroy(g);
+    entry.launches = h->launches - before;
+    it = h->graphs.emplace(key, entry).first;
+    h->launches = before;
+  }
+  CK(cudaGraphLaunch(it->second.exec, h->stream));
+  h->launches += it->second.launches;
+}
+
+std::string ptr_key(const void* p) { return std::to_string(reinterpret_cast<uintptr_t>(p)); }
 
 double kernel_pair(srtt_handle* h, int i) {
   float ms = 0;
@@ -870,36 +931,45 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   for (auto& it : blob.items) std::memcpy(hp + it.first, it.second.data(), it.second.size());
   std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * d);
   std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * d);
-  CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
-  tm.mark();  // 2
-
-  // --- K1: grouped gather + sketch over all modes
-  CK(srtt_launch_sketch(reinterpret_cast<const SketchTarget*>(dp + off_sk), d, ctas, cmax, h->stream));
-  h->launches++;
-  tm.mark();  // 3
-  // --- K2: basis of every sketch
-  h->launches += launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt), lists, dp,
-                                    reinterpret_cast<double*>(ws + off_pad), max_n);
-  tm.mark();  // 4
-  // --- K3: core pass
-  std::vector<const double*> ucp(uptr.begin(), uptr.end());
-  if (d >= 2) {
-    h->launches += launch_core_pass(h, cp, x, ucp, d_core, ws, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
-  } else {
-    TtmParams T{};
-    T.in = x;
-    T.u = ucp[0];
-    T.out = d_core;
-    T.g = 1;
-    T.n = dims[0];
-    T.post = 1;
-    T.rr = ranks[0];
-    T.transpose = 1;
-    T.nparts = 1;
-    CK(srtt_launch_ttm(T, h->stream));
+  std::string key = "T";
+  for (int k = 0; k < d; ++k)
+    key += "|" + std::to_string(dims[k]) + "," + std::to_string(ranks[k]) + "," + std::to_string(samples[k]) + "," +
+           ptr_key(uptr[k]);
+  key += "|" + std::to_string(p) + "|" + ptr_key(x) + "|" + ptr_key(d_core) + "|" + ptr_key(ws) + "|" + ptr_key(dp) +
+         "|" + ptr_key(hp) + "|" + ptr_key(h->stream) + "|" + std::to_string(blob.lay.off);
+  run_enqueue(h, key, [&] {
+    CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
+    tm.n = 2;
+    tm.mark();  // 2
+    // --- K1: grouped gather + sketch over all modes
+    CK(srtt_launch_sketch(reinterpret_cast<const SketchTarget*>(dp + off_sk), d, ctas, cmax, h->stream));
     h->launches++;
-  }
-  tm.mark();  // 5
+    tm.mark();  // 3
+    // --- K2: basis of every sketch
+    h->launches += launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt), lists, dp,
+                                      reinterpret_cast<double*>(ws + off_pad), max_n);
+    tm.mark();  // 4
+    // --- K3: core pass
+    std::vector<const double*> ucp(uptr.begin(), uptr.end());
+    if (d >= 2) {
+      h->launches += launch_core_pass(h, cp, x, ucp, d_core, ws, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+    } else {
+      TtmParams T{};
+      T.in = x;
+      T.u = ucp[0];
+      T.out = d_core;
+      T.g = 1;
+      T.n = dims[0];
+      T.post = 1;
+      T.rr = ranks[0];
+      T.transpose = 1;
+      T.nparts = 1;
+      CK(srtt_launch_ttm(T, h->stream));
+      h->launches++;
+    }
+    tm.mark();  // 5
+  });
+  tm.n = 6;
   // --- outputs (host destinations only; device outputs were written in place)
   if (!out_on_device) {
     copy_out(h, core_out, d_core, sizeof(double) * prod(ranks), 0);
@@ -1292,26 +1362,42 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * nt);
   std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * nt);
   if (!tt.empty()) std::memcpy(hp + off_tt, tt.data(), sizeof(TransferTarget) * tt.size());
-  CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
-  tm.mark();  // 2
-  CK(srtt_launch_sketch(reinterpret_cast<const SketchTarget*>(dp + off_sk), nt, ctas, cmax, h->stream));
-  h->launches++;
-  tm.mark();  // 3
-  h->launches += launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt), lists, dp,
-                                    reinterpret_cast<double*>(ws + off_pad), max_n);
-  tm.mark();  // 4
-  if (!tt.empty()) {
-    CK(srtt_launch_transfer(reinterpret_cast<const TransferTarget*>(dp + off_tt), (int)tt.size(), tctas, max_rl,
-                            max_rr, h->stream));
-    h->launches++;
+  std::string key = "H";
+  for (int k = 0; k < d; ++k) key += "|" + std::to_string(dims[k]);
+  for (int i = 0; i < nn; ++i)
+    key += "|" + std::to_string(ranks[i]) + "," + std::to_string(samples[i]) + "," + std::to_string(tr.left[i]) + "," +
+           std::to_string(tr.modes[i].size());
+  key += "|" + std::to_string(p) + "|" + ptr_key(x) + "|" + ptr_key(ws) + "|" + ptr_key(dp) + "|" + ptr_key(hp) + "|" +
+         ptr_key(h->stream) + "|" + std::to_string(blob.lay.off) + "|" + std::to_string(out_on_device);
+  if (out_on_device) {
+    for (int k = 0; k < d; ++k) key += "|" + ptr_key(leaf_out[k]);
+    if (transfers_out)
+      for (int i = 0; i < nn; ++i) key += "|" + ptr_key(transfers_out[i]);
   }
-  tm.mark();  // 5
-  // root transfer: the K3 engine on M = X viewed as n_l x n_r (htucker.hpp:67-85)
-  std::vector<const double*> ur = {ubasis(tr.left[0]), ubasis(tr.right[0])};
   double* d_root = (out_on_device && transfers_out && transfers_out[0]) ? transfers_out[0]
                                                                        : reinterpret_cast<double*>(ws + off_b[0]);
-  h->launches += launch_core_pass(h, cp, x, ur, d_root, ws, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
-  tm.mark();  // 6
+  run_enqueue(h, key, [&] {
+    tm.n = 2;
+    CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
+    tm.mark();  // 2
+    CK(srtt_launch_sketch(reinterpret_cast<const SketchTarget*>(dp + off_sk), nt, ctas, cmax, h->stream));
+    h->launches++;
+    tm.mark();  // 3
+    h->launches += launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt), lists, dp,
+                                      reinterpret_cast<double*>(ws + off_pad), max_n);
+    tm.mark();  // 4
+    if (!tt.empty()) {
+      CK(srtt_launch_transfer(reinterpret_cast<const TransferTarget*>(dp + off_tt), (int)tt.size(), tctas, max_rl,
+                              max_rr, h->stream));
+      h->launches++;
+    }
+    tm.mark();  // 5
+    // root transfer: the K3 engine on M = X viewed as n_l x n_r (htucker.hpp:67-85)
+    std::vector<const double*> ur = {ubasis(tr.left[0]), ubasis(tr.right[0])};
+    h->launches += launch_core_pass(h, cp, x, ur, d_root, ws, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+    tm.mark();  // 6
+  });
+  tm.n = 7;
   if (!out_on_device) {
     for (int i = 1; i < nn; ++i)
       if (tr.leaf(i)) {

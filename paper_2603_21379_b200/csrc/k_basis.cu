@@ -45,10 +45,59 @@ __device__ double block_sum(double v, double* red) {
 // Householder QR of the m x n column-major matrix A (ld = lda) held in
 // shared memory: R in the upper triangle, reflector tails below the
 // diagonal (v_j(j) = 1 implicit), tau[j] (LAPACK dlarfg convention).
-__device__ void householder_qr(double* A, int m, int n, int lda, double* tau, double* scal_beta) {
+// With `vn` (n doubles of scratch) the columns are pivoted by largest
+// remaining norm (QRCP, norms downdated as in dgeqp3): R comes out graded,
+// which makes the one-sided Jacobi on its rows converge in a few sweeps
+// (Drmac-Veselic preconditioning). Column order never matters downstream:
+// only R's rows (and Q) are used.
+__device__ void householder_qr(double* A, int m, int n, int lda, double* tau, double* scal_beta,
+                               double* vn = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int k = min(m, n);
+  __shared__ int piv_s;
+  if (vn) {
+    for (int jj = warp; jj < n; jj += kWarps) {
+      const double* cj = A + (size_t)jj * lda;
+      double s = 0.0;
+      for (int i = lane; i < m; i += 32) s += cj[i] * cj[i];
+      s = warp_sum(s);
+      if (lane == 0) vn[jj] = sqrt(s);
+    }
+    __syncthreads();
+  }
   for (int j = 0; j < k; ++j) {
+    if (vn) {
+      if (warp == 0) {
+        double best = -1.0;
+        int bi = j;
+        for (int l = j + lane; l < n; l += 32)
+          if (vn[l] > best) { best = vn[l]; bi = l; }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (lane == 0) piv_s = bi;
+      }
+      __syncthreads();
+      const int piv = piv_s;
+      if (piv != j) {
+        double* a = A + (size_t)j * lda;
+        double* b = A + (size_t)piv * lda;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+          const double t = a[i];
+          a[i] = b[i];
+          b[i] = t;
+        }
+        if (threadIdx.x == 0) {
+          const double t = vn[j];
+          vn[j] = vn[piv];
+          vn[piv] = t;
+        }
+      }
+      __syncthreads();
+    }
     double* col = A + (size_t)j * lda;
     if (warp == 0) {
       double s = 0.0;
@@ -76,15 +125,19 @@ __device__ void householder_qr(double* A, int m, int n, int lda, double* tau, do
     }
     __syncthreads();
     if (threadIdx.x == 0) col[j] = scal_beta[1];
-    if (t != 0.0) {
-      for (int jj = j + 1 + warp; jj < n; jj += kWarps) {
-        double* cj = A + (size_t)jj * lda;
+    for (int jj = j + 1 + warp; jj < n; jj += kWarps) {
+      double* cj = A + (size_t)jj * lda;
+      if (t != 0.0) {
         double s = (lane == 0) ? cj[j] : 0.0;
         for (int i = j + 1 + lane; i < m; i += 32) s += col[i] * cj[i];
         s = warp_sum(s);
         const double ts = t * s;
         if (lane == 0) cj[j] -= ts;
         for (int i = j + 1 + lane; i < m; i += 32) cj[i] -= ts * col[i];
+      }
+      if (vn && lane == 0) {
+        const double r = cj[j];
+        vn[jj] = sqrt(fmax(0.0, vn[jj] * vn[jj] - r * r));
       }
     }
     __syncthreads();
@@ -263,6 +316,7 @@ __device__ void pad_columns(double* Y, int64_t n, int64_t ldy, int q, int r, uin
 }
 
 struct TopSmem {
+  double* vn;
   double* A;
   double* B;
   double* V;
@@ -281,6 +335,7 @@ __device__ TopSmem carve_top(unsigned char* raw, int m, int c, int r) {
   const int k = min(m, c);
   TopSmem s;
   double* p = reinterpret_cast<double*>(raw);
+  s.vn = p; p += c;
   s.A = p; p += (size_t)m * c;
   s.B = p; p += (size_t)k * c;
   s.V = p; p += (size_t)k * k;
@@ -316,7 +371,7 @@ __global__ void __launch_bounds__(kThreads) basis_top_kernel(const BasisTarget* 
     s.A[idx] = L.a[(int64_t)j * L.n + i];
   }
   __syncthreads();
-  householder_qr(s.A, m, c, m, s.tau, s.scal_beta);
+  householder_qr(s.A, m, c, m, s.tau, s.scal_beta, s.vn);
   // B = R (k x c, row-major), V = I.
   for (int idx = threadIdx.x; idx < k * c; idx += blockDim.x) {
     const int i = idx / c, j = idx % c;
@@ -477,6 +532,7 @@ __global__ void __launch_bounds__(kThreads) pad_kernel(const BasisTarget* __rest
 // Gram-Schmidt padding from the same stream.
 // ===========================================================================
 struct SmallSmem {
+  double* vn;  // c column norms (QRCP)
   double* A;   // m x c, ld = lda (odd)
   double* B;   // k x c rows, ld = ldb (odd)
   double* V;   // k x k, ld = ldv (odd)
@@ -498,6 +554,7 @@ __device__ SmallSmem carve_small(unsigned char* raw, int m, int c, int r) {
   s.ldb = odd_ld(c);
   s.ldv = odd_ld(k);
   double* p = reinterpret_cast<double*>(raw);
+  s.vn = p; p += c;
   s.A = p; p += (size_t)s.lda * c;
   s.B = p; p += (size_t)s.ldb * k;
   s.V = p; p += (size_t)s.ldv * k;
@@ -540,8 +597,50 @@ __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __re
     s.A[(size_t)j * s.lda + i] = z[idx];
   }
   __syncwarp();
-  // ---- Householder QR, lanes own the trailing columns
+  // ---- Householder QR with column pivoting (QRCP), 4-lane groups own the
+  // trailing columns; pivoting preconditions the Jacobi below.
+  {
+    const int grp = lane >> 2, gl = lane & 3;
+    for (int jb = 0; jb < c; jb += 8) {
+      const int jj = jb + grp;
+      double sq = 0.0;
+      if (jj < c)
+        for (int i = gl; i < m; i += 4) sq += s.A[(size_t)jj * s.lda + i] * s.A[(size_t)jj * s.lda + i];
+      sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+      sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+      if (jj < c && gl == 0) s.vn[jj] = sqrt(sq);
+    }
+    __syncwarp();
+  }
   for (int j = 0; j < k; ++j) {
+    {  // pivot: largest remaining column norm
+      double best = -1.0;
+      int bi = j;
+      for (int l = j + lane; l < c; l += 32)
+        if (s.vn[l] > best) { best = s.vn[l]; bi = l; }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (bi != j) {
+        double* a = s.A + (size_t)j * s.lda;
+        double* b = s.A + (size_t)bi * s.lda;
+        for (int i = lane; i < m; i += 32) {
+          const double t = a[i];
+          a[i] = b[i];
+          b[i] = t;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          const double t = s.vn[j];
+          s.vn[j] = s.vn[bi];
+          s.vn[bi] = t;
+        }
+      }
+      __syncwarp();
+    }
     double* col = s.A + (size_t)j * s.lda;
     double part = 0.0;
     for (int i = j + 1 + lane; i < m; i += 32) part += col[i] * col[i];
@@ -561,21 +660,26 @@ __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __re
       col[j] = beta;
       s.tau[j] = t;
     }
-    if (t != 0.0) {
+    {
       const int grp = lane >> 2, gl = lane & 3;
       for (int jb = j + 1; jb < c; jb += 8) {
         const int jj = jb + grp;
         double* cj = s.A + (size_t)min(jj, c - 1) * s.lda;
         double w = 0.0;
-        if (jj < c)
+        if (t != 0.0 && jj < c)
           for (int i = j + 1 + gl; i < m; i += 4) w += col[i] * cj[i];
         w += __shfl_xor_sync(0xffffffffu, w, 1);
         w += __shfl_xor_sync(0xffffffffu, w, 2);
         if (jj < c) {
           const double tw = t * (w + cj[j]);
           __syncwarp(0xffffffffu);
-          if (gl == 0) cj[j] -= tw;
-          for (int i = j + 1 + gl; i < m; i += 4) cj[i] -= tw * col[i];
+          if (gl == 0) {
+            cj[j] -= tw;
+            const double r = cj[j];
+            s.vn[jj] = sqrt(fmax(0.0, s.vn[jj] * s.vn[jj] - r * r));
+          }
+          if (t != 0.0)
+            for (int i = j + 1 + gl; i < m; i += 4) cj[i] -= tw * col[i];
         } else {
           __syncwarp(0xffffffffu);
         }
@@ -700,7 +804,7 @@ __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __re
 
 size_t srtt_basis_top_smem(int m, int c, int r) {
   const int k = m < c ? m : c;
-  size_t doubles = (size_t)m * c + (size_t)k * c + (size_t)k * k + (size_t)m * r + c + k + r + 32 + m + 2;
+  size_t doubles = (size_t)c + (size_t)m * c + (size_t)k * c + (size_t)k * k + (size_t)m * r + c + k + r + 32 + m + 2;
   return doubles * sizeof(double) + 2 * sizeof(int) * (size_t)(k + 2);
 }
 
@@ -712,7 +816,7 @@ int srtt_basis_threads() { return kThreads; }
 
 size_t srtt_basis_small_smem(int m, int c, int r) {
   const int k = m < c ? m : c;
-  const size_t doubles = (size_t)odd_ld(m) * c + (size_t)odd_ld(c) * k + (size_t)odd_ld(k) * k +
+  const size_t doubles = (size_t)c + (size_t)odd_ld(m) * c + (size_t)odd_ld(c) * k + (size_t)odd_ld(k) * k +
                          (size_t)odd_ld(m) * r + c + k + r + m + 2;
   return doubles * sizeof(double) + sizeof(int) * (size_t)(k + 2);
 }
@@ -720,7 +824,7 @@ size_t srtt_basis_small_smem(int m, int c, int r) {
 cudaError_t srtt_launch_basis_small(const BasisTarget* d_targets, const int* d_list, int n, size_t smem,
                                     cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
-  cudaFuncSetAttribute(basis_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  SRTT_ENSURE_SMEM((basis_small_kernel), smem);
   basis_small_kernel<<<n, 32, smem, stream>>>(d_targets, d_list);
   return cudaGetLastError();
 }
@@ -728,7 +832,7 @@ cudaError_t srtt_launch_basis_small(const BasisTarget* d_targets, const int* d_l
 cudaError_t srtt_launch_basis_top(const BasisTarget* d_targets, const int* d_list, int ntargets, size_t smem,
                                   cudaStream_t stream) {
   if (ntargets <= 0) return cudaSuccess;
-  cudaFuncSetAttribute(basis_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  SRTT_ENSURE_SMEM((basis_top_kernel), smem);
   basis_top_kernel<<<ntargets, kThreads, smem, stream>>>(d_targets, d_list);
   return cudaGetLastError();
 }
@@ -736,7 +840,7 @@ cudaError_t srtt_launch_basis_top(const BasisTarget* d_targets, const int* d_lis
 cudaError_t srtt_launch_tsqr_factor(const BasisTarget* d_targets, const int2* d_map, int level, int nctas,
                                     size_t smem, cudaStream_t stream) {
   if (nctas <= 0) return cudaSuccess;
-  cudaFuncSetAttribute(tsqr_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  SRTT_ENSURE_SMEM((tsqr_factor_kernel), smem);
   tsqr_factor_kernel<<<nctas, kThreads, smem, stream>>>(d_targets, d_map, level);
   return cudaGetLastError();
 }
@@ -744,7 +848,7 @@ cudaError_t srtt_launch_tsqr_factor(const BasisTarget* d_targets, const int2* d_
 cudaError_t srtt_launch_tsqr_apply(const BasisTarget* d_targets, const int2* d_map, int level, int nctas,
                                    size_t smem, cudaStream_t stream) {
   if (nctas <= 0) return cudaSuccess;
-  cudaFuncSetAttribute(tsqr_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  SRTT_ENSURE_SMEM((tsqr_apply_kernel), smem);
   tsqr_apply_kernel<<<nctas, kThreads, smem, stream>>>(d_targets, d_map, level);
   return cudaGetLastError();
 }

@@ -492,8 +492,7 @@ __global__ void prep_all_kernel(const PrepJobs J) {
 
 template <int MT, int NT1, bool M3, int TPB, int WARPS>
 cudaError_t launch_w(const CUtensorMap* tmap, const CoreParams& P, int grid, size_t smem, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(core_kernel<MT, NT1, M3, TPB, WARPS>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = SRTT_ENSURE_SMEM((core_kernel<MT, NT1, M3, TPB, WARPS>), smem);
   if (e != cudaSuccess) return e;
   core_kernel<MT, NT1, M3, TPB, WARPS><<<grid, WARPS * 32, smem, s>>>(*tmap, P);
   return cudaGetLastError();

@@ -104,7 +104,7 @@ cudaError_t srtt_launch_transfer(const TransferTarget* d_targets, int ntargets, 
                                  int max_rr, cudaStream_t s) {
   if (nctas <= 0) return cudaSuccess;
   const size_t smem = ((size_t)max_rl * kChunkB + (size_t)max_rl * max_rr) * sizeof(double);
-  cudaFuncSetAttribute(transfer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  SRTT_ENSURE_SMEM((transfer_kernel), smem);
   transfer_kernel<<<nctas, kThreads, smem, s>>>(d_targets, ntargets);
   return cudaGetLastError();
 }

@@ -151,13 +151,13 @@ cudaError_t srtt_launch_sketch(const SketchTarget* d_targets, int ntargets, int6
   if (total_ctas <= 0) return cudaSuccess;
   const size_t smem = srtt_sketch_smem_bytes(cmax);
   if (cmax <= 16) {
-    cudaFuncSetAttribute(sketch_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    SRTT_ENSURE_SMEM((sketch_kernel<16>), smem);
     sketch_kernel<16><<<(unsigned)total_ctas, kThreads, smem, stream>>>(d_targets, ntargets);
   } else if (cmax <= 32) {
-    cudaFuncSetAttribute(sketch_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    SRTT_ENSURE_SMEM((sketch_kernel<32>), smem);
     sketch_kernel<32><<<(unsigned)total_ctas, kThreads, smem, stream>>>(d_targets, ntargets);
   } else {
-    cudaFuncSetAttribute(sketch_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    SRTT_ENSURE_SMEM((sketch_kernel<64>), smem);
     sketch_kernel<64><<<(unsigned)total_ctas, kThreads, smem, stream>>>(d_targets, ntargets);
   }
   return cudaGetLastError();

@@ -7,6 +7,19 @@
 
 namespace srtt_dev {
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when the requested
+// size grows (the attribute call costs microseconds on every launch); one
+// static watermark per call site / kernel.
+template <class K>
+inline cudaError_t ensure_smem_at(size_t& current, K kernel, size_t bytes) {
+  if (bytes <= current) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) current = bytes;
+  return e;
+}
+#define SRTT_ENSURE_SMEM(kernel, bytes) \
+  ([&]() { static size_t wm_ = 0; return ::srtt_dev::ensure_smem_at(wm_, kernel, bytes); }())
+
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
 

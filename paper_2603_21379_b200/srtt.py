@@ -168,7 +168,7 @@ def _flat_f64(x):
 class Handle:
     """Owns a device, a stream, the workspace arena and pinned staging."""
 
-    def __init__(self, device: int = 0, use_graphs: bool = False):
+    def __init__(self, device: int = 0, use_graphs: bool = True):
         self._h = C.c_void_p()
         opts = _Options(device=device, use_graphs=int(use_graphs))
         _check(_L().srtt_create(C.byref(opts), C.byref(self._h)))
@@ -379,33 +379,57 @@ def _alloc_out(shape_list, device_out, like):
     return [np.zeros(int(np.prod(s))) for s in shape_list]
 
 
+class _TuckerCall:
+    """Per-signature cache of the ctypes argument blocks of one Tucker call
+    (keeps the per-call Python overhead to a handful of microseconds)."""
+
+    def __init__(self, dims, target, samples):
+        d = len(dims)
+        self.d = d
+        self.dims_a, self.ranks_a, self.samp_a = _i64(dims), _i64(target), _i64(samples)
+        self.ach, self.sc = np.zeros(d, np.int64), np.zeros(d, np.int64)
+        self.wbuf = C.create_string_buffer(8192)
+        self.rep = _Report(self.sc.ctypes.data_as(C.POINTER(C.c_int64)),
+                           self.ach.ctypes.data_as(C.POINTER(C.c_int64)), C.cast(self.wbuf, C.c_char_p), 8192, 0)
+        self.fptrs = (C.c_void_p * d)()
+
+
+_CALLS = {}
+
+
 def sub_r_hosvd(x, target, oversampling, samples, seed, exec_policy=None, report=None, *, dims=None,
-                handle=None, device_out=False):
+                handle=None, device_out=False, out=None):
     """tucker.hpp:177-242.  ``x``: numpy nd-array (dims taken from its shape)
-    or a flat float64 array / CUDA tensor together with ``dims``."""
+    or a flat float64 array / CUDA tensor together with ``dims``.
+    ``out=(core, [factors])`` reuses caller-allocated outputs (flat, device
+    tensors when ``device_out``)."""
     h = handle or default_handle()
     if dims is None:
         dims = list(np.shape(x))
     d = len(dims)
     xf = _flat_f64(x)
     xp, xdev = _ptr(xf)
-    dims_a, ranks_a, samp_a = _i64(dims), _i64(target), _i64(samples)
-    if len(ranks_a) != d:
+    if len(target) != d:
         raise InvalidArgument("sub_r_hosvd: rank vector order mismatch")
-    if len(samp_a) != len(ranks_a):
+    if len(samples) != len(target):
         raise InvalidArgument("sub_r_hosvd: samples vector order mismatch")
-    outs = _alloc_out([ranks_a] + [(dims[k], target[k]) for k in range(d)], device_out, xf)
-    fptrs = (C.c_void_p * d)(*[_ptr(o)[0] for o in outs[1:]])
-    ach, sc = np.zeros(d, np.int64), np.zeros(d, np.int64)
-    wbuf = C.create_string_buffer(8192)
-    crep = _Report(sc.ctypes.data_as(C.POINTER(C.c_int64)), ach.ctypes.data_as(C.POINTER(C.c_int64)),
-                   C.cast(wbuf, C.c_char_p), 8192, 0)
+    key = (tuple(dims), tuple(target), tuple(samples))
+    call = _CALLS.get(key)
+    if call is None:
+        call = _CALLS.setdefault(key, _TuckerCall(dims, target, samples))
+    if out is None:
+        outs = _alloc_out([call.ranks_a] + [(dims[k], target[k]) for k in range(d)], device_out, xf)
+    else:
+        outs = [out[0]] + list(out[1])
+    for k in range(d):
+        call.fptrs[k] = _ptr(outs[k + 1])[0]
     ex = exec_policy._c() if exec_policy is not None else None
-    _check(_L().srtt_sub_r_hosvd(h._h, xp, xdev, d, dims_a.ctypes.data, ranks_a.ctypes.data, int(oversampling),
-                                 samp_a.ctypes.data, int(seed) & (2**64 - 1),
-                                 C.byref(ex) if ex is not None else None, _ptr(outs[0])[0], fptrs,
-                                 int(device_out), C.byref(crep)))
-    _report_from(crep, d, ach, sc, report, h)
+    _check(_L().srtt_sub_r_hosvd(h._h, xp, xdev, d, call.dims_a.ctypes.data, call.ranks_a.ctypes.data,
+                                 int(oversampling), call.samp_a.ctypes.data, int(seed) & (2**64 - 1),
+                                 C.byref(ex) if ex is not None else None, _ptr(outs[0])[0], call.fptrs,
+                                 int(device_out), C.byref(call.rep)))
+    if report is not None:
+        _report_from(call.rep, d, call.ach, call.sc, report, h)
     if device_out:
         return TuckerDecomposition(core=outs[0], factors=outs[1:])
     core = outs[0].reshape(tuple(int(r) for r in target), order="F")
