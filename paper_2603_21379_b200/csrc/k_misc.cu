@@ -26,11 +26,15 @@ typedef struct GatherParams {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kChunkB = 512;  // columns of the reshaped U_S(:, i) per pass
+constexpr int kChunkA = 256;  // rows of U_l staged per pass
+constexpr int kMaxR = 64;     // rank limit of the transfer kernel
 
 // B(i, j, k) = sum_{a,b} U_l(a, j) U_S(a + b n_l, i) U_r(b, k)
-// (htucker.hpp:44-63): T = U_l^T reshape(U_S(:, i)) then B_i = T U_r,
-// streamed over chunks of the n_r columns; one CTA per (node, i).
+// (htucker.hpp:44-63): T = U_l^T reshape(U_S(:, i)) then B_i = T U_r; one
+// CTA per (node, i). A thread owns one column b of the n_l x n_r block
+// (contiguous in U_S(:, i)) and accumulates T(:, b) with U_l rows broadcast
+// from shared memory; T and U_r chunks then meet in shared memory.
+template <int RMAX>
 __global__ void __launch_bounds__(kThreads) transfer_kernel(const TransferTarget* __restrict__ targets,
                                                             int ntargets) {
   extern __shared__ double sm[];
@@ -44,30 +48,52 @@ __global__ void __launch_bounds__(kThreads) transfer_kernel(const TransferTarget
     tsel = lo;
   }
   __syncthreads();
-  const TransferTarget& T = targets[tsel];
+  const TransferTarget T = targets[tsel];
   const int i = blockIdx.x - T.cta_begin;
   const int rl = T.rl, rr = T.rr;
-  double* tt = sm;                       // rl x chunk
-  double* bacc = sm + (size_t)rl * kChunkB;  // rl x rr
+  const int64_t nl = T.nl, nr = T.nr;
+  // smem: U_l^T rows [a][j] for an a-chunk, T chunk [j][b], B accumulator
+  double* ul_s = sm;                              // kChunkA x rl
+  double* t_s = ul_s + (size_t)kChunkA * rl;      // rl x kThreads
+  double* bacc = t_s + (size_t)rl * kThreads;     // rl x rr
   for (int e = threadIdx.x; e < rl * rr; e += kThreads) bacc[e] = 0.0;
-  const double* usi = T.us + (int64_t)i * T.nl * T.nr;
-  for (int64_t b0 = 0; b0 < T.nr; b0 += kChunkB) {
-    const int bn = (int)srtt_dev::min64(kChunkB, T.nr - b0);
-    __syncthreads();
-    for (int e = threadIdx.x; e < rl * bn; e += kThreads) {
-      const int j = e % rl, bb = e / rl;
-      const double* col = usi + (b0 + bb) * T.nl;
-      const double* ulj = T.ul + (int64_t)j * T.nl;
-      double s = 0.0;
-      for (int64_t a = 0; a < T.nl; ++a) s += ulj[a] * col[a];
-      tt[j + rl * bb] = s;
+  const double* usi = T.us + (int64_t)i * nl * nr;
+  for (int64_t b0 = 0; b0 < nr; b0 += kThreads) {
+    const int64_t bcol = b0 + threadIdx.x;
+    double tacc[RMAX];
+#pragma unroll
+    for (int j = 0; j < RMAX; ++j) tacc[j] = 0.0;
+    for (int64_t a0 = 0; a0 < nl; a0 += kChunkA) {
+      const int an = (int)srtt_dev::min64(kChunkA, nl - a0);
+      __syncthreads();
+      for (int e = threadIdx.x; e < an * rl; e += kThreads) {
+        const int aa = e / rl, j = e % rl;
+        ul_s[aa * rl + j] = T.ul[(a0 + aa) + nl * j];
+      }
+      __syncthreads();
+      if (bcol < nr) {
+        const double* col = usi + bcol * nl + a0;
+#pragma unroll 8
+        for (int aa = 0; aa < an; ++aa) {
+          const double m = col[aa];
+          const double* ur = ul_s + aa * rl;
+#pragma unroll
+          for (int j = 0; j < RMAX; ++j)
+            if (j < rl) tacc[j] += ur[j] * m;
+        }
+      }
     }
     __syncthreads();
+#pragma unroll
+    for (int j = 0; j < RMAX; ++j)
+      if (j < rl) t_s[j * kThreads + threadIdx.x] = (bcol < nr) ? tacc[j] : 0.0;
+    __syncthreads();
+    const int bn = (int)srtt_dev::min64(kThreads, nr - b0);
     for (int e = threadIdx.x; e < rl * rr; e += kThreads) {
       const int j = e % rl, k = e / rl;
-      const double* urk = T.ur + (int64_t)k * T.nr + b0;
+      const double* urk = T.ur + (int64_t)k * nr + b0;
       double s = 0.0;
-      for (int bb = 0; bb < bn; ++bb) s += tt[j + rl * bb] * urk[bb];
+      for (int bb = 0; bb < bn; ++bb) s += t_s[j * kThreads + bb] * urk[bb];
       bacc[e] += s;
     }
   }
@@ -103,9 +129,18 @@ __global__ void gather_kernel(const GatherParams P) {
 cudaError_t srtt_launch_transfer(const TransferTarget* d_targets, int ntargets, int nctas, int max_rl,
                                  int max_rr, cudaStream_t s) {
   if (nctas <= 0) return cudaSuccess;
-  const size_t smem = ((size_t)max_rl * kChunkB + (size_t)max_rl * max_rr) * sizeof(double);
-  SRTT_ENSURE_SMEM((transfer_kernel), smem);
-  transfer_kernel<<<nctas, kThreads, smem, s>>>(d_targets, ntargets);
+  if (max_rl > kMaxR) return cudaErrorInvalidValue;
+  const size_t smem = ((size_t)kChunkA * max_rl + (size_t)max_rl * kThreads + (size_t)max_rl * max_rr) * sizeof(double);
+  if (max_rl <= 16) {
+    SRTT_ENSURE_SMEM((transfer_kernel<16>), smem);
+    transfer_kernel<16><<<nctas, kThreads, smem, s>>>(d_targets, ntargets);
+  } else if (max_rl <= 32) {
+    SRTT_ENSURE_SMEM((transfer_kernel<32>), smem);
+    transfer_kernel<32><<<nctas, kThreads, smem, s>>>(d_targets, ntargets);
+  } else {
+    SRTT_ENSURE_SMEM((transfer_kernel<64>), smem);
+    transfer_kernel<64><<<nctas, kThreads, smem, s>>>(d_targets, ntargets);
+  }
   return cudaGetLastError();
 }
 
