@@ -18,6 +18,12 @@
  * Pointer location: `*_on_device` = 0 means host memory (the library copies
  * host<->device inside the call; pinned host buffers make this fast),
  * 1 means CUDA device memory on the handle's device.
+ *
+ * Synchronisation: a decomposition with host outputs or a non-NULL report
+ * returns after the work completed. With device outputs and rep == NULL,
+ * srtt_sub_r_hosvd is stream-ordered like a cuBLAS call: it returns once
+ * the work is enqueued on the handle's stream (srtt_set_stream), so
+ * back-to-back calls overlap host preparation with device execution.
  */
 #ifndef SRTT_B200_H
 #define SRTT_B200_H

@@ -207,9 +207,10 @@ void encode_tmap(CUtensorMap* map, const double* x, int64_t n0, int64_t Q, int W
   if (r != CUDA_SUCCESS) fail(SRTT_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
-int64_t prod(const std::vector<int64_t>& v, size_t lo = 0, size_t hi = SIZE_MAX) {
+int64_t prod(const std::vector<int64_t>& v, int lo = 0, int hi = 1 << 30) {
   int64_t p = 1;
-  for (size_t i = lo; i < std::min(hi, v.size()); ++i) p *= v[i];
+  const int e = std::min<int>(hi, (int)v.size());
+  for (int i = lo; i < e; ++i) p *= v[static_cast<size_t>(i)];
   return p;
 }
 
@@ -230,8 +231,19 @@ struct srtt_handle {
   cudaEvent_t kev[8] = {};  // per-kernel pairs: [2i] start, [2i+1] end
   DevBuf xbuf;     // device copy of host inputs
   DevBuf ws;       // workspace arena
-  DevBuf dparams;  // device copy of the parameter blob
-  HostBuf hparams; // pinned parameter blob
+  // Double-buffered parameter blobs (pinned host + device copy): a call
+  // may return before its graph ran (device outputs, no report), so the
+  // next call writes the other set; a set is reused only after the call
+  // that last used it completed (event).
+  struct ParamSet {
+    DevBuf d;
+    HostBuf hst;
+    cudaEvent_t done = nullptr;
+    bool recorded = false;
+  };
+  ParamSet psets[2];
+  int cur = 0;
+  ParamSet& pset() { return psets[cur]; }
   int32_t* hinfo = nullptr;   // mapped pinned: per-target info + flags, written by kernels
   int32_t* dinfo = nullptr;   // device alias of hinfo
   DevBuf ones;
@@ -241,6 +253,18 @@ struct srtt_handle {
     int64_t launches = 0;
   };
   std::map<std::string, Graph> graphs;
+  // Per-signature prepared Tucker calls: the seed-independent parameter
+  // blob image and where the seed-dependent fields live inside it.
+  struct Prepared {
+    std::vector<unsigned char> image;
+    std::vector<size_t> off_cols;
+    size_t off_sk = 0, off_bt = 0;
+    std::string graph_key;
+    const void *ws = nullptr, *dp = nullptr, *hp = nullptr;
+    std::vector<const double*> udev;  // device factors (workspace or user buffers)
+    const double* d_core = nullptr;
+  };
+  std::map<std::string, Prepared> prepared;
   ~srtt_handle() {
     for (auto& g : graphs)
       if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
@@ -764,6 +788,25 @@ struct Timer {
   }
 };
 
+// Start of a decomposition: switch to the other parameter set and wait
+// until the call that last used it has finished with it.
+void begin_call(srtt_handle* h) {
+  h->cur ^= 1;
+  auto& ps = h->pset();
+  if (ps.recorded) CK(cudaEventSynchronize(ps.done));
+}
+
+// End of the enqueue part: mark the parameter set busy until the stream
+// reaches this point. Returns true when the caller must synchronise
+// (host outputs or a report requested); otherwise the call is
+// stream-ordered and returns immediately.
+bool end_call(srtt_handle* h, bool must_sync) {
+  auto& ps = h->pset();
+  CK(cudaEventRecord(ps.done, h->stream));
+  ps.recorded = true;
+  return must_sync;
+}
+
 // Issues the device work of one decomposition: directly, or (use_graphs)
 // captured once per signature into a CUDA graph and replayed. The key holds
 // every pointer the work bakes in (workspace, parameter blob, input,
@@ -814,6 +857,44 @@ double kernel_pair(srtt_handle* h, int i) {
 // ==================================================================================
 // Sub-R-HOSVD
 // ==================================================================================
+// Synchronises the call and fills the report (achieved ranks come back
+// through mapped pinned memory written by the basis kernels).
+void finish_tucker(srtt_handle* h, Timer& tm, int d, const std::vector<int64_t>& ranks,
+                   const std::vector<int64_t>& samples, double t_sampling, std::vector<std::string>& warnings,
+                   srtt_report* rep) {
+  CK(cudaStreamSynchronize(h->stream));
+  CK(cudaGetLastError());
+  const int32_t* hi = h->hinfo;
+  for (int k = 0; k < d; ++k) {
+    const int q = hi[4 * k];
+    if (rep && rep->achieved_ranks) rep->achieved_ranks[k] = q;
+    if (q < ranks[k])
+      warnings.push_back("mode " + std::to_string(k) + ": sketch revealed rank " + std::to_string(q) +
+                         " < target " + std::to_string(ranks[k]) + "; basis padded");
+  }
+  if (rep) {
+    if (rep->sample_counts)
+      for (int k = 0; k < d; ++k) rep->sample_counts[k] = samples[k];
+    std::memset(rep->stage_seconds, 0, sizeof(rep->stage_seconds));
+    rep->stage_seconds[SRTT_STAGE_SAMPLING] = t_sampling;
+    rep->stage_seconds[SRTT_STAGE_H2D] = tm.between(0, 1);
+    rep->stage_seconds[SRTT_STAGE_SKETCH] = tm.between(2, 3);
+    rep->stage_seconds[SRTT_STAGE_SVD] = tm.between(3, 4);
+    rep->stage_seconds[SRTT_STAGE_TTM] = tm.between(4, 5);
+    rep->stage_seconds[SRTT_STAGE_FACTOR_WALL] = t_sampling + tm.between(2, 4);
+    rep->stage_seconds[SRTT_STAGE_D2H] = tm.between(5, 6);
+    rep->flags = hi[4 * d];
+    rep->reserved = 0;  // max Jacobi sweeps over the targets
+    for (int k = 0; k < d; ++k) rep->reserved = std::max(rep->reserved, hi[4 * k + 2]);
+    rep->kernel_seconds[0] = tm.between(2, 3);
+    rep->kernel_seconds[1] = tm.between(3, 4);
+    rep->kernel_seconds[2] = d >= 2 ? kernel_pair(h, 2) : 0.0;
+    rep->kernel_seconds[3] = 0.0;
+    rep->launches = h->launches;
+    write_warnings(rep, warnings);
+  }
+}
+
 void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d, const int64_t* dims_p,
                      const int64_t* ranks_p, int64_t p, const int64_t* samples_p, uint64_t seed,
                      const srtt_exec_policy* exec, double* core_out, double* const* factors_out,
@@ -842,6 +923,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
 
   DeviceGuard guard(h->device);
   h->launches = 0;
+  begin_call(h);
   Timer tm{h};
   tm.mark();  // 0
   const double* x = stage_input(h, x_in, x_on_device, N);
@@ -865,6 +947,52 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     state0[k] = srtt_host::stream_state0(seed, (uint64_t)k);
   }
   const double t_sampling = now_s() - ts0;
+
+  // --- fast path: a prepared call with the same signature only needs the
+  // seed-dependent blob fields patched and its CUDA graph replayed
+  std::string pkey;
+  if (h->use_graphs) {
+    pkey.reserve(256);
+    for (int k = 0; k < d; ++k) {
+      pkey += std::to_string(dims[k]);
+      pkey += ',';
+      pkey += std::to_string(ranks[k]);
+      pkey += ',';
+      pkey += std::to_string(samples[k]);
+      pkey += ',';
+      pkey += out_on_device ? ptr_key(factors_out[k]) : "h";
+      pkey += '|';
+    }
+    pkey += std::to_string(p) + "|" + ptr_key(x) + "|" + (out_on_device ? ptr_key(core_out) : "h") + "|" +
+            ptr_key(h->stream) + "|" + std::to_string(partitions) + "|" + std::to_string(h->cur);
+    auto pit = h->prepared.find(pkey);
+    if (pit != h->prepared.end() && pit->second.ws == h->ws.p && pit->second.dp == h->pset().d.p &&
+        pit->second.hp == h->pset().hst.p && h->graphs.count(pit->second.graph_key)) {
+      const srtt_handle::Prepared& pr = pit->second;
+      char* hp = reinterpret_cast<char*>(h->pset().hst.p);
+      std::memcpy(hp, pr.image.data(), pr.image.size());
+      for (int k = 0; k < d; ++k) {
+        std::memcpy(hp + pr.off_cols[k], cols[k].data(), sizeof(int64_t) * cols[k].size());
+        SketchTarget* skp = reinterpret_cast<SketchTarget*>(hp + pr.off_sk) + k;
+        skp->state0 = state0[k];
+        skp->draw_offset = draws[k];
+        BasisTarget* btp = reinterpret_cast<BasisTarget*>(hp + pr.off_bt) + k;
+        btp->state0 = state0[k];
+        btp->draw_offset = draws[k];
+      }
+      std::memset(h->hinfo, 0, sizeof(int32_t) * 4 * (d + 1));
+      tm.n = 2;
+      run_enqueue(h, pr.graph_key, [] { fail(SRTT_ERR_INTERNAL, "prepared graph missing"); });
+      tm.n = 6;
+      if (!out_on_device) {
+        copy_out(h, core_out, pr.d_core, sizeof(double) * prod(ranks), 0);
+        for (int k = 0; k < d; ++k) copy_out(h, factors_out[k], pr.udev[k], sizeof(double) * dims[k] * ranks[k], 0);
+      }
+      tm.mark();  // 6
+      if (end_call(h, rep || !out_on_device)) finish_tucker(h, tm, d, ranks, samples, t_sampling, warnings, rep);
+      return;
+    }
+  }
 
   // --- workspace layout
   Layout L;
@@ -911,8 +1039,8 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   std::vector<SketchTarget> sk(d);
   std::vector<BasisTarget> bt(d);
   int64_t ctas = 0;
-  h->dparams.ensure(blob.lay.off + 4096);
-  char* dp = reinterpret_cast<char*>(h->dparams.p);
+  h->pset().d.ensure(blob.lay.off + 4096);
+  char* dp = reinterpret_cast<char*>(h->pset().d.p);
   for (int k = 0; k < d; ++k) {
     const int c = (int)(ranks[k] + p);
     sk[k] = make_sketch_target(x, dims, {k}, samples[k], c);
@@ -927,10 +1055,10 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   }
   assign_basis_ctas(bt);
   const BasisLists lists = make_basis_lists(bt, blob);
-  h->dparams.ensure(blob.lay.off);
-  h->hparams.ensure(blob.lay.off);
-  dp = reinterpret_cast<char*>(h->dparams.p);
-  char* hp = reinterpret_cast<char*>(h->hparams.p);
+  h->pset().d.ensure(blob.lay.off);
+  h->pset().hst.ensure(blob.lay.off);
+  dp = reinterpret_cast<char*>(h->pset().d.p);
+  char* hp = reinterpret_cast<char*>(h->pset().hst.p);
   for (auto& it : blob.items) std::memcpy(hp + it.first, it.second.data(), it.second.size());
   std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * d);
   std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * d);
@@ -979,37 +1107,22 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     for (int k = 0; k < d; ++k) copy_out(h, factors_out[k], uptr[k], sizeof(double) * dims[k] * ranks[k], 0);
   }
   tm.mark();  // 6
-  CK(cudaStreamSynchronize(h->stream));
-  CK(cudaGetLastError());
-
-  for (int k = 0; k < d; ++k) {
-    const int q = hi[4 * k];
-    if (rep && rep->achieved_ranks) rep->achieved_ranks[k] = q;
-    if (q < ranks[k])
-      warnings.push_back("mode " + std::to_string(k) + ": sketch revealed rank " + std::to_string(q) +
-                         " < target " + std::to_string(ranks[k]) + "; basis padded");
+  if (h->use_graphs) {
+    srtt_handle::Prepared pr;
+    pr.image.assign(hp, hp + blob.lay.off);
+    pr.off_cols = off_cols;
+    pr.off_sk = off_sk;
+    pr.off_bt = off_bt;
+    pr.graph_key = key;
+    pr.ws = h->ws.p;
+    pr.dp = h->pset().d.p;
+    pr.hp = h->pset().hst.p;
+    pr.udev.assign(uptr.begin(), uptr.end());
+    pr.d_core = d_core;
+    if (h->prepared.size() > 64) h->prepared.clear();
+    h->prepared[pkey] = std::move(pr);
   }
-  if (rep) {
-    if (rep->sample_counts)
-      for (int k = 0; k < d; ++k) rep->sample_counts[k] = samples[k];
-    std::memset(rep->stage_seconds, 0, sizeof(rep->stage_seconds));
-    rep->stage_seconds[SRTT_STAGE_SAMPLING] = t_sampling;
-    rep->stage_seconds[SRTT_STAGE_H2D] = tm.between(0, 1);
-    rep->stage_seconds[SRTT_STAGE_SKETCH] = tm.between(2, 3);
-    rep->stage_seconds[SRTT_STAGE_SVD] = tm.between(3, 4);
-    rep->stage_seconds[SRTT_STAGE_TTM] = tm.between(4, 5);
-    rep->stage_seconds[SRTT_STAGE_FACTOR_WALL] = t_sampling + tm.between(2, 4);
-    rep->stage_seconds[SRTT_STAGE_D2H] = tm.between(5, 6);
-    rep->flags = hi[4 * d];
-    rep->reserved = 0;  // max Jacobi sweeps over the targets
-    for (int k = 0; k < d; ++k) rep->reserved = std::max(rep->reserved, hi[4 * k + 2]);
-    rep->kernel_seconds[0] = tm.between(2, 3);
-    rep->kernel_seconds[1] = tm.between(3, 4);
-    rep->kernel_seconds[2] = d >= 2 ? kernel_pair(h, 2) : 0.0;
-    rep->kernel_seconds[3] = 0.0;
-    rep->launches = h->launches;
-    write_warnings(rep, warnings);
-  }
+  if (end_call(h, rep || !out_on_device)) finish_tucker(h, tm, d, ranks, samples, t_sampling, warnings, rep);
 }
 
 }  // namespace
@@ -1039,6 +1152,7 @@ int srtt_create(const srtt_options* opts, srtt_handle** out) {
     CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
     for (auto& e : h->fj) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& ps : h->psets) CK(cudaEventCreateWithFlags(&ps.done, cudaEventDisableTiming));
     h->stream = h->own_stream;
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
     for (auto& e : h->kev) CK(cudaEventCreate(&e));
@@ -1062,6 +1176,7 @@ int srtt_destroy(srtt_handle* h) {
       cudaStreamDestroy(h->own_stream);
       cudaStreamDestroy(h->side);
       for (auto& e : h->fj) cudaEventDestroy(e);
+      for (auto& ps : h->psets) cudaEventDestroy(ps.done);
       if (h->hinfo) cudaFreeHost(h->hinfo);
     }
     delete h;
@@ -1245,6 +1360,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
 
   DeviceGuard guard(h->device);
   h->launches = 0;
+  begin_call(h);
   Timer tm{h};
   tm.mark();  // 0
   const double* x = stage_input(h, x_in, x_on_device, N);
@@ -1317,8 +1433,8 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   const size_t off_sk = blob.reserve(sizeof(SketchTarget) * nt);
   const size_t off_bt = blob.reserve(sizeof(BasisTarget) * nt);
   const size_t off_tt = blob.reserve(sizeof(TransferTarget) * std::max<size_t>(1, internal.size()));
-  h->dparams.ensure(blob.lay.off + 4096);
-  char* dp = reinterpret_cast<char*>(h->dparams.p);
+  h->pset().d.ensure(blob.lay.off + 4096);
+  char* dp = reinterpret_cast<char*>(h->pset().d.p);
   std::vector<SketchTarget> sk(nt);
   std::vector<BasisTarget> bt(nt);
   int64_t ctas = 0;
@@ -1342,9 +1458,9 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   }
   assign_basis_ctas(bt);
   const BasisLists lists = make_basis_lists(bt, blob);
-  h->dparams.ensure(blob.lay.off);
-  h->hparams.ensure(blob.lay.off);
-  char* hp = reinterpret_cast<char*>(h->hparams.p);
+  h->pset().d.ensure(blob.lay.off);
+  h->pset().hst.ensure(blob.lay.off);
+  char* hp = reinterpret_cast<char*>(h->pset().hst.p);
   for (auto& it : blob.items) std::memcpy(hp + it.first, it.second.data(), it.second.size());
   std::vector<TransferTarget> tt;
   int tctas = 0, max_rl = 1, max_rr = 1;
@@ -1437,6 +1553,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     }
   }
   tm.mark();  // 7
+  end_call(h, true);
   CK(cudaStreamSynchronize(h->stream));
   CK(cudaGetLastError());
   for (int t = 0; t < nt; ++t) {

@@ -47,6 +47,28 @@ struct Stream {
   }
 };
 
+// Open-addressing set of sampled indices (membership is all Floyd needs;
+// the reference's std::unordered_set gives identical results).
+struct IndexSet {
+  std::vector<int64_t> keys;
+  uint64_t mask = 0;
+  void reset(int64_t n) {
+    uint64_t cap = 16;
+    while (cap < static_cast<uint64_t>(4 * n + 4)) cap <<= 1;
+    keys.assign(cap, -1);
+    mask = cap - 1;
+  }
+  bool insert(int64_t k) {  // true if newly inserted
+    uint64_t i = mix64(static_cast<uint64_t>(k)) & mask;
+    while (keys[i] != -1) {
+      if (keys[i] == k) return false;
+      i = (i + 1) & mask;
+    }
+    keys[i] = k;
+    return true;
+  }
+};
+
 // Floyd's algorithm, indices in sampled order (sampling.hpp:14-32).
 inline void sample_indices(int64_t m, int64_t s, Stream& rng, std::vector<int64_t>& out) {
   if (s < 1 || s > m)
@@ -54,11 +76,11 @@ inline void sample_indices(int64_t m, int64_t s, Stream& rng, std::vector<int64_
                                 " m=" + std::to_string(m));
   out.clear();
   out.reserve(static_cast<size_t>(s));
-  std::unordered_set<int64_t> chosen;
-  chosen.reserve(static_cast<size_t>(s) * 2);
+  thread_local IndexSet chosen;
+  chosen.reset(s);
   for (int64_t j = m - s; j < m; ++j) {
     const int64_t t = static_cast<int64_t>(rng.bounded(static_cast<uint64_t>(j) + 1));
-    if (chosen.insert(t).second) {
+    if (chosen.insert(t)) {
       out.push_back(t);
     } else {
       chosen.insert(j);

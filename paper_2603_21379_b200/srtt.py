@@ -424,10 +424,12 @@ def sub_r_hosvd(x, target, oversampling, samples, seed, exec_policy=None, report
     for k in range(d):
         call.fptrs[k] = _ptr(outs[k + 1])[0]
     ex = exec_policy._c() if exec_policy is not None else None
+    # device outputs without a report: stream-ordered (asynchronous) call
+    rep_arg = C.byref(call.rep) if (report is not None or not device_out) else None
     _check(_L().srtt_sub_r_hosvd(h._h, xp, xdev, d, call.dims_a.ctypes.data, call.ranks_a.ctypes.data,
                                  int(oversampling), call.samp_a.ctypes.data, int(seed) & (2**64 - 1),
                                  C.byref(ex) if ex is not None else None, _ptr(outs[0])[0], call.fptrs,
-                                 int(device_out), C.byref(call.rep)))
+                                 int(device_out), rep_arg))
     if report is not None:
         _report_from(call.rep, d, call.ach, call.sc, report, h)
     if device_out:
