@@ -196,6 +196,33 @@ int srtt_root_transfer(srtt_handle* h, const double* x, int32_t x_on_device, int
                        int32_t rr, int32_t factors_on_device, double* b_out,
                        int32_t out_on_device);
 
+/* ---- slab-sharded Sub-R-HOSVD (one process per GPU) --------------------
+ * X is split along its LAST mode: the caller holds X[..., lo:hi) as a flat
+ * first-index-fastest tensor with dims[d-1] replaced by hi - lo; `dims`
+ * below are the GLOBAL extents. Every rank samples the same fibres and the
+ * same Omega (same seed). The three phases and the exchanges between them
+ * (the caller's collectives, e.g. NCCL via torch.distributed):
+ *   1. srtt_shard_sketches: z_out[k], k < d-1: dims[k] x (r_k+p) PARTIAL
+ *      sketch (fibres of other slabs contribute zero)  -> allreduce(sum);
+ *      z_out[d-1]: rows [lo, hi) of Z_{d-1}, (hi-lo) x (r+p) -> allgather.
+ *   2. srtt_bases_from_sketches: identical factors on every rank.
+ *   3. srtt_shard_core: this slab's partial core (U_{d-1} restricted to
+ *      rows [lo, hi))                                      -> allreduce(sum).
+ * This is sliced_core's slab algebra (parallel.hpp:355-445) across GPUs. */
+int srtt_shard_sketches(srtt_handle* h, const double* x_local, int32_t x_on_device, int32_t d,
+                        const int64_t* dims, int64_t slab_lo, int64_t slab_hi, const int64_t* ranks,
+                        int64_t oversampling, const int64_t* samples, uint64_t seed,
+                        const srtt_exec_policy* exec, double* const* z_out, int32_t out_on_device);
+int srtt_bases_from_sketches(srtt_handle* h, int32_t d, const int64_t* dims, const int64_t* ranks,
+                             int64_t oversampling, const int64_t* samples, uint64_t seed,
+                             const srtt_exec_policy* exec, const double* const* z, int32_t z_on_device,
+                             double* const* factors_out, int32_t out_on_device,
+                             int64_t* achieved_ranks);
+int srtt_shard_core(srtt_handle* h, const double* x_local, int32_t x_on_device, int32_t d,
+                    const int64_t* dims, int64_t slab_lo, int64_t slab_hi, const int64_t* ranks,
+                    const double* const* factors, int32_t factors_on_device, double* core_partial_out,
+                    int32_t out_on_device);
+
 #ifdef __cplusplus
 }
 #endif

@@ -749,6 +749,7 @@ SketchTarget make_sketch_target(const double* x, const std::vector<int64_t>& dim
   T.w = w;
   T.c = c;
   T.row_tile = (int)std::min<int64_t>(T.rows, 64);
+  T.slab_digit = -1;
   return T;
 }
 
@@ -1843,6 +1844,211 @@ int srtt_root_transfer(srtt_handle* h, const double* x, int32_t x_on_device, int
     // identical to the 2-mode core: B(0, j, k) = (U_l^T M U_r)(j, k)
     const int rc = srtt_multi_ttm_core(h, x, x_on_device, 2, dims2, ranks2, f, factors_on_device, b_out,
                                        out_on_device);
+    if (rc != SRTT_OK) throw Error{rc, g_last_error};
+  });
+}
+
+}  // extern "C"
+
+// ==================================================================================
+// Slab-sharded Sub-R-HOSVD phases (last-mode slabs)
+// ==================================================================================
+namespace {
+
+struct SampledModes {
+  std::vector<std::vector<int64_t>> cols;
+  std::vector<uint64_t> draws, state0;
+};
+
+SampledModes sample_all_modes(int d, const std::vector<int64_t>& dims, const std::vector<int64_t>& samples,
+                              uint64_t seed, int64_t partitions) {
+  SampledModes S;
+  S.cols.resize(d);
+  S.draws.resize(d);
+  S.state0.resize(d);
+  const int64_t N = prod(dims);
+  for (int k = 0; k < d; ++k) {
+    srtt_host::Stream rng(seed, (uint64_t)k);
+    try {
+      if (partitions > 1)
+        srtt_host::sample_indices_partitioned(N / dims[k], samples[k], partitions, rng, S.cols[k]);
+      else
+        srtt_host::sample_indices(N / dims[k], samples[k], rng, S.cols[k]);
+    } catch (const std::exception& e) {
+      fail(SRTT_ERR_JOB, "job " + std::to_string(k) + ": " + e.what());
+    }
+    S.draws[k] = rng.draws;
+    S.state0[k] = srtt_host::stream_state0(seed, (uint64_t)k);
+  }
+  return S;
+}
+
+void validate_tucker(int d, const std::vector<int64_t>& dims, const std::vector<int64_t>& ranks,
+                     const std::vector<int64_t>& samples, int64_t p) {
+  if (d < 2 || d > SRTT_MAX_ORDER) invalid("sub_r_hosvd: unsupported order");
+  for (int k = 0; k < d; ++k)
+    if (dims[k] < 1) invalid("Shape: dimensions must be >= 1");
+  const int64_t N = prod(dims);
+  for (int k = 0; k < d; ++k)
+    if (ranks[k] < 1 || ranks[k] > dims[k]) invalid("sub_r_hosvd: rank out of range in mode " + std::to_string(k));
+  for (int k = 0; k < d; ++k) {
+    if (samples[k] < ranks[k] + p)
+      invalid("sub_r_hosvd: samples below rank + oversampling in mode " + std::to_string(k));
+    if (samples[k] > N / dims[k]) invalid("sub_r_hosvd: more samples than fibers in mode " + std::to_string(k));
+    if (ranks[k] + p > SRTT_MAX_SKETCH_COLS)
+      invalid("sub_r_hosvd: rank + oversampling above 64 is not supported by the B200 basis kernel");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int srtt_shard_sketches(srtt_handle* h, const double* x_local, int32_t x_on_device, int32_t d, const int64_t* dims_p,
+                        int64_t slab_lo, int64_t slab_hi, const int64_t* ranks_p, int64_t p, const int64_t* samples_p,
+                        uint64_t seed, const srtt_exec_policy* exec, double* const* z_out, int32_t out_on_device) {
+  return guarded([&] {
+    if (!h) invalid("srtt: null handle");
+    std::vector<int64_t> dims(dims_p, dims_p + d), ranks(ranks_p, ranks_p + d), samples(samples_p, samples_p + d);
+    validate_tucker(d, dims, ranks, samples, p);
+    const int L = d - 1;
+    if (slab_lo < 0 || slab_hi > dims[L] || slab_lo >= slab_hi) invalid("shard: slab out of range");
+    std::vector<int64_t> ldims = dims;
+    ldims[L] = slab_hi - slab_lo;
+    const int64_t Nl = prod(ldims);
+    DeviceGuard g(h->device);
+    CompBufs B;
+    const double* x = to_device(h, B.a, x_local, Nl, x_on_device);
+    const SampledModes S = sample_all_modes(d, dims, samples, seed, exec ? exec->index_partitions : 1);
+    Layout Lw;
+    std::vector<size_t> off_z(d), off_cols(d);
+    int cmax = 0;
+    for (int k = 0; k < d; ++k) {
+      const int c = (int)(ranks[k] + p);
+      cmax = std::max(cmax, c);
+      off_z[k] = Lw.take(sizeof(double) * (k == L ? ldims[k] : dims[k]) * c);
+      off_cols[k] = Lw.take(sizeof(int64_t) * samples[k]);
+    }
+    const size_t off_t = Lw.take(sizeof(SketchTarget) * d);
+    const size_t off_flags = Lw.take(sizeof(int32_t) * 4);
+    B.b.ensure(Lw.off);
+    char* ws = reinterpret_cast<char*>(B.b.p);
+    std::vector<SketchTarget> sk(d);
+    int64_t ctas = 0;
+    for (int k = 0; k < d; ++k) {
+      const int c = (int)(ranks[k] + p);
+      if (k == L) {
+        sk[k] = make_sketch_target(x, ldims, {k}, samples[k], c);
+      } else {
+        sk[k] = make_sketch_target(x, dims, {k}, samples[k], c);  // decode columns over GLOBAL extents
+        sk[k].slab_digit = sk[k].ncol_modes - 1;                   // mode d-1 is the last complement digit
+        sk[k].slab_lo = slab_lo;
+        sk[k].slab_hi = slab_hi;
+      }
+      sk[k].cols = reinterpret_cast<const int64_t*>(ws + off_cols[k]);
+      sk[k].z = reinterpret_cast<double*>(ws + off_z[k]);
+      sk[k].state0 = S.state0[k];
+      sk[k].draw_offset = S.draws[k];
+      sk[k].cta_begin = ctas;
+      sk[k].flags = reinterpret_cast<int32_t*>(ws + off_flags);
+      ctas += (sk[k].rows + sk[k].row_tile - 1) / sk[k].row_tile;
+      CK(cudaMemcpyAsync(ws + off_cols[k], S.cols[k].data(), sizeof(int64_t) * samples[k], cudaMemcpyHostToDevice,
+                         h->stream));
+    }
+    CK(cudaMemsetAsync(ws + off_flags, 0, sizeof(int32_t) * 4, h->stream));
+    CK(cudaMemcpyAsync(ws + off_t, sk.data(), sizeof(SketchTarget) * d, cudaMemcpyHostToDevice, h->stream));
+    CK(srtt_launch_sketch(reinterpret_cast<const SketchTarget*>(ws + off_t), d, ctas, cmax, h->stream));
+    for (int k = 0; k < d; ++k)
+      copy_out(h, z_out[k], ws + off_z[k], sizeof(double) * sk[k].rows * sk[k].c, out_on_device);
+    CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int srtt_bases_from_sketches(srtt_handle* h, int32_t d, const int64_t* dims_p, const int64_t* ranks_p, int64_t p,
+                             const int64_t* samples_p, uint64_t seed, const srtt_exec_policy* exec,
+                             const double* const* z, int32_t z_on_device, double* const* factors_out,
+                             int32_t out_on_device, int64_t* achieved_ranks) {
+  return guarded([&] {
+    if (!h) invalid("srtt: null handle");
+    std::vector<int64_t> dims(dims_p, dims_p + d), ranks(ranks_p, ranks_p + d), samples(samples_p, samples_p + d);
+    validate_tucker(d, dims, ranks, samples, p);
+    DeviceGuard g(h->device);
+    const SampledModes S = sample_all_modes(d, dims, samples, seed, exec ? exec->index_partitions : 1);
+    CompBufs B;
+    Layout Lw;
+    std::vector<size_t> off_z(d), off_u(d);
+    std::vector<BasisPlan> bp(d);
+    std::vector<BasisBuffers> bb(d);
+    int64_t max_n = 0;
+    for (int k = 0; k < d; ++k) {
+      const int c = (int)(ranks[k] + p);
+      off_z[k] = Lw.take(sizeof(double) * dims[k] * c);
+      off_u[k] = Lw.take(sizeof(double) * dims[k] * ranks[k]);
+      bp[k] = plan_basis(dims[k], c, (int)ranks[k]);
+      bb[k] = layout_basis(Lw, bp[k]);
+      max_n = std::max(max_n, dims[k]);
+    }
+    const size_t off_pad = Lw.take(sizeof(double) * max_n * d);
+    const size_t off_t = Lw.take(sizeof(BasisTarget) * d);
+    const size_t off_info = Lw.take(sizeof(int32_t) * 4 * d);
+    B.b.ensure(Lw.off);
+    char* ws = reinterpret_cast<char*>(B.b.p);
+    std::vector<BasisTarget> bt(d);
+    for (int k = 0; k < d; ++k) {
+      const int c = (int)(ranks[k] + p);
+      // the basis overwrites its sketch: work on a private copy
+      CK(cudaMemcpyAsync(ws + off_z[k], z[k], sizeof(double) * dims[k] * c,
+                         z_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
+      bt[k] = fill_basis(bp[k], bb[k], ws, reinterpret_cast<double*>(ws + off_z[k]),
+                         reinterpret_cast<double*>(ws + off_u[k]), S.state0[k], S.draws[k], samples[k] * c,
+                         reinterpret_cast<int32_t*>(ws + off_info) + 4 * k);
+    }
+    assign_basis_ctas(bt);
+    Blob blob;
+    const BasisLists lists = make_basis_lists(bt, blob);
+    std::vector<unsigned char> hb(blob.lay.off);
+    for (auto& it : blob.items) std::memcpy(hb.data() + it.first, it.second.data(), it.second.size());
+    B.c.ensure(hb.size() + 64);
+    CK(cudaMemcpyAsync(B.c.p, hb.data(), hb.size(), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(ws + off_t, bt.data(), sizeof(BasisTarget) * d, cudaMemcpyHostToDevice, h->stream));
+    launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(ws + off_t), lists,
+                       reinterpret_cast<const char*>(B.c.p), reinterpret_cast<double*>(ws + off_pad), max_n);
+    for (int k = 0; k < d; ++k)
+      copy_out(h, factors_out[k], ws + off_u[k], sizeof(double) * dims[k] * ranks[k], out_on_device);
+    std::vector<int32_t> info(4 * d);
+    CK(cudaMemcpyAsync(info.data(), ws + off_info, sizeof(int32_t) * 4 * d, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (achieved_ranks)
+      for (int k = 0; k < d; ++k) achieved_ranks[k] = info[4 * k];
+  });
+}
+
+int srtt_shard_core(srtt_handle* h, const double* x_local, int32_t x_on_device, int32_t d, const int64_t* dims_p,
+                    int64_t slab_lo, int64_t slab_hi, const int64_t* ranks_p, const double* const* factors,
+                    int32_t factors_on_device, double* core_partial_out, int32_t out_on_device) {
+  return guarded([&] {
+    if (!h) invalid("srtt: null handle");
+    if (d < 2 || d > SRTT_MAX_ORDER) invalid("shard_core: unsupported order");
+    std::vector<int64_t> dims(dims_p, dims_p + d), ranks(ranks_p, ranks_p + d);
+    const int L = d - 1;
+    if (slab_lo < 0 || slab_hi > dims[L] || slab_lo >= slab_hi) invalid("shard: slab out of range");
+    std::vector<int64_t> ldims = dims;
+    ldims[L] = slab_hi - slab_lo;
+    DeviceGuard g(h->device);
+    CompBufs B;
+    // U_{d-1} rows [lo, hi) as a contiguous (hi-lo) x r block
+    const int64_t nl = slab_hi - slab_lo;
+    B.d.ensure(sizeof(double) * nl * ranks[L]);
+    CK(cudaMemcpy2DAsync(B.d.p, sizeof(double) * nl, factors[L] + slab_lo, sizeof(double) * dims[L],
+                         sizeof(double) * nl, ranks[L],
+                         factors_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
+    std::vector<const double*> f(factors, factors + d);
+    f[L] = reinterpret_cast<const double*>(B.d.p);
+    // the local factor is on the device now; stage the others the same way
+    std::vector<DevBuf> fb(d);
+    for (int k = 0; k < L; ++k) f[k] = to_device(h, fb[k], factors[k], dims[k] * ranks[k], factors_on_device);
+    const int rc = srtt_multi_ttm_core(h, x_local, x_on_device, d, ldims.data(), ranks.data(), f.data(), 1,
+                                       core_partial_out, out_on_device);
     if (rc != SRTT_OK) throw Error{rc, g_last_error};
   });
 }

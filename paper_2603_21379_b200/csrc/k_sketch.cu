@@ -88,20 +88,26 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
       int64_t col = T.cols[j0 + jl], b = 0;
       for (int mm = 0; mm < T.ncol_modes; ++mm) {
         const int64_t dm = T.col_dim[mm];
-        b += (col % dm) * T.col_stride[mm];
+        int64_t dig = col % dm;
+        if (mm == T.slab_digit) {
+          if (dig < T.slab_lo || dig >= T.slab_hi) b = INT64_MIN / 2;  // not in this slab
+          dig -= T.slab_lo;
+        }
+        b += dig * T.col_stride[mm];
         col /= dm;
       }
-      base[jl] = b;
+      base[jl] = b < 0 ? -1 : b;
     }
     __syncthreads();
     if (active) {
       int jl = js;
       // 4 independent loads in flight per thread before the FMAs.
       for (; jl + 3 * JS < jn; jl += 4 * JS) {
-        const double v0 = __ldg(x + base[jl] + roff);
-        const double v1 = __ldg(x + base[jl + JS] + roff);
-        const double v2 = __ldg(x + base[jl + 2 * JS] + roff);
-        const double v3 = __ldg(x + base[jl + 3 * JS] + roff);
+        const int64_t b0 = base[jl], b1 = base[jl + JS], b2 = base[jl + 2 * JS], b3 = base[jl + 3 * JS];
+        const double v0 = b0 >= 0 ? __ldg(x + b0 + roff) : 0.0;
+        const double v1 = b1 >= 0 ? __ldg(x + b1 + roff) : 0.0;
+        const double v2 = b2 >= 0 ? __ldg(x + b2 + roff) : 0.0;
+        const double v3 = b3 >= 0 ? __ldg(x + b3 + roff) : 0.0;
         const double* o0 = om + jl * c;
         const double* o1 = o0 + JS * c;
         const double* o2 = o1 + JS * c;
@@ -111,7 +117,8 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
           if (cc < c) acc[cc] += v0 * o0[cc] + v1 * o1[cc] + v2 * o2[cc] + v3 * o3[cc];
       }
       for (; jl < jn; jl += JS) {
-        const double v = __ldg(x + base[jl] + roff);
+        const int64_t bj = base[jl];
+        const double v = bj >= 0 ? __ldg(x + bj + roff) : 0.0;
         const double* o = om + jl * c;
 #pragma unroll
         for (int cc = 0; cc < CMAX; ++cc)

@@ -33,6 +33,12 @@ typedef struct SketchTarget {
   uint64_t draw_offset;   // u64 draws consumed by the sampling step
   int64_t cta_begin;      // first CTA index of this target in the grouped grid
   int32_t* flags;         // device status word (bit 0: Box-Muller u1 == 0 met)
+  // slab sharding: the column digit at position slab_digit (of the
+  // complement decode) must lie in [slab_lo, slab_hi); fibres outside the
+  // local slab contribute zero, inside ones are shifted by slab_lo*stride
+  int32_t slab_digit;     // -1: no slab restriction
+  int32_t pad0;
+  int64_t slab_lo, slab_hi;
 } SketchTarget;
 
 // ---------------------------------------------------------------------------
