@@ -12,8 +12,12 @@ Tucker 40^5, 1.02e8 entries, 819 MB > L2, so no L2 flush is needed).
 numpy + OpenBLAS on all host cores; the reference itself needs Eigen, absent
 in this image) on the same config.
 
-Multi-GPU (torchrun): each rank decomposes its own replica (seed = rank),
-weak scaling, no data-path collective; time = max over ranks.
+Multi-GPU (torchrun): by default each rank decomposes its own replica
+(seed = rank), weak scaling, no data-path collective; time = max over ranks.
+``--mode sharded`` instead decomposes ONE tensor whose last mode is split
+into per-rank slabs of the config's size (global last extent = N x the
+config's), through paper_2603_21379_b200.sharded (partial sketches ->
+NCCL allreduce/allgather -> bases -> partial core -> allreduce).
 """
 from __future__ import annotations
 
@@ -313,6 +317,65 @@ def run_product(args):
         torch.distributed.destroy_process_group()
 
 
+def run_sharded(args):
+    """One slab-sharded decomposition per step (Tucker configs)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = _dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if not dist.is_initialized():
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    import paper_2603_21379_b200 as P
+    from paper_2603_21379_b200 import sharded, synth
+
+    cfg = synth.CONFIGS[args.config]
+    if cfg.kind != "tucker":
+        raise SystemExit("--mode sharded runs the Tucker configs (c1, c2, c3, c5)")
+    dims = list(cfg.dims[:-1]) + [cfg.dims[-1] * world]
+    x_local = synth.make_tensor(cfg, seed=rank, backend="torch", device=f"cuda:{local}")   # this rank's slab
+    h = P.Handle(local, use_graphs=False)
+    stream = torch.cuda.current_stream()
+    h.set_stream(stream.cuda_stream)
+    ph = sharded.GpuShardPhases(h)
+    ranks = [cfg.rank] * cfg.order
+    samples = [min(4 * (cfg.rank + cfg.p), int(np.prod(dims)) // n) for n in dims]
+
+    def step():
+        return sharded.sub_r_hosvd_sharded(x_local, dims, ranks, cfg.p, samples, 0, phases=ph)
+
+    for _ in range(args.warmup):
+        step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    ev1.synchronize()
+    sampler.stop()
+    el = torch.tensor([ev0.elapsed_time(ev1) / 1e3], dtype=torch.float64, device=dev)
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    elapsed = float(el.item())
+    total = int(np.prod(dims))
+    line = {"metric": METRIC, "value": total * args.steps / elapsed, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": dict(_config_dict(cfg), dims=dims, entries=total, parallelism=f"slab-sharded x{world}"),
+            "clocks": sampler.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def _traffic_from_profiles(cfg_name):
     """dram bytes per core-kernel launch from the committed ncu capture."""
     path = os.path.join(ROOT, "profiles", f"ncu_core_{cfg_name}.json")
@@ -331,11 +394,15 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", choices=["replicas", "sharded"], default="replicas",
+                    help="N>1: independent replicas (default) or one slab-sharded tensor")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.mode == "sharded":
+        run_sharded(args)
     else:
         run_product(args)
 

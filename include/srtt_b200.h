@@ -196,6 +196,34 @@ int srtt_root_transfer(srtt_handle* h, const double* x, int32_t x_on_device, int
                        int32_t rr, int32_t factors_on_device, double* b_out,
                        int32_t out_on_device);
 
+/* ---- reconstruction and error (the step after the path) -----------------
+ * rel_error(reference, approx) = ||ref - approx||_F / ||ref||_F
+ * (tensor.hpp:241-249; zero-norm reference -> INVALID_ARGUMENT). */
+int srtt_rel_error(srtt_handle* h, const double* ref, const double* approx, int32_t on_device, int64_t n,
+                   double* rel_error);
+/* reconstruct (tucker.hpp:18-28): out = G x_0 U_0 ... x_{d-1} U_{d-1}
+ * (prod dims doubles, first index fastest). core: prod ranks; factors[k]:
+ * dims[k] x ranks[k] column-major. */
+int srtt_tucker_reconstruct(srtt_handle* h, int32_t d, const int64_t* dims, const int64_t* ranks,
+                            const double* core, const double* const* factors, int32_t in_on_device,
+                            double* out, int32_t out_on_device);
+/* rel_error(x, reconstruct(t)) streamed tile by tile: X-hat is never
+ * materialised (experiment.cpp:248). */
+int srtt_tucker_rel_error(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d,
+                          const int64_t* dims, const int64_t* ranks, const double* core,
+                          const double* const* factors, int32_t in_on_device, double* rel_error);
+/* ht_reconstruct (htucker.hpp:346-378); leaf_factors by MODE, transfers by
+ * node id as srtt_sub_r_rtl_ht returns them; ranks per node (root = 1). */
+int srtt_ht_reconstruct(srtt_handle* h, int32_t d, const int64_t* dims, const srtt_tree* tree,
+                        const int64_t* ranks, const double* const* leaf_factors,
+                        const double* const* transfers, int32_t in_on_device, double* out,
+                        int32_t out_on_device);
+/* rel_error(x, ht_reconstruct(h)) streamed (experiment.cpp:266). */
+int srtt_ht_rel_error(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d,
+                      const int64_t* dims, const srtt_tree* tree, const int64_t* ranks,
+                      const double* const* leaf_factors, const double* const* transfers,
+                      int32_t in_on_device, double* rel_error);
+
 /* ---- slab-sharded Sub-R-HOSVD (one process per GPU) --------------------
  * X is split along its LAST mode: the caller holds X[..., lo:hi) as a flat
  * first-index-fastest tensor with dims[d-1] replaced by hi - lo; `dims`

@@ -43,6 +43,14 @@ cudaError_t srtt_launch_transpose(const double*, int64_t, int, double*, cudaStre
 cudaError_t srtt_launch_prep_all(const CoreParams&, CoreItem*, const double*, int64_t, int, int, int, int, double*,
                                  int, const double* const*, double* const*, const int64_t*, const int*, cudaStream_t);
 cudaError_t srtt_launch_ttm(const TtmParams&, cudaStream_t);
+int srtt_residual_grid(int sms, int64_t nA, int K);
+int srtt_residual_tile_rows(int64_t nA);
+cudaError_t srtt_launch_residual(const CUtensorMap*, const ResidualParams&, int, double*, cudaStream_t);
+cudaError_t srtt_launch_pad_rows(const double*, int64_t, int64_t, int64_t, double*, cudaStream_t);
+int srtt_residual_tile_cols(int64_t nA, int K);
+cudaError_t srtt_launch_diff_norm(const double*, const double*, int64_t, int, double*, double*, cudaStream_t);
+cudaError_t srtt_launch_kron_rows(const KronParams&, cudaStream_t);
+cudaError_t srtt_launch_mat_transpose(const double*, int64_t, int64_t, double*, cudaStream_t);
 
 typedef struct TransferTarget {
   const double* us;
@@ -207,6 +215,18 @@ void encode_tmap(CUtensorMap* map, const double* x, int64_t n0, int64_t Q, int W
   if (r != CUDA_SUCCESS) fail(SRTT_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
+// Plain (unswizzled) 2-D fp64 map: d0 fastest, row pitch ld0 elements.
+void encode_tmap_plain(CUtensorMap* map, const double* p, int64_t d0, int64_t d1, int64_t ld0, int box0, int box1) {
+  cuuint64_t gdim[2] = {(cuuint64_t)d0, (cuuint64_t)d1};
+  cuuint64_t gstride[1] = {(cuuint64_t)ld0 * sizeof(double)};
+  cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)box1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(p), gdim, gstride, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(SRTT_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
 int64_t prod(const std::vector<int64_t>& v, int lo = 0, int hi = 1 << 30) {
   int64_t p = 1;
   const int e = std::min<int>(hi, (int)v.size());
@@ -231,6 +251,7 @@ struct srtt_handle {
   cudaEvent_t kev[8] = {};  // per-kernel pairs: [2i] start, [2i+1] end
   DevBuf xbuf;     // device copy of host inputs
   DevBuf ws;       // workspace arena
+  DevBuf rb[6];    // reconstruction / error buffers (At, Ct ping-pong, staging), reused across calls
   // Double-buffered parameter blobs (pinned host + device copy): a call
   // may return before its graph ran (device outputs, no report), so the
   // next call writes the other set; a set is reused only after the call
@@ -2050,6 +2071,360 @@ int srtt_shard_core(srtt_handle* h, const double* x_local, int32_t x_on_device, 
     const int rc = srtt_multi_ttm_core(h, x_local, x_on_device, d, ldims.data(), ranks.data(), f.data(), 1,
                                        core_partial_out, out_on_device);
     if (rc != SRTT_OK) throw Error{rc, g_last_error};
+  });
+}
+
+}  // extern "C"
+
+// ==================================================================================
+// Reconstruction and streaming reconstruction error
+// ==================================================================================
+namespace {
+
+// out = in x_mode U with in viewed as g x r x post and U an n x r factor,
+// given column-major (kfast = false) or K-fastest r x n (kfast = true).
+void ttm_expand(srtt_handle* h, const double* in, int64_t g, int64_t r, int64_t post, const double* u, int64_t n,
+                bool kfast, double* out) {
+  TtmParams T{};
+  T.in = in;
+  T.u = u;
+  T.out = out;
+  T.g = g;
+  T.n = r;
+  T.post = post;
+  T.rr = n;
+  T.transpose = kfast ? 1 : 0;
+  T.nparts = 1;
+  CK(srtt_launch_ttm(T, h->stream));
+}
+
+// Low-rank view X-hat = A C^T of the n_A x n_B unfolding, factors K-fastest
+// with K zero-padded to a multiple of 8 (At: K x n_A, Ct: K x n_B).
+struct LowRank {
+  const double* at = nullptr;
+  const double* ct = nullptr;
+  int64_t nA = 0, nB = 0;
+  int K = 0;
+};
+
+int64_t pad8(int64_t k) { return (k + 7) / 8 * 8; }
+
+// Streams A C^T against x (norms) or into out (reconstruction).
+void run_residual(srtt_handle* h, const LowRank& lr, const double* x, double* out, double* sums_host) {
+  const int grid = srtt_residual_grid(h->sms, lr.nA, lr.K);
+  DevBuf& part = h->rb[4];
+  part.ensure(sizeof(double) * (2 * grid + 2));
+  ResidualParams P{};
+  P.x = x;
+  P.at = lr.at;
+  P.ct = lr.ct;
+  P.out = out;
+  P.partial = reinterpret_cast<double*>(part.p);
+  P.nA = lr.nA;
+  P.nB = lr.nB;
+  P.K = lr.K;
+  const int tm = srtt_residual_tile_rows(lr.nA), tn = srtt_residual_tile_cols(lr.nA, lr.K);
+  CUtensorMap tmx;
+  std::memset(&tmx, 0, sizeof(tmx));
+  // TMA needs a 16-byte row pitch: odd n_A streams X with cp.async instead
+  P.x_tma = (x != nullptr && lr.nA % 2 == 0) ? 1 : 0;
+  if (P.x_tma) encode_tmap_plain(&tmx, x, lr.nA, lr.nB, lr.nA, tm, tn);
+  double* sums = reinterpret_cast<double*>(part.p) + 2 * grid;
+  CK(srtt_launch_residual(&tmx, P, grid, sums, h->stream));
+  if (!out) {
+    CK(cudaMemcpyAsync(sums_host, sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  }
+}
+
+double rel_from_sums(const double* s) {
+  if (s[1] == 0.0) invalid("rel_error: reference tensor has zero norm");
+  return std::sqrt(s[0]) / std::sqrt(s[1]);
+}
+
+// Tucker: X-hat_(0..m-1) = (U_{m-1} (x) ... (x) U_0) [G x_m U_m ... x_{d-1} U_{d-1}]^T.
+// The split m comes from a cost model: FP64 FMAs of the tiled residual
+// vs the bytes of X and Ct.
+struct TuckerLowRank {
+  explicit TuckerLowRank(srtt_handle* h) : at(h->rb[0]), tmp(h->rb[1]), c0(h->rb[2]), c1(h->rb[3]) {}
+  LowRank lr;
+  DevBuf &at, &tmp, &c0, &c1;
+  std::vector<DevBuf> fb;
+  DevBuf gb;
+};
+
+void build_tucker_lowrank(srtt_handle* h, TuckerLowRank& T, int d, const std::vector<int64_t>& dims,
+                          const std::vector<int64_t>& ranks, const double* core, const double* const* factors,
+                          int on_device) {
+  for (int k = 0; k < d; ++k)
+    if (ranks[k] < 1 || ranks[k] > dims[k] || dims[k] < 1)
+      invalid("reconstruct: factor/core mismatch in mode " + std::to_string(k));
+  if (ranks[0] > 64) invalid("reconstruct: ranks above 64 are not supported by the B200 residual kernel");
+  T.fb.resize(d);
+  std::vector<const double*> u(d);
+  for (int k = 0; k < d; ++k) u[k] = to_device(h, T.fb[k], factors[k], dims[k] * ranks[k], on_device);
+  const double* g = to_device(h, T.gb, core, prod(ranks), on_device);
+  int best = 1;
+  double best_cost = 0;
+  int64_t KA = 1, nA = 1;
+  for (int m = 1; m < d; ++m) {
+    KA *= ranks[m - 1];
+    nA *= dims[m - 1];
+    if (KA > 64) break;
+    const int64_t nB = prod(dims) / nA;
+    const int tm = srtt_residual_tile_rows(nA);
+    const double rows_eff = (double)((nA + tm - 1) / tm * tm);
+    const double fma_s = rows_eff * nB * (double)pad8(KA) / (58.0 * h->sms * 1.9e9);
+    const double mem_s = (8.0 * nA * nB + 16.0 * nB * pad8(KA)) / 6.5e12;
+    const double cost = std::max(fma_s, mem_s);
+    if (m == 1 || cost < best_cost) {
+      best = m;
+      best_cost = cost;
+    }
+  }
+  const int m = best;
+  int64_t K = 1;
+  T.lr.nA = 1;
+  for (int k = 0; k < m; ++k) {
+    K *= ranks[k];
+    T.lr.nA *= dims[k];
+  }
+  const int64_t Kp = pad8(K);
+  T.lr.nB = prod(dims) / T.lr.nA;
+  T.lr.K = (int)Kp;
+  // At = (U_{m-1} (x) ... (x) U_0)^T, K x n_A, then zero-padded to Kp rows
+  T.tmp.ensure(sizeof(double) * std::max<int64_t>(K * T.lr.nA, prod(ranks)));
+  double* tmp = reinterpret_cast<double*>(T.tmp.p);
+  if (m == 1) {
+    CK(srtt_launch_mat_transpose(u[0], dims[0], ranks[0], tmp, h->stream));
+  } else {
+    KronParams kp{};
+    for (int k = 0; k < m; ++k) {
+      kp.u[k] = u[k];
+      kp.n[k] = dims[k];
+      kp.r[k] = ranks[k];
+    }
+    kp.at = tmp;
+    kp.K = K;
+    kp.nA = T.lr.nA;
+    kp.m = m;
+    CK(srtt_launch_kron_rows(kp, h->stream));
+  }
+  T.at.ensure(sizeof(double) * Kp * T.lr.nA);
+  CK(srtt_launch_pad_rows(tmp, K, T.lr.nA, Kp, reinterpret_cast<double*>(T.at.p), h->stream));
+  // Ct = G' x_1 U_m ... with G' the core as Kp x r_m x ... (zero rows K..Kp-1)
+  std::vector<int64_t> ext = {Kp}, full = {Kp};
+  for (int k = m; k < d; ++k) {
+    ext.push_back(ranks[k]);
+    full.push_back(dims[k]);
+  }
+  const int e = (int)ext.size();
+  size_t maxe = (size_t)prod(ext);
+  {
+    std::vector<int64_t> cur = ext;
+    for (int k = 1; k < e; ++k) {
+      cur[k] = full[k];
+      maxe = std::max<size_t>(maxe, (size_t)prod(cur));
+    }
+  }
+  T.c0.ensure(sizeof(double) * maxe);
+  T.c1.ensure(sizeof(double) * maxe);
+  double* bufs[2] = {reinterpret_cast<double*>(T.c0.p), reinterpret_cast<double*>(T.c1.p)};
+  CK(srtt_launch_pad_rows(g, K, prod(ranks) / K, Kp, bufs[1], h->stream));
+  const double* cur = bufs[1];
+  for (int k = 1; k < e; ++k) {
+    int64_t gpre = 1, post = 1;
+    for (int j = 0; j < k; ++j) gpre *= ext[j];
+    for (int j = k + 1; j < e; ++j) post *= ext[j];
+    double* o = bufs[(k - 1) & 1];
+    ttm_expand(h, cur, gpre, ext[k], post, u[m + k - 1], full[k], false, o);
+    ext[k] = full[k];
+    cur = o;
+  }
+  T.lr.at = reinterpret_cast<const double*>(T.at.p);
+  T.lr.ct = cur;
+}
+
+// H-Tucker: node bases rebuilt bottom-up in K-fastest layout (r_S x n_S),
+// then At = U_left^T, Ct = B_0 U_right^T (htucker.hpp:346-378).
+struct HtLowRank {
+  explicit HtLowRank(srtt_handle* h) : w(h->rb[1]), at(h->rb[0]), ct(h->rb[2]) {}
+  LowRank lr;
+  std::vector<DevBuf> nb;     // per node: K-fastest basis (internal nodes) / staged leaf factor
+  std::vector<DevBuf> tb;     // staged transfers
+  DevBuf &w, &at, &ct;
+  DevBuf tmp, b0;
+};
+
+void build_ht_lowrank(srtt_handle* h, HtLowRank& H, const Tree& tr, const std::vector<int64_t>& dims,
+                      const std::vector<int64_t>& ranks, const double* const* leaf_factors,
+                      const double* const* transfers, int on_device) {
+  const int nn = tr.n;
+  auto rows = [&](int i) {
+    int64_t r = 1;
+    for (int m : tr.modes[i]) r *= dims[m];
+    return r;
+  };
+  if (ranks[0] != 1) invalid("ht_reconstruct: root rank must be 1");
+  for (int i = 1; i < nn; ++i)
+    if (ranks[i] < 1) invalid("ht_reconstruct: rank out of range at node " + std::to_string(i));
+  H.nb.resize(nn);
+  H.tb.resize(nn);
+  std::vector<const double*> basis(nn, nullptr), B(nn, nullptr);
+  std::vector<bool> kfast(nn, false);
+  for (int i = 0; i < nn; ++i) {
+    if (tr.leaf(i)) {
+      const int m = tr.modes[i][0];
+      basis[i] = to_device(h, H.nb[i], leaf_factors[m], dims[m] * ranks[i], on_device);
+    } else {
+      const int64_t cnt = ranks[i] * ranks[tr.left[i]] * ranks[tr.right[i]];
+      B[i] = to_device(h, H.tb[i], transfers[i], cnt, on_device);
+    }
+  }
+  // bottom-up: deepest nodes first
+  std::vector<int> order;
+  for (int i = 1; i < nn; ++i)
+    if (!tr.leaf(i)) order.push_back(i);
+  std::vector<int> depth(nn, 0);
+  for (int i = 1; i < nn; ++i) depth[i] = depth[tr.parent[i]] + 1;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return depth[a] > depth[b]; });
+  size_t wmax = 1;
+  for (int i : order)
+    wmax = std::max<size_t>(wmax, (size_t)(ranks[i] * rows(tr.left[i]) * ranks[tr.right[i]]));
+  H.w.ensure(sizeof(double) * wmax);
+  for (int i : order) {
+    const int l = tr.left[i], r = tr.right[i];
+    const int64_t rs = ranks[i], rl = ranks[l], rr = ranks[r], nl = rows(l), nr = rows(r);
+    double* w = reinterpret_cast<double*>(H.w.p);
+    // W = B x_2 U_l: (rs, nl, rr); V = W x_3 U_r: (rs, nl, nr) = K-fastest basis
+    ttm_expand(h, B[i], rs, rl, rr, basis[l], nl, kfast[l], w);
+    H.nb[i].ensure(sizeof(double) * rs * nl * nr);
+    ttm_expand(h, w, rs * nl, rr, 1, basis[r], nr, kfast[r], reinterpret_cast<double*>(H.nb[i].p));
+    basis[i] = reinterpret_cast<const double*>(H.nb[i].p);
+    kfast[i] = true;
+  }
+  const int l = tr.left[0], r = tr.right[0];
+  const int64_t rl = ranks[l], rr = ranks[r], nl = rows(l), nr = rows(r);
+  if (rl > 64) invalid("ht_reconstruct: root-child ranks above 64 are not supported by the B200 residual kernel");
+  const int64_t Kp = pad8(rl);
+  const double* at_k = basis[l];
+  if (!kfast[l]) {
+    H.tmp.ensure(sizeof(double) * rl * nl);
+    CK(srtt_launch_mat_transpose(basis[l], nl, rl, reinterpret_cast<double*>(H.tmp.p), h->stream));
+    at_k = reinterpret_cast<const double*>(H.tmp.p);
+  }
+  H.at.ensure(sizeof(double) * Kp * nl);
+  CK(srtt_launch_pad_rows(at_k, rl, nl, Kp, reinterpret_cast<double*>(H.at.p), h->stream));
+  H.b0.ensure(sizeof(double) * Kp * rr);
+  CK(srtt_launch_pad_rows(B[0], rl, rr, Kp, reinterpret_cast<double*>(H.b0.p), h->stream));
+  H.ct.ensure(sizeof(double) * Kp * nr);
+  ttm_expand(h, reinterpret_cast<const double*>(H.b0.p), Kp, rr, 1, basis[r], nr, kfast[r],
+             reinterpret_cast<double*>(H.ct.p));
+  H.lr.at = reinterpret_cast<const double*>(H.at.p);
+  H.lr.ct = reinterpret_cast<const double*>(H.ct.p);
+  H.lr.nA = nl;
+  H.lr.nB = nr;
+  H.lr.K = (int)Kp;
+}
+
+void finish_reconstruct(srtt_handle* h, const LowRank& lr, double* out, int out_on_device) {
+  const int64_t N = lr.nA * lr.nB;
+  DevBuf ob;
+  double* dst = out;
+  if (!out_on_device) {
+    ob.ensure(sizeof(double) * N);
+    dst = reinterpret_cast<double*>(ob.p);
+  }
+  run_residual(h, lr, nullptr, dst, nullptr);
+  if (!out_on_device) copy_out(h, out, dst, sizeof(double) * N, 0);
+  CK(cudaStreamSynchronize(h->stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+int srtt_rel_error(srtt_handle* h, const double* ref, const double* approx, int32_t on_device, int64_t n,
+                   double* rel_error) {
+  return guarded([&] {
+    if (!h) invalid("srtt: null handle");
+    if (n < 1) invalid("rel_error: empty tensor");
+    DeviceGuard g(h->device);
+    CompBufs B;
+    const double* x = to_device(h, B.a, ref, n, on_device);
+    const double* y = to_device(h, B.b, approx, n, on_device);
+    const int grid = 2 * h->sms;
+    B.c.ensure(sizeof(double) * (2 * grid + 2));
+    double* part = reinterpret_cast<double*>(B.c.p);
+    CK(srtt_launch_diff_norm(x, y, n, grid, part, part + 2 * grid, h->stream));
+    double s[2];
+    CK(cudaMemcpyAsync(s, part + 2 * grid, sizeof(s), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    *rel_error = rel_from_sums(s);
+  });
+}
+
+int srtt_tucker_reconstruct(srtt_handle* h, int32_t d, const int64_t* dims, const int64_t* ranks, const double* core,
+                            const double* const* factors, int32_t in_on_device, double* out, int32_t out_on_device) {
+  return guarded([&] {
+    if (!h) invalid("srtt: null handle");
+    if (d < 2 || d > SRTT_MAX_ORDER) invalid("reconstruct: unsupported order");
+    DeviceGuard g(h->device);
+    TuckerLowRank T(h);
+    build_tucker_lowrank(h, T, d, std::vector<int64_t>(dims, dims + d), std::vector<int64_t>(ranks, ranks + d), core,
+                         factors, in_on_device);
+    finish_reconstruct(h, T.lr, out, out_on_device);
+  });
+}
+
+int srtt_tucker_rel_error(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d, const int64_t* dims,
+                          const int64_t* ranks, const double* core, const double* const* factors,
+                          int32_t in_on_device, double* rel_error) {
+  return guarded([&] {
+    if (!h) invalid("srtt: null handle");
+    if (d < 2 || d > SRTT_MAX_ORDER) invalid("rel_error: unsupported order");
+    DeviceGuard g(h->device);
+    std::vector<int64_t> dv(dims, dims + d);
+    TuckerLowRank T(h);
+    build_tucker_lowrank(h, T, d, dv, std::vector<int64_t>(ranks, ranks + d), core, factors, in_on_device);
+    CompBufs B;
+    const double* dx = to_device(h, B.a, x, prod(dv), x_on_device);
+    double s[2];
+    run_residual(h, T.lr, dx, nullptr, s);
+    *rel_error = rel_from_sums(s);
+  });
+}
+
+int srtt_ht_reconstruct(srtt_handle* h, int32_t d, const int64_t* dims, const srtt_tree* tree, const int64_t* ranks,
+                        const double* const* leaf_factors, const double* const* transfers, int32_t in_on_device,
+                        double* out, int32_t out_on_device) {
+  return guarded([&] {
+    if (!h) invalid("srtt: null handle");
+    const Tree tr = read_tree(tree, d);
+    DeviceGuard g(h->device);
+    HtLowRank H(h);
+    build_ht_lowrank(h, H, tr, std::vector<int64_t>(dims, dims + d), std::vector<int64_t>(ranks, ranks + tr.n),
+                     leaf_factors, transfers, in_on_device);
+    finish_reconstruct(h, H.lr, out, out_on_device);
+  });
+}
+
+int srtt_ht_rel_error(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d, const int64_t* dims,
+                      const srtt_tree* tree, const int64_t* ranks, const double* const* leaf_factors,
+                      const double* const* transfers, int32_t in_on_device, double* rel_error) {
+  return guarded([&] {
+    if (!h) invalid("srtt: null handle");
+    const Tree tr = read_tree(tree, d);
+    DeviceGuard g(h->device);
+    std::vector<int64_t> dv(dims, dims + d);
+    HtLowRank H(h);
+    build_ht_lowrank(h, H, tr, dv, std::vector<int64_t>(ranks, ranks + tr.n), leaf_factors, transfers,
+                     in_on_device);
+    CompBufs B;
+    const double* dx = to_device(h, B.a, x, prod(dv), x_on_device);
+    double s[2];
+    run_residual(h, H.lr, dx, nullptr, s);
+    *rel_error = rel_from_sums(s);
   });
 }
 

@@ -124,6 +124,27 @@ typedef struct CoreParams {
 // out(g, b, post) = sum_i in(g, i, post) * U(i, b)   (U given as n x r).
 // When nparts > 1 the input is a sum of nparts partial tensors spaced by
 // part_stride (fixed summation order: deterministic).
+typedef struct ResidualParams {
+  const double* x;       // n_A x n_B (first index fastest); unused when out is set
+  const double* at;      // K x n_A
+  const double* ct;      // K x n_B
+  double* out;           // optional: write A C^T instead of the norms
+  double* partial;       // 2 doubles per CTA
+  int64_t nA, nB;
+  int32_t K;             // padded to a multiple of 8 (zero rows in At / Ct)
+  int32_t x_tma;         // X through a TMA map (n_A even) or cp.async
+  int32_t stages;        // set by the launcher
+  int32_t pad;
+} ResidualParams;
+
+typedef struct KronParams {
+  const double* u[16];   // U_k, n_k x r_k column-major
+  int64_t n[16], r[16];
+  double* at;            // K x n_A
+  int64_t K, nA;
+  int32_t m, pad;
+} KronParams;
+
 typedef struct TtmParams {
   const double* in;
   const double* u;       // column-major n x rr (ld = n); transpose flag picks U vs U^T

@@ -133,6 +133,11 @@ def _L():
         lib.srtt_multi_ttm_core.argtypes = [vp, vp, i32, i32, vp, vp, vp, i32, vp, i32]
         lib.srtt_transfer_tensor.argtypes = [vp, vp, vp, vp, i64, i64, i32, i32, i32, i32, vp]
         lib.srtt_root_transfer.argtypes = [vp, vp, i32, i64, i64, vp, i32, vp, i32, i32, vp, i32]
+        lib.srtt_rel_error.argtypes = [vp, vp, vp, i32, i64, vp]
+        lib.srtt_tucker_reconstruct.argtypes = [vp, i32, vp, vp, vp, vp, i32, vp, i32]
+        lib.srtt_tucker_rel_error.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, i32, vp]
+        lib.srtt_ht_reconstruct.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, vp, i32]
+        lib.srtt_ht_rel_error.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, vp, i32, vp]
         _LIB = lib
     return _LIB
 
@@ -328,6 +333,7 @@ def node_sample_counts(tree, dims, alpha):
     out = [1] * tree.num_nodes
     for i in range(1, tree.num_nodes):
         out[i] = min(int(math.ceil(alpha * tree.node_rows(i, dims))), tree.node_cols(i, dims))
+    return out
     return out
 
 
@@ -601,3 +607,133 @@ def root_transfer(x, u_left, u_right, *, handle=None):
     _check(_L().srtt_root_transfer(h._h, xf.ctypes.data, 0, nl, nr, a.ctypes.data, rl, b.ctypes.data, rr, 0,
                                    out.ctypes.data, 0))
     return out.reshape((1, rl, rr), order="F")
+
+
+# ---------------------------------------------------------------------------
+# reconstruction and error (the step after the path, experiment.cpp:248/266)
+# ---------------------------------------------------------------------------
+def _is_dev(a):
+    return hasattr(a, "is_cuda") and a.is_cuda
+
+
+def _mat_f64(a):
+    """Flat column-major float64 buffer of a factor / core / transfer."""
+    if _is_dev(a):
+        return _flat_f64(a.reshape(-1) if a.is_contiguous() else a.contiguous().reshape(-1))
+    return np.ascontiguousarray(np.ravel(np.asarray(a, dtype=np.float64), order="F"))
+
+
+def _numel(a):
+    return int(a.numel()) if _is_dev(a) else int(np.size(a))
+
+
+def _tucker_args(t, dims):
+    factors = [_mat_f64(u) for u in t.factors]
+    core = _mat_f64(t.core)
+    if dims is None:
+        dims = [int(np.shape(u)[0]) for u in t.factors]
+        if any(np.ndim(u) != 2 for u in t.factors):
+            raise InvalidArgument("reconstruct: pass dims= for flat factors")
+    ranks = [_numel(f) // n for f, n in zip(factors, dims)]
+    if int(np.prod(ranks)) != _numel(core):
+        raise InvalidArgument("reconstruct: factor/core mismatch")
+    ondev = {_is_dev(a) for a in factors + [core]}
+    if len(ondev) != 1:
+        raise InvalidArgument("reconstruct: core and factors must all be host or all be device buffers")
+    fp = (C.c_void_p * len(factors))(*[_ptr(f)[0] for f in factors])
+    return factors, core, list(dims), ranks, fp, int(ondev.pop())
+
+
+def reconstruct(t, *, dims=None, handle=None, device_out=False):
+    """tucker.hpp:18-28: G x_0 U_0 ... x_{d-1} U_{d-1} on the GPU."""
+    h = handle or default_handle()
+    factors, core, dims, ranks, fp, dev = _tucker_args(t, dims)
+    out = _alloc_out([(int(np.prod(dims)),)], device_out, core if dev else np.zeros(1))[0]
+    dims_a, ranks_a = _i64(dims), _i64(ranks)
+    _check(_L().srtt_tucker_reconstruct(h._h, len(dims), dims_a.ctypes.data, ranks_a.ctypes.data, _ptr(core)[0], fp,
+                                        dev, _ptr(out)[0], int(device_out)))
+    return out if device_out else out.reshape(tuple(dims), order="F")
+
+
+def tucker_rel_error(x, t, *, dims=None, handle=None):
+    """rel_error(x, reconstruct(t)) (experiment.cpp:248) streamed on the GPU:
+    X-hat is recomputed tile by tile and never materialised."""
+    h = handle or default_handle()
+    factors, core, dims, ranks, fp, dev = _tucker_args(t, dims)
+    xf = _flat_f64(x)
+    xp, xdev = _ptr(xf)
+    if _numel(xf) != int(np.prod(dims)):
+        raise InvalidArgument("rel_error: shape mismatch")
+    out = C.c_double()
+    dims_a, ranks_a = _i64(dims), _i64(ranks)
+    _check(_L().srtt_tucker_rel_error(h._h, xp, xdev, len(dims), dims_a.ctypes.data, ranks_a.ctypes.data,
+                                      _ptr(core)[0], fp, dev, C.byref(out)))
+    return float(out.value)
+
+
+def _ht_args(hd, dims):
+    tree = hd.tree
+    d = tree.order
+    leaf = [_mat_f64(u) for u in hd.leaf_factors]
+    if dims is None:
+        dims = [int(np.shape(u)[0]) for u in hd.leaf_factors]
+    ranks = [0] * tree.num_nodes
+    for i in tree.leaves():
+        m = tree.node(i).modes[0]
+        ranks[i] = _numel(leaf[m]) // dims[m]
+    trs = [None if b is None else _mat_f64(b) for b in hd.transfers]
+    for i in tree.internal_nodes_bottom_up() + [0]:
+        n = tree.node(i)
+        ranks[i] = _numel(trs[i]) // (ranks[n.left] * ranks[n.right])
+    if ranks[0] != 1:
+        raise InvalidArgument("ht_reconstruct: root rank must be 1")
+    bufs = leaf + [b for b in trs if b is not None]
+    ondev = {_is_dev(a) for a in bufs}
+    if len(ondev) != 1:
+        raise InvalidArgument("ht_reconstruct: leaf factors and transfers must all be host or all be device")
+    lp = (C.c_void_p * d)(*[_ptr(u)[0] for u in leaf])
+    tp = (C.c_void_p * tree.num_nodes)(*[None if b is None else _ptr(b)[0] for b in trs])
+    return leaf, trs, list(dims), ranks, lp, tp, int(ondev.pop()), bufs
+
+
+def ht_reconstruct(hd, *, dims=None, handle=None, device_out=False):
+    """htucker.hpp:346-378 on the GPU."""
+    h = handle or default_handle()
+    leaf, trs, dims, ranks, lp, tp, dev, keep = _ht_args(hd, dims)
+    out = _alloc_out([(int(np.prod(dims)),)], device_out, keep[0] if dev else np.zeros(1))[0]
+    dims_a, ranks_a = _i64(dims), _i64(ranks)
+    ct = hd.tree._c()
+    _check(_L().srtt_ht_reconstruct(h._h, len(dims), dims_a.ctypes.data, C.byref(ct), ranks_a.ctypes.data, lp, tp,
+                                    dev, _ptr(out)[0], int(device_out)))
+    return out if device_out else out.reshape(tuple(dims), order="F")
+
+
+def ht_rel_error(x, hd, *, dims=None, handle=None):
+    """rel_error(x, ht_reconstruct(h)) (experiment.cpp:266), streamed."""
+    h = handle or default_handle()
+    leaf, trs, dims, ranks, lp, tp, dev, keep = _ht_args(hd, dims)
+    xf = _flat_f64(x)
+    xp, xdev = _ptr(xf)
+    if _numel(xf) != int(np.prod(dims)):
+        raise InvalidArgument("rel_error: shape mismatch")
+    out = C.c_double()
+    dims_a, ranks_a = _i64(dims), _i64(ranks)
+    ct = hd.tree._c()
+    _check(_L().srtt_ht_rel_error(h._h, xp, xdev, len(dims), dims_a.ctypes.data, C.byref(ct), ranks_a.ctypes.data,
+                                  lp, tp, dev, C.byref(out)))
+    return float(out.value)
+
+
+def rel_error(reference, approx, *, handle=None):
+    """tensor.hpp:241-249."""
+    h = handle or default_handle()
+    a, b = _flat_f64(reference), _flat_f64(approx)
+    if np.shape(reference) != np.shape(approx) and not (_is_dev(a) and a.numel() == b.numel()):
+        raise InvalidArgument("rel_error: shape mismatch")
+    pa, da = _ptr(a)
+    pb, db = _ptr(b)
+    if da != db:
+        raise InvalidArgument("rel_error: both tensors must be host or both device buffers")
+    out = C.c_double()
+    _check(_L().srtt_rel_error(h._h, pa, pb, da, _numel(a), C.byref(out)))
+    return float(out.value)
