@@ -41,6 +41,7 @@ extern "C" {
 #define SRTT_ERR_NCCL 4
 #define SRTT_ERR_OUT_OF_MEMORY 5
 #define SRTT_ERR_INTERNAL 6
+#define SRTT_ERR_IO 8  /* IoError (io.hpp:10-13): bad magic/version, truncation, open failure */
 #define SRTT_ERR_JOB 7 /* JobError(job): message starts with "job <index>: " */
 
 /* Stage names of the reference's StageTimings (parallel.hpp:30-40) plus the
@@ -223,6 +224,32 @@ int srtt_ht_rel_error(srtt_handle* h, const double* x, int32_t x_on_device, int3
                       const int64_t* dims, const srtt_tree* tree, const int64_t* ranks,
                       const double* const* leaf_factors, const double* const* transfers,
                       int32_t in_on_device, double* rel_error);
+
+/* ---- containers (io.hpp:15-33) ----------------------------------------------
+ * "SRTT" dense tensor: magic, u32 version 1, u64 order, u64 dims, binary64
+ * values (first index fastest), all little-endian. */
+int srtt_tensor_file_info(const char* path, int32_t* order, int64_t* dims, int32_t dims_capacity,
+                          int64_t* data_offset);
+/* read_tensor (io.cpp:106-117). slab_lo = slab_hi = -1 reads everything;
+ * otherwise only X[..., lo:hi) (one contiguous byte range), e.g. a rank's
+ * slab for srtt_shard_*. out_on_device: streamed through pinned staging
+ * (file reads overlap H2D copies on the handle's stream). */
+int srtt_read_tensor(srtt_handle* h, const char* path, int64_t slab_lo, int64_t slab_hi, double* out,
+                     int32_t out_on_device, int64_t out_capacity);
+/* write_tensor (io.cpp:92-104); x may live on the device (h required). */
+int srtt_write_tensor(srtt_handle* h, const char* path, int32_t d, const int64_t* dims, const double* x,
+                      int32_t x_on_device);
+/* "SRHT" hierarchical container (io.cpp:123-217), host buffers; layouts as
+ * srtt_sub_r_rtl_ht returns them (ranks per node, root 1). */
+int srtt_write_htucker(const char* path, int32_t d, const int64_t* dims, const srtt_tree* tree,
+                       const int64_t* ranks, const double* const* leaf_factors,
+                       const double* const* transfers);
+/* Two-pass read: NULL arrays query order / num_nodes / num_modes; then pass
+ * mode_begin[num_nodes+1], modes[num_modes], left/right/ranks[num_nodes],
+ * dims[order] and the block buffers (NULL entries are skipped). */
+int srtt_read_htucker(const char* path, int32_t* order, int32_t* num_nodes, int32_t* num_modes,
+                      int32_t* mode_begin, int32_t* modes, int32_t* left, int32_t* right, int64_t* ranks,
+                      int64_t* dims, double* const* leaf_factors, double* const* transfers);
 
 /* ---- slab-sharded Sub-R-HOSVD (one process per GPU) --------------------
  * X is split along its LAST mode: the caller holds X[..., lo:hi) as a flat

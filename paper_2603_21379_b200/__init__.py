@@ -10,4 +10,5 @@ from .srtt import (  # noqa: F401
     multi_ttm_core, node_sample_counts, range_basis_of_sketch, root_transfer, sample_indices, sketch,
     sliced_core, stream_normals, sub_r_hosvd, sub_r_rtl_ht, transfer_tensor, uniform_node_ranks,
     reconstruct, ht_reconstruct, rel_error, tucker_rel_error, ht_rel_error,
+    IoError, read_tensor, write_tensor, tensor_file_info, read_htucker, write_htucker,
 )

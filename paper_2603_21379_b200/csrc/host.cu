@@ -2429,3 +2429,8 @@ int srtt_ht_rel_error(srtt_handle* h, const double* x, int32_t x_on_device, int3
 }
 
 }  // extern "C"
+
+// ---- accessors for the IO module (io.cu) -------------------------------------
+cudaStream_t srtt_internal_stream(srtt_handle* h) { return h->stream; }
+int srtt_internal_device(srtt_handle* h) { return h->device; }
+void srtt_internal_set_error(const std::string& msg) { g_last_error = msg; }

@@ -96,6 +96,19 @@ class GpuShardPhases:
         return g
 
 
+def load_slab(path, *, group=None, handle=None):
+    """This rank's slab of an SRTT file, read straight into its GPU: the
+    last-mode slab is one contiguous byte range of the file (io.cpp:106-117),
+    so no rank touches another's bytes. Returns (x_local, dims, (lo, hi))."""
+    import torch.distributed as dist
+
+    dims, _ = _s.tensor_file_info(path)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    me = dist.get_rank(group) if dist.is_initialized() else 0
+    lo, hi = slab_bounds(dims[-1], world, me)
+    return _s.read_tensor(path, slab=(lo, hi), device=True, handle=handle), dims, (lo, hi)
+
+
 @dataclass
 class ShardedTucker:
     core: object          # flat tensor, prod(ranks), first index fastest (identical on every rank)

@@ -35,6 +35,7 @@ SRTT_ERR_NCCL = 4
 SRTT_ERR_OUT_OF_MEMORY = 5
 SRTT_ERR_INTERNAL = 6
 SRTT_ERR_JOB = 7
+SRTT_ERR_IO = 8
 
 STAGES = ["sampling", "extract", "sketch", "svd", "transfer", "ttm", "gather", "serial_tail",
           "factor_wall", "h2d", "d2h"]
@@ -67,6 +68,10 @@ class CudaError(SrttError):
     pass
 
 
+class IoError(RuntimeError):
+    """io.hpp:10-13."""
+
+
 def _check(rc):
     if rc == SRTT_OK:
         return
@@ -77,6 +82,8 @@ def _check(rc):
         raise OutOfRange(msg)
     if rc == SRTT_ERR_JOB:
         raise JobError(msg)
+    if rc == SRTT_ERR_IO:
+        raise IoError(msg)
     if rc in (SRTT_ERR_CUDA, SRTT_ERR_OUT_OF_MEMORY):
         raise CudaError(msg)
     raise SrttError(f"srtt error {rc}: {msg}")
@@ -134,6 +141,11 @@ def _L():
         lib.srtt_transfer_tensor.argtypes = [vp, vp, vp, vp, i64, i64, i32, i32, i32, i32, vp]
         lib.srtt_root_transfer.argtypes = [vp, vp, i32, i64, i64, vp, i32, vp, i32, i32, vp, i32]
         lib.srtt_rel_error.argtypes = [vp, vp, vp, i32, i64, vp]
+        lib.srtt_tensor_file_info.argtypes = [C.c_char_p, vp, vp, i32, vp]
+        lib.srtt_read_tensor.argtypes = [vp, C.c_char_p, i64, i64, vp, i32, i64]
+        lib.srtt_write_tensor.argtypes = [vp, C.c_char_p, i32, vp, vp, i32]
+        lib.srtt_write_htucker.argtypes = [C.c_char_p, i32, vp, vp, vp, vp, vp]
+        lib.srtt_read_htucker.argtypes = [C.c_char_p] + [vp] * 11
         lib.srtt_tucker_reconstruct.argtypes = [vp, i32, vp, vp, vp, vp, i32, vp, i32]
         lib.srtt_tucker_rel_error.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, i32, vp]
         lib.srtt_ht_reconstruct.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, vp, i32]
@@ -737,3 +749,111 @@ def rel_error(reference, approx, *, handle=None):
     out = C.c_double()
     _check(_L().srtt_rel_error(h._h, pa, pb, da, _numel(a), C.byref(out)))
     return float(out.value)
+
+
+# ---------------------------------------------------------------------------
+# containers (io.hpp:15-33)
+# ---------------------------------------------------------------------------
+def _path(p):
+    import os
+
+    return os.fsencode(p)
+
+
+def tensor_file_info(path):
+    """Dimensions and payload offset of an SRTT file."""
+    order = C.c_int32()
+    dims = np.zeros(64, np.int64)
+    off = C.c_int64()
+    _check(_L().srtt_tensor_file_info(_path(path), C.byref(order), dims.ctypes.data, 64, C.byref(off)))
+    return [int(v) for v in dims[:order.value]], int(off.value)
+
+
+def read_tensor(path, *, slab=None, device=False, handle=None):
+    """read_tensor (io.cpp:106-117).  ``slab=(lo, hi)`` reads X[..., lo:hi)
+    only (one contiguous byte range).  ``device=True`` returns a flat CUDA
+    float64 tensor streamed through pinned staging; otherwise a numpy array
+    of the (slab) shape."""
+    dims, _ = tensor_file_info(path)
+    lo, hi = (-1, -1) if slab is None else (int(slab[0]), int(slab[1]))
+    shape = list(dims) if slab is None else dims[:-1] + [hi - lo]
+    if slab is not None and not (0 <= lo < hi <= dims[-1]):
+        raise InvalidArgument("read_tensor: slab out of range")
+    n = int(np.prod(shape))
+    if device:
+        import torch
+
+        h = handle or default_handle()
+        out = torch.empty(n, dtype=torch.float64, device=f"cuda:{h.device}")
+        _check(_L().srtt_read_tensor(h._h, _path(path), lo, hi, out.data_ptr(), 1, n))
+        return out
+    out = np.empty(n, dtype=np.float64)
+    _check(_L().srtt_read_tensor(handle._h if handle else None, _path(path), lo, hi, out.ctypes.data, 0, n))
+    return out.reshape(tuple(shape), order="F")
+
+
+def write_tensor(path, x, *, dims=None, handle=None):
+    """write_tensor (io.cpp:92-104); x: numpy array or flat CUDA tensor (dims=)."""
+    if dims is None:
+        dims = list(np.shape(x))
+    xf = _flat_f64(x)
+    p, dev = _ptr(xf)
+    h = (handle or default_handle()) if dev else handle
+    dims_a = _i64(dims)
+    _check(_L().srtt_write_tensor(h._h if h else None, _path(path), len(dims), dims_a.ctypes.data, p, dev))
+
+
+def write_htucker(path, hd):
+    """write_htucker (io.cpp:123-150), host arrays."""
+    tree = hd.tree
+    d = tree.order
+    dims = [int(np.shape(hd.leaf_factors[m])[0]) for m in range(d)]
+    ranks = [0] * tree.num_nodes
+    for i in tree.leaves():
+        ranks[i] = int(np.shape(hd.leaf_factors[tree.node(i).modes[0]])[1])
+    for i in range(tree.num_nodes):
+        if not tree.node(i).is_leaf():
+            ranks[i] = int(np.shape(hd.transfers[i])[0])
+    leaf = [np.ascontiguousarray(np.ravel(u, order="F"), dtype=np.float64) for u in hd.leaf_factors]
+    trs = [None if b is None else np.ascontiguousarray(np.ravel(b, order="F"), dtype=np.float64)
+           for b in hd.transfers]
+    lp = (C.c_void_p * d)(*[u.ctypes.data for u in leaf])
+    tp = (C.c_void_p * tree.num_nodes)(*[None if b is None else b.ctypes.data for b in trs])
+    ct = tree._c()
+    dims_a, ranks_a = _i64(dims), _i64(ranks)
+    _check(_L().srtt_write_htucker(_path(path), d, dims_a.ctypes.data, C.byref(ct), ranks_a.ctypes.data, lp, tp))
+
+
+def read_htucker(path):
+    """read_htucker (io.cpp:152-212) -> HTuckerDecomposition (host arrays)."""
+    lib = _L()
+    order, nn, nm = C.c_int32(), C.c_int32(), C.c_int32()
+    _check(lib.srtt_read_htucker(_path(path), C.byref(order), C.byref(nn), C.byref(nm), *([None] * 8)))
+    d, n = order.value, nn.value
+    mb = np.zeros(n + 1, np.int32)
+    modes = np.zeros(max(nm.value, 1), np.int32)
+    left, right = np.zeros(n, np.int32), np.zeros(n, np.int32)
+    ranks, dims = np.zeros(n, np.int64), np.zeros(d, np.int64)
+    _check(lib.srtt_read_htucker(_path(path), None, None, None, mb.ctypes.data, modes.ctypes.data,
+                                 left.ctypes.data, right.ctypes.data, ranks.ctypes.data, dims.ctypes.data,
+                                 None, None))
+    parent, level = [-1] * n, [0] * n
+    for i in range(n):
+        if left[i] >= 0:
+            parent[left[i]] = parent[right[i]] = i
+    for i in range(1, n):
+        level[i] = level[parent[i]] + 1
+    nodes = [TreeNode(modes[mb[i]:mb[i + 1]], int(left[i]), int(right[i]), parent[i], level[i]) for i in range(n)]
+    tree = DimensionTree(nodes)
+    leaf = [None] * d
+    trs = [None] * n
+    for i in range(n):
+        if left[i] < 0:
+            m = int(modes[mb[i]])
+            leaf[m] = np.zeros((int(dims[m]), int(ranks[i])), order="F")
+        else:
+            trs[i] = np.zeros((int(ranks[i]), int(ranks[left[i]]), int(ranks[right[i]])), order="F")
+    lp = (C.c_void_p * d)(*[u.ctypes.data for u in leaf])
+    tp = (C.c_void_p * n)(*[None if b is None else b.ctypes.data for b in trs])
+    _check(lib.srtt_read_htucker(_path(path), None, None, None, None, None, None, None, None, None, lp, tp))
+    return HTuckerDecomposition(tree, leaf, trs)
