@@ -8,6 +8,9 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libsrtt_b200.so")
+# development only: SRTT_PROFILE_BUILD=1 loads the phase-clock build (make PROF=1)
+if os.environ.get("SRTT_PROFILE_BUILD") == "1":
+    LIB_PATH = os.path.join(HERE, "libsrtt_b200_prof.so")
 
 
 def build(force: bool = False) -> str:

@@ -29,7 +29,9 @@ size_t srtt_basis_top_smem(int m, int c, int r);
 size_t srtt_basis_level_smem(int mb, int c);
 cudaError_t srtt_launch_basis_top(const BasisTarget*, const int*, int, size_t, cudaStream_t);
 size_t srtt_basis_small_smem(int m, int c, int r);
-cudaError_t srtt_launch_basis_small(const BasisTarget*, const int*, int, size_t, cudaStream_t);
+cudaError_t srtt_launch_basis_small(int, const BasisTarget*, const int*, int, size_t, cudaStream_t);
+int srtt_basis_small_variant(int m, int c);
+constexpr int kSmallVariants = 3;
 cudaError_t srtt_launch_tsqr_factor(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_tsqr_apply(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_pad(const BasisTarget*, int, double*, int64_t, cudaStream_t);
@@ -427,7 +429,9 @@ bool basis_is_small(const BasisTarget& t) {
 
 struct BasisLists {
   std::vector<int> small, big;
+  std::vector<int> small_v[kSmallVariants];  // small targets by kernel variant
   size_t off_small = 0, off_big = 0;  // blob offsets
+  size_t off_small_v[kSmallVariants] = {};
   size_t off_map[SRTT_MAX_QR_LEVELS] = {};  // per TSQR level: CTA -> (target, block)
 };
 
@@ -444,6 +448,9 @@ BasisLists make_basis_lists(const std::vector<BasisTarget>& targets, Blob& blob)
   }
   const int zero = 0;
   L.off_small = blob.add(L.small.empty() ? &zero : L.small.data(), sizeof(int) * std::max<size_t>(1, L.small.size()));
+  for (int i : L.small) L.small_v[srtt_basis_small_variant((int)targets[i].n, targets[i].c)].push_back(i);
+  for (int v = 0; v < kSmallVariants; ++v)
+    if (!L.small_v[v].empty()) L.off_small_v[v] = blob.add(L.small_v[v].data(), sizeof(int) * L.small_v[v].size());
   L.off_big = blob.add(L.big.empty() ? &zero : L.big.data(), sizeof(int) * std::max<size_t>(1, L.big.size()));
   return L;
 }
@@ -456,12 +463,13 @@ int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const 
   int maxlev = 0;
   for (auto& t : targets) maxlev = std::max(maxlev, t.nlevels);
   const int nt = (int)targets.size();
-  if (!lists.small.empty()) {
+  for (int v = 0; v < kSmallVariants; ++v) {
+    if (lists.small_v[v].empty()) continue;
     size_t smem = 0;
-    for (int i : lists.small)
+    for (int i : lists.small_v[v])
       smem = std::max(smem, srtt_basis_small_smem((int)targets[i].n, targets[i].c, targets[i].r));
-    CK(srtt_launch_basis_small(dT, reinterpret_cast<const int*>(dblob + lists.off_small), (int)lists.small.size(),
-                               smem, small_stream ? small_stream : h->stream));
+    CK(srtt_launch_basis_small(v, dT, reinterpret_cast<const int*>(dblob + lists.off_small_v[v]),
+                               (int)lists.small_v[v].size(), smem, small_stream ? small_stream : h->stream));
     ++launches;
   }
   if (lists.big.empty()) return launches;

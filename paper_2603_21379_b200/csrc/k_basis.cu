@@ -21,6 +21,8 @@
 // same code: R is then n x c upper-trapezoidal and J is n x n.
 #include <float.h>
 
+#include <utility>
+
 #include "srtt_device.cuh"
 #include "srtt_params.h"
 
@@ -30,6 +32,21 @@ using srtt_dev::warp_sum;
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+
+// Development-only phase clock (make PROF=1): block 0 of basis_small_kernel
+// records clock64() at phase boundaries.
+#ifdef SRTT_PROF
+__device__ long long g_basis_clk[16];
+#define PROF_MARK(i) \
+  do {               \
+    __syncwarp();    \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_basis_clk[i] = clock64(); \
+  } while (0)
+#else
+#define PROF_MARK(i) \
+  do {               \
+  } while (0)
+#endif
 
 __device__ double block_sum(double v, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -186,15 +203,19 @@ __device__ void build_pairs(unsigned short* pairs, int kk) {
   }
 }
 
-// Jacobi rotation zeroing apq: t = sign(d) 2 apq / (|d| + sqrt(d^2 + 4 apq^2)),
-// d = aqq - app (Rutishauser's tan(theta), one sqrt + one division).
+// Jacobi rotation zeroing apq (|theta| <= pi/4, Rutishauser's choice of
+// t = tan(theta) = sign(d) 2 apq / (|d| + h), d = aqq - app,
+// h = sqrt(d^2 + 4 apq^2)), evaluated with two reciprocal square roots and
+// no division: cos(2 theta) = |d| / h, c = sqrt((1 + cos 2theta) / 2),
+// s = sign(d) (2 apq / h) / (2 c).
 __device__ __forceinline__ void jacobi_rotation(double app, double aqq, double apq, double* cs, double* sn) {
   const double dd = aqq - app;
   const double ta = 2.0 * apq;
-  const double t = copysign(1.0, dd) * ta / (fabs(dd) + sqrt(dd * dd + ta * ta));
-  const double c = rsqrt(1.0 + t * t);
-  *cs = c;
-  *sn = c * t;
+  const double rh = rsqrt(fma(dd, dd, ta * ta));
+  const double w = fma(0.5 * fabs(dd), rh, 0.5);
+  const double rw = rsqrt(w);
+  *cs = w * rw;
+  *sn = copysign(1.0, dd) * (0.5 * ta * rh) * rw;
 }
 
 // One-sided Jacobi on the rows of B (k x c, row-major, ld = ldb) with
@@ -268,6 +289,110 @@ __device__ int jacobi_rows_g4(double* B, int ldb, int k, int c, double* V, int l
     if (!any) break;
   }
   if (nwarps > 1) __syncthreads(); else __syncwarp();
+  return sweep;
+}
+
+// Register-resident one-sided Jacobi for one warp (k <= 32 / G * 2 rows).
+// Round-robin by the circle method: lane group g (G lanes) holds the two
+// players in positions g and kk-1-g -- their rows of B (length c) and of V
+// (length k), E = ceil(max(c, k) / G) values per lane each. After a round,
+// position 0 stays and the others advance one place, so rows move between
+// neighbouring groups by shuffles instead of through shared memory. Every
+// pair meets once per sweep; sweeps repeat until none rotates.
+template <int G, int E>
+__device__ int jacobi_rows_reg(double* B, int ldb, int k, int c, double* V, int ldv) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane / G, gl = lane % G;
+  const int kk = (k + 1) & ~1;
+  const int np = kk / 2;
+  const bool grp_live = g < np;
+  const double tol2 = 4.0 * DBL_EPSILON * DBL_EPSILON;
+  int tp = g, bp = kk - 1 - g;  // players held by this group
+  double tb[E], bb[E], tv[E], bv[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int j = gl + G * e;
+    tb[e] = (grp_live && tp < k && j < c) ? B[(size_t)tp * ldb + j] : 0.0;
+    bb[e] = (grp_live && bp < k && j < c) ? B[(size_t)bp * ldb + j] : 0.0;
+    tv[e] = (grp_live && tp < k && j < k) ? V[(size_t)tp * ldv + j] : 0.0;
+    bv[e] = (grp_live && bp < k && j < k) ? V[(size_t)bp * ldv + j] : 0.0;
+  }
+  const int src_prev = (lane - G) & 31, src_next = (lane + G) & 31;
+  int sweep = 0;
+  if (k >= 2) {
+    for (; sweep < 80; ++sweep) {
+      int rotated = 0;
+      for (int rd = 0; rd < kk - 1; ++rd) {
+        double app = 0.0, aqq = 0.0, apq = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          app = fma(tb[e], tb[e], app);
+          aqq = fma(bb[e], bb[e], aqq);
+          apq = fma(tb[e], bb[e], apq);
+        }
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) {
+          app += __shfl_xor_sync(0xffffffffu, app, o);
+          aqq += __shfl_xor_sync(0xffffffffu, aqq, o);
+          apq += __shfl_xor_sync(0xffffffffu, apq, o);
+        }
+        if (grp_live && apq != 0.0 && apq * apq > tol2 * app * aqq) {
+          double cs, sn;
+          jacobi_rotation(app, aqq, apq, &cs, &sn);
+          // the top player plays "p": any plane rotation that zeroes the
+          // pair's inner product with |theta| <= pi/4 serves
+          const double s2 = sn;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const double x = tb[e], y = bb[e];
+            tb[e] = cs * x - s2 * y;
+            bb[e] = s2 * x + cs * y;
+            const double u = tv[e], v = bv[e];
+            tv[e] = cs * u - s2 * v;
+            bv[e] = s2 * u + cs * v;
+          }
+          rotated = 1;
+        }
+        // advance: top[0] stays, top[1] <- bot[0], top[g] <- top[g-1],
+        // bot[g] <- bot[g+1], bot[np-1] <- top[np-1]
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const double pt = __shfl_sync(0xffffffffu, tb[e], src_prev);
+          const double pb = __shfl_sync(0xffffffffu, bb[e], src_prev);
+          const double nb = __shfl_sync(0xffffffffu, bb[e], src_next);
+          const double qt = __shfl_sync(0xffffffffu, tv[e], src_prev);
+          const double qb = __shfl_sync(0xffffffffu, bv[e], src_prev);
+          const double mb = __shfl_sync(0xffffffffu, bv[e], src_next);
+          const double otb = tb[e], otv = tv[e];
+          if (g >= 1) {
+            tb[e] = g == 1 ? pb : pt;
+            tv[e] = g == 1 ? qb : qt;
+          }
+          bb[e] = g == np - 1 ? otb : nb;
+          bv[e] = g == np - 1 ? otv : mb;
+        }
+        {
+          const int ptp = __shfl_sync(0xffffffffu, tp, src_prev);
+          const int pbp = __shfl_sync(0xffffffffu, bp, src_prev);
+          const int nbp = __shfl_sync(0xffffffffu, bp, src_next);
+          const int otp = tp;
+          if (g >= 1) tp = g == 1 ? pbp : ptp;
+          bp = g == np - 1 ? otp : nbp;
+        }
+      }
+      if (!__any_sync(0xffffffffu, rotated)) break;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int j = gl + G * e;
+    if (grp_live && tp < k && j < c) B[(size_t)tp * ldb + j] = tb[e];
+    if (grp_live && bp < k && j < c) B[(size_t)bp * ldb + j] = bb[e];
+    if (grp_live && tp < k && j < k) V[(size_t)tp * ldv + j] = tv[e];
+    if (grp_live && bp < k && j < k) V[(size_t)bp * ldv + j] = bv[e];
+  }
+  __syncwarp();
   return sweep;
 }
 
@@ -580,6 +705,128 @@ __device__ __forceinline__ double dot4(const double* a, const double* b, int lo,
   return (s0 + s1) + (s2 + s3);
 }
 
+// ---- lane-per-column Householder QR / back-application for one warp -----
+// For c <= 32: lane l owns column l of A (shared memory, odd leading
+// dimension, so the 32 lanes hit 32 different banks at the same row). A
+// reflector costs one warp reduction (column norm) and then every lane runs
+// its own dot product and update down the rows -- no shuffles, compact
+// loops (a single warp runs this code once, so instruction-cache footprint
+// matters more than unrolling). Rows move through registers in batches of
+// 8 so the shared-memory loads of a batch are in flight together. No column
+// pivoting.
+constexpr int kRowBatch = 8;
+
+// w = v_j + sum_{i > j} v[i] x[i]  (v[j] = 1 implied), x and v in shared memory.
+__device__ __forceinline__ double reflector_dot(const double* v, const double* x, int j, int m) {
+  double acc[kRowBatch];
+#pragma unroll
+  for (int u = 0; u < kRowBatch; ++u) acc[u] = 0.0;
+  int i = j + 1;
+  for (; i + kRowBatch <= m; i += kRowBatch) {
+    double vv[kRowBatch], xx[kRowBatch];
+#pragma unroll
+    for (int u = 0; u < kRowBatch; ++u) {
+      vv[u] = v[i + u];
+      xx[u] = x[i + u];
+    }
+#pragma unroll
+    for (int u = 0; u < kRowBatch; ++u) acc[u] = fma(vv[u], xx[u], acc[u]);
+  }
+  for (; i < m; ++i) acc[0] = fma(v[i], x[i], acc[0]);
+  double w = x[j];
+#pragma unroll
+  for (int u = 0; u < kRowBatch; ++u) w += acc[u];
+  return w;
+}
+
+// x[j] -= tw; x[i] -= tw v[i] for i > j.
+__device__ __forceinline__ void reflector_update(const double* v, double* x, int j, int m, double tw) {
+  x[j] -= tw;
+  int i = j + 1;
+  for (; i + kRowBatch <= m; i += kRowBatch) {
+    double vv[kRowBatch], xx[kRowBatch];
+#pragma unroll
+    for (int u = 0; u < kRowBatch; ++u) {
+      vv[u] = v[i + u];
+      xx[u] = x[i + u];
+    }
+#pragma unroll
+    for (int u = 0; u < kRowBatch; ++u) x[i + u] = fma(-tw, vv[u], xx[u]);
+  }
+  for (; i < m; ++i) x[i] = fma(-tw, v[i], x[i]);
+}
+
+__device__ void qr_cols_lane(const double* __restrict__ z, int m, int c, double* A, int lda, double* tau) {
+  const int lane = threadIdx.x & 31;
+  const int k = min(m, c);
+  for (int idx0 = 0; idx0 < m * c; idx0 += 32 * kRowBatch) {
+    double buf[kRowBatch];
+#pragma unroll
+    for (int u = 0; u < kRowBatch; ++u) {
+      const int idx = idx0 + 32 * u + lane;
+      buf[u] = idx < m * c ? __ldg(z + idx) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kRowBatch; ++u) {
+      const int idx = idx0 + 32 * u + lane;
+      if (idx < m * c) A[(size_t)(idx / m) * lda + idx % m] = buf[u];
+    }
+  }
+  __syncwarp();
+  for (int j = 0; j < k; ++j) {
+    double* col = A + (size_t)j * lda;
+    double part = 0.0;
+    for (int i = j + 1 + lane; i < m; i += 32) part = fma(col[i], col[i], part);
+    const double ss = warp_sum(part);
+    const double alpha = col[j];
+    double tj = 0.0, scal = 0.0, beta = alpha;
+    if (ss != 0.0) {
+      const double nrm = sqrt(fma(alpha, alpha, ss));
+      beta = -copysign(nrm, alpha);
+      tj = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (tj != 0.0)
+      for (int i = j + 1 + lane; i < m; i += 32) col[i] *= scal;
+    __syncwarp();
+    if (tj != 0.0 && lane > j && lane < c) {  // lane l owns trailing column l
+      double* cl = A + (size_t)lane * lda;
+      reflector_update(col, cl, j, m, tj * reflector_dot(col, cl, j, m));
+    }
+    __syncwarp();
+    if (lane == 0) {
+      col[j] = beta;
+      tau[j] = tj;
+    }
+    __syncwarp();
+  }
+}
+
+// Y(:, 0:q) = Q [V(:, perm[0:q]); 0], q <= 32: lane `col` owns output
+// column col and applies the k reflectors in reverse order.
+__device__ void apply_cols_lane(const double* A, int lda, const double* tau, int m, int k, const double* V,
+                                int ldv, const int* perm, int q, double* Y, int ldy) {
+  const int lane = threadIdx.x & 31;
+  if (lane < q) {
+    double* y = Y + (size_t)lane * ldy;
+    const double* vc = V + (size_t)perm[lane] * ldv;
+    for (int i = 0; i < m; ++i) y[i] = i < k ? vc[i] : 0.0;
+    for (int j = k - 1; j >= 0; --j) {
+      const double tj = tau[j];
+      if (tj == 0.0) continue;
+      const double* v = A + (size_t)j * lda;
+      reflector_update(v, y, j, m, tj * reflector_dot(v, y, j, m));
+    }
+  }
+  __syncwarp();
+}
+
+// Variants (compile-time paths, so each instantiation gets its own register
+// budget): QRR = 1: lane-per-column QR / back-application (c <= 32), 0:
+// shared-memory QRCP with 4-lane column groups,
+// (JG, JE) = register Jacobi lane-group width / values per lane (JG = 0:
+// shared-memory Jacobi).
+template <int QRR, int JG, int JE>
 __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __restrict__ targets,
                                                          const int* __restrict__ list) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -591,102 +838,111 @@ __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __re
   const int m = (int)T.n, c = T.c, r = T.r;
   const int k = min(m, c);
   SmallSmem s = carve_small(smem_raw, m, c, r);
+  PROF_MARK(0);
   const double* z = T.lv[0].a;
-  for (int idx = lane; idx < m * c; idx += 32) {
-    const int i = idx % m, j = idx / m;
-    s.A[(size_t)j * s.lda + i] = z[idx];
-  }
-  __syncwarp();
-  // ---- Householder QR with column pivoting (QRCP), 4-lane groups own the
-  // trailing columns; pivoting preconditions the Jacobi below.
-  {
-    const int grp = lane >> 2, gl = lane & 3;
-    for (int jb = 0; jb < c; jb += 8) {
-      const int jj = jb + grp;
-      double sq = 0.0;
-      if (jj < c)
-        for (int i = gl; i < m; i += 4) sq += s.A[(size_t)jj * s.lda + i] * s.A[(size_t)jj * s.lda + i];
-      sq += __shfl_xor_sync(0xffffffffu, sq, 1);
-      sq += __shfl_xor_sync(0xffffffffu, sq, 2);
-      if (jj < c && gl == 0) s.vn[jj] = sqrt(sq);
+  // register-resident QR / back-application for small sketches
+  if constexpr (QRR > 0) {
+    qr_cols_lane(z, m, c, s.A, s.lda, s.tau);
+    PROF_MARK(1);
+  } else {
+    for (int idx = lane; idx < m * c; idx += 32) {
+      const int i = idx % m, j = idx / m;
+      s.A[(size_t)j * s.lda + i] = z[idx];
     }
     __syncwarp();
-  }
-  for (int j = 0; j < k; ++j) {
-    {  // pivot: largest remaining column norm
-      double best = -1.0;
-      int bi = j;
-      for (int l = j + lane; l < c; l += 32)
-        if (s.vn[l] > best) { best = s.vn[l]; bi = l; }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    PROF_MARK(1);
+    // ---- Householder QR with column pivoting (QRCP), 4-lane groups own the
+    // trailing columns; pivoting preconditions the Jacobi below.
+    {
+      const int grp = lane >> 2, gl = lane & 3;
+      for (int jb = 0; jb < c; jb += 8) {
+        const int jj = jb + grp;
+        double sq = 0.0;
+        if (jj < c)
+          for (int i = gl; i < m; i += 4) sq += s.A[(size_t)jj * s.lda + i] * s.A[(size_t)jj * s.lda + i];
+        sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+        sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+        if (jj < c && gl == 0) s.vn[jj] = sqrt(sq);
       }
-      if (bi != j) {
-        double* a = s.A + (size_t)j * s.lda;
-        double* b = s.A + (size_t)bi * s.lda;
-        for (int i = lane; i < m; i += 32) {
-          const double t = a[i];
-          a[i] = b[i];
-          b[i] = t;
+      __syncwarp();
+    }
+    for (int j = 0; j < k; ++j) {
+      {  // pivot: largest remaining column norm
+        double best = -1.0;
+        int bi = j;
+        for (int l = j + lane; l < c; l += 32)
+          if (s.vn[l] > best) { best = s.vn[l]; bi = l; }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (bi != j) {
+          double* a = s.A + (size_t)j * s.lda;
+          double* b = s.A + (size_t)bi * s.lda;
+          for (int i = lane; i < m; i += 32) {
+            const double t = a[i];
+            a[i] = b[i];
+            b[i] = t;
+          }
+          __syncwarp();
+          if (lane == 0) {
+            const double t = s.vn[j];
+            s.vn[j] = s.vn[bi];
+            s.vn[bi] = t;
+          }
         }
         __syncwarp();
-        if (lane == 0) {
-          const double t = s.vn[j];
-          s.vn[j] = s.vn[bi];
-          s.vn[bi] = t;
+      }
+      double* col = s.A + (size_t)j * s.lda;
+      double part = 0.0;
+      for (int i = j + 1 + lane; i < m; i += 32) part += col[i] * col[i];
+      const double ss = warp_sum(part);
+      const double alpha = col[j];
+      double t = 0.0, scal = 0.0, beta = alpha;
+      if (ss != 0.0) {
+        const double nrm = sqrt(alpha * alpha + ss);
+        beta = -copysign(nrm, alpha);
+        t = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      if (t != 0.0)
+        for (int i = j + 1 + lane; i < m; i += 32) col[i] *= scal;
+      __syncwarp();
+      if (lane == 0) {
+        col[j] = beta;
+        s.tau[j] = t;
+      }
+      {
+        const int grp = lane >> 2, gl = lane & 3;
+        for (int jb = j + 1; jb < c; jb += 8) {
+          const int jj = jb + grp;
+          double* cj = s.A + (size_t)min(jj, c - 1) * s.lda;
+          double w = 0.0;
+          if (t != 0.0 && jj < c)
+            for (int i = j + 1 + gl; i < m; i += 4) w += col[i] * cj[i];
+          w += __shfl_xor_sync(0xffffffffu, w, 1);
+          w += __shfl_xor_sync(0xffffffffu, w, 2);
+          if (jj < c) {
+            const double tw = t * (w + cj[j]);
+            __syncwarp(0xffffffffu);
+            if (gl == 0) {
+              cj[j] -= tw;
+              const double r = cj[j];
+              s.vn[jj] = sqrt(fmax(0.0, s.vn[jj] * s.vn[jj] - r * r));
+            }
+            if (t != 0.0)
+              for (int i = j + 1 + gl; i < m; i += 4) cj[i] -= tw * col[i];
+          } else {
+            __syncwarp(0xffffffffu);
+          }
         }
       }
       __syncwarp();
     }
-    double* col = s.A + (size_t)j * s.lda;
-    double part = 0.0;
-    for (int i = j + 1 + lane; i < m; i += 32) part += col[i] * col[i];
-    const double ss = warp_sum(part);
-    const double alpha = col[j];
-    double t = 0.0, scal = 0.0, beta = alpha;
-    if (ss != 0.0) {
-      const double nrm = sqrt(alpha * alpha + ss);
-      beta = -copysign(nrm, alpha);
-      t = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
-    }
-    if (t != 0.0)
-      for (int i = j + 1 + lane; i < m; i += 32) col[i] *= scal;
-    __syncwarp();
-    if (lane == 0) {
-      col[j] = beta;
-      s.tau[j] = t;
-    }
-    {
-      const int grp = lane >> 2, gl = lane & 3;
-      for (int jb = j + 1; jb < c; jb += 8) {
-        const int jj = jb + grp;
-        double* cj = s.A + (size_t)min(jj, c - 1) * s.lda;
-        double w = 0.0;
-        if (t != 0.0 && jj < c)
-          for (int i = j + 1 + gl; i < m; i += 4) w += col[i] * cj[i];
-        w += __shfl_xor_sync(0xffffffffu, w, 1);
-        w += __shfl_xor_sync(0xffffffffu, w, 2);
-        if (jj < c) {
-          const double tw = t * (w + cj[j]);
-          __syncwarp(0xffffffffu);
-          if (gl == 0) {
-            cj[j] -= tw;
-            const double r = cj[j];
-            s.vn[jj] = sqrt(fmax(0.0, s.vn[jj] * s.vn[jj] - r * r));
-          }
-          if (t != 0.0)
-            for (int i = j + 1 + gl; i < m; i += 4) cj[i] -= tw * col[i];
-        } else {
-          __syncwarp(0xffffffffu);
-        }
-      }
-    }
-    __syncwarp();
   }
+  PROF_MARK(2);
   // ---- R rows -> B, V = I
   for (int idx = lane; idx < k * c; idx += 32) {
     const int i = idx / c, j = idx % c;
@@ -697,10 +953,17 @@ __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __re
     s.V[(size_t)j * s.ldv + i] = (i == j) ? 1.0 : 0.0;
   }
   __syncwarp();
-  // ---- one-sided Jacobi on rows (4-lane groups own pairs)
-  build_pairs(pairs, (k + 1) & ~1);
-  __syncwarp();
-  const int sweeps = jacobi_rows_g4(s.B, s.ldb, k, c, s.V, s.ldv, pairs);
+  // ---- one-sided Jacobi on rows: register-resident for k <= 32 (4-lane
+  // groups up to 16 rows, 2-lane groups up to 32), shared-memory otherwise
+  int sweeps;
+  if constexpr (JG > 0) {
+    sweeps = jacobi_rows_reg<JG, JE>(s.B, s.ldb, k, c, s.V, s.ldv);
+  } else {
+    build_pairs(pairs, (k + 1) & ~1);
+    __syncwarp();
+    sweeps = jacobi_rows_g4(s.B, s.ldb, k, c, s.V, s.ldv, pairs);
+  }
+  PROF_MARK(3);
   // ---- singular values, ordering, rank decision
   for (int i = lane; i < k; i += 32) {
     const double* bi = s.B + (size_t)i * s.ldb;
@@ -725,40 +988,46 @@ __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __re
   }
   if (T.sv)
     for (int i = lane; i < k; i += 32) T.sv[i] = s.sig[s.perm[i]];
-  // ---- Y = Q [V(:, perm[:q]); 0], 4-lane groups own output columns
-  {
-    const int grp = lane >> 2, gl = lane & 3;
-    for (int cb = 0; cb < q; cb += 8) {
-      const int col = cb + grp;
-      const bool act = col < q;
-      double* y = s.Y + (size_t)min(col, q - 1) * s.lda;
-      if (act) {
-        const double* vc = s.V + (size_t)s.perm[col] * s.ldv;
-        for (int i = gl; i < m; i += 4) y[i] = i < k ? vc[i] : 0.0;
-      }
-      __syncwarp();
-      for (int j = k - 1; j >= 0; --j) {
-        const double t = s.tau[j];
-        if (t == 0.0) continue;
-        const double* vj = s.A + (size_t)j * s.lda;
-        double w = 0.0;
-        if (act)
-          for (int i = j + 1 + gl; i < m; i += 4) w += vj[i] * y[i];
-        w += __shfl_xor_sync(0xffffffffu, w, 1);
-        w += __shfl_xor_sync(0xffffffffu, w, 2);
+  PROF_MARK(4);
+  // ---- Y = Q [V(:, perm[:q]); 0]
+  if constexpr (QRR > 0) {
+    apply_cols_lane(s.A, s.lda, s.tau, m, k, s.V, s.ldv, s.perm, q, s.Y, s.lda);
+  } else {
+    {
+      const int grp = lane >> 2, gl = lane & 3;
+      for (int cb = 0; cb < q; cb += 8) {
+        const int col = cb + grp;
+        const bool act = col < q;
+        double* y = s.Y + (size_t)min(col, q - 1) * s.lda;
         if (act) {
-          const double tw = t * (w + y[j]);
-          __syncwarp(0xffffffffu);
-          if (gl == 0) y[j] -= tw;
-          for (int i = j + 1 + gl; i < m; i += 4) y[i] -= tw * vj[i];
-        } else {
-          __syncwarp(0xffffffffu);
+          const double* vc = s.V + (size_t)s.perm[col] * s.ldv;
+          for (int i = gl; i < m; i += 4) y[i] = i < k ? vc[i] : 0.0;
         }
         __syncwarp();
+        for (int j = k - 1; j >= 0; --j) {
+          const double t = s.tau[j];
+          if (t == 0.0) continue;
+          const double* vj = s.A + (size_t)j * s.lda;
+          double w = 0.0;
+          if (act)
+            for (int i = j + 1 + gl; i < m; i += 4) w += vj[i] * y[i];
+          w += __shfl_xor_sync(0xffffffffu, w, 1);
+          w += __shfl_xor_sync(0xffffffffu, w, 2);
+          if (act) {
+            const double tw = t * (w + y[j]);
+            __syncwarp(0xffffffffu);
+            if (gl == 0) y[j] -= tw;
+            for (int i = j + 1 + gl; i < m; i += 4) y[i] -= tw * vj[i];
+          } else {
+            __syncwarp(0xffffffffu);
+          }
+          __syncwarp();
+        }
       }
     }
+    __syncwarp();
   }
-  __syncwarp();
+  PROF_MARK(5);
   // ---- Gaussian padding (sketch.hpp:48-65), same stream as Omega
   uint64_t tn = (uint64_t)T.normal_base;
   for (int j = q; j < r; ++j) {
@@ -794,10 +1063,12 @@ __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __re
       __syncwarp();
     }
   }
+  PROF_MARK(6);
   for (int idx = lane; idx < m * r; idx += 32) {
     const int i = idx % m, col = idx / m;
     T.u[idx] = s.Y[(size_t)col * s.lda + i];
   }
+  PROF_MARK(7);
 }
 
 }  // namespace
@@ -821,11 +1092,31 @@ size_t srtt_basis_small_smem(int m, int c, int r) {
   return doubles * sizeof(double) + sizeof(int) * (size_t)(k + 2);
 }
 
-cudaError_t srtt_launch_basis_small(const BasisTarget* d_targets, const int* d_list, int n, size_t smem,
+// Variant of a small target (see basis_small_kernel).
+int srtt_basis_small_variant(int m, int c) {
+  const int k = m < c ? m : c;
+  if (c <= 16) return 0;              // <1, 4, 4>
+  if (k <= 32 && c <= 32) return 1;   // <1, 2, 16>
+  return 2;                           // <0, 0, 0>
+}
+
+cudaError_t srtt_launch_basis_small(int variant, const BasisTarget* d_targets, const int* d_list, int n, size_t smem,
                                     cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
-  SRTT_ENSURE_SMEM((basis_small_kernel), smem);
-  basis_small_kernel<<<n, 32, smem, stream>>>(d_targets, d_list);
+  switch (variant) {
+    case 0:
+      SRTT_ENSURE_SMEM((basis_small_kernel<1, 4, 4>), smem);
+      basis_small_kernel<1, 4, 4><<<n, 32, smem, stream>>>(d_targets, d_list);
+      break;
+    case 1:
+      SRTT_ENSURE_SMEM((basis_small_kernel<1, 2, 16>), smem);
+      basis_small_kernel<1, 2, 16><<<n, 32, smem, stream>>>(d_targets, d_list);
+      break;
+    default:
+      SRTT_ENSURE_SMEM((basis_small_kernel<0, 0, 0>), smem);
+      basis_small_kernel<0, 0, 0><<<n, 32, smem, stream>>>(d_targets, d_list);
+      break;
+  }
   return cudaGetLastError();
 }
 
@@ -859,3 +1150,9 @@ cudaError_t srtt_launch_pad(const BasisTarget* d_targets, int ntargets, double* 
   pad_kernel<<<ntargets, kThreads, 0, stream>>>(d_targets, scratch, scratch_stride);
   return cudaGetLastError();
 }
+
+#ifdef SRTT_PROF
+extern "C" int srtt_debug_basis_clocks(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_basis_clk, sizeof(long long) * 16);
+}
+#endif

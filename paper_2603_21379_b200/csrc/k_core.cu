@@ -428,6 +428,57 @@ __global__ void ttm_kernel(const TtmParams T) {
   }
 }
 
+// Latency-bound variant for small outputs: S lanes share one output, each
+// summing every S-th term of the contraction (and of the part sum), then a
+// fixed xor-tree combines them -- about one memory round trip per output
+// instead of n / 4. Deterministic (fixed order).
+template <int S>
+__global__ void ttm_split_kernel(const TtmParams T) {
+  const int64_t total = T.g * T.rr * T.post;
+  const int lane = threadIdx.x & 31, sub = lane % S;
+  const int64_t per_warp = 32 / S;
+  const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  for (int64_t o0 = warp_id * per_warp; o0 < total; o0 += nwarps * per_warp) {
+    const int64_t o = o0 + lane / S;
+    const bool act = o < total;
+    double s0 = 0.0, s1 = 0.0;
+    if (act) {
+      const int64_t gi = o % T.g;
+      const int64_t rest = o / T.g;
+      const int64_t b = rest % T.rr;
+      const int64_t pi = rest / T.rr;
+      const double* in = T.in + gi + T.g * T.n * pi;
+      const int64_t cs = T.transpose ? 1 : T.rr;
+      const double* cf = T.transpose ? T.u + T.n * b : T.u + b;
+      int64_t i = sub;
+      if (T.nparts == 1) {
+        for (; i + S < T.n; i += 2 * S) {
+          s0 = fma(in[T.g * i], cf[cs * i], s0);
+          s1 = fma(in[T.g * (i + S)], cf[cs * (i + S)], s1);
+        }
+        if (i < T.n) s0 = fma(in[T.g * i], cf[cs * i], s0);
+      } else {
+        for (; i < T.n; i += S) {
+          const double* pp = in + T.g * i;
+          double v0 = pp[0], v1 = 0.0;
+          int q = 1;
+          for (; q + 1 < T.nparts; q += 2) {
+            v0 += pp[q * T.part_stride];
+            v1 += pp[(q + 1) * T.part_stride];
+          }
+          if (q < T.nparts) v0 += pp[q * T.part_stride];
+          s0 = fma(v0 + v1, cf[cs * i], s0);
+        }
+      }
+    }
+    double s = s0 + s1;
+#pragma unroll
+    for (int off = S / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (act && sub == 0) T.out[o] = s;
+  }
+}
+
 // All factor reformatting of a core pass in one launch: blockIdx.y = 0
 // builds U0's fragments, 1..2 transpose U1, U2 to row-major.
 struct PrepJobs {
@@ -609,6 +660,13 @@ cudaError_t srtt_launch_transpose(const double* u, int64_t n, int r, double* ut,
 
 cudaError_t srtt_launch_ttm(const TtmParams& T, cudaStream_t s) {
   const int64_t total = T.g * T.rr * T.post;
+  if (total <= 148 * 256 * 2 && T.n >= 8) {
+    // few outputs: spread each contraction over 8 lanes
+    const int64_t threads = total * 8;
+    const int blocks = (int)min64(148 * 8, (threads + 255) / 256);
+    ttm_split_kernel<8><<<blocks > 0 ? blocks : 1, 256, 0, s>>>(T);
+    return cudaGetLastError();
+  }
   const int blocks = (int)min64(148 * 16, (total + 255) / 256);
   ttm_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(T);
   return cudaGetLastError();
