@@ -10,6 +10,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -564,26 +566,25 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
   const double tp_bytes = 16.0 * P.RB * 8.0;
   for (int m = 2; m <= std::min(3, d); ++m) {
     if (force_m && m != force_m) continue;
-    CoreParams T = P;
-    T.m = m;
-    T.A = (int)(ranks[0] * ranks[1] * (m == 3 ? ranks[2] : 1));
-    // 16 warps when the rank tiles are small (register budget 128/thread);
-    // widest box that still leaves a ring of >= 3 boxes per warp
-    T.warps = (P.NT * P.NT1 <= 4) ? 16 : 8;
-    int tpb = 0, ns = 0;
-    for (int tb : {2, 1}) {
-      if (tb == 2 && (P.NT > 2 || P.NT1 > 2)) continue;
-      T.tpb = tb;
-      const int n = srtt_core_max_stages(T, kCoreSmem);
-      if (n >= 3 || (tb == 1 && n >= 2)) {
-        tpb = tb;
-        ns = n;
-        break;
-      }
-    }
-    if (!tpb && T.warps == 16) {  // fall back to 8 warps
-      T.warps = 8;
+    // warps per CTA: 16 when the rank tiles are small (register budget
+    // 128/thread), else 8; each with the widest box that leaves a ring of
+    // >= 3 boxes per warp (2 for single-tile boxes)
+    // development aid: SRTT_FORCE_CORE="warps,tpb" pins the candidate
+    int force_w = 0, force_tpb = 0;
+    if (const char* fc = std::getenv("SRTT_FORCE_CORE")) std::sscanf(fc, "%d,%d", &force_w, &force_tpb);
+    // (measured on C2/C3/C4: 10 or 12 warps balance an item's tile groups
+    // better but lose more in latency hiding than they gain, within +-3 %)
+    for (int W : {16, 8}) {
+      if (W == 16 && P.NT * P.NT1 > 4) continue;
+      if (force_w && W != force_w) continue;
+      CoreParams T = P;
+      T.m = m;
+      T.A = (int)(ranks[0] * ranks[1] * (m == 3 ? ranks[2] : 1));
+      T.warps = W;
+      int tpb = 0, ns = 0;
       for (int tb : {2, 1}) {
+        if (tb == 2 && (P.NT > 2 || P.NT1 > 2)) continue;
+        if (force_tpb && tb != force_tpb) continue;
         T.tpb = tb;
         const int n = srtt_core_max_stages(T, kCoreSmem);
         if (n >= 3 || (tb == 1 && n >= 2)) {
@@ -592,42 +593,47 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
           break;
         }
       }
-    }
-    if (!tpb) continue;
-    const int64_t bc = 16 * tpb;
-    const int64_t GS = prod(dims, 1, m);
-    const int64_t G = Q / GS;
-    const int64_t max_s = (GS + bc - 1) / bc;
-    for (int64_t S = 1; S <= max_s; S = S < 8 ? S + 1 : S * 2) {
-      if (force_S && S != force_S) continue;
-      const int64_t SL = ((GS + S - 1) / S + bc - 1) / bc * bc;
-      const int64_t Se = (GS + SL - 1) / SL;
-      const int64_t items = P.nrb * G * Se;
-      const int64_t ntg = SL / bc;
-      const int64_t grid = std::min<int64_t>(items, sms);
-      const int64_t rounds = (items + grid - 1) / grid;
-      const int W = T.warps;
-      const double item_units = (double)((ntg + W - 1) / W) * tpb + 0.5;  // +0.5: item-end barrier/reduction
-      const double stream = (double)rounds * grid * W * item_units * tp_bytes;
-      const double out = 2.0 * (double)items * T.A * 8.0;
-      const double cost = stream + out;
-      if (cost < best.cost) {
-        best.m = m;
-        best.S = (int)Se;
-        best.ns = ns;
-        best.tpb = tpb;
-        best.warps = T.warps;
-        best.SL = SL;
-        best.G = G;
-        best.GS = GS;
-        best.items = items;
-        best.A = T.A;
-        best.cost = cost;
+      if (!tpb) continue;
+      const int64_t bc = 16 * tpb;
+      const int64_t GS = prod(dims, 1, m);
+      const int64_t G = Q / GS;
+      const int64_t max_s = (GS + bc - 1) / bc;
+      for (int64_t S = 1; S <= max_s; S = S < 8 ? S + 1 : S * 2) {
+        if (force_S && S != force_S) continue;
+        const int64_t SL = ((GS + S - 1) / S + bc - 1) / bc * bc;
+        const int64_t Se = (GS + SL - 1) / SL;
+        const int64_t items = P.nrb * G * Se;
+        const int64_t ntg = SL / bc;
+        const int64_t grid = std::min<int64_t>(items, sms);
+        const int64_t rounds = (items + grid - 1) / grid;
+        // time ~ the slowest warp: ceil(ntg / W) tile groups per item, each
+        // worth W/W_all of the SM's stream; +0.5 item-end barrier/reduction;
+        // a small penalty for fewer warps (less latency hiding)
+        const double item_units = (double)((ntg + W - 1) / W) * tpb + 0.5;
+        const double stream = (double)rounds * grid * W * item_units * tp_bytes * (W == 16 ? 1.0 : 1.45);
+        const double out = 2.0 * (double)items * T.A * 8.0;
+        const double cost = stream + out;
+        if (cost < best.cost) {
+          best.m = m;
+          best.S = (int)Se;
+          best.ns = ns;
+          best.tpb = tpb;
+          best.warps = W;
+          best.SL = SL;
+          best.G = G;
+          best.GS = GS;
+          best.items = items;
+          best.A = T.A;
+          best.cost = cost;
+        }
+        if (S >= max_s) break;
       }
-      if (S >= max_s) break;
     }
   }
   if (best.m == 0) invalid("core: no feasible work decomposition");
+  if (std::getenv("SRTT_DEBUG_PLAN"))  // development aid
+    std::fprintf(stderr, "core plan: m=%d S=%d SL=%lld items=%lld warps=%d tpb=%d ns=%d RB=%d cost=%.3g\n", best.m,
+                 best.S, (long long)best.SL, (long long)best.items, best.warps, best.tpb, best.ns, P.RB, best.cost);
   P.m = best.m;
   P.S = best.S;
   P.SL = best.SL;
