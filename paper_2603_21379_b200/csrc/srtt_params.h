@@ -120,10 +120,7 @@ typedef struct CoreParams {
   int32_t warps;           // warps per CTA (8 or 16)
 } CoreParams;
 
-// Generic small TTM used by the tail of the core pass and by reconstruct:
-// out(g, b, post) = sum_i in(g, i, post) * U(i, b)   (U given as n x r).
-// When nparts > 1 the input is a sum of nparts partial tensors spaced by
-// part_stride (fixed summation order: deterministic).
+// Streamed reconstruction error (k_recon.cu).
 typedef struct ResidualParams {
   const double* x;       // n_A x n_B (first index fastest); unused when out is set
   const double* at;      // K x n_A
@@ -145,6 +142,10 @@ typedef struct KronParams {
   int32_t m, pad;
 } KronParams;
 
+// Generic small TTM used by the tail of the core pass and by reconstruct:
+// out(g, b, post) = sum_i in(g, i, post) * U(i, b)   (U given as n x r).
+// When nparts > 1 the input is a sum of nparts partial tensors spaced by
+// part_stride (fixed summation order: deterministic).
 typedef struct TtmParams {
   const double* in;
   const double* u;       // column-major n x rr (ld = n); transpose flag picks U vs U^T
