@@ -563,7 +563,6 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
     int A = 0;
     double cost = 1e300;
   } best;
-  const double tp_bytes = 16.0 * P.RB * 8.0;
   for (int m = 2; m <= std::min(3, d); ++m) {
     if (force_m && m != force_m) continue;
     // warps per CTA: 16 when the rank tiles are small (register budget
@@ -604,15 +603,26 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
         const int64_t Se = (GS + SL - 1) / SL;
         const int64_t items = P.nrb * G * Se;
         const int64_t ntg = SL / bc;
+        // Wall-time model: CTAs run items in rounds; an item takes the larger
+        // of its share of HBM bandwidth and its FP64 tensor-core time, scaled
+        // by the slowest warp's share of the item's tile groups.
         const int64_t grid = std::min<int64_t>(items, sms);
-        const int64_t rounds = (items + grid - 1) / grid;
-        // time ~ the slowest warp: ceil(ntg / W) tile groups per item, each
-        // worth W/W_all of the SM's stream; +0.5 item-end barrier/reduction;
-        // a small penalty for fewer warps (less latency hiding)
-        const double item_units = (double)((ntg + W - 1) / W) * tpb + 0.5;
-        const double stream = (double)rounds * grid * W * item_units * tp_bytes * (W == 16 ? 1.0 : 1.45);
-        const double out = 2.0 * (double)items * T.A * 8.0;
-        const double cost = stream + out;
+        const int64_t full = items / grid, last = items % grid;
+        const double rows = (double)std::min<int64_t>(P.RB, n0);
+        const double bytes_item = rows * (double)SL * 8.0;
+        const double flops_item = (double)SL * (16.0 * P.NT * P.RB + 128.0 * P.NT * P.NT1);
+        const double imb = (double)((ntg + W - 1) / W) * W / (double)ntg;
+        const double kBw = 6.5e12 * 0.85, kDmmaSm = 37.1e12 / 148.0 * 0.9, kItemOverhead = 1.5e-6;
+        auto t_item = [&](int64_t active) {
+          const double t_mem = bytes_item * (double)active / kBw;
+          const double t_cmp = flops_item / kDmmaSm;
+          // 8 warps hide less latency: measured 1.45x per item on C2
+          return std::max(t_mem, t_cmp) * imb * (W == 16 ? 1.0 : 1.45) + kItemOverhead;
+        };
+        // tail: partials written + re-read by the tail TTMs (measured ~10x
+        // slower than streaming: strided small reductions) + a launch each
+        const double out = 2.0 * (double)items * T.A * 8.0 / (0.1 * kBw) + 5e-6 * (d - m);
+        const double cost = (double)full * t_item(grid) + (last ? t_item(last) : 0.0) + out;
         if (cost < best.cost) {
           best.m = m;
           best.S = (int)Se;

@@ -479,6 +479,53 @@ __global__ void ttm_split_kernel(const TtmParams T) {
   }
 }
 
+// Input-once variant: one thread per (gi, pi) accumulates all rr outputs in
+// registers, so every input element (and the part sum) is read exactly once;
+// consecutive threads take consecutive gi (coalesced loads and stores).
+template <int RR>
+__global__ void ttm_all_kernel(const TtmParams T) {
+  const int64_t pairs = T.g * T.post;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < pairs;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gi = o % T.g, pi = o / T.g;
+    const double* in = T.in + gi + T.g * T.n * pi;
+    double acc[RR];
+#pragma unroll
+    for (int b = 0; b < RR; ++b) acc[b] = 0.0;
+    // coefficient (i, b): U^T (u is n x rr) or U (u is rr x n)
+    const int64_t cs = T.transpose ? T.n : 1, ci = T.transpose ? 1 : T.rr;
+    constexpr int kB = 8;  // rows per batch: their loads are in flight together
+    for (int64_t i0 = 0; i0 < T.n; i0 += kB) {
+      double v[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int64_t i = i0 + u;
+        v[u] = 0.0;
+        if (i < T.n) {
+          const double* pp = in + T.g * i;
+          double s0 = pp[0];
+          for (int q = 1; q < T.nparts; ++q) s0 += pp[q * T.part_stride];
+          v[u] = s0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int64_t i = i0 + u;
+        if (i < T.n) {
+          const double* cf = T.u + ci * i;
+#pragma unroll
+          for (int b = 0; b < RR; ++b)
+            if (b < T.rr) acc[b] = fma(v[u], __ldg(cf + cs * b), acc[b]);
+        }
+      }
+    }
+    double* out = T.out + gi + T.g * T.rr * pi;
+#pragma unroll
+    for (int b = 0; b < RR; ++b)
+      if (b < T.rr) out[T.g * b] = acc[b];
+  }
+}
+
 // All factor reformatting of a core pass in one launch: blockIdx.y = 0
 // builds U0's fragments, 1..2 transpose U1, U2 to row-major.
 struct PrepJobs {
@@ -660,6 +707,16 @@ cudaError_t srtt_launch_transpose(const double* u, int64_t n, int r, double* ut,
 
 cudaError_t srtt_launch_ttm(const TtmParams& T, cudaStream_t s) {
   const int64_t total = T.g * T.rr * T.post;
+  const int64_t pairs = T.g * T.post;
+  const double in_bytes = 8.0 * (double)T.g * T.n * T.post * T.nparts;
+  if (T.rr <= 32 && pairs >= 148 * 128 && in_bytes * T.rr > 64e6) {
+    // large input re-read rr times by the per-output kernels: read it once
+    const int blocks = (int)min64(148 * 8, (pairs + 127) / 128);
+    if (T.rr <= 8) ttm_all_kernel<8><<<blocks, 128, 0, s>>>(T);
+    else if (T.rr <= 16) ttm_all_kernel<16><<<blocks, 128, 0, s>>>(T);
+    else ttm_all_kernel<32><<<blocks, 128, 0, s>>>(T);
+    return cudaGetLastError();
+  }
   if (total <= 148 * 256 * 2 && T.n >= 8) {
     // few outputs: spread each contraction over 8 lanes
     const int64_t threads = total * 8;
