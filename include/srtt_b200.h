@@ -21,9 +21,10 @@
  *
  * Synchronisation: a decomposition with host outputs or a non-NULL report
  * returns after the work completed. With device outputs and rep == NULL,
- * srtt_sub_r_hosvd is stream-ordered like a cuBLAS call: it returns once
- * the work is enqueued on the handle's stream (srtt_set_stream), so
- * back-to-back calls overlap host preparation with device execution.
+ * srtt_sub_r_hosvd and srtt_sub_r_rtl_ht are stream-ordered like a cuBLAS
+ * call: they return once the work is enqueued on the handle's stream
+ * (srtt_set_stream), so back-to-back calls overlap host preparation with
+ * device execution.
  */
 #ifndef SRTT_B200_H
 #define SRTT_B200_H

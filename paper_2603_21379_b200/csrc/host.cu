@@ -1599,7 +1599,12 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     }
   }
   tm.mark();  // 7
-  end_call(h, true);
+  // device outputs and no report: stream-ordered, return without waiting
+  // (the next call's host work overlaps this one's kernels)
+  if (!end_call(h, !out_on_device || rep != nullptr)) {
+    CK(cudaGetLastError());
+    return;
+  }
   CK(cudaStreamSynchronize(h->stream));
   CK(cudaGetLastError());
   for (int t = 0; t < nt; ++t) {

@@ -493,11 +493,14 @@ def sub_r_rtl_ht(x, tree, ranks, samples, oversampling, seed, exec_policy=None, 
                    C.cast(wbuf, C.c_char_p), 8192, 0)
     ct = tree._c()
     ex = exec_policy._c() if exec_policy is not None else None
+    # device outputs and no report: the call is stream-ordered (returns
+    # before the kernels finish, like sub_r_hosvd)
+    rep_arg = None if (device_out and report is None) else C.byref(crep)
     _check(_L().srtt_sub_r_rtl_ht(h._h, xp, xdev, d, dims_a.ctypes.data, C.byref(ct), ranks_a.ctypes.data,
                                   samp_a.ctypes.data, int(oversampling), int(seed) & (2**64 - 1),
-                                  C.byref(ex) if ex is not None else None, lp, tp, int(device_out),
-                                  C.byref(crep)))
-    _report_from(crep, nn, ach, sc, report, h)
+                                  C.byref(ex) if ex is not None else None, lp, tp, int(device_out), rep_arg))
+    if rep_arg is not None:
+        _report_from(crep, nn, ach, sc, report, h)
     if device_out:
         return HTuckerDecomposition(tree, leaf, [trs.get(i) for i in range(nn)])
     leaf_np = [leaf[m].reshape(leaf_shape[m], order="F") for m in range(d)]
