@@ -29,7 +29,8 @@ size_t srtt_sketch_smem_bytes(int cmax);
 cudaError_t srtt_launch_sketch(const SketchTarget*, int, int64_t, int, cudaStream_t);
 size_t srtt_basis_top_smem(int m, int c, int r);
 size_t srtt_basis_level_smem(int mb, int c);
-cudaError_t srtt_launch_basis_top(const BasisTarget*, const int*, int, size_t, cudaStream_t);
+cudaError_t srtt_launch_basis_top(int, const BasisTarget*, const int*, int, size_t, cudaStream_t);
+int srtt_basis_top_variant(int c);
 size_t srtt_basis_small_smem(int m, int c, int r);
 cudaError_t srtt_launch_basis_small(int, const BasisTarget*, const int*, int, size_t, cudaStream_t);
 int srtt_basis_small_variant(int m, int c);
@@ -432,6 +433,8 @@ bool basis_is_small(const BasisTarget& t) {
 struct BasisLists {
   std::vector<int> small, big;
   std::vector<int> small_v[kSmallVariants];  // small targets by kernel variant
+  std::vector<int> big_v[3];                  // big targets by top-kernel variant
+  size_t off_big_v[3] = {};
   size_t off_small = 0, off_big = 0;  // blob offsets
   size_t off_small_v[kSmallVariants] = {};
   size_t off_map[SRTT_MAX_QR_LEVELS] = {};  // per TSQR level: CTA -> (target, block)
@@ -453,6 +456,9 @@ BasisLists make_basis_lists(const std::vector<BasisTarget>& targets, Blob& blob)
   for (int i : L.small) L.small_v[srtt_basis_small_variant((int)targets[i].n, targets[i].c)].push_back(i);
   for (int v = 0; v < kSmallVariants; ++v)
     if (!L.small_v[v].empty()) L.off_small_v[v] = blob.add(L.small_v[v].data(), sizeof(int) * L.small_v[v].size());
+  for (int i : L.big) L.big_v[srtt_basis_top_variant(targets[i].c)].push_back(i);
+  for (int v = 0; v < 3; ++v)
+    if (!L.big_v[v].empty()) L.off_big_v[v] = blob.add(L.big_v[v].data(), sizeof(int) * L.big_v[v].size());
   L.off_big = blob.add(L.big.empty() ? &zero : L.big.data(), sizeof(int) * std::max<size_t>(1, L.big.size()));
   return L;
 }
@@ -487,12 +493,15 @@ int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const 
                                h->stream));
     ++launches;
   }
-  size_t smem = 0;
-  for (int i : lists.big)
-    smem = std::max(smem, srtt_basis_top_smem((int)targets[i].lv[targets[i].nlevels].n, targets[i].c, targets[i].r));
-  CK(srtt_launch_basis_top(dT, reinterpret_cast<const int*>(dblob + lists.off_big), (int)lists.big.size(), smem,
-                           h->stream));
-  ++launches;
+  for (int v = 0; v < 3; ++v) {
+    if (lists.big_v[v].empty()) continue;
+    size_t smem = 0;
+    for (int i : lists.big_v[v])
+      smem = std::max(smem, srtt_basis_top_smem((int)targets[i].lv[targets[i].nlevels].n, targets[i].c, targets[i].r));
+    CK(srtt_launch_basis_top(v, dT, reinterpret_cast<const int*>(dblob + lists.off_big_v[v]),
+                             (int)lists.big_v[v].size(), smem, h->stream));
+    ++launches;
+  }
   for (int l = maxlev - 1; l >= 0; --l) {
     int nctas = 0;
     size_t sm = 0;

@@ -42,7 +42,15 @@ __device__ long long g_basis_clk[16];
     __syncwarp();    \
     if (blockIdx.x == 0 && threadIdx.x == 0) g_basis_clk[i] = clock64(); \
   } while (0)
+#define PROF_MARK_CTA(i) \
+  do {                   \
+    __syncthreads();     \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_basis_clk[i] = clock64(); \
+  } while (0)
 #else
+#define PROF_MARK_CTA(i) \
+  do {                   \
+  } while (0)
 #define PROF_MARK(i) \
   do {               \
   } while (0)
@@ -440,6 +448,8 @@ __device__ void pad_columns(double* Y, int64_t n, int64_t ldy, int q, int r, uin
   __syncthreads();
 }
 
+__host__ __device__ inline int odd_ld(int n) { return n | 1; }
+
 struct TopSmem {
   double* vn;
   double* A;
@@ -461,14 +471,14 @@ __device__ TopSmem carve_top(unsigned char* raw, int m, int c, int r) {
   TopSmem s;
   double* p = reinterpret_cast<double*>(raw);
   s.vn = p; p += c;
-  s.A = p; p += (size_t)m * c;
+  s.A = p; p += (size_t)odd_ld(m) * c;
   s.B = p; p += (size_t)k * c;
   s.V = p; p += (size_t)k * k;
   s.Y = p; p += (size_t)m * r;
   s.tau = p; p += c;
   s.sig = p; p += k;
   s.dots = p; p += r;
-  s.red = p; p += 32;
+  s.red = p; p += kWarps * 32 + 64;
   s.vpad = p; p += m;
   s.scal_beta = p; p += 2;
   s.perm = reinterpret_cast<int*>(p);
@@ -477,6 +487,124 @@ __device__ TopSmem carve_top(unsigned char* raw, int m, int c, int r) {
 }
 
 // Top of the TSQR tree (or the whole basis for single-block targets).
+// CTA-wide lane-per-column QR / back-application for tall small-c matrices
+// (the stacked R of a TSQR top level): lane l owns column l (c <= 32), the
+// kWarps warps own contiguous row slices; each reflector costs a few CTA
+// barriers, per-lane dot/update loops over ~m/kWarps rows and one
+// cross-warp reduction of 32 partial dots. red: kWarps * 32 + 64 doubles.
+__device__ void qr_cols_cta(const double* __restrict__ z, int m, int c, double* A, int lda, double* tau,
+                            double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int k = min(m, c);
+  double* wsum = red + kWarps * 32;  // 32 scaled dots
+  double* bc = wsum + 32;            // tau, scal, beta
+  for (int idx = threadIdx.x; idx < m * c; idx += kThreads) A[(size_t)(idx / m) * lda + idx % m] = __ldg(z + idx);
+  __syncthreads();
+  const int rows_per = (m + kWarps - 1) / kWarps;
+  const int r_lo = warp * rows_per, r_hi = min(m, r_lo + rows_per);
+  for (int j = 0; j < k; ++j) {
+    double* col = A + (size_t)j * lda;
+    const int i0 = max(r_lo, j + 1);
+    double part = 0.0;
+    for (int i = i0 + lane; i < r_hi; i += 32) part = fma(col[i], col[i], part);
+    part = warp_sum(part);
+    if (lane == 0) red[warp * 32] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double ss = 0.0;
+      for (int w = 0; w < kWarps; ++w) ss += red[w * 32];
+      const double alpha = col[j];
+      double tj = 0.0, scal = 0.0, beta = alpha;
+      if (ss != 0.0) {
+        const double nrm = sqrt(fma(alpha, alpha, ss));
+        beta = -copysign(nrm, alpha);
+        tj = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      bc[0] = tj;
+      bc[1] = scal;
+      bc[2] = beta;
+      tau[j] = tj;
+    }
+    __syncthreads();
+    const double tj = bc[0];
+    if (tj != 0.0) {
+      const double scal = bc[1];
+      for (int i = i0 + lane; i < r_hi; i += 32) col[i] *= scal;
+      __syncthreads();
+      double p = 0.0;
+      if (lane > j && lane < c) {
+        const double* cl = A + (size_t)lane * lda;
+        for (int i = i0; i < r_hi; ++i) p = fma(col[i], cl[i], p);
+      }
+      red[warp * 32 + lane] = p;
+      __syncthreads();
+      if (warp == 0 && lane > j && lane < c) {
+        double t = A[(size_t)lane * lda + j];
+        for (int w = 0; w < kWarps; ++w) t += red[w * 32 + lane];
+        wsum[lane] = tj * t;
+      }
+      __syncthreads();
+      if (lane > j && lane < c) {
+        double* cl = A + (size_t)lane * lda;
+        const double tw = wsum[lane];
+        for (int i = i0; i < r_hi; ++i) cl[i] = fma(-tw, col[i], cl[i]);
+        if (j >= r_lo && j < r_hi) cl[j] -= tw;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) col[j] = bc[2];
+    __syncthreads();
+  }
+}
+
+__device__ void apply_cols_cta(const double* A, int lda, const double* tau, int m, int k, const double* V, int ldv,
+                               const int* perm, int q, double* Y, int ldy, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* wsum = red + kWarps * 32;
+  for (int idx = threadIdx.x; idx < m * q; idx += kThreads) {
+    const int i = idx % m, col = idx / m;
+    Y[(size_t)col * ldy + i] = i < k ? V[(size_t)perm[col] * ldv + i] : 0.0;
+  }
+  __syncthreads();
+  const int rows_per = (m + kWarps - 1) / kWarps;
+  const int r_lo = warp * rows_per, r_hi = min(m, r_lo + rows_per);
+  for (int j = k - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj == 0.0) continue;
+    const double* v = A + (size_t)j * lda;
+    const int i0 = max(r_lo, j + 1);
+    double p = 0.0;
+    if (lane < q) {
+      const double* y = Y + (size_t)lane * ldy;
+      for (int i = i0; i < r_hi; ++i) p = fma(v[i], y[i], p);
+    }
+    red[warp * 32 + lane] = p;
+    __syncthreads();
+    if (warp == 0 && lane < q) {
+      double t = Y[(size_t)lane * ldy + j];
+      for (int w = 0; w < kWarps; ++w) t += red[w * 32 + lane];
+      wsum[lane] = tj * t;
+    }
+    __syncthreads();
+    if (lane < q) {
+      double* y = Y + (size_t)lane * ldy;
+      const double tw = wsum[lane];
+      for (int i = i0; i < r_hi; ++i) y[i] = fma(-tw, v[i], y[i]);
+      if (j >= r_lo && j < r_hi) y[j] -= tw;
+    }
+    __syncthreads();
+  }
+}
+
+__device__ void qr_cols_lane(const double* __restrict__ z, int m, int c, double* A, int lda, double* tau);
+__device__ void apply_cols_lane(const double* A, int lda, const double* tau, int m, int k, const double* V,
+                                int ldv, const int* perm, int q, double* Y, int ldy);
+
+// JG > 0: warp 0 runs the lane-per-column QR, the register Jacobi <JG, JE>
+// and the lane-per-column back-application (c <= 32, the latency chain of a
+// small stacked R); JG = 0: the CTA-wide shared-memory QRCP / 4-lane Jacobi.
+template <int JG, int JE>
 __global__ void __launch_bounds__(kThreads) basis_top_kernel(const BasisTarget* __restrict__ targets,
                                                             const int* __restrict__ list) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -490,25 +618,40 @@ __global__ void __launch_bounds__(kThreads) basis_top_kernel(const BasisTarget* 
   const int c = T.c, r = T.r;
   const int k = min(m, c);
   TopSmem s = carve_top(smem_raw, m, c, r);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lda = JG > 0 ? odd_ld(m) : m;
+  PROF_MARK_CTA(8);
 
-  for (int idx = threadIdx.x; idx < m * c; idx += blockDim.x) {
-    const int i = idx % m, j = idx / m;
-    s.A[idx] = L.a[(int64_t)j * L.n + i];
+  if constexpr (JG > 0) {
+    qr_cols_cta(L.a, m, c, s.A, lda, s.tau, s.red);
+  } else {
+    for (int idx = threadIdx.x; idx < m * c; idx += blockDim.x) {
+      const int i = idx % m, j = idx / m;
+      s.A[idx] = L.a[(int64_t)j * L.n + i];
+    }
+    __syncthreads();
+    householder_qr(s.A, m, c, m, s.tau, s.scal_beta, s.vn);
   }
   __syncthreads();
-  householder_qr(s.A, m, c, m, s.tau, s.scal_beta, s.vn);
+  PROF_MARK_CTA(9);
   // B = R (k x c, row-major), V = I.
   for (int idx = threadIdx.x; idx < k * c; idx += blockDim.x) {
     const int i = idx / c, j = idx % c;
-    s.B[idx] = (j >= i) ? s.A[(size_t)j * m + i] : 0.0;
+    s.B[idx] = (j >= i) ? s.A[(size_t)j * lda + i] : 0.0;
   }
   for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) s.V[idx] = (idx % k == idx / k) ? 1.0 : 0.0;
   __syncthreads();
-  build_pairs(pairs, (k + 1) & ~1);
-  __syncthreads();
-  const int sweeps = jacobi_rows_g4(s.B, c, k, c, s.V, k, pairs);
+  int sweeps = 0;
+  if constexpr (JG > 0) {
+    if (warp == 0) sweeps = jacobi_rows_reg<JG, JE>(s.B, c, k, c, s.V, k);
+    __syncthreads();
+  } else {
+    build_pairs(pairs, (k + 1) & ~1);
+    __syncthreads();
+    sweeps = jacobi_rows_g4(s.B, c, k, c, s.V, k, pairs);
+  }
+  PROF_MARK_CTA(10);
   // Singular values = row norms; sort descending (ties by index).
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = warp; i < k; i += kWarps) {
     double ss = 0.0;
     for (int j = lane; j < c; j += 32) ss += s.B[(size_t)i * c + j] * s.B[(size_t)i * c + j];
@@ -535,14 +678,20 @@ __global__ void __launch_bounds__(kThreads) basis_top_kernel(const BasisTarget* 
   }
   if (T.sv)
     for (int i = threadIdx.x; i < k; i += blockDim.x) T.sv[i] = s.sig[s.perm[i]];
+  PROF_MARK_CTA(11);
   // Y = Q [V(:, perm[:q]); 0]
-  for (int idx = threadIdx.x; idx < m * q; idx += blockDim.x) {
-    const int i = idx % m, col = idx / m;
-    s.Y[idx] = (i < k) ? s.V[(size_t)s.perm[col] * k + i] : 0.0;
+  if constexpr (JG > 0) {
+    apply_cols_cta(s.A, lda, s.tau, m, k, s.V, k, s.perm, q, s.Y, m, s.red);
+  } else {
+    for (int idx = threadIdx.x; idx < m * q; idx += blockDim.x) {
+      const int i = idx % m, col = idx / m;
+      s.Y[idx] = (i < k) ? s.V[(size_t)s.perm[col] * k + i] : 0.0;
+    }
+    __syncthreads();
+    for (int col = warp; col < q; col += kWarps) apply_q_warp(s.A, m, k, m, s.tau, s.Y + (size_t)col * m);
   }
   __syncthreads();
-  for (int col = warp; col < q; col += kWarps) apply_q_warp(s.A, m, k, m, s.tau, s.Y + (size_t)col * m);
-  __syncthreads();
+  PROF_MARK_CTA(12);
   if (top == 0) {
     // Single block: Y already spans the final rows; pad in shared memory.
     if (q < r)
@@ -555,6 +704,7 @@ __global__ void __launch_bounds__(kThreads) basis_top_kernel(const BasisTarget* 
       L.y[(int64_t)col * L.n + i] = s.Y[idx];
     }
   }
+  PROF_MARK_CTA(13);
 }
 
 // One TSQR level below the top: factor each row block, stack its R.
@@ -670,7 +820,6 @@ struct SmallSmem {
   int lda, ldb, ldv;
 };
 
-__host__ __device__ inline int odd_ld(int n) { return n | 1; }
 
 __device__ SmallSmem carve_small(unsigned char* raw, int m, int c, int r) {
   const int k = min(m, c);
@@ -1075,7 +1224,7 @@ __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __re
 
 size_t srtt_basis_top_smem(int m, int c, int r) {
   const int k = m < c ? m : c;
-  size_t doubles = (size_t)c + (size_t)m * c + (size_t)k * c + (size_t)k * k + (size_t)m * r + c + k + r + 32 + m + 2;
+  size_t doubles = (size_t)kWarps * 32 + 32 + (size_t)c + (size_t)(m | 1) * c + (size_t)k * c + (size_t)k * k + (size_t)m * r + c + k + r + 32 + m + 2;
   return doubles * sizeof(double) + 2 * sizeof(int) * (size_t)(k + 2);
 }
 
@@ -1120,11 +1269,25 @@ cudaError_t srtt_launch_basis_small(int variant, const BasisTarget* d_targets, c
   return cudaGetLastError();
 }
 
-cudaError_t srtt_launch_basis_top(const BasisTarget* d_targets, const int* d_list, int ntargets, size_t smem,
-                                  cudaStream_t stream) {
+int srtt_basis_top_variant(int c) { return c <= 16 ? 0 : (c <= 32 ? 1 : 2); }
+
+cudaError_t srtt_launch_basis_top(int variant, const BasisTarget* d_targets, const int* d_list, int ntargets,
+                                  size_t smem, cudaStream_t stream) {
   if (ntargets <= 0) return cudaSuccess;
-  SRTT_ENSURE_SMEM((basis_top_kernel), smem);
-  basis_top_kernel<<<ntargets, kThreads, smem, stream>>>(d_targets, d_list);
+  switch (variant) {
+    case 0:
+      SRTT_ENSURE_SMEM((basis_top_kernel<4, 4>), smem);
+      basis_top_kernel<4, 4><<<ntargets, kThreads, smem, stream>>>(d_targets, d_list);
+      break;
+    case 1:
+      SRTT_ENSURE_SMEM((basis_top_kernel<2, 16>), smem);
+      basis_top_kernel<2, 16><<<ntargets, kThreads, smem, stream>>>(d_targets, d_list);
+      break;
+    default:
+      SRTT_ENSURE_SMEM((basis_top_kernel<0, 0>), smem);
+      basis_top_kernel<0, 0><<<ntargets, kThreads, smem, stream>>>(d_targets, d_list);
+      break;
+  }
   return cudaGetLastError();
 }
 

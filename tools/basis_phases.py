@@ -31,4 +31,8 @@ for name in sys.argv[1:] or ["c2"]:
     srtt._L().srtt_debug_basis_clocks(clk)
     v = list(clk)[:8]
     d = np.diff(v)
-    print(name, "cycles:", " ".join(f"{n}={int(c)}" for n, c in zip(names[1:], d)), "total", v[7] - v[0])
+    print(name, "small cycles:", " ".join(f"{n}={int(c)}" for n, c in zip(names, d)), "total", v[7] - v[0])
+    t = list(clk)[8:14]
+    if t[0]:
+        tn = ["qr", "jacobi", "sigma", "apply", "store"]
+        print(name, "top cycles:", " ".join(f"{n}={int(b - a)}" for n, a, b in zip(tn, t[:-1], t[1:])))
