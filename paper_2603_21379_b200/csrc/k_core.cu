@@ -451,24 +451,20 @@ __global__ void ttm_split_kernel(const TtmParams T) {
       const double* in = T.in + gi + T.g * T.n * pi;
       const int64_t cs = T.transpose ? 1 : T.rr;
       const double* cf = T.transpose ? T.u + T.n * b : T.u + b;
-      int64_t i = sub;
       if (T.nparts == 1) {
+        int64_t i = sub;
         for (; i + S < T.n; i += 2 * S) {
           s0 = fma(in[T.g * i], cf[cs * i], s0);
           s1 = fma(in[T.g * (i + S)], cf[cs * (i + S)], s1);
         }
         if (i < T.n) s0 = fma(in[T.g * i], cf[cs * i], s0);
       } else {
-        for (; i < T.n; i += S) {
-          const double* pp = in + T.g * i;
-          double v0 = pp[0], v1 = 0.0;
-          int q = 1;
-          for (; q + 1 < T.nparts; q += 2) {
-            v0 += pp[q * T.part_stride];
-            v1 += pp[(q + 1) * T.part_stride];
-          }
-          if (q < T.nparts) v0 += pp[q * T.part_stride];
-          s0 = fma(v0 + v1, cf[cs * i], s0);
+        // lanes split the flattened (i, part) space: lane sub takes every
+        // S-th (i, q) pair in i-major order (fixed order per lane)
+        const int64_t np = T.nparts, total_iq = T.n * np;
+        for (int64_t e = sub; e < total_iq; e += S) {
+          const int64_t i = e / np, q = e - i * np;
+          s0 = fma(in[T.g * i + q * T.part_stride], cf[cs * i], s0);
         }
       }
     }
@@ -717,8 +713,8 @@ cudaError_t srtt_launch_ttm(const TtmParams& T, cudaStream_t s) {
     else ttm_all_kernel<32><<<blocks, 128, 0, s>>>(T);
     return cudaGetLastError();
   }
-  if (total <= 148 * 256 * 2 && T.n >= 8) {
-    // few outputs: spread each contraction over 8 lanes
+  if (total <= 148 * 256 * 2 && T.n * T.nparts >= 8) {
+    // few outputs: spread each contraction (and part sum) over 8 lanes
     const int64_t threads = total * 8;
     const int blocks = (int)min64(148 * 8, (threads + 255) / 256);
     ttm_split_kernel<8><<<blocks > 0 ? blocks : 1, 256, 0, s>>>(T);
