@@ -139,11 +139,33 @@ def _run_oracle(O, cfg, X, seed):
     return O.sub_r_rtl_ht(X, tree, ranks, samples, cfg.p, seed)
 
 
+# CPU samples of tensors larger than CPU_SAMPLE_BYTES are cut to a leading
+# slab of about CPU_SLAB_BYTES along the last mode (a contiguous byte range of
+# X; same ranks, oversampling and fibre counts) -- C5 only
+CPU_SAMPLE_BYTES = 16e9
+CPU_SLAB_BYTES = 2.2e9
+
+
+def cpu_sample(cfg, x_host_flat):
+    """(config, flat data, description) of the bounded CPU sample of `cfg`."""
+    import dataclasses
+
+    if cfg.entries * 8 <= CPU_SAMPLE_BYTES:
+        return cfg, x_host_flat, f"full {cfg.name} decomposition (N={cfg.entries})"
+    inner = cfg.entries // cfg.dims[-1]
+    last = max(cfg.rank, int(CPU_SLAB_BYTES // (8 * inner)))
+    dims = tuple(cfg.dims[:-1]) + (last,)
+    sub = dataclasses.replace(cfg, dims=dims)
+    return sub, None if x_host_flat is None else x_host_flat[: inner * last], (f"leading slab {'x'.join(map(str, dims))} of {cfg.name} "
+                                              f"(N={sub.entries}, same r/p/s) decomposed as one tensor")
+
+
 def cpu_baseline(cfg, x_host_flat, seed, budget_s=20.0, max_runs=5):
     """Oracle port on the host cores, bounded to ~budget_s of CPU work."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import srtt_oracle as O
 
+    cfg, x_host_flat, what = cpu_sample(cfg, x_host_flat)
     X = O.as_tensor(x_host_flat, cfg.dims)
     _run_oracle(O, cfg, X, seed)  # warm-up (BLAS threads, page faults)
     times = []
@@ -154,7 +176,7 @@ def cpu_baseline(cfg, x_host_flat, seed, budget_s=20.0, max_runs=5):
         times.append(time.perf_counter() - t0)
     med = statistics.median(times)
     return {"value": cfg.entries / med, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-            "sample": f"full {cfg.name} decomposition (N={cfg.entries}), median of {len(times)} runs, numpy+OpenBLAS "
+            "sample": f"{what}, median of {len(times)} runs, numpy+OpenBLAS "
                       f"restatement in oracle/ (reference needs Eigen, absent)",
             "seconds_per_step": med}
 
@@ -171,8 +193,13 @@ def run_reference(args):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import srtt_oracle as O
 
-    cfg = synth.CONFIGS[args.config]
-    x = synth.make_tensor(cfg, seed=0, backend="numpy")
+    full = synth.CONFIGS[args.config]
+    if full.entries * 8 > CPU_SAMPLE_BYTES:
+        cfg, _, what = cpu_sample(full, None)
+        x = synth.make_tensor(full, seed=0, backend="numpy", dims=cfg.dims)
+    else:
+        cfg, what = full, f"full {full.name} decomposition per step"
+        x = synth.make_tensor(cfg, seed=0, backend="numpy")
     X = O.as_tensor(x, cfg.dims)
     for _ in range(args.warmup):
         _run_oracle(O, cfg, X, 0)
@@ -184,12 +211,56 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": _config_dict(cfg),
+            "data": "synthetic", "config": _config_dict(full),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                             "sample": f"full {cfg.name} decomposition per step (numpy+OpenBLAS restatement of the "
+                             "sample": f"{what} (numpy+OpenBLAS restatement of the "
                                        f"reference in oracle/; the reference needs Eigen, absent in this image)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# FP64 tensor-core (DMMA.8x8x4) peak measured on this pool's B200
+# (profiles/r01_fp64_peak_microbench.txt); the bf16 figure in
+# MEASURED_PEAKS.json does not apply to an fp64 kernel.
+DMMA_PEAK_TFLOPS = 37.07
+
+
+def core_flops(cfg):
+    """Algorithmic flops of the core pass: the TTM chain in mode order
+    2 N r0 + 2 (N/n0) r0 r1 + ..., no padding."""
+    n = float(cfg.entries)
+    f, cur = 0.0, n
+    for k, nk in enumerate(cfg.dims):
+        r = cfg.rank if cfg.kind == "tucker" else (cfg.rank if k == 0 else 0)
+        if r == 0:
+            break
+        f += 2.0 * cur * r
+        cur = cur / nk * r
+    if cfg.kind == "htucker":  # root transfer: 2 N r_left (+ tiny second GEMM)
+        f = 2.0 * n * cfg.rank
+    return f
+
+
+def core_roofline(cfg, core_s, peaks, peak_kind):
+    """Roofline of the dominant kernel (core pass, X streamed once): HBM-bound
+    when its arithmetic intensity on the DMMA pipe is under the ridge, else
+    FP64-tensor-bound (C5: 2 r0 = 64 flop per 8-byte entry)."""
+    alg_bytes = 8.0 * cfg.entries
+    flops = core_flops(cfg)
+    ridge = DMMA_PEAK_TFLOPS * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    gbs = alg_bytes / core_s / 1e9 if core_s > 0 else None
+    tfs = flops / core_s / 1e12 if core_s > 0 else None
+    common = {"kernel": "core_kernel (K3/K5 streaming multi-TTM)", "traffic": _traffic_from_profiles(cfg.name),
+              "algorithmic_bytes_per_launch": alg_bytes, "algorithmic_flops_per_launch": flops,
+              "kernel_ms": core_s * 1e3}
+    if flops / alg_bytes > ridge:
+        return dict(common, bound="tensor", achieved=tfs, peak=DMMA_PEAK_TFLOPS,
+                    peak_kind="measured (fp64 DMMA microbench, profiles/r01_fp64_peak_microbench.txt)",
+                    unit="TFLOP/s", frac=(tfs / DMMA_PEAK_TFLOPS) if tfs else None,
+                    hbm={"achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": (gbs / peaks["hbm_gbs"]) if gbs else None})
+    return dict(common, bound="hbm", achieved=gbs, peak=peaks["hbm_gbs"], peak_kind=peak_kind, unit="GB/s",
+                frac=(gbs / peaks["hbm_gbs"]) if gbs else None)
 
 
 def _config_dict(cfg):
@@ -280,6 +351,12 @@ def run_product(args):
     # e2e: through the C-ABI with X in pinned host memory, outputs to host
     x_host = x.cpu().pin_memory()
     xh = x_host.numpy()
+    if 2 * cfg.entries * 8 > 0.6 * torch.cuda.get_device_properties(dev).total_memory:
+        # the library stages X into its own device buffer: drop the resident
+        # copy first (C5: 68.7 GB twice does not fit with the workspace)
+        del x
+        _OUT.clear()
+        torch.cuda.empty_cache()
     for _ in range(max(1, min(args.warmup, 2))):
         _run_product(P, cfg, xh, dims, 0, h, device_out=False)
     e2e_steps = max(1, min(args.steps, 20))
@@ -303,14 +380,8 @@ def run_product(args):
 
     peaks, peak_kind = _peaks()
     core_med = statistics.median(core_t) if core_t else 0.0
-    alg_bytes = 8.0 * cfg.entries
-    achieved = alg_bytes / core_med / 1e9 if core_med > 0 else None
-    roofline = {"bound": "hbm", "kernel": "core_kernel (K3/K5 streaming multi-TTM)",
-                "achieved": achieved, "peak": peaks["hbm_gbs"], "peak_kind": peak_kind, "unit": "GB/s",
-                "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
-                "traffic": _traffic_from_profiles(cfg.name),
-                "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": core_med * 1e3,
-                "kernel_share_of_step": core_med / (elapsed / args.steps)}
+    roofline = core_roofline(cfg, core_med, peaks, peak_kind)
+    roofline["kernel_share_of_step"] = core_med / (elapsed / args.steps)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",

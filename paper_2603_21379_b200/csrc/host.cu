@@ -538,8 +538,11 @@ struct CorePlan {
   std::vector<int64_t> dims;   // modes of the (possibly reshaped) tensor
   std::vector<int64_t> ranks;
   int64_t part_doubles = 0;
+  int64_t rec_doubles = 0;   // flat mode: record slots
+  int64_t cnt_words = 0;     // flat mode: group counters
   size_t ufrag_doubles = 0;
   size_t off_items = 0;
+  size_t off_rec = 0, off_cnt = 0;
 };
 
 int pad_tiles(int64_t r) { return r <= 8 ? 1 : (r <= 16 ? 2 : (r <= 32 ? 4 : 0)); }
@@ -567,11 +570,16 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
   P.frank[0] = (int)ranks[1];
 
   struct Cand {
-    int m = 0, S = 0, ns = 0, tpb = 1, warps = 8;
-    int64_t SL = 0, G = 0, GS = 0, items = 0;
+    int m = 0, S = 0, ns = 0, tpb = 1, warps = 8, flat = 0;
+    int64_t SL = 0, G = 0, GS = 0, items = 0, grid = 0;
     int A = 0;
     double cost = 1e300;
   } best;
+  // flat mode (one row block): balanced per-warp tile ranges, records
+  // reduced inside the kernel. development aid: SRTT_FORCE_FLAT=0/1
+  int force_flat = -1;
+  if (const char* ff = std::getenv("SRTT_FORCE_FLAT")) force_flat = std::atoi(ff);
+  const bool flat_ok = P.nrb == 1 && force_flat != 0;
   for (int m = 2; m <= std::min(3, d); ++m) {
     if (force_m && m != force_m) continue;
     // warps per CTA: 16 when the rank tiles are small (register budget
@@ -606,6 +614,41 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
       const int64_t GS = prod(dims, 1, m);
       const int64_t G = Q / GS;
       const int64_t max_s = (GS + bc - 1) / bc;
+      const double kBw = 6.5e12 * 0.85, kDmmaSm = 37.1e12 / 148.0 * 0.9;
+      const int64_t ntiles_f = (Q + bc - 1) / bc;
+      if (flat_ok && ntiles_f >= W) {
+        // every warp owns >= 1 tile (the group counters count all warps
+        // between a group's first and last owner)
+        const int64_t ntiles = ntiles_f;
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(sms, ntiles / W));
+        const int64_t nw = grid * W;
+        const double imb = (double)((ntiles + nw - 1) / nw) * (double)nw / (double)ntiles;
+        const double rows = (double)std::min<int64_t>(P.RB, n0);
+        const double t_mem = rows * (double)Q * 8.0 / kBw * ((double)sms / (double)grid);
+        const double t_cmp = (double)Q * (16.0 * P.NT * P.RB + 128.0 * P.NT * P.NT1) / (kDmmaSm * (double)grid);
+        // records written and reduced through L2 + compact R read by the tail
+        const double recs = (double)(nw + G) * T.A * 8.0 * 2.0 / (0.3 * kBw) +
+                            // one warp sums a group's records (~20 GB/s per warp)
+                            (double)((GS + bc - 1) / bc * nw / ntiles + 2) * T.A * 8.0 / 20e9;
+        const double out = 2.0 * (double)G * T.A * 8.0 / (0.1 * kBw) + 5e-6 * (d - m);
+        const double cost = std::max(t_mem, t_cmp) * imb * (W == 16 ? 1.0 : 1.45) + recs + out + 1.5e-6;
+        if ((force_flat == 1 && !best.flat) || cost < best.cost) {
+          best = Cand{};
+          best.m = m;
+          best.S = 1;
+          best.ns = ns;
+          best.tpb = tpb;
+          best.warps = W;
+          best.flat = 1;
+          best.G = G;
+          best.GS = GS;
+          best.grid = grid;
+          best.items = ntiles;
+          best.A = T.A;
+          best.cost = cost;
+        }
+        if (force_flat == 1) continue;
+      }
       for (int64_t S = 1; S <= max_s; S = S < 8 ? S + 1 : S * 2) {
         if (force_S && S != force_S) continue;
         const int64_t SL = ((GS + S - 1) / S + bc - 1) / bc * bc;
@@ -621,7 +664,7 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
         const double bytes_item = rows * (double)SL * 8.0;
         const double flops_item = (double)SL * (16.0 * P.NT * P.RB + 128.0 * P.NT * P.NT1);
         const double imb = (double)((ntg + W - 1) / W) * W / (double)ntg;
-        const double kBw = 6.5e12 * 0.85, kDmmaSm = 37.1e12 / 148.0 * 0.9, kItemOverhead = 1.5e-6;
+        const double kItemOverhead = 1.5e-6;
         auto t_item = [&](int64_t active) {
           const double t_mem = bytes_item * (double)active / kBw;
           const double t_cmp = flops_item / kDmmaSm;
@@ -633,6 +676,7 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
         const double out = 2.0 * (double)items * T.A * 8.0 / (0.1 * kBw) + 5e-6 * (d - m);
         const double cost = (double)full * t_item(grid) + (last ? t_item(last) : 0.0) + out;
         if (cost < best.cost) {
+          best = Cand{};
           best.m = m;
           best.S = (int)Se;
           best.ns = ns;
@@ -651,8 +695,9 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
   }
   if (best.m == 0) invalid("core: no feasible work decomposition");
   if (std::getenv("SRTT_DEBUG_PLAN"))  // development aid
-    std::fprintf(stderr, "core plan: m=%d S=%d SL=%lld items=%lld warps=%d tpb=%d ns=%d RB=%d cost=%.3g\n", best.m,
-                 best.S, (long long)best.SL, (long long)best.items, best.warps, best.tpb, best.ns, P.RB, best.cost);
+    std::fprintf(stderr, "core plan: flat=%d m=%d S=%d SL=%lld items=%lld warps=%d tpb=%d ns=%d RB=%d cost=%.3g\n",
+                 best.flat, best.m, best.S, (long long)best.SL, (long long)best.items, best.warps, best.tpb, best.ns,
+                 P.RB, best.cost);
   P.m = best.m;
   P.S = best.S;
   P.SL = best.SL;
@@ -667,7 +712,18 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
     P.fdim[1] = dims[2];
     P.frank[1] = (int)ranks[2];
   }
-  cp.part_doubles = best.items * best.A;
+  P.flat = best.flat;
+  if (best.flat) {
+    P.nitems = 0;
+    P.ntiles = best.items;
+    P.nw = (int)(best.grid * best.warps);
+    cp.grid = (int)best.grid;
+    cp.part_doubles = best.G * best.A;
+    cp.rec_doubles = (P.nw + best.G) * best.A;
+    cp.cnt_words = best.G;
+  } else {
+    cp.part_doubles = best.items * best.A;
+  }
   cp.ufrag_doubles = (size_t)P.nrb * P.RB * P.NT * 8;
   return cp;
 }
@@ -698,6 +754,10 @@ int launch_core_pass(srtt_handle* h, CorePlan& cp, const double* x, const std::v
     }
     CoreItem* items = reinterpret_cast<CoreItem*>(ws + off_items);
     P.items = items;
+    if (P.flat) {
+      P.rec = reinterpret_cast<double*>(ws + cp.off_rec);
+      P.cnt = reinterpret_cast<uint32_t*>(ws + cp.off_cnt);
+    }
     CK(srtt_launch_prep_all(P, items, u[0], P.n0, P.r0, P.RB, P.NT, P.nrb, const_cast<double*>(P.ufrag), P.m - 1,
                             us, uts, ns, rs, h->stream));
     ++launches;
@@ -706,13 +766,14 @@ int launch_core_pass(srtt_handle* h, CorePlan& cp, const double* x, const std::v
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
   if (P.use_tma) encode_tmap(&tmap, x, P.n0, P.Q, 16 * P.tpb);
-  cp.grid = (int)std::min<int64_t>(P.nitems, (int64_t)h->sms);
+  if (!P.flat) cp.grid = (int)std::min<int64_t>(P.nitems, (int64_t)h->sms);
   record_event(h->kev[4], h->stream);
   CK(srtt_launch_core(&tmap, P, cp.grid, h->stream));
   record_event(h->kev[5], h->stream);
   ++launches;
   // tail: fixed-order reduction of the item partials + TTMs of modes m..d-1
-  const int nparts = P.nrb * P.S;
+  // (flat mode: the kernel already reduced its records into compact R_m)
+  const int nparts = P.flat ? 1 : P.nrb * P.S;
   if (P.m == d) {
     TtmParams T{};
     T.in = P.part;
@@ -763,6 +824,8 @@ void layout_core(Layout& L, CorePlan& cp, size_t& off_ufrag, std::vector<size_t>
   off_fu.assign(d, 0);
   for (int k = 1; k < cp.P.m; ++k) off_fu[k] = L.take(sizeof(double) * cp.dims[k] * cp.ranks[k]);
   off_part = L.take(sizeof(double) * cp.part_doubles);
+  cp.off_rec = L.take(sizeof(double) * cp.rec_doubles);
+  cp.off_cnt = L.take(sizeof(uint32_t) * cp.cnt_words);
   // largest intermediate of the tail
   int64_t g = cp.P.A, big = 1;
   for (int k = cp.P.m; k < d; ++k) {

@@ -358,6 +358,313 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   }
 }
 
+// ---- flat mode (single row block, n0 <= 256) --------------------------------
+// Global warp gw owns tiles [T*gw/NW, T*(gw+1)/NW) of BC columns: every warp
+// streams the same number of tiles (+-1), with no CTA barrier after the
+// start, so an item's slowest warp no longer sets the pace. A warp folds its
+// columns exactly as core_kernel does and emits one record per level-m group
+// its range touches; the warp whose record completes a group sums the
+// group's records in warp order (deterministic) into the compact R_m.
+__device__ __forceinline__ int64_t flat_tile_lo(int64_t T, int64_t gw, int64_t nw) { return T * gw / nw; }
+// the (non-empty) warp whose tile range contains tile t
+__device__ __forceinline__ int64_t flat_warp_of(int64_t T, int64_t t, int64_t nw) {
+  return ((t + 1) * nw + T - 1) / T - 1;
+}
+
+template <int WARPS>
+__device__ __forceinline__ void flat_emit(const CoreParams& P, int64_t gw, int64_t p, int lane, int BC) {
+  // record of (gw, p) is in global memory (written by all lanes); publish it
+  __threadfence();
+  __syncwarp();
+  uint32_t last = 0;
+  const int64_t c_first = p * P.GS, c_last = min64((p + 1) * P.GS, P.Q) - 1;
+  const int64_t w_lo = flat_warp_of(P.ntiles, c_first / BC, P.nw);
+  const int64_t w_hi = flat_warp_of(P.ntiles, c_last / BC, P.nw);
+  if (lane == 0) {
+    const uint32_t old = atomicAdd(P.cnt + p, 1u);
+    last = (old == (uint32_t)(w_hi - w_lo)) ? 1u : 0u;
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  __threadfence();
+  for (int e = lane; e < P.A; e += 32) {
+    double sum = __ldcg(P.rec + (w_lo + p) * P.A + e);
+    for (int64_t w = w_lo + 1; w <= w_hi; ++w) sum += __ldcg(P.rec + (w + p) * P.A + e);
+    P.part[p * P.A + e] = sum;
+  }
+  if (lane == 0) P.cnt[p] = 0u;  // ready for the next call (stream order)
+}
+
+template <int MT, int NT1, bool M3, int TPB, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    core_flat_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CoreParams P) {
+  constexpr int BC = 16 * TPB;
+  constexpr int BOX = 16 * BC;
+  constexpr int KP = MT == 1 ? 2 : 1;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const int NS = P.nstages;
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  double* rings = reinterpret_cast<double*>(smem_raw + pad);
+  double* ufrag = rings + (size_t)WARPS * NS * BOX;
+  double* slots = ufrag + (size_t)(P.RB / 4) * MT * 32;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + (size_t)WARPS * P.A);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  double* ring = rings + (size_t)warp * NS * BOX;
+  uint64_t* bar = bars + warp * NS;
+  double* slot = slots + (size_t)warp * P.A;
+
+  const int r0 = P.r0, r1 = P.frank[0];
+  const int n1 = (int)P.fdim[0];
+  const double* __restrict__ U1 = P.fu[0];
+  const int nbox = (int)((P.n0 + 15) / 16);
+
+  int boff[2][4];
+#pragma unroll
+  for (int par = 0; par < 2; ++par)
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int col = 2 * g + par, row = 4 * ks + tq;
+      boff[par][ks] = col * 16 + ((((row >> 1) ^ (col & 7)) << 1) | (row & 1));
+    }
+
+  for (int e = threadIdx.x; e < (P.RB / 4) * MT * 32; e += WARPS * 32) ufrag[e] = P.ufrag[e];
+  if (lane == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  if (M3)
+    for (int e = lane; e < P.A; e += 32) slot[e] = 0.0;
+  __syncthreads();
+
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
+  const int64_t t_lo = flat_tile_lo(P.ntiles, gw, P.nw), t_hi = flat_tile_lo(P.ntiles, gw + 1, P.nw);
+  if (t_lo >= t_hi) return;
+
+  // producer walk over (tile, box)
+  int64_t pt = t_lo;
+  int pb = 0;
+  if (P.use_tma && lane == 0) {
+    prefetch_tmap(&tmap);
+    for (int s = 0; s < NS && pt < t_hi; ++s) {
+      mbar_arrive_expect_tx(&bar[s], BOX * sizeof(double));
+      tma_load_2d(ring + s * BOX, &tmap, &bar[s], 16 * pb, (int32_t)(BC * pt));
+      if (++pb == nbox) {
+        pb = 0;
+        ++pt;
+      }
+    }
+  }
+
+  int stage = 0;
+  uint32_t phase = 0;
+  double r2[MT][NT1][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT1; ++nt) r2[mt][nt][0] = r2[mt][nt][1] = 0.0;
+  int64_t cur_g2 = -1;  // level-2 group held in r2
+  int64_t cur_p = -1;   // level-3 group held in the slot (M3)
+  const int64_t n2 = M3 ? P.fdim[1] : 1;
+
+  // r2 (level-2 group g2) -> record (m = 2) or -> slot of its level-3 group
+  auto retire = [&](int64_t g2) {
+    if (M3) {
+      const int64_t p = g2 / n2;
+      if (p != cur_p) {
+        if (cur_p >= 0) {
+          __syncwarp();
+          double* dst = P.rec + (gw + cur_p) * P.A;
+          for (int e = lane; e < P.A; e += 32) {
+            dst[e] = slot[e];
+            slot[e] = 0.0;
+          }
+          flat_emit<WARPS>(P, gw, cur_p, lane, BC);
+          __syncwarp();
+        }
+        cur_p = p;
+      }
+      const int r2n = P.frank[1];
+      const double* __restrict__ U2 = P.fu[1] + (g2 % n2) * r2n;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT1; ++nt)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int a0 = g + 8 * mt, a1 = 2 * tq + v + 8 * nt;
+            if (a0 < r0 && a1 < r1) {
+              const double val = r2[mt][nt][v];
+              double* dst = slot + a0 + r0 * a1;
+              for (int a2 = 0; a2 < r2n; ++a2) dst[(size_t)r0 * r1 * a2] += val * __ldg(U2 + a2);
+            }
+            r2[mt][nt][v] = 0.0;
+          }
+      __syncwarp();
+    } else {
+      double* dst = P.rec + (gw + g2) * P.A;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT1; ++nt)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int a0 = g + 8 * mt, a1 = 2 * tq + v + 8 * nt;
+            if (a0 < r0 && a1 < r1) dst[a0 + r0 * a1] = r2[mt][nt][v];
+            r2[mt][nt][v] = 0.0;
+          }
+      flat_emit<WARPS>(P, gw, g2, lane, BC);
+    }
+  };
+
+  int64_t grp = (t_lo * BC) / n1;
+  int off = (int)(t_lo * BC - grp * n1);
+  for (int64_t t = t_lo; t < t_hi; ++t) {
+    const int64_t c0 = (int64_t)BC * t;
+    double tacc[TPB][2][MT][KP][2];
+#pragma unroll
+    for (int h = 0; h < TPB; ++h)
+#pragma unroll
+      for (int par = 0; par < 2; ++par)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int kp = 0; kp < KP; ++kp) tacc[h][par][mt][kp][0] = tacc[h][par][mt][kp][1] = 0.0;
+    const double* uf = ufrag + lane;
+    for (int b = 0; b < nbox; ++b, uf += 4 * MT * 32) {
+      double* st = ring + stage * BOX;
+      if (P.use_tma) {
+        mbar_wait(&bar[stage], phase);
+      } else {
+        const int64_t row0 = 16 * b;
+        for (int e = lane; e < BOX; e += 32) {
+          const int jj = e >> 4, ii = e & 15;
+          const int64_t row = row0 + ii, col = c0 + jj;
+          const double v = (row < P.n0 && col < P.Q) ? P.x[col * P.n0 + row] : 0.0;
+          st[jj * 16 + ((((ii >> 1) ^ (jj & 7)) << 1) | (ii & 1))] = v;
+        }
+        __syncwarp();
+      }
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        double a[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) a[mt] = uf[(ks * MT + mt) * 32];
+#pragma unroll
+        for (int h = 0; h < TPB; ++h) {
+          const double x0 = st[h * 256 + boff[0][ks]];
+          const double x1 = st[h * 256 + boff[1][ks]];
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            double* d0 = tacc[h][0][mt][ks % KP];
+            double* d1 = tacc[h][1][mt][ks % KP];
+            dmma_8x8x4(d0[0], d0[1], a[mt], x0);
+            dmma_8x8x4(d1[0], d1[1], a[mt], x1);
+          }
+        }
+      }
+      __syncwarp();
+      if (P.use_tma && lane == 0 && pt < t_hi) {
+        mbar_arrive_expect_tx(&bar[stage], BOX * sizeof(double));
+        tma_load_2d(st, &tmap, &bar[stage], 16 * pb, (int32_t)(BC * pt));
+        if (++pb == nbox) {
+          pb = 0;
+          ++pt;
+        }
+      }
+      if (++stage == NS) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    if (KP == 2) {
+#pragma unroll
+      for (int h = 0; h < TPB; ++h)
+#pragma unroll
+        for (int par = 0; par < 2; ++par)
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            tacc[h][par][mt][0][0] += tacc[h][par][mt][KP - 1][0];
+            tacc[h][par][mt][0][1] += tacc[h][par][mt][KP - 1][1];
+          }
+    }
+#pragma unroll
+    for (int h = 0; h < TPB; ++h) {
+      const int64_t ch = c0 + 16 * h;
+      if (ch >= P.Q) break;
+      const int lim = (int)min64(16, P.Q - ch);
+      if (off + 16 <= n1 && lim == 16) {
+        if (grp != cur_g2) {
+          if (cur_g2 >= 0) retire(cur_g2);
+          cur_g2 = grp;
+        }
+        const double* urow = U1 + (off + 4 * tq) * r1 + g;
+#pragma unroll
+        for (int par = 0; par < 2; ++par)
+#pragma unroll
+          for (int s2 = 0; s2 < 2; ++s2) {
+            double bv[NT1];
+#pragma unroll
+            for (int nt = 0; nt < NT1; ++nt)
+              bv[nt] = (g + 8 * nt < r1) ? __ldg(urow + (2 * s2 + par) * r1 + 8 * nt) : 0.0;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+              for (int nt = 0; nt < NT1; ++nt)
+                dmma_8x8x4(r2[mt][nt][0], r2[mt][nt][1], tacc[h][par][mt][0][s2], bv[nt]);
+          }
+      } else {
+        int64_t gg = grp;
+        int oo = off;
+        for (int lo = 0; lo < lim;) {
+          const int hi = min(lim, lo + n1 - oo);
+          if (gg != cur_g2) {
+            if (cur_g2 >= 0) retire(cur_g2);
+            cur_g2 = gg;
+          }
+          const double* ubase = U1 + (oo - lo) * r1 + g;
+#pragma unroll
+          for (int par = 0; par < 2; ++par)
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+              const int j = 4 * tq + 2 * s2 + par;
+              const bool ok = j >= lo && j < hi;
+              double bv[NT1];
+#pragma unroll
+              for (int nt = 0; nt < NT1; ++nt)
+                bv[nt] = (ok && g + 8 * nt < r1) ? __ldg(ubase + j * r1 + 8 * nt) : 0.0;
+#pragma unroll
+              for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < NT1; ++nt)
+                  dmma_8x8x4(r2[mt][nt][0], r2[mt][nt][1], tacc[h][par][mt][0][s2], bv[nt]);
+            }
+          oo += hi - lo;
+          lo = hi;
+          if (oo >= n1) {
+            oo -= n1;
+            ++gg;
+          }
+        }
+      }
+      off += 16;
+      while (off >= n1) {
+        off -= n1;
+        ++grp;
+      }
+    }
+  }
+  // range end: retire the open level-2 group, then (M3) the open slot
+  if (cur_g2 >= 0) retire(cur_g2);
+  if (M3 && cur_p >= 0) {
+    __syncwarp();
+    double* dst = P.rec + (gw + cur_p) * P.A;
+    for (int e = lane; e < P.A; e += 32) dst[e] = slot[e];
+    flat_emit<WARPS>(P, gw, cur_p, lane, BC);
+  }
+}
+
 // U0 -> fragment order [rho][kstep][mt][lane] = U0[rho*RB + 4 kstep + lane%4][8 mt + lane/4].
 __global__ void prep_kernel(const double* __restrict__ u0, int64_t n0, int r0, int RB, int NT, int nrb,
                             double* __restrict__ ufrag) {
@@ -522,6 +829,65 @@ __global__ void ttm_all_kernel(const TtmParams T) {
   }
 }
 
+// Bandwidth variant for large inputs: CTA (pi, gi-block) with 64 gi x 4
+// i-groups; each thread accumulates all rr outputs of its gi over every 4th
+// i (coalesced 512-byte rows of the input, U through shared memory), then
+// the 4 i-groups are combined in a fixed order (deterministic).
+template <int RR>
+__global__ void __launch_bounds__(256) ttm_block_kernel(const TtmParams T) {
+  __shared__ double red[4][RR][64];
+  extern __shared__ double ush[];  // n x rr coefficients, [i][b]
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  const int64_t pi = blockIdx.x;
+  const int64_t gi = (int64_t)blockIdx.y * 64 + tx;
+  const int64_t cs = T.transpose ? T.n : 1, ci = T.transpose ? 1 : T.rr;
+  for (int64_t e = threadIdx.x; e < T.n * T.rr; e += 256) {
+    const int64_t i = e / T.rr, b = e % T.rr;
+    ush[e] = T.u[ci * i + cs * b];
+  }
+  __syncthreads();
+  double acc[RR];
+#pragma unroll
+  for (int b = 0; b < RR; ++b) acc[b] = 0.0;
+  if (gi < T.g) {
+    const double* in = T.in + gi + T.g * T.n * pi;
+    constexpr int kB = 4;
+    for (int64_t i0 = ty; i0 < T.n; i0 += 4 * kB) {
+      double v[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int64_t i = i0 + 4 * u;
+        v[u] = 0.0;
+        if (i < T.n) {
+          const double* pp = in + T.g * i;
+          double s0 = pp[0];
+          for (int q = 1; q < T.nparts; ++q) s0 += pp[q * T.part_stride];
+          v[u] = s0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int64_t i = i0 + 4 * u;
+        if (i < T.n) {
+          const double* uc = ush + i * T.rr;
+#pragma unroll
+          for (int b = 0; b < RR; ++b)
+            if (b < T.rr) acc[b] = fma(v[u], uc[b], acc[b]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < RR; ++b) red[ty][b][tx] = acc[b];
+  __syncthreads();
+  for (int e = threadIdx.x; e < RR * 64; e += 256) {
+    const int b = e / 64, x = e % 64;
+    const int64_t go = (int64_t)blockIdx.y * 64 + x;
+    if (b < T.rr && go < T.g)
+      T.out[go + T.g * (b + T.rr * pi)] = ((red[0][b][x] + red[1][b][x]) + red[2][b][x]) + red[3][b][x];
+  }
+}
+
 // All factor reformatting of a core pass in one launch: blockIdx.y = 0
 // builds U0's fragments, 1..2 transpose U1, U2 to row-major.
 struct PrepJobs {
@@ -537,10 +903,15 @@ struct PrepJobs {
   int64_t n[2];
   int r[2];
   int njobs;
+  uint32_t* cnt;  // flat mode: group counters to clear
+  int64_t ncnt;
 };
 
 __global__ void prep_all_kernel(const PrepJobs J) {
   if ((int)blockIdx.y == J.njobs + 1) {
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < J.ncnt;
+         it += (int64_t)gridDim.x * blockDim.x)
+      J.cnt[it] = 0u;
     // item table, rho-major: consecutive items of a CTA share the row block
     for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < J.nitems;
          it += (int64_t)gridDim.x * blockDim.x) {
@@ -586,6 +957,12 @@ __global__ void prep_all_kernel(const PrepJobs J) {
 
 template <int MT, int NT1, bool M3, int TPB, int WARPS>
 cudaError_t launch_w(const CUtensorMap* tmap, const CoreParams& P, int grid, size_t smem, cudaStream_t s) {
+  if (P.flat) {
+    cudaError_t e = SRTT_ENSURE_SMEM((core_flat_kernel<MT, NT1, M3, TPB, WARPS>), smem);
+    if (e != cudaSuccess) return e;
+    core_flat_kernel<MT, NT1, M3, TPB, WARPS><<<grid, WARPS * 32, smem, s>>>(*tmap, P);
+    return cudaGetLastError();
+  }
   cudaError_t e = SRTT_ENSURE_SMEM((core_kernel<MT, NT1, M3, TPB, WARPS>), smem);
   if (e != cudaSuccess) return e;
   core_kernel<MT, NT1, M3, TPB, WARPS><<<grid, WARPS * 32, smem, s>>>(*tmap, P);
@@ -682,6 +1059,8 @@ cudaError_t srtt_launch_prep_all(const CoreParams& P, CoreItem* items, const dou
   J.NT = NT;
   J.nrb = nrb;
   J.njobs = njobs;
+  J.cnt = P.flat ? P.cnt : nullptr;
+  J.ncnt = P.flat ? P.G : 0;
   for (int j = 0; j < njobs; ++j) {
     J.u[j] = u[j];
     J.ut[j] = ut[j];
@@ -705,6 +1084,16 @@ cudaError_t srtt_launch_ttm(const TtmParams& T, cudaStream_t s) {
   const int64_t total = T.g * T.rr * T.post;
   const int64_t pairs = T.g * T.post;
   const double in_bytes = 8.0 * (double)T.g * T.n * T.post * T.nparts;
+  if (T.rr <= 16 && T.post >= 64 && T.post < 65536 && in_bytes * T.rr > 64e6 && T.n * T.rr * 8 <= 48 * 1024) {
+    // large input, many slabs: CTA per (slab, 64 rows), i split over 4 groups
+    const dim3 grid((unsigned)T.post, (unsigned)((T.g + 63) / 64));
+    const size_t sm = (size_t)T.n * T.rr * sizeof(double);
+    cudaError_t e = T.rr <= 8 ? SRTT_ENSURE_SMEM(ttm_block_kernel<8>, sm) : SRTT_ENSURE_SMEM(ttm_block_kernel<16>, sm);
+    if (e != cudaSuccess) return e;
+    if (T.rr <= 8) ttm_block_kernel<8><<<grid, 256, sm, s>>>(T);
+    else ttm_block_kernel<16><<<grid, 256, sm, s>>>(T);
+    return cudaGetLastError();
+  }
   if (T.rr <= 32 && pairs >= 148 * 128 && in_bytes * T.rr > 64e6) {
     // large input re-read rr times by the per-output kernels: read it once
     const int blocks = (int)min64(148 * 8, (pairs + 127) / 128);

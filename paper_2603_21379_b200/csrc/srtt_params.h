@@ -118,6 +118,16 @@ typedef struct CoreParams {
   int32_t nstages;         // per-warp TMA ring depth
   int32_t tpb;             // 16-column tile pairs per TMA box (1 or 2)
   int32_t warps;           // warps per CTA (8 or 16)
+  // flat mode (single row block): instead of items, global warp gw owns the
+  // contiguous tile range [ntiles*gw/nw, ntiles*(gw+1)/nw) of BC-column
+  // tiles; it writes one record per level-m group its range touches into
+  // rec[(gw + p) * A], and the warp completing group p (counter cnt[p])
+  // sums the group's records in warp order into part[p * A] (compact R_m).
+  int32_t flat;
+  int32_t nw;              // total warps of the grid (flat mode)
+  int64_t ntiles;          // BC-column tiles of M (flat mode)
+  double* rec;             // flat mode: (nw + G) * A record slots
+  uint32_t* cnt;           // flat mode: G completion counters (zero between calls)
 } CoreParams;
 
 // Streamed reconstruction error (k_recon.cu).
