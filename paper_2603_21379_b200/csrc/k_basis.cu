@@ -421,7 +421,7 @@ __device__ void pad_columns(double* Y, int64_t n, int64_t ldy, int q, int r, uin
       __syncthreads();
       for (int round = 0; round < 2; ++round) {
         if (j == 0) break;
-        for (int jj = warp; jj < j; jj += kWarps) {
+        for (int jj = warp; jj < j; jj += (int)(blockDim.x >> 5)) {
           const double* yc = Y + (int64_t)jj * ldy;
           double s = 0.0;
           for (int64_t i = lane; i < n; i += 32) s += yc[i] * v[i];
@@ -486,124 +486,17 @@ __device__ TopSmem carve_top(unsigned char* raw, int m, int c, int r) {
   return s;
 }
 
-// Top of the TSQR tree (or the whole basis for single-block targets).
-// CTA-wide lane-per-column QR / back-application for tall small-c matrices
-// (the stacked R of a TSQR top level): lane l owns column l (c <= 32), the
-// kWarps warps own contiguous row slices; each reflector costs a few CTA
-// barriers, per-lane dot/update loops over ~m/kWarps rows and one
-// cross-warp reduction of 32 partial dots. red: kWarps * 32 + 64 doubles.
-__device__ void qr_cols_cta(const double* __restrict__ z, int m, int c, double* A, int lda, double* tau,
-                            double* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int k = min(m, c);
-  double* wsum = red + kWarps * 32;  // 32 scaled dots
-  double* bc = wsum + 32;            // tau, scal, beta
-  for (int idx = threadIdx.x; idx < m * c; idx += kThreads) A[(size_t)(idx / m) * lda + idx % m] = __ldg(z + idx);
-  __syncthreads();
-  const int rows_per = (m + kWarps - 1) / kWarps;
-  const int r_lo = warp * rows_per, r_hi = min(m, r_lo + rows_per);
-  for (int j = 0; j < k; ++j) {
-    double* col = A + (size_t)j * lda;
-    const int i0 = max(r_lo, j + 1);
-    double part = 0.0;
-    for (int i = i0 + lane; i < r_hi; i += 32) part = fma(col[i], col[i], part);
-    part = warp_sum(part);
-    if (lane == 0) red[warp * 32] = part;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double ss = 0.0;
-      for (int w = 0; w < kWarps; ++w) ss += red[w * 32];
-      const double alpha = col[j];
-      double tj = 0.0, scal = 0.0, beta = alpha;
-      if (ss != 0.0) {
-        const double nrm = sqrt(fma(alpha, alpha, ss));
-        beta = -copysign(nrm, alpha);
-        tj = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
-      }
-      bc[0] = tj;
-      bc[1] = scal;
-      bc[2] = beta;
-      tau[j] = tj;
-    }
-    __syncthreads();
-    const double tj = bc[0];
-    if (tj != 0.0) {
-      const double scal = bc[1];
-      for (int i = i0 + lane; i < r_hi; i += 32) col[i] *= scal;
-      __syncthreads();
-      double p = 0.0;
-      if (lane > j && lane < c) {
-        const double* cl = A + (size_t)lane * lda;
-        for (int i = i0; i < r_hi; ++i) p = fma(col[i], cl[i], p);
-      }
-      red[warp * 32 + lane] = p;
-      __syncthreads();
-      if (warp == 0 && lane > j && lane < c) {
-        double t = A[(size_t)lane * lda + j];
-        for (int w = 0; w < kWarps; ++w) t += red[w * 32 + lane];
-        wsum[lane] = tj * t;
-      }
-      __syncthreads();
-      if (lane > j && lane < c) {
-        double* cl = A + (size_t)lane * lda;
-        const double tw = wsum[lane];
-        for (int i = i0; i < r_hi; ++i) cl[i] = fma(-tw, col[i], cl[i]);
-        if (j >= r_lo && j < r_hi) cl[j] -= tw;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) col[j] = bc[2];
-    __syncthreads();
-  }
-}
-
-__device__ void apply_cols_cta(const double* A, int lda, const double* tau, int m, int k, const double* V, int ldv,
-                               const int* perm, int q, double* Y, int ldy, double* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* wsum = red + kWarps * 32;
-  for (int idx = threadIdx.x; idx < m * q; idx += kThreads) {
-    const int i = idx % m, col = idx / m;
-    Y[(size_t)col * ldy + i] = i < k ? V[(size_t)perm[col] * ldv + i] : 0.0;
-  }
-  __syncthreads();
-  const int rows_per = (m + kWarps - 1) / kWarps;
-  const int r_lo = warp * rows_per, r_hi = min(m, r_lo + rows_per);
-  for (int j = k - 1; j >= 0; --j) {
-    const double tj = tau[j];
-    if (tj == 0.0) continue;
-    const double* v = A + (size_t)j * lda;
-    const int i0 = max(r_lo, j + 1);
-    double p = 0.0;
-    if (lane < q) {
-      const double* y = Y + (size_t)lane * ldy;
-      for (int i = i0; i < r_hi; ++i) p = fma(v[i], y[i], p);
-    }
-    red[warp * 32 + lane] = p;
-    __syncthreads();
-    if (warp == 0 && lane < q) {
-      double t = Y[(size_t)lane * ldy + j];
-      for (int w = 0; w < kWarps; ++w) t += red[w * 32 + lane];
-      wsum[lane] = tj * t;
-    }
-    __syncthreads();
-    if (lane < q) {
-      double* y = Y + (size_t)lane * ldy;
-      const double tw = wsum[lane];
-      for (int i = i0; i < r_hi; ++i) y[i] = fma(-tw, v[i], y[i]);
-      if (j >= r_lo && j < r_hi) y[j] -= tw;
-    }
-    __syncthreads();
-  }
-}
-
+__device__ void qr_cols_warps(const double* __restrict__ z, int m, int c, double* A, int lda, double* tau);
+__device__ void apply_cols_warps(const double* A, int lda, const double* tau, int m, int k, const double* V,
+                                 int ldv, const int* perm, int q, double* Y, int ldy);
 __device__ void qr_cols_lane(const double* __restrict__ z, int m, int c, double* A, int lda, double* tau);
 __device__ void apply_cols_lane(const double* A, int lda, const double* tau, int m, int k, const double* V,
                                 int ldv, const int* perm, int q, double* Y, int ldy);
 
-// JG > 0: warp 0 runs the lane-per-column QR, the register Jacobi <JG, JE>
-// and the lane-per-column back-application (c <= 32, the latency chain of a
-// small stacked R); JG = 0: the CTA-wide shared-memory QRCP / 4-lane Jacobi.
+// Top of the TSQR tree (or the whole basis for single-block targets).
+// JG > 0: warp-per-column QR and back-application over the CTA's warps
+// (qr_cols_warps / apply_cols_warps) around warp 0's register Jacobi
+// <JG, JE> (c <= 32); JG = 0: the CTA-wide shared-memory QRCP / 4-lane Jacobi.
 template <int JG, int JE>
 __global__ void __launch_bounds__(kThreads) basis_top_kernel(const BasisTarget* __restrict__ targets,
                                                             const int* __restrict__ list) {
@@ -623,7 +516,7 @@ __global__ void __launch_bounds__(kThreads) basis_top_kernel(const BasisTarget* 
   PROF_MARK_CTA(8);
 
   if constexpr (JG > 0) {
-    qr_cols_cta(L.a, m, c, s.A, lda, s.tau, s.red);
+    qr_cols_warps(L.a, m, c, s.A, lda, s.tau);
   } else {
     for (int idx = threadIdx.x; idx < m * c; idx += blockDim.x) {
       const int i = idx % m, j = idx / m;
@@ -681,7 +574,7 @@ __global__ void __launch_bounds__(kThreads) basis_top_kernel(const BasisTarget* 
   PROF_MARK_CTA(11);
   // Y = Q [V(:, perm[:q]); 0]
   if constexpr (JG > 0) {
-    apply_cols_cta(s.A, lda, s.tau, m, k, s.V, k, s.perm, q, s.Y, m, s.red);
+    apply_cols_warps(s.A, lda, s.tau, m, k, s.V, k, s.perm, q, s.Y, m);
   } else {
     for (int idx = threadIdx.x; idx < m * q; idx += blockDim.x) {
       const int i = idx % m, col = idx / m;
@@ -1220,6 +1113,196 @@ __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __re
   PROF_MARK(7);
 }
 
+// ---- CTA-wide small basis (c <= 32) ---------------------------------------
+// Same algorithm as basis_small_kernel<1, JG, JE> (Householder QR, register
+// Jacobi on the rows of R, back-application, Gaussian padding), but the QR
+// and the back-application are spread over the CTA's warps: warp w owns the
+// columns l = w (mod W); a reflector step is one warp reduction per owned
+// column plus one CTA barrier, and the owner of column j+1 builds reflector
+// j+1 right after updating that column (look-ahead), so a step costs about
+// two warp reductions of latency instead of a serial row loop per lane.
+constexpr int kCtaMaxOwn = 4;  // columns per warp (c <= 32, 8 warps)
+
+// reflector j from column j (called by the owning warp): v below the
+// diagonal (scaled in place), beta on the diagonal, tau[j]
+__device__ __forceinline__ void cta_make_reflector(double* A, int lda, int m, int j, double* tau) {
+  const int lane = threadIdx.x & 31;
+  double* col = A + (size_t)j * lda;
+  double part = 0.0;
+  for (int i = j + 1 + lane; i < m; i += 32) part = fma(col[i], col[i], part);
+  const double ss = warp_sum(part);
+  const double alpha = col[j];
+  double tj = 0.0, scal = 0.0, beta = alpha;
+  if (ss != 0.0) {
+    const double nrm = sqrt(fma(alpha, alpha, ss));
+    beta = -copysign(nrm, alpha);
+    tj = (beta - alpha) / beta;
+    scal = 1.0 / (alpha - beta);
+  }
+  if (tj != 0.0)
+    for (int i = j + 1 + lane; i < m; i += 32) col[i] *= scal;
+  if (lane == 0) {
+    col[j] = beta;  // v_j = 1 is implicit: the diagonal slot is free
+    tau[j] = tj;
+  }
+  __syncwarp();
+}
+
+__device__ void qr_cols_warps(const double* __restrict__ z, int m, int c, double* A, int lda, double* tau) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int k = min(m, c);
+  for (int idx = threadIdx.x; idx < m * c; idx += blockDim.x) A[(size_t)(idx / m) * lda + idx % m] = __ldg(z + idx);
+  __syncthreads();
+  if (k > 0 && warp == 0) cta_make_reflector(A, lda, m, 0, tau);
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    const double tj = tau[j];
+    const double* v = A + (size_t)j * lda;
+    if (tj != 0.0) {
+      double w[kCtaMaxOwn];
+#pragma unroll
+      for (int t = 0; t < kCtaMaxOwn; ++t) {
+        const int l = warp + nw * t;
+        double p = 0.0;
+        if (l > j && l < c) {
+          const double* cl = A + (size_t)l * lda;
+          for (int i = j + 1 + lane; i < m; i += 32) p = fma(v[i], cl[i], p);
+        }
+        w[t] = p;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int t = 0; t < kCtaMaxOwn; ++t) w[t] += __shfl_xor_sync(0xffffffffu, w[t], o);
+#pragma unroll
+      for (int t = 0; t < kCtaMaxOwn; ++t) {
+        const int l = warp + nw * t;
+        if (l > j && l < c) {
+          double* cl = A + (size_t)l * lda;
+          const double tw = tj * (w[t] + cl[j]);
+          for (int i = j + 1 + lane; i < m; i += 32) cl[i] = fma(-tw, v[i], cl[i]);
+          if (lane == 0) cl[j] -= tw;
+        }
+      }
+      __syncwarp();
+    }
+    if (j + 1 < k && (j + 1) % nw == warp) cta_make_reflector(A, lda, m, j + 1, tau);
+    __syncthreads();
+  }
+}
+
+// Y(:, 0:q) = Q [V(:, perm[0:q]); 0]; warp w owns output columns w (mod W)
+// and applies the k reflectors to them in reverse order (no CTA barriers).
+__device__ void apply_cols_warps(const double* A, int lda, const double* tau, int m, int k, const double* V,
+                                 int ldv, const int* perm, int q, double* Y, int ldy) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int idx = threadIdx.x; idx < m * q; idx += blockDim.x) {
+    const int i = idx % m, col = idx / m;
+    Y[(size_t)col * ldy + i] = i < k ? V[(size_t)perm[col] * ldv + i] : 0.0;
+  }
+  __syncthreads();
+  if (warp < q) {
+    for (int j = k - 1; j >= 0; --j) {
+      const double tj = tau[j];
+      if (tj == 0.0) continue;
+      const double* v = A + (size_t)j * lda;
+      double w[kCtaMaxOwn];
+#pragma unroll
+      for (int t = 0; t < kCtaMaxOwn; ++t) {
+        const int col = warp + nw * t;
+        double p = 0.0;
+        if (col < q) {
+          const double* y = Y + (size_t)col * ldy;
+          for (int i = j + 1 + lane; i < m; i += 32) p = fma(v[i], y[i], p);
+        }
+        w[t] = p;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int t = 0; t < kCtaMaxOwn; ++t) w[t] += __shfl_xor_sync(0xffffffffu, w[t], o);
+#pragma unroll
+      for (int t = 0; t < kCtaMaxOwn; ++t) {
+        const int col = warp + nw * t;
+        if (col < q) {
+          double* y = Y + (size_t)col * ldy;
+          const double tw = tj * (w[t] + y[j]);
+          for (int i = j + 1 + lane; i < m; i += 32) y[i] = fma(-tw, v[i], y[i]);
+          if (lane == 0) y[j] -= tw;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+template <int JG, int JE>
+__global__ void __launch_bounds__(kThreads) basis_cta_kernel(const BasisTarget* __restrict__ targets,
+                                                             const int* __restrict__ list) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ BasisTarget T;
+  __shared__ double red[64];
+  stage_target(&T, &targets[list[blockIdx.x]]);
+  __syncthreads();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = (int)T.n, c = T.c, r = T.r;
+  const int k = min(m, c);
+  SmallSmem s = carve_small(smem_raw, m, c, r);
+  PROF_MARK_CTA(0);
+  qr_cols_warps(T.lv[0].a, m, c, s.A, s.lda, s.tau);
+  PROF_MARK_CTA(1);
+  PROF_MARK_CTA(2);
+  for (int idx = tid; idx < k * c; idx += blockDim.x) {
+    const int i = idx / c, j = idx % c;
+    s.B[(size_t)i * s.ldb + j] = (j >= i) ? s.A[(size_t)j * s.lda + i] : 0.0;
+  }
+  for (int idx = tid; idx < k * k; idx += blockDim.x) {
+    const int i = idx % k, j = idx / k;
+    s.V[(size_t)j * s.ldv + i] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  int sweeps = 0;
+  if (warp == 0) sweeps = jacobi_rows_reg<JG, JE>(s.B, s.ldb, k, c, s.V, s.ldv);
+  __syncthreads();
+  PROF_MARK_CTA(3);
+  for (int i = tid; i < k; i += blockDim.x) {
+    const double* bi = s.B + (size_t)i * s.ldb;
+    s.sig[i] = sqrt(dot4(bi, bi, 0, c));
+  }
+  __syncthreads();
+  for (int i = tid; i < k; i += blockDim.x) {
+    int rank = 0;
+    for (int j = 0; j < k; ++j) rank += (s.sig[j] > s.sig[i]) || (s.sig[j] == s.sig[i] && j < i);
+    s.perm[rank] = i;
+  }
+  __syncthreads();
+  const double smax = s.sig[s.perm[0]];
+  const double tol_rank = (double)max(m, c) * DBL_EPSILON * smax;
+  int nrank = 0;
+  for (int i = 0; i < k; ++i) nrank += s.sig[i] > tol_rank;
+  const int q = min(nrank, r);
+  if (tid == 0) {
+    T.info[0] = q;
+    T.info[1] = nrank;
+    T.info[2] = sweeps;
+  }
+  if (T.sv)
+    for (int i = tid; i < k; i += blockDim.x) T.sv[i] = s.sig[s.perm[i]];
+  PROF_MARK_CTA(4);
+  apply_cols_warps(s.A, s.lda, s.tau, m, k, s.V, s.ldv, s.perm, q, s.Y, s.lda);
+  PROF_MARK_CTA(5);
+  if (q < r)
+    pad_columns(s.Y, m, s.lda, q, r, T.state0, T.draw_offset, (uint64_t)T.normal_base, s.v, s.dots, red);
+  PROF_MARK_CTA(6);
+  for (int idx = tid; idx < m * r; idx += blockDim.x) {
+    const int i = idx % m, col = idx / m;
+    T.u[idx] = s.Y[(size_t)col * s.lda + i];
+  }
+  (void)lane;
+  PROF_MARK_CTA(7);
+}
+
 }  // namespace
 
 size_t srtt_basis_top_smem(int m, int c, int r) {
@@ -1254,12 +1337,12 @@ cudaError_t srtt_launch_basis_small(int variant, const BasisTarget* d_targets, c
   if (n <= 0) return cudaSuccess;
   switch (variant) {
     case 0:
-      SRTT_ENSURE_SMEM((basis_small_kernel<1, 4, 4>), smem);
-      basis_small_kernel<1, 4, 4><<<n, 32, smem, stream>>>(d_targets, d_list);
+      SRTT_ENSURE_SMEM((basis_cta_kernel<4, 4>), smem);
+      basis_cta_kernel<4, 4><<<n, kThreads, smem, stream>>>(d_targets, d_list);
       break;
     case 1:
-      SRTT_ENSURE_SMEM((basis_small_kernel<1, 2, 16>), smem);
-      basis_small_kernel<1, 2, 16><<<n, 32, smem, stream>>>(d_targets, d_list);
+      SRTT_ENSURE_SMEM((basis_cta_kernel<2, 16>), smem);
+      basis_cta_kernel<2, 16><<<n, kThreads, smem, stream>>>(d_targets, d_list);
       break;
     default:
       SRTT_ENSURE_SMEM((basis_small_kernel<0, 0, 0>), smem);

@@ -33,6 +33,10 @@ for name in sys.argv[1:] or ["c2"]:
     d = np.diff(v)
     print(name, "small cycles:", " ".join(f"{n}={int(c)}" for n, c in zip(names, d)), "total", v[7] - v[0])
     t = list(clk)[8:14]
+    if os.environ.get("HJ"):
+        print(name, "hj cycles: load", t[1] - t[0], "jacobi", t[2] - t[1], "rank", t[3] - t[2], "out", t[4] - t[3],
+              "sweeps", clk[15])
+        continue
     if t[0]:
         tn = ["qr", "jacobi", "sigma", "apply", "store"]
         print(name, "top cycles:", " ".join(f"{n}={int(b - a)}" for n, a, b in zip(tn, t[:-1], t[1:])))
