@@ -486,7 +486,12 @@ __device__ TopSmem carve_top(unsigned char* raw, int m, int c, int r) {
   return s;
 }
 
-__device__ void qr_cols_warps(const double* __restrict__ z, int m, int c, double* A, int lda, double* tau);
+template <int OWN>
+__device__ void qr_cols_warps(const double* __restrict__ z, int64_t ldz, int m, int c, double* A, int lda,
+                              double* tau);
+template <int OWN>
+__device__ void apply_reflectors_warps(const double* A, int lda, const double* tau, int m, int k, int q, double* Y,
+                                       int ldy);
 __device__ void apply_cols_warps(const double* A, int lda, const double* tau, int m, int k, const double* V,
                                  int ldv, const int* perm, int q, double* Y, int ldy);
 __device__ void qr_cols_lane(const double* __restrict__ z, int m, int c, double* A, int lda, double* tau);
@@ -516,7 +521,7 @@ __global__ void __launch_bounds__(kThreads) basis_top_kernel(const BasisTarget* 
   PROF_MARK_CTA(8);
 
   if constexpr (JG > 0) {
-    qr_cols_warps(L.a, m, c, s.A, lda, s.tau);
+    qr_cols_warps<4>(L.a, m, m, c, s.A, lda, s.tau);
   } else {
     for (int idx = threadIdx.x; idx < m * c; idx += blockDim.x) {
       const int i = idx % m, j = idx / m;
@@ -618,12 +623,18 @@ __global__ void __launch_bounds__(kThreads) tsqr_factor_kernel(const BasisTarget
   double* A = reinterpret_cast<double*>(smem_raw);
   double* tau = A + (size_t)mb * c;
   double* sb = tau + c;
-  for (int idx = threadIdx.x; idx < mb * c; idx += blockDim.x) {
-    const int i = idx % mb, j = idx / mb;
-    A[idx] = L.a[(int64_t)j * L.n + r0 + i];
+  if (c <= 32) {
+    qr_cols_warps<4>(L.a + r0, L.n, mb, c, A, mb, tau);
+  } else if (c <= 64) {
+    qr_cols_warps<8>(L.a + r0, L.n, mb, c, A, mb, tau);
+  } else {
+    for (int idx = threadIdx.x; idx < mb * c; idx += blockDim.x) {
+      const int i = idx % mb, j = idx / mb;
+      A[idx] = L.a[(int64_t)j * L.n + r0 + i];
+    }
+    __syncthreads();
+    householder_qr(A, mb, c, mb, tau, sb);
   }
-  __syncthreads();
-  householder_qr(A, mb, c, mb, tau, sb);
   for (int idx = threadIdx.x; idx < mb * c; idx += blockDim.x) {
     const int i = idx % mb, j = idx / mb;
     L.a[(int64_t)j * L.n + r0 + i] = A[idx];
@@ -667,9 +678,8 @@ __global__ void __launch_bounds__(kThreads) tsqr_apply_kernel(const BasisTarget*
     Y[idx] = (i < kb) ? P.y[(int64_t)col * P.n + (int64_t)b * c + i] : 0.0;
   }
   __syncthreads();
-  const int warp = threadIdx.x >> 5;
-  for (int col = warp; col < q; col += kWarps) apply_q_warp(A, mb, kb, mb, tau, Y + (size_t)col * mb);
-  __syncthreads();
+  if (q <= 32) apply_reflectors_warps<4>(A, mb, tau, mb, kb, q, Y, mb);
+  else apply_reflectors_warps<8>(A, mb, tau, mb, kb, q, Y, mb);
   for (int idx = threadIdx.x; idx < mb * q; idx += blockDim.x) {
     const int i = idx % mb, col = idx / mb;
     L.y[(int64_t)col * L.n + r0 + i] = Y[idx];
@@ -1121,16 +1131,21 @@ __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __re
 // column plus one CTA barrier, and the owner of column j+1 builds reflector
 // j+1 right after updating that column (look-ahead), so a step costs about
 // two warp reductions of latency instead of a serial row loop per lane.
-constexpr int kCtaMaxOwn = 4;  // columns per warp (c <= 32, 8 warps)
+// columns per warp: OWN = 4 covers c <= 32 with 8 warps, OWN = 8 c <= 64
 
 // reflector j from column j (called by the owning warp): v below the
 // diagonal (scaled in place), beta on the diagonal, tau[j]
 __device__ __forceinline__ void cta_make_reflector(double* A, int lda, int m, int j, double* tau) {
   const int lane = threadIdx.x & 31;
   double* col = A + (size_t)j * lda;
-  double part = 0.0;
-  for (int i = j + 1 + lane; i < m; i += 32) part = fma(col[i], col[i], part);
-  const double ss = warp_sum(part);
+  double p0 = 0.0, p1 = 0.0;
+  int i = j + 1 + lane;
+  for (; i + 32 < m; i += 64) {
+    p0 = fma(col[i], col[i], p0);
+    p1 = fma(col[i + 32], col[i + 32], p1);
+  }
+  if (i < m) p0 = fma(col[i], col[i], p0);
+  const double ss = warp_sum(p0 + p1);
   const double alpha = col[j];
   double tj = 0.0, scal = 0.0, beta = alpha;
   if (ss != 0.0) {
@@ -1140,7 +1155,7 @@ __device__ __forceinline__ void cta_make_reflector(double* A, int lda, int m, in
     scal = 1.0 / (alpha - beta);
   }
   if (tj != 0.0)
-    for (int i = j + 1 + lane; i < m; i += 32) col[i] *= scal;
+    for (int ii = j + 1 + lane; ii < m; ii += 32) col[ii] *= scal;
   if (lane == 0) {
     col[j] = beta;  // v_j = 1 is implicit: the diagonal slot is free
     tau[j] = tj;
@@ -1148,93 +1163,91 @@ __device__ __forceinline__ void cta_make_reflector(double* A, int lda, int m, in
   __syncwarp();
 }
 
-__device__ void qr_cols_warps(const double* __restrict__ z, int m, int c, double* A, int lda, double* tau) {
+// Apply reflector (v = A(:, j), tau tj) to the OWN columns X(:, l) this warp
+// owns (l = warp + nw*t, active when lo <= l < hi): w = x_j + v^T x below j,
+// x -= tj w v. Two partial sums per column break the FMA chains.
+template <int OWN>
+__device__ __forceinline__ void warp_reflect_cols(const double* v, double tj, int j, int m, double* X, int ldx,
+                                                  int lo, int hi) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double w[OWN];
+#pragma unroll
+  for (int t = 0; t < OWN; ++t) {
+    const int l = warp + nw * t;
+    double p0 = 0.0, p1 = 0.0;
+    if (l >= lo && l < hi) {
+      const double* x = X + (size_t)l * ldx;
+      int i = j + 1 + lane;
+      for (; i + 32 < m; i += 64) {
+        p0 = fma(v[i], x[i], p0);
+        p1 = fma(v[i + 32], x[i + 32], p1);
+      }
+      if (i < m) p0 = fma(v[i], x[i], p0);
+    }
+    w[t] = p0 + p1;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int t = 0; t < OWN; ++t) w[t] += __shfl_xor_sync(0xffffffffu, w[t], o);
+#pragma unroll
+  for (int t = 0; t < OWN; ++t) {
+    const int l = warp + nw * t;
+    if (l >= lo && l < hi) {
+      double* x = X + (size_t)l * ldx;
+      const double tw = tj * (w[t] + x[j]);
+      for (int i = j + 1 + lane; i < m; i += 32) x[i] = fma(-tw, v[i], x[i]);
+      if (lane == 0) x[j] -= tw;
+    }
+  }
+  __syncwarp();
+}
+
+// Householder QR of z (m x c, ld ldz) into A (ld lda) over the CTA's warps.
+template <int OWN>
+__device__ void qr_cols_warps(const double* __restrict__ z, int64_t ldz, int m, int c, double* A, int lda,
+                              double* tau) {
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int k = min(m, c);
-  for (int idx = threadIdx.x; idx < m * c; idx += blockDim.x) A[(size_t)(idx / m) * lda + idx % m] = __ldg(z + idx);
+  for (int idx = threadIdx.x; idx < m * c; idx += blockDim.x) {
+    const int i = idx % m, j = idx / m;
+    A[(size_t)j * lda + i] = __ldg(z + (int64_t)j * ldz + i);
+  }
   __syncthreads();
   if (k > 0 && warp == 0) cta_make_reflector(A, lda, m, 0, tau);
   __syncthreads();
   for (int j = 0; j < k; ++j) {
     const double tj = tau[j];
-    const double* v = A + (size_t)j * lda;
-    if (tj != 0.0) {
-      double w[kCtaMaxOwn];
-#pragma unroll
-      for (int t = 0; t < kCtaMaxOwn; ++t) {
-        const int l = warp + nw * t;
-        double p = 0.0;
-        if (l > j && l < c) {
-          const double* cl = A + (size_t)l * lda;
-          for (int i = j + 1 + lane; i < m; i += 32) p = fma(v[i], cl[i], p);
-        }
-        w[t] = p;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int t = 0; t < kCtaMaxOwn; ++t) w[t] += __shfl_xor_sync(0xffffffffu, w[t], o);
-#pragma unroll
-      for (int t = 0; t < kCtaMaxOwn; ++t) {
-        const int l = warp + nw * t;
-        if (l > j && l < c) {
-          double* cl = A + (size_t)l * lda;
-          const double tw = tj * (w[t] + cl[j]);
-          for (int i = j + 1 + lane; i < m; i += 32) cl[i] = fma(-tw, v[i], cl[i]);
-          if (lane == 0) cl[j] -= tw;
-        }
-      }
-      __syncwarp();
-    }
+    if (tj != 0.0) warp_reflect_cols<OWN>(A + (size_t)j * lda, tj, j, m, A, lda, j + 1, c);
     if (j + 1 < k && (j + 1) % nw == warp) cta_make_reflector(A, lda, m, j + 1, tau);
     __syncthreads();
   }
 }
 
-// Y(:, 0:q) = Q [V(:, perm[0:q]); 0]; warp w owns output columns w (mod W)
-// and applies the k reflectors to them in reverse order (no CTA barriers).
+// Y(:, 0:q) <- Q Y(:, 0:q) with Q = H_0 ... H_{k-1}: warp w owns output
+// columns w (mod W) and applies the reflectors in reverse order (no CTA
+// barriers; A is read-only).
+template <int OWN>
+__device__ void apply_reflectors_warps(const double* A, int lda, const double* tau, int m, int k, int q, double* Y,
+                                       int ldy) {
+  const int warp = threadIdx.x >> 5;
+  if (warp < q)
+    for (int j = k - 1; j >= 0; --j) {
+      const double tj = tau[j];
+      if (tj != 0.0) warp_reflect_cols<OWN>(A + (size_t)j * lda, tj, j, m, Y, ldy, 0, q);
+    }
+  __syncthreads();
+}
+
+// Y(:, 0:q) = Q [V(:, perm[0:q]); 0]
 __device__ void apply_cols_warps(const double* A, int lda, const double* tau, int m, int k, const double* V,
                                  int ldv, const int* perm, int q, double* Y, int ldy) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int idx = threadIdx.x; idx < m * q; idx += blockDim.x) {
     const int i = idx % m, col = idx / m;
     Y[(size_t)col * ldy + i] = i < k ? V[(size_t)perm[col] * ldv + i] : 0.0;
   }
   __syncthreads();
-  if (warp < q) {
-    for (int j = k - 1; j >= 0; --j) {
-      const double tj = tau[j];
-      if (tj == 0.0) continue;
-      const double* v = A + (size_t)j * lda;
-      double w[kCtaMaxOwn];
-#pragma unroll
-      for (int t = 0; t < kCtaMaxOwn; ++t) {
-        const int col = warp + nw * t;
-        double p = 0.0;
-        if (col < q) {
-          const double* y = Y + (size_t)col * ldy;
-          for (int i = j + 1 + lane; i < m; i += 32) p = fma(v[i], y[i], p);
-        }
-        w[t] = p;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int t = 0; t < kCtaMaxOwn; ++t) w[t] += __shfl_xor_sync(0xffffffffu, w[t], o);
-#pragma unroll
-      for (int t = 0; t < kCtaMaxOwn; ++t) {
-        const int col = warp + nw * t;
-        if (col < q) {
-          double* y = Y + (size_t)col * ldy;
-          const double tw = tj * (w[t] + y[j]);
-          for (int i = j + 1 + lane; i < m; i += 32) y[i] = fma(-tw, v[i], y[i]);
-          if (lane == 0) y[j] -= tw;
-        }
-      }
-      __syncwarp();
-    }
-  }
-  __syncthreads();
+  apply_reflectors_warps<4>(A, lda, tau, m, k, q, Y, ldy);
 }
 
 template <int JG, int JE>
@@ -1250,7 +1263,7 @@ __global__ void __launch_bounds__(kThreads) basis_cta_kernel(const BasisTarget* 
   const int k = min(m, c);
   SmallSmem s = carve_small(smem_raw, m, c, r);
   PROF_MARK_CTA(0);
-  qr_cols_warps(T.lv[0].a, m, c, s.A, s.lda, s.tau);
+  qr_cols_warps<4>(T.lv[0].a, m, m, c, s.A, s.lda, s.tau);
   PROF_MARK_CTA(1);
   PROF_MARK_CTA(2);
   for (int idx = tid; idx < k * c; idx += blockDim.x) {
