@@ -724,6 +724,33 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
   } else {
     cp.part_doubles = best.items * best.A;
   }
+  // whole-column boxes for short columns (flat, r0 <= 8, n0 <= 64, n0 even
+  // and not a multiple of 16): one TMA box per tile instead of ceil(n0/16),
+  // k-steps over RB = n0 rounded to 4 rows instead of 16.
+  // development aid: SRTT_FORCE_CB=0 keeps the 16-row swizzled boxes
+  const char* fcb = std::getenv("SRTT_FORCE_CB");
+  if (P.flat && P.NT == 1 && P.use_tma && n0 <= 64 && n0 % 16 != 0 && !(fcb && fcb[0] == '0')) {
+    CoreParams T = P;
+    T.tpb = 1;
+    T.RB = (int)((n0 + 3) / 4 * 4);
+    T.cb = T.RB % 4 == 2 ? T.RB : T.RB + 2;  // = 2 (mod 4), >= RB
+    const int ns = srtt_core_max_stages(T, kCoreSmem);
+    if (ns >= 2) {
+      const int64_t ntiles = (P.Q + 15) / 16;
+      const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(sms, ntiles / P.warps));
+      if (ntiles >= P.warps) {
+        P = T;
+        P.nstages = ns;
+        P.ntiles = ntiles;
+        P.nw = (int)(grid * P.warps);
+        cp.grid = (int)grid;
+        cp.rec_doubles = (P.nw + P.G) * P.A;
+        if (std::getenv("SRTT_DEBUG_PLAN"))
+          std::fprintf(stderr, "core plan: whole-column boxes cb=%d RB=%d ns=%d tiles=%lld\n", P.cb, P.RB, ns,
+                       (long long)ntiles);
+      }
+    }
+  }
   cp.ufrag_doubles = (size_t)P.nrb * P.RB * P.NT * 8;
   return cp;
 }
@@ -765,7 +792,10 @@ int launch_core_pass(srtt_handle* h, CorePlan& cp, const double* x, const std::v
   if (P.m == 2) P.fu[1] = nullptr;
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
-  if (P.use_tma) encode_tmap(&tmap, x, P.n0, P.Q, 16 * P.tpb);
+  if (P.use_tma) {
+    if (P.cb) encode_tmap_plain(&tmap, x, P.n0, P.Q, P.n0, P.cb, 16 * P.tpb);
+    else encode_tmap(&tmap, x, P.n0, P.Q, 16 * P.tpb);
+  }
   if (!P.flat) cp.grid = (int)std::min<int64_t>(P.nitems, (int64_t)h->sms);
   record_event(h->kev[4], h->stream);
   CK(srtt_launch_core(&tmap, P, cp.grid, h->stream));

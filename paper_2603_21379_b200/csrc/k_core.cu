@@ -395,11 +395,11 @@ __device__ __forceinline__ void flat_emit(const CoreParams& P, int64_t gw, int64
   if (lane == 0) P.cnt[p] = 0u;  // ready for the next call (stream order)
 }
 
-template <int MT, int NT1, bool M3, int TPB, int WARPS>
+template <int MT, int NT1, bool M3, int TPB, int WARPS, bool CB>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     core_flat_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CoreParams P) {
   constexpr int BC = 16 * TPB;
-  constexpr int BOX = 16 * BC;
+  const int BOX = CB ? P.cb * BC : 16 * BC;  // doubles per TMA box
   constexpr int KP = MT == 1 ? 2 : 1;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int NS = P.nstages;
@@ -418,7 +418,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   const int r0 = P.r0, r1 = P.frank[0];
   const int n1 = (int)P.fdim[0];
   const double* __restrict__ U1 = P.fu[0];
-  const int nbox = (int)((P.n0 + 15) / 16);
+  const int nbox = CB ? 1 : (int)((P.n0 + 15) / 16);
+  const int KS = P.RB / 4;  // k-steps of a whole-column box (CB)
+  // CB: column (2g + par) of the box, row tq; + 4 ks per k-step, + 16 cb per h
+  const int boffc0 = (2 * g) * P.cb + tq, boffc1 = boffc0 + P.cb;
 
   int boff[2][4];
 #pragma unroll
@@ -456,6 +459,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       }
     }
   }
+  (void)pb;
 
   int stage = 0;
   uint32_t phase = 0;
@@ -532,7 +536,43 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 #pragma unroll
           for (int kp = 0; kp < KP; ++kp) tacc[h][par][mt][kp][0] = tacc[h][par][mt][kp][1] = 0.0;
     const double* uf = ufrag + lane;
-    for (int b = 0; b < nbox; ++b, uf += 4 * MT * 32) {
+    if constexpr (CB) {
+      // one box = BC whole columns (pitch cb), KS k-steps of 4 rows each
+      double* st = ring + stage * BOX;
+      mbar_wait(&bar[stage], phase);
+      auto kstep = [&](int ks, int kp) {
+        double a[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) a[mt] = uf[(ks * MT + mt) * 32];
+#pragma unroll
+        for (int h = 0; h < TPB; ++h) {
+          const double x0 = st[h * 16 * P.cb + boffc0 + 4 * ks];
+          const double x1 = st[h * 16 * P.cb + boffc1 + 4 * ks];
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            dmma_8x8x4(tacc[h][0][mt][kp][0], tacc[h][0][mt][kp][1], a[mt], x0);
+            dmma_8x8x4(tacc[h][1][mt][kp][0], tacc[h][1][mt][kp][1], a[mt], x1);
+          }
+        }
+      };
+      int ks = 0;
+      for (; ks + 1 < KS; ks += 2) {
+        kstep(ks, 0);
+        kstep(ks + 1, KP - 1);
+      }
+      if (ks < KS) kstep(ks, 0);
+      __syncwarp();
+      if (lane == 0 && pt < t_hi) {
+        mbar_arrive_expect_tx(&bar[stage], BOX * sizeof(double));
+        tma_load_2d(st, &tmap, &bar[stage], 0, (int32_t)(BC * pt));
+        ++pt;
+      }
+      if (++stage == NS) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    for (int b = 0; b < (CB ? 0 : nbox); ++b, uf += 4 * MT * 32) {
       double* st = ring + stage * BOX;
       if (P.use_tma) {
         mbar_wait(&bar[stage], phase);
@@ -958,9 +998,18 @@ __global__ void prep_all_kernel(const PrepJobs J) {
 template <int MT, int NT1, bool M3, int TPB, int WARPS>
 cudaError_t launch_w(const CUtensorMap* tmap, const CoreParams& P, int grid, size_t smem, cudaStream_t s) {
   if (P.flat) {
-    cudaError_t e = SRTT_ENSURE_SMEM((core_flat_kernel<MT, NT1, M3, TPB, WARPS>), smem);
+    if constexpr (MT == 1 && TPB == 1) {
+      if (P.cb) {
+        cudaError_t e = SRTT_ENSURE_SMEM((core_flat_kernel<MT, NT1, M3, TPB, WARPS, true>), smem);
+        if (e != cudaSuccess) return e;
+        core_flat_kernel<MT, NT1, M3, TPB, WARPS, true><<<grid, WARPS * 32, smem, s>>>(*tmap, P);
+        return cudaGetLastError();
+      }
+    }
+    if (P.cb) return cudaErrorInvalidValue;
+    cudaError_t e = SRTT_ENSURE_SMEM((core_flat_kernel<MT, NT1, M3, TPB, WARPS, false>), smem);
     if (e != cudaSuccess) return e;
-    core_flat_kernel<MT, NT1, M3, TPB, WARPS><<<grid, WARPS * 32, smem, s>>>(*tmap, P);
+    core_flat_kernel<MT, NT1, M3, TPB, WARPS, false><<<grid, WARPS * 32, smem, s>>>(*tmap, P);
     return cudaGetLastError();
   }
   cudaError_t e = SRTT_ENSURE_SMEM((core_kernel<MT, NT1, M3, TPB, WARPS>), smem);
@@ -1007,7 +1056,8 @@ int srtt_core_threads() { return 256; }
 // Shared memory of the core kernel for a given stage count.
 size_t srtt_core_smem_bytes(const CoreParams& P) {
   const size_t w = P.warps;
-  const size_t doubles = w * P.nstages * 256 * P.tpb + (size_t)(P.RB / 4) * P.NT * 32 + w * P.A;
+  const size_t box = P.cb ? (size_t)P.cb * 16 * P.tpb : (size_t)256 * P.tpb;
+  const size_t doubles = w * P.nstages * box + (size_t)(P.RB / 4) * P.NT * 32 + w * P.A;
   return 1024 + doubles * sizeof(double) + w * P.nstages * sizeof(uint64_t);
 }
 

@@ -128,6 +128,11 @@ typedef struct CoreParams {
   int64_t ntiles;          // BC-column tiles of M (flat mode)
   double* rec;             // flat mode: (nw + G) * A record slots
   uint32_t* cnt;           // flat mode: G completion counters (zero between calls)
+  // flat mode, short columns (n0 <= 64, r0 <= 8): one unswizzled TMA box
+  // holds whole columns, pitch cb rows (cb >= n0, cb = 2 mod 4: the DMMA B
+  // fragments of a half-warp then hit 16 distinct bank pairs); 0 = off
+  int32_t cb;
+  int32_t pad_cb;
 } CoreParams;
 
 // Streamed reconstruction error (k_recon.cu).
