@@ -133,3 +133,23 @@ def test_transfer_and_root_transfer(handle):
         ur = np.linalg.qr(rng.standard_normal((nr, 3)))[0]
         b = P.root_transfer(x, ul, ur, handle=handle)
         assert np.max(np.abs(b - O.root_transfer(x, ul, ur))) <= 1e-12
+
+
+@pytest.mark.parametrize("mode", ["items", "flat", "flat_swizzled"])
+@pytest.mark.parametrize("dims,ranks", [((40, 40, 30, 7), (6, 6, 6, 3)), ((42, 9, 11, 13), (5, 4, 3, 2)),
+                                        ((6, 70, 33), (2, 8, 5)), ((22, 17, 150), (8, 7, 9)),
+                                        ((40, 40, 40, 40), (6, 6, 6, 6)), ((200, 30, 31), (12, 10, 9))])
+def test_core_pass_work_decompositions(handle, monkeypatch, mode, dims, ranks):
+    """The planner's core-pass variants agree with multi_ttm (1e-12) and are
+    bitwise reproducible: item mode (CTA barriers per item), flat mode
+    (per-warp tile ranges, in-kernel record reduction with group counters;
+    groups covered by many warps and ragged last tiles) with whole-column
+    boxes (n0 = 2 mod 4 pitch) or 16-row swizzled boxes."""
+    monkeypatch.setenv("SRTT_FORCE_FLAT", "0" if mode == "items" else "1")
+    monkeypatch.setenv("SRTT_FORCE_CB", "0" if mode == "flat_swizzled" else "1")
+    x = rng.standard_normal(dims)
+    f = [np.linalg.qr(rng.standard_normal((n, r)))[0] for n, r in zip(dims, ranks)]
+    ref = O.core_from_factors(x, f)
+    core = P.multi_ttm_core(x, f, handle=handle)
+    assert np.linalg.norm(core - ref) / np.linalg.norm(ref) <= 1e-12
+    assert np.array_equal(core, P.multi_ttm_core(x, f, handle=handle))
