@@ -118,8 +118,11 @@ int srtt_version(void);
 /* Number of kernel launches issued by the last decomposition call. */
 int64_t srtt_last_launch_count(srtt_handle* h);
 /* Run all work of this handle on an external cudaStream_t (passed as void*;
- * NULL restores the handle's own stream). Lets a caller time calls with
- * its own CUDA events. */
+ * NULL restores the handle's own (non-blocking) stream, which is NOT ordered
+ * with the caller's streams). cudaStreamLegacy / cudaStreamPerThread are
+ * accepted: the work is then ordered with that default stream (CUDA graphs
+ * are captured on the own stream and launched into it). Lets a caller time
+ * calls with its own CUDA events and consume device outputs in order. */
 int srtt_set_stream(srtt_handle* h, void* stream);
 
 /* ---- host-side sampling (bit-exact with the reference) ------------------ */

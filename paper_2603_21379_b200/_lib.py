@@ -11,6 +11,9 @@ LIB_PATH = os.path.join(HERE, "libsrtt_b200.so")
 # development only: SRTT_PROFILE_BUILD=1 loads the phase-clock build (make PROF=1)
 if os.environ.get("SRTT_PROFILE_BUILD") == "1":
     LIB_PATH = os.path.join(HERE, "libsrtt_b200_prof.so")
+# development only: A/B runs against another in-tree build of the engine
+if os.environ.get("SRTT_LIB_AB"):
+    LIB_PATH = os.path.join(HERE, os.environ["SRTT_LIB_AB"])
 
 
 def build(force: bool = False) -> str:

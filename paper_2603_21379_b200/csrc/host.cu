@@ -563,14 +563,12 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
   P.NT = pad_tiles(ranks[0]);
   P.NT1 = pad_tiles(ranks[1]);
   if (!P.NT || !P.NT1) invalid("core: ranks above 32 in modes 0 and 1 are not supported by the B200 core kernel");
-  P.RB = n0 <= 256 ? (int)((n0 + 15) / 16 * 16) : 256;
-  P.nrb = (int)((n0 + P.RB - 1) / P.RB);
   P.use_tma = (n0 % 2 == 0) ? 1 : 0;
   P.fdim[0] = dims[1];
   P.frank[0] = (int)ranks[1];
 
   struct Cand {
-    int m = 0, S = 0, ns = 0, tpb = 1, warps = 8, flat = 0;
+    int m = 0, S = 0, ns = 0, tpb = 1, warps = 8, flat = 0, RB = 0, slot_ch = 0;
     int64_t SL = 0, G = 0, GS = 0, items = 0, grid = 0;
     int A = 0;
     double cost = 1e300;
@@ -579,9 +577,24 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
   // reduced inside the kernel. development aid: SRTT_FORCE_FLAT=0/1
   int force_flat = -1;
   if (const char* ff = std::getenv("SRTT_FORCE_FLAT")) force_flat = std::atoi(ff);
+  // row blocks: the whole column up to 256 rows; longer columns in blocks
+  // of 256 or (m = 2) 512 rows -- the mode-1 fold runs once per row block,
+  // so 512 halves its DMMA work (C5: 12.5 % -> 6 % of the pass) at the price
+  // of a 2x larger U0 in shared memory and a chunked CTA reduction
+  // development aid: SRTT_FORCE_RB=256/512
+  int force_rb = 0;
+  if (const char* fr = std::getenv("SRTT_FORCE_RB")) force_rb = std::atoi(fr);
+  std::vector<int> rb_choices;
+  if (n0 <= 256) rb_choices.push_back((int)((n0 + 15) / 16 * 16));
+  else for (int rb : {256, 512}) if (!force_rb || force_rb == rb) rb_choices.push_back(rb);
+  for (int RBc : rb_choices) {
+  P.RB = RBc;
+  P.nrb = (int)((n0 + P.RB - 1) / P.RB);
+  P.slot_ch = 0;
   const bool flat_ok = P.nrb == 1 && force_flat != 0;
   for (int m = 2; m <= std::min(3, d); ++m) {
     if (force_m && m != force_m) continue;
+    if (RBc > 256 && m != 2) continue;
     // warps per CTA: 16 when the rank tiles are small (register budget
     // 128/thread), else 8; each with the widest box that leaves a ring of
     // >= 3 boxes per warp (2 for single-tile boxes)
@@ -597,6 +610,7 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
       T.m = m;
       T.A = (int)(ranks[0] * ranks[1] * (m == 3 ? ranks[2] : 1));
       T.warps = W;
+      if (RBc > 256) T.slot_ch = std::min(T.A, 256);
       int tpb = 0, ns = 0;
       for (int tb : {2, 1}) {
         if (tb == 2 && (P.NT > 2 || P.NT1 > 2)) continue;
@@ -634,6 +648,8 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
         const double cost = std::max(t_mem, t_cmp) * imb * (W == 16 ? 1.0 : 1.45) + recs + out + 1.5e-6;
         if ((force_flat == 1 && !best.flat) || cost < best.cost) {
           best = Cand{};
+          best.RB = RBc;
+          best.slot_ch = T.slot_ch;
           best.m = m;
           best.S = 1;
           best.ns = ns;
@@ -677,6 +693,8 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
         const double cost = (double)full * t_item(grid) + (last ? t_item(last) : 0.0) + out;
         if (cost < best.cost) {
           best = Cand{};
+          best.RB = RBc;
+          best.slot_ch = T.slot_ch;
           best.m = m;
           best.S = (int)Se;
           best.ns = ns;
@@ -693,11 +711,15 @@ CorePlan plan_core(const std::vector<int64_t>& dims, const std::vector<int64_t>&
       }
     }
   }
+  }  // row-block choices
   if (best.m == 0) invalid("core: no feasible work decomposition");
+  P.RB = best.RB;
+  P.nrb = (int)((n0 + P.RB - 1) / P.RB);
+  P.slot_ch = best.slot_ch;
   if (std::getenv("SRTT_DEBUG_PLAN"))  // development aid
-    std::fprintf(stderr, "core plan: flat=%d m=%d S=%d SL=%lld items=%lld warps=%d tpb=%d ns=%d RB=%d cost=%.3g\n",
-                 best.flat, best.m, best.S, (long long)best.SL, (long long)best.items, best.warps, best.tpb, best.ns,
-                 P.RB, best.cost);
+    std::fprintf(stderr, "core plan: flat=%d m=%d S=%d SL=%lld items=%lld warps=%d tpb=%d ns=%d RB=%d slot_ch=%d "
+                 "cost=%.3g\n", best.flat, best.m, best.S, (long long)best.SL, (long long)best.items, best.warps,
+                 best.tpb, best.ns, best.RB, best.slot_ch, best.cost);
   P.m = best.m;
   P.S = best.S;
   P.SL = best.SL;
@@ -959,6 +981,10 @@ bool end_call(srtt_handle* h, bool must_sync) {
 // captured once per signature into a CUDA graph and replayed. The key holds
 // every pointer the work bakes in (workspace, parameter blob, input,
 // outputs, stream), so buffer growth simply creates a new graph.
+bool is_default_stream(cudaStream_t s) {
+  return s == nullptr || s == cudaStreamLegacy || s == cudaStreamPerThread;
+}
+
 template <class F>
 void run_enqueue(srtt_handle* h, const std::string& key, F&& enqueue) {
   if (!h->use_graphs) {
@@ -971,6 +997,10 @@ void run_enqueue(srtt_handle* h, const std::string& key, F&& enqueue) {
       for (auto& g : h->graphs) cudaGraphExecDestroy(g.second.exec);
       h->graphs.clear();
     }
+    // the legacy / per-thread default streams cannot be captured: capture on
+    // the handle's own stream, launch the graph into the caller's stream
+    const cudaStream_t launch_stream = h->stream;
+    if (is_default_stream(launch_stream)) h->stream = h->own_stream;
     CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
     const int64_t before = h->launches;
     try {
@@ -978,11 +1008,14 @@ void run_enqueue(srtt_handle* h, const std::string& key, F&& enqueue) {
     } catch (...) {
       cudaGraph_t g;
       cudaStreamEndCapture(h->stream, &g);
+      h->stream = launch_stream;
       if (g) cudaGraphDestroy(g);
       throw;
     }
     cudaGraph_t g;
-    CK(cudaStreamEndCapture(h->stream, &g));
+    const cudaError_t ce = cudaStreamEndCapture(h->stream, &g);
+    h->stream = launch_stream;
+    CK(ce);
     srtt_handle::Graph entry;
     CK(cudaGraphInstantiate(&entry.exec, g, 0));
     cudaGraphDestroy(g);
@@ -1117,6 +1150,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     if (pit != h->prepared.end() && pit->second.ws == h->ws.p && pit->second.dp == h->pset().d.p &&
         pit->second.hp == h->pset().hst.p && h->graphs.count(pit->second.graph_key)) {
       const srtt_handle::Prepared& pr = pit->second;
+      if (std::getenv("SRTT_DEBUG_CALLS")) std::fprintf(stderr, "tucker call: prepared graph, set %d\n", h->cur);
       char* hp = reinterpret_cast<char*>(h->pset().hst.p);
       std::memcpy(hp, pr.image.data(), pr.image.size());
       for (int k = 0; k < d; ++k) {
@@ -1142,6 +1176,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     }
   }
 
+  if (std::getenv("SRTT_DEBUG_CALLS")) std::fprintf(stderr, "tucker call: full path, set %d\n", h->cur);
   // --- workspace layout
   Layout L;
   std::vector<size_t> off_z(d), off_u(d);

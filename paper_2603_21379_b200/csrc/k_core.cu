@@ -102,14 +102,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   double* rings = reinterpret_cast<double*>(smem_raw + pad);
   double* ufrag = rings + (size_t)WARPS * NS * BOX;
+  // m = 2 with a large r0 r1 (C5: 1024) reduces the warp partials in
+  // chunks of P.slot_ch entries, so 512-row blocks fit next to U0
+  const int SLOT = (!M3 && P.slot_ch) ? P.slot_ch : P.A;
   double* slots = ufrag + (size_t)(P.RB / 4) * MT * 32;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + (size_t)WARPS * P.A);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + (size_t)WARPS * SLOT);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
   double* ring = rings + (size_t)warp * NS * BOX;
   uint64_t* bar = bars + warp * NS;
-  double* slot = slots + (size_t)warp * P.A;
+  double* slot = slots + (size_t)warp * SLOT;
 
   const int r0 = P.r0, r1 = P.frank[0];
   const int n1 = (int)P.fdim[0];
@@ -333,28 +336,32 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       }
     }
     // ---- item end: warp partial -> slot, fixed-order CTA reduction
-    if (M3) {
-      if (cur_g2 >= 0) flush(cur_g2);
-    } else {
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < NT1; ++nt)
-#pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            const int a0 = g + 8 * mt, a1 = 2 * tq + v + 8 * nt;
-            if (a0 < r0 && a1 < r1) slot[a0 + r0 * a1] = r2[mt][nt][v];
-          }
-    }
-    __syncthreads();
+    // (chunks of SLOT entries; one chunk unless P.slot_ch is set)
     double* out = P.part + I.out_off;
-    for (int e = threadIdx.x; e < P.A; e += WARPS * 32) {
-      double sum = 0.0;
+    if (M3 && cur_g2 >= 0) flush(cur_g2);
+    for (int c0 = 0; c0 < P.A; c0 += SLOT) {
+      if (!M3) {
 #pragma unroll
-      for (int w = 0; w < WARPS; ++w) sum += slots[(size_t)w * P.A + e];
-      out[e] = sum;
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT1; ++nt)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int a0 = g + 8 * mt, a1 = 2 * tq + v + 8 * nt;
+              const int e = a0 + r0 * a1 - c0;
+              if (a0 < r0 && a1 < r1 && e >= 0 && e < SLOT) slot[e] = r2[mt][nt][v];
+            }
+      }
+      __syncthreads();
+      const int ce = min(SLOT, P.A - c0);
+      for (int e = threadIdx.x; e < ce; e += WARPS * 32) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) sum += slots[(size_t)w * SLOT + e];
+        out[c0 + e] = sum;
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
@@ -1057,7 +1064,8 @@ int srtt_core_threads() { return 256; }
 size_t srtt_core_smem_bytes(const CoreParams& P) {
   const size_t w = P.warps;
   const size_t box = P.cb ? (size_t)P.cb * 16 * P.tpb : (size_t)256 * P.tpb;
-  const size_t doubles = w * P.nstages * box + (size_t)(P.RB / 4) * P.NT * 32 + w * P.A;
+  const size_t slot = (P.m == 2 && P.slot_ch && !P.flat) ? (size_t)P.slot_ch : (size_t)P.A;
+  const size_t doubles = w * P.nstages * box + (size_t)(P.RB / 4) * P.NT * 32 + w * slot;
   return 1024 + doubles * sizeof(double) + w * P.nstages * sizeof(uint64_t);
 }
 

@@ -132,7 +132,7 @@ typedef struct CoreParams {
   // holds whole columns, pitch cb rows (cb >= n0, cb = 2 mod 4: the DMMA B
   // fragments of a half-warp then hit 16 distinct bank pairs); 0 = off
   int32_t cb;
-  int32_t pad_cb;
+  int32_t slot_ch;         // item mode, m = 2: CTA reduction chunk (0 = all A at once)
 } CoreParams;
 
 // Streamed reconstruction error (k_recon.cu).

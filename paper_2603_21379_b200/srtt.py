@@ -182,6 +182,9 @@ def _flat_f64(x):
 # ---------------------------------------------------------------------------
 # handle
 # ---------------------------------------------------------------------------
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
+
+
 class Handle:
     """Owns a device, a stream, the workspace arena and pinned staging."""
 
@@ -201,8 +204,17 @@ class Handle:
 
     def set_stream(self, stream_ptr):
         """Run on an external cudaStream_t (int handle, e.g. torch's
-        ``torch.cuda.current_stream().cuda_stream``); None = own stream."""
-        _check(_L().srtt_set_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
+        ``torch.cuda.current_stream().cuda_stream``); None = the handle's own
+        stream. ``0`` is torch's default stream, i.e. the legacy default
+        stream (``cudaStreamLegacy``): the engine's work is then ordered with
+        it (graphs are captured on the own stream and launched into it)."""
+        if stream_ptr is None:
+            ptr = None
+        elif stream_ptr == 0:
+            ptr = C.c_void_p(CUDA_STREAM_LEGACY)
+        else:
+            ptr = C.c_void_p(stream_ptr)
+        _check(_L().srtt_set_stream(self._h, ptr))
 
     @property
     def last_launch_count(self) -> int:
