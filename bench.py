@@ -302,6 +302,17 @@ def run_product(args):
     torch.cuda.synchronize()
     launches_per_step = rep.launches
 
+    last = {}
+
+    def digest(res):
+        """All outputs of one decomposition, flattened (device -> host copy on
+        the current stream, i.e. ordered after the recorded work)."""
+        if hasattr(res, "core"):
+            ts = [res.core] + list(res.factors)
+        else:
+            ts = list(res.leaf_factors) + [t for t in res.transfers if t is not None and t.numel() > 0]
+        return torch.cat([t.reshape(-1) for t in ts]).cpu()
+
     def timed_loop(n):
         # one event pair around all n stream-ordered calls (device outputs, no
         # report): host preparation of step i+1 overlaps the kernels of step i,
@@ -313,9 +324,10 @@ def run_product(args):
         for _ in range(n):
             if flush is not None:
                 flush.fill_(1.0)
-            _run_product(P, cfg, x, dims, 0, h)
+            last["res"] = _run_product(P, cfg, x, dims, 0, h)
         e1.record(stream)
         e1.synchronize()
+        last["digest"] = digest(last["res"])  # read right after the span: must already be complete
         return e0.elapsed_time(e1) / 1e3
 
     def kernel_samples(n):
@@ -330,10 +342,16 @@ def run_product(args):
 
     if world > 1:
         torch.distributed.barrier()
+    out_buf = _OUT.get(cfg.name)
+    if out_buf is not None:  # outputs the timed calls must rewrite
+        out_buf[0].zero_()
+        for f in out_buf[1]:
+            f.zero_()
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
     elapsed = timed_loop(args.steps)
+    timed_digest = last["digest"]
     torch.cuda.synchronize()
     # keep the same workload running until the clock sampler has >= 3 samples
     t_extra = time.perf_counter()
@@ -342,6 +360,11 @@ def run_product(args):
     sampler.stop()
     clocks = sampler.summary()
     core_t = kernel_samples(8)
+    # the last timed call's outputs equal a synchronous call's, bit for bit
+    # (deterministic engine): guards the timed span against unordered work
+    torch.cuda.synchronize()
+    ref_digest = digest(_run_product(P, cfg, x, dims, 0, h, report=P.SubsampleReport()))
+    verified = bool(torch.equal(timed_digest, ref_digest))
     el = torch.tensor([elapsed], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(el, op=torch.distributed.ReduceOp.MAX)
@@ -387,6 +410,7 @@ def run_product(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(_config_dict(cfg), parallelism=f"replicas x{world}" if world > 1 else "single GPU"),
             "clocks": clocks, "gpu_launches": launches_per_step * args.steps,
+            "outputs_verified": verified,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "steps": e2e_steps},
             "roofline": roofline}
