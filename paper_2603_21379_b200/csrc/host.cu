@@ -539,6 +539,8 @@ struct CorePlan {
   std::vector<int64_t> ranks;
   int64_t part_doubles = 0;
   int64_t rec_doubles = 0;   // flat mode: record slots
+  int64_t scratch_doubles = 0;  // split-K partials of the first tail TTM
+  size_t off_scratch = 0;
   int64_t cnt_words = 0;     // flat mode: group counters
   size_t ufrag_doubles = 0;
   size_t off_items = 0;
@@ -856,6 +858,10 @@ int launch_core_pass(srtt_handle* h, CorePlan& cp, const double* x, const std::v
       T.transpose = 1;
       T.nparts = np;
       T.part_stride = (int64_t)P.G * P.A;
+      if (k == P.m && cp.scratch_doubles) {
+        T.scratch = reinterpret_cast<double*>(ws + cp.off_scratch);
+        T.scratch_doubles = cp.scratch_doubles;
+      }
       T.out = (k == d - 1) ? out : reinterpret_cast<double*>(ws + (((k - P.m) % 2) ? off_tmp1 : off_tmp0));
       CK(srtt_launch_ttm(T, h->stream));
       ++launches;
@@ -878,6 +884,14 @@ void layout_core(Layout& L, CorePlan& cp, size_t& off_ufrag, std::vector<size_t>
   off_part = L.take(sizeof(double) * cp.part_doubles);
   cp.off_rec = L.take(sizeof(double) * cp.rec_doubles);
   cp.off_cnt = L.take(sizeof(uint32_t) * cp.cnt_words);
+  // split-K partials of the first tail TTM (long mode m, few slabs)
+  if (cp.P.m < d) {
+    const int64_t m = cp.P.m;
+    const int64_t s1 = (int64_t)cp.P.A * cp.ranks[m] * prod(cp.dims, (int)m + 1);
+    const int64_t nch = std::min<int64_t>(148 * 4, cp.dims[m] / 64 + 1);
+    cp.scratch_doubles = s1 * nch;
+    cp.off_scratch = L.take(sizeof(double) * cp.scratch_doubles);
+  }
   // largest intermediate of the tail
   int64_t g = cp.P.A, big = 1;
   for (int k = cp.P.m; k < d; ++k) {

@@ -29,6 +29,8 @@
 // so the core is bitwise reproducible run to run. X is read exactly once.
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "srtt_device.cuh"
 #include "srtt_params.h"
 
@@ -935,6 +937,86 @@ __global__ void __launch_bounds__(256) ttm_block_kernel(const TtmParams T) {
   }
 }
 
+// Few slabs (post < 64), long contraction: split the mode over gridDim.y
+// chunks; CTA (gi-block, chunk) writes a partial of its 64 rows x rr
+// outputs, and ttm_splitk_reduce_kernel sums the chunks in order
+// (deterministic). post is looped inside the CTA.
+template <int RR>
+__global__ void __launch_bounds__(256) ttm_splitk_kernel(const TtmParams T, int64_t chunk, double* partial) {
+  __shared__ double red[2][RR][64];
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  const int64_t gi = (int64_t)blockIdx.x * 64 + tx;
+  const int64_t i_lo = (int64_t)blockIdx.y * chunk, i_hi = min64(T.n, i_lo + chunk);
+  const int64_t cs = T.transpose ? T.n : 1, ci = T.transpose ? 1 : T.rr;
+  for (int64_t pi = 0; pi < T.post; ++pi) {
+    double acc[RR];
+#pragma unroll
+    for (int b = 0; b < RR; ++b) acc[b] = 0.0;
+    if (gi < T.g) {
+      const double* in = T.in + gi + T.g * T.n * pi;
+      constexpr int kB = 4;
+      for (int64_t i0 = i_lo + ty; i0 < i_hi; i0 += 4 * kB) {
+        double v[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int64_t i = i0 + 4 * u;
+          v[u] = 0.0;
+          if (i < i_hi) {
+            const double* pp = in + T.g * i;
+            double s0 = pp[0];
+            for (int q = 1; q < T.nparts; ++q) s0 += pp[q * T.part_stride];
+            v[u] = s0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int64_t i = i0 + 4 * u;
+          if (i < i_hi) {
+            const double* cf = T.u + ci * i;
+#pragma unroll
+            for (int b = 0; b < RR; ++b)
+              if (b < T.rr) acc[b] = fma(v[u], __ldg(cf + cs * b), acc[b]);
+          }
+        }
+      }
+    }
+    // fixed-order combine of the 4 i-groups: (g0 + g2) + (g1 + g3)
+    __syncthreads();
+    if (ty >= 2)
+#pragma unroll
+      for (int b = 0; b < RR; ++b) red[ty - 2][b][tx] = acc[b];
+    __syncthreads();
+    if (ty < 2)
+#pragma unroll
+      for (int b = 0; b < RR; ++b) acc[b] += red[ty][b][tx];
+    __syncthreads();
+    if (ty == 1)
+#pragma unroll
+      for (int b = 0; b < RR; ++b) red[0][b][tx] = acc[b];
+    __syncthreads();
+    if (ty == 0) {
+      const int64_t go = (int64_t)blockIdx.x * 64 + tx;
+      if (go < T.g)
+#pragma unroll
+        for (int b = 0; b < RR; ++b)
+          if (b < T.rr)
+            partial[(((int64_t)blockIdx.y * T.post + pi) * T.rr + b) * T.g + go] = acc[b] + red[0][b][tx];
+    }
+  }
+}
+
+__global__ void ttm_splitk_reduce_kernel(const TtmParams T, int nchunks, const double* __restrict__ partial) {
+  const int64_t total = T.g * T.rr * T.post;  // output order: gi fastest, then b, then pi
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gi = o % T.g, rest = o / T.g;
+    const int64_t b = rest % T.rr, pi = rest / T.rr;
+    double sum = 0.0;
+    for (int c = 0; c < nchunks; ++c) sum += partial[(((int64_t)c * T.post + pi) * T.rr + b) * T.g + gi];
+    T.out[o] = sum;
+  }
+}
+
 // All factor reformatting of a core pass in one launch: blockIdx.y = 0
 // builds U0's fragments, 1..2 transpose U1, U2 to row-major.
 struct PrepJobs {
@@ -1151,6 +1233,26 @@ cudaError_t srtt_launch_ttm(const TtmParams& T, cudaStream_t s) {
     if (T.rr <= 8) ttm_block_kernel<8><<<grid, 256, sm, s>>>(T);
     else ttm_block_kernel<16><<<grid, 256, sm, s>>>(T);
     return cudaGetLastError();
+  }
+  if (T.rr <= 32 && T.post < 64 && T.scratch && in_bytes > 16e6) {
+    // few slabs, long contraction (C5 tail: 1024 x 2048 x 4 parts): split-K
+    const int64_t gblk = (T.g + 63) / 64;
+    int64_t nch = std::max<int64_t>(1, std::min<int64_t>((148 * 4 + gblk - 1) / gblk, (T.n + 63) / 64));
+    nch = std::min<int64_t>(nch, T.scratch_doubles / std::max<int64_t>(1, T.g * T.rr * T.post));
+    if (nch >= 2) {
+      const int64_t chunk = (T.n + nch - 1) / nch;
+      nch = (T.n + chunk - 1) / chunk;
+      const dim3 grid((unsigned)gblk, (unsigned)nch);
+      if (T.rr <= 8) ttm_splitk_kernel<8><<<grid, 256, 0, s>>>(T, chunk, T.scratch);
+      else if (T.rr <= 16) ttm_splitk_kernel<16><<<grid, 256, 0, s>>>(T, chunk, T.scratch);
+      else ttm_splitk_kernel<32><<<grid, 256, 0, s>>>(T, chunk, T.scratch);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      const int64_t total = T.g * T.rr * T.post;
+      ttm_splitk_reduce_kernel<<<(unsigned)min64(148 * 8, (total + 255) / 256), 256, 0, s>>>(T, (int)nch,
+                                                                                            T.scratch);
+      return cudaGetLastError();
+    }
   }
   if (T.rr <= 32 && pairs >= 148 * 128 && in_bytes * T.rr > 64e6) {
     // large input re-read rr times by the per-output kernels: read it once

@@ -170,4 +170,6 @@ typedef struct TtmParams {
   int32_t transpose;     // 1: contract with U^T (u is n x rr) ; 0: with U (u is rr x n)
   int32_t nparts;
   int64_t part_stride;
+  double* scratch;          // optional workspace for split-K partials (NULL: not used)
+  int64_t scratch_doubles;
 } TtmParams;
