@@ -257,6 +257,7 @@ struct srtt_handle {
   DevBuf xbuf;     // device copy of host inputs
   DevBuf ws;       // workspace arena
   DevBuf rb[6];    // reconstruction / error buffers (At, Ct ping-pong, staging), reused across calls
+  DevBuf comp[6];  // scratch of the synchronous component / shard-phase calls, reused across calls
   // Double-buffered parameter blobs (pinned host + device copy): a call
   // may return before its graph ran (device outputs, no report), so the
   // next call writes the other set; a set is reused only after the call
@@ -1807,6 +1808,13 @@ const double* to_device(srtt_handle* h, DevBuf& buf, const double* src, int64_t 
 struct CompBufs {
   DevBuf a, b, c, d, e, idx;
 };
+// The handle's persistent scratch for calls that synchronise before they
+// return (no cudaMalloc / cudaFree per call: a free synchronises the device
+// and an allocation costs milliseconds).
+struct CompRef {
+  DevBuf &a, &b, &c, &d, &e, &idx;
+};
+CompRef comp_bufs(srtt_handle* h) { return {h->comp[0], h->comp[1], h->comp[2], h->comp[3], h->comp[4], h->comp[5]}; }
 
 void validate_modes(int d, const int64_t* dims, int nmodes, const int32_t* modes, const char* what) {
   if (nmodes < 1) invalid("ModeSet: must be non-empty");
@@ -1987,7 +1995,7 @@ int srtt_multi_ttm_core(srtt_handle* h, const double* x, int32_t x_on_device, in
       if (dv[k] < 1 || rv[k] < 1 || rv[k] > dv[k]) invalid("sliced_core: factor rows mismatch in mode " + std::to_string(k));
     DeviceGuard g(h->device);
     const int64_t N = prod(dv);
-    CompBufs B;
+    CompRef B = comp_bufs(h);
     const double* dx = to_device(h, B.a, x, N, x_on_device);
     std::vector<DevBuf> ub(d);
     std::vector<const double*> u(d);
@@ -2118,7 +2126,7 @@ int srtt_shard_sketches(srtt_handle* h, const double* x_local, int32_t x_on_devi
     ldims[L] = slab_hi - slab_lo;
     const int64_t Nl = prod(ldims);
     DeviceGuard g(h->device);
-    CompBufs B;
+    CompRef B = comp_bufs(h);
     const double* x = to_device(h, B.a, x_local, Nl, x_on_device);
     const SampledModes S = sample_all_modes(d, dims, samples, seed, exec ? exec->index_partitions : 1);
     Layout Lw;
@@ -2175,7 +2183,7 @@ int srtt_bases_from_sketches(srtt_handle* h, int32_t d, const int64_t* dims_p, c
     validate_tucker(d, dims, ranks, samples, p);
     DeviceGuard g(h->device);
     const SampledModes S = sample_all_modes(d, dims, samples, seed, exec ? exec->index_partitions : 1);
-    CompBufs B;
+    CompRef B = comp_bufs(h);
     Layout Lw;
     std::vector<size_t> off_z(d), off_u(d);
     std::vector<BasisPlan> bp(d);
@@ -2236,7 +2244,7 @@ int srtt_shard_core(srtt_handle* h, const double* x_local, int32_t x_on_device, 
     std::vector<int64_t> ldims = dims;
     ldims[L] = slab_hi - slab_lo;
     DeviceGuard g(h->device);
-    CompBufs B;
+    CompRef B = comp_bufs(h);
     // U_{d-1} rows [lo, hi) as a contiguous (hi-lo) x r block
     const int64_t nl = slab_hi - slab_lo;
     B.d.ensure(sizeof(double) * nl * ranks[L]);

@@ -64,7 +64,14 @@ class GpuShardPhases:
 
         d = len(dims)
         rows = [dims[k] if k < d - 1 else hi - lo for k in range(d)]
-        zs = [torch.empty(rows[k] * (ranks[k] + p), dtype=torch.float64, device=x_local.device) for k in range(d)]
+        sizes = [rows[k] * (ranks[k] + p) for k in range(d)]
+        # the summed sketches (k < d-1) are views of ONE buffer, so a single
+        # all_reduce exchanges them (self.partial_sums)
+        flat = torch.empty(sum(sizes[:-1]), dtype=torch.float64, device=x_local.device)
+        offs = np.cumsum([0] + sizes[:-1])
+        zs = [flat[offs[k]:offs[k + 1]] for k in range(d - 1)]
+        zs.append(torch.empty(sizes[-1], dtype=torch.float64, device=x_local.device))
+        self.partial_sums = flat
         zp = (C.c_void_p * d)(*[z.data_ptr() for z in zs])
         dims_a, ranks_a, samp_a = _s._i64(dims), _s._i64(ranks), _s._i64(samples)
         _s._check(self.lib.srtt_shard_sketches(self.h._h, x_local.data_ptr(), 1, d, dims_a.ctypes.data, lo, hi,
@@ -154,8 +161,12 @@ def sub_r_hosvd_sharded(x_local, dims, target, oversampling, samples, seed, *, g
         raise _s.InvalidArgument("sharded sub_r_hosvd: local slab size mismatch")
     ph = phases or GpuShardPhases()
     zs = ph.shard_sketches(x_local, dims, lo, hi, target, oversampling, samples, seed)
-    for k in range(L):
-        dist.all_reduce(zs[k], group=group)
+    partial = getattr(ph, "partial_sums", None)
+    if partial is not None:  # one collective for all summed sketches
+        dist.all_reduce(partial, group=group)
+    else:
+        for k in range(L):
+            dist.all_reduce(zs[k], group=group)
     zs[L] = _gather_rows(zs[L], hi - lo, target[L] + oversampling, counts, group)
     factors, achieved = ph.bases_from_sketches(dims, target, oversampling, samples, seed, zs)
     core = ph.shard_core(x_local, dims, lo, hi, target, factors)
