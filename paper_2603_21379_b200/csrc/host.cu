@@ -358,9 +358,22 @@ BasisPlan plan_basis(int64_t n, int c, int r) {
   b.n = n;
   b.c = c;
   b.r = r;
-  const int tmax = top_max_rows(c, r);
-  const int blk = level_block_rows(c);
+  int tmax = top_max_rows(c, r);
+  int blk = level_block_rows(c);
   if (tmax < c) invalid("range_basis_of_sketch: sketch too wide for the B200 basis kernel");
+  if (n > tmax && c <= 32) {
+    // Tall sketch: the TSQR step is a latency chain whose cost grows with
+    // the rows one CTA factors, not with the CTA count. Short row blocks
+    // (about 64 per level, >= 128 rows) and a short top (<= 4c rows) give
+    // more, cheaper levels (C4 level-1 nodes: 302 -> 286 us of TSQR; wide
+    // sketches, c > 32, keep the large blocks: their top dominates).
+    // development aid: SRTT_TSQR="blk,top"
+    int fb = 0, ft = 0;
+    if (const char* e = std::getenv("SRTT_TSQR")) std::sscanf(e, "%d,%d", &fb, &ft);
+    const int64_t want = ((n + 63) / 64 + 31) / 32 * 32;
+    blk = fb ? fb : (int)std::min<int64_t>(blk, std::max<int64_t>(std::max(128, 2 * c), want));
+    tmax = ft ? std::min(ft, tmax) : std::min(tmax, std::max(4 * c, 64));
+  }
   int64_t nl = n;
   int l = 0;
   while (nl > tmax) {
