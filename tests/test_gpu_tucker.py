@@ -115,3 +115,38 @@ def test_device_resident_inputs_and_outputs(handle):
     assert np.array_equal(td.core.cpu().numpy(), np.ravel(th.core, order="F"))
     for k in range(3):
         assert np.array_equal(td.factors[k].cpu().numpy(), np.ravel(th.factors[k], order="F"))
+
+
+@pytest.mark.parametrize("use_torch_default_stream", [True, False])
+def test_stream_ordered_calls_are_ordered_with_the_callers_stream(use_torch_default_stream):
+    """Device-output calls without a report return once enqueued. Bound to
+    the caller's stream (torch's default = the legacy stream, or a side
+    stream), every call must rewrite its outputs before work the caller
+    enqueues afterwards -- also the first calls after a synchronising one,
+    when both parameter sets are free (this once ran unordered)."""
+    import torch
+
+    dims, r = [40, 36, 30], 5
+    x_np, _, _ = planted_tucker(tuple(dims), (r,) * 3, 3)
+    h = P.Handle(0, use_graphs=True)
+    side = torch.cuda.Stream()
+    ctx = torch.cuda.stream(side) if not use_torch_default_stream else torch.cuda.stream(torch.cuda.current_stream())
+    with ctx:
+        s = torch.cuda.current_stream()
+        h.set_stream(s.cuda_stream)
+        x = torch.from_numpy(np.ravel(x_np, order="F").copy()).cuda()
+        core = torch.empty(r ** 3, dtype=torch.float64, device="cuda")
+        facs = [torch.empty(n * r, dtype=torch.float64, device="cuda") for n in dims]
+
+        def call(rep=None):
+            P.sub_r_hosvd(x, [r] * 3, 4, [36] * 3, 7, dims=dims, handle=h, device_out=True, out=(core, facs),
+                          report=rep)
+
+        call(P.SubsampleReport())  # synchronous reference call
+        torch.cuda.synchronize()
+        ref = core.cpu().numpy().copy()
+        for _ in range(4):
+            core.zero_()
+            call()
+            got = core.cpu().numpy()  # ordered after the call on the caller's stream, no extra sync
+            assert np.array_equal(got, ref)
