@@ -34,7 +34,7 @@ int srtt_basis_top_variant(int c);
 size_t srtt_basis_small_smem(int m, int c, int r);
 cudaError_t srtt_launch_basis_small(int, const BasisTarget*, const int*, int, size_t, cudaStream_t);
 int srtt_basis_small_variant(int m, int c);
-constexpr int kSmallVariants = 4;
+constexpr int kSmallVariants = 5;
 cudaError_t srtt_launch_tsqr_factor(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_tsqr_apply(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_pad(const BasisTarget*, int, double*, int64_t, cudaStream_t);

@@ -1340,6 +1340,7 @@ size_t srtt_basis_small_smem(int m, int c, int r) {
 // Variant of a small target (see basis_small_kernel).
 int srtt_basis_small_variant(int m, int c) {
   const int k = m < c ? m : c;
+  if (c <= 12) return 4;              // CTA kernel, Jacobi <4, 3> (C2: c = 11)
   if (c <= 16) return 0;              // CTA kernel, Jacobi <4, 4>
   if (k <= 24 && c <= 24) return 3;   // CTA kernel, Jacobi <2, 12> (C3: c = 20)
   if (k <= 32 && c <= 32) return 1;   // CTA kernel, Jacobi <2, 16>
@@ -1357,6 +1358,10 @@ cudaError_t srtt_launch_basis_small(int variant, const BasisTarget* d_targets, c
     case 1:
       SRTT_ENSURE_SMEM((basis_cta_kernel<2, 16>), smem);
       basis_cta_kernel<2, 16><<<n, kThreads, smem, stream>>>(d_targets, d_list);
+      break;
+    case 4:
+      SRTT_ENSURE_SMEM((basis_cta_kernel<4, 3>), smem);
+      basis_cta_kernel<4, 3><<<n, kThreads, smem, stream>>>(d_targets, d_list);
       break;
     case 3:
       SRTT_ENSURE_SMEM((basis_cta_kernel<2, 12>), smem);
