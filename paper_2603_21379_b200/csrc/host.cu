@@ -275,6 +275,9 @@ struct srtt_handle {
   int32_t* dinfo = nullptr;   // device alias of hinfo
   DevBuf ones;
   int64_t launches = 0;
+  // timing events (stage marks, per-kernel pairs) are recorded only for
+  // calls that return a report: they are graph nodes between the kernels
+  bool timing = true;
   struct Graph {
     cudaGraphExec_t exec = nullptr;
     int64_t launches = 0;
@@ -835,9 +838,9 @@ int launch_core_pass(srtt_handle* h, CorePlan& cp, const double* x, const std::v
     else encode_tmap(&tmap, x, P.n0, P.Q, 16 * P.tpb);
   }
   if (!P.flat) cp.grid = (int)std::min<int64_t>(P.nitems, (int64_t)h->sms);
-  record_event(h->kev[4], h->stream);
+  if (h->timing) record_event(h->kev[4], h->stream);
   CK(srtt_launch_core(&tmap, P, cp.grid, h->stream));
-  record_event(h->kev[5], h->stream);
+  if (h->timing) record_event(h->kev[5], h->stream);
   ++launches;
   // tail: fixed-order reduction of the item partials + TTMs of modes m..d-1
   // (flat mode: the kernel already reduced its records into compact R_m)
@@ -978,7 +981,10 @@ const double* stage_input(srtt_handle* h, const double* x, int on_device, int64_
 struct Timer {
   srtt_handle* h;
   int n = 0;
-  void mark() { record_event(h->ev[n++], h->stream); }
+  void mark() {
+    if (h->timing) record_event(h->ev[n], h->stream);
+    ++n;
+  }
   double between(int a, int b) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, h->ev[a], h->ev[b]));
@@ -1133,6 +1139,11 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   DeviceGuard guard(h->device);
   h->launches = 0;
   begin_call(h);
+  h->timing = rep != nullptr;  // restored to true when the call returns
+  struct TimingReset {
+    srtt_handle* h;
+    ~TimingReset() { h->timing = true; }
+  } timing_reset{h};
   Timer tm{h};
   tm.mark();  // 0
   const double* x = stage_input(h, x_in, x_on_device, N);
@@ -1173,7 +1184,8 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
       pkey += '|';
     }
     pkey += std::to_string(p) + "|" + ptr_key(x) + "|" + (out_on_device ? ptr_key(core_out) : "h") + "|" +
-            ptr_key(h->stream) + "|" + std::to_string(partitions) + "|" + std::to_string(h->cur);
+            ptr_key(h->stream) + "|" + std::to_string(partitions) + "|" + std::to_string(h->cur) +
+            (h->timing ? "|t" : "|n");
     auto pit = h->prepared.find(pkey);
     if (pit != h->prepared.end() && pit->second.ws == h->ws.p && pit->second.dp == h->pset().d.p &&
         pit->second.hp == h->pset().hst.p && h->graphs.count(pit->second.graph_key)) {
@@ -1278,7 +1290,8 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     key += "|" + std::to_string(dims[k]) + "," + std::to_string(ranks[k]) + "," + std::to_string(samples[k]) + "," +
            ptr_key(uptr[k]);
   key += "|" + std::to_string(p) + "|" + ptr_key(x) + "|" + ptr_key(d_core) + "|" + ptr_key(ws) + "|" + ptr_key(dp) +
-         "|" + ptr_key(hp) + "|" + ptr_key(h->stream) + "|" + std::to_string(blob.lay.off);
+         "|" + ptr_key(hp) + "|" + ptr_key(h->stream) + "|" + std::to_string(blob.lay.off) +
+         (h->timing ? "|t" : "|n");
   run_enqueue(h, key, [&] {
     CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
     tm.n = 2;
