@@ -1585,6 +1585,11 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   DeviceGuard guard(h->device);
   h->launches = 0;
   begin_call(h);
+  h->timing = rep != nullptr;  // restored to true when the call returns
+  struct TimingReset {
+    srtt_handle* h;
+    ~TimingReset() { h->timing = true; }
+  } timing_reset{h};
   Timer tm{h};
   tm.mark();  // 0
   const double* x = stage_input(h, x_in, x_on_device, N);
@@ -1715,7 +1720,8 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     key += "|" + std::to_string(ranks[i]) + "," + std::to_string(samples[i]) + "," + std::to_string(tr.left[i]) + "," +
            std::to_string(tr.modes[i].size());
   key += "|" + std::to_string(p) + "|" + ptr_key(x) + "|" + ptr_key(ws) + "|" + ptr_key(dp) + "|" + ptr_key(hp) + "|" +
-         ptr_key(h->stream) + "|" + std::to_string(blob.lay.off) + "|" + std::to_string(out_on_device);
+         ptr_key(h->stream) + "|" + std::to_string(blob.lay.off) + "|" + std::to_string(out_on_device) +
+         (h->timing ? "|t" : "|n");
   if (out_on_device) {
     for (int k = 0; k < d; ++k) key += "|" + ptr_key(leaf_out[k]);
     if (transfers_out)
