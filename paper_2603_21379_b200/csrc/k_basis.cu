@@ -494,9 +494,6 @@ __device__ void apply_reflectors_warps(const double* A, int lda, const double* t
                                        int ldy);
 __device__ void apply_cols_warps(const double* A, int lda, const double* tau, int m, int k, const double* V,
                                  int ldv, const int* perm, int q, double* Y, int ldy);
-__device__ void qr_cols_lane(const double* __restrict__ z, int m, int c, double* A, int lda, double* tau);
-__device__ void apply_cols_lane(const double* A, int lda, const double* tau, int m, int k, const double* V,
-                                int ldv, const int* perm, int q, double* Y, int ldy);
 
 // Top of the TSQR tree (or the whole basis for single-block targets).
 // JG > 0: warp-per-column QR and back-application over the CTA's warps
@@ -757,128 +754,10 @@ __device__ __forceinline__ double dot4(const double* a, const double* b, int lo,
   return (s0 + s1) + (s2 + s3);
 }
 
-// ---- lane-per-column Householder QR / back-application for one warp -----
-// For c <= 32: lane l owns column l of A (shared memory, odd leading
-// dimension, so the 32 lanes hit 32 different banks at the same row). A
-// reflector costs one warp reduction (column norm) and then every lane runs
-// its own dot product and update down the rows -- no shuffles, compact
-// loops (a single warp runs this code once, so instruction-cache footprint
-// matters more than unrolling). Rows move through registers in batches of
-// 8 so the shared-memory loads of a batch are in flight together. No column
-// pivoting.
-constexpr int kRowBatch = 8;
-
-// w = v_j + sum_{i > j} v[i] x[i]  (v[j] = 1 implied), x and v in shared memory.
-__device__ __forceinline__ double reflector_dot(const double* v, const double* x, int j, int m) {
-  double acc[kRowBatch];
-#pragma unroll
-  for (int u = 0; u < kRowBatch; ++u) acc[u] = 0.0;
-  int i = j + 1;
-  for (; i + kRowBatch <= m; i += kRowBatch) {
-    double vv[kRowBatch], xx[kRowBatch];
-#pragma unroll
-    for (int u = 0; u < kRowBatch; ++u) {
-      vv[u] = v[i + u];
-      xx[u] = x[i + u];
-    }
-#pragma unroll
-    for (int u = 0; u < kRowBatch; ++u) acc[u] = fma(vv[u], xx[u], acc[u]);
-  }
-  for (; i < m; ++i) acc[0] = fma(v[i], x[i], acc[0]);
-  double w = x[j];
-#pragma unroll
-  for (int u = 0; u < kRowBatch; ++u) w += acc[u];
-  return w;
-}
-
-// x[j] -= tw; x[i] -= tw v[i] for i > j.
-__device__ __forceinline__ void reflector_update(const double* v, double* x, int j, int m, double tw) {
-  x[j] -= tw;
-  int i = j + 1;
-  for (; i + kRowBatch <= m; i += kRowBatch) {
-    double vv[kRowBatch], xx[kRowBatch];
-#pragma unroll
-    for (int u = 0; u < kRowBatch; ++u) {
-      vv[u] = v[i + u];
-      xx[u] = x[i + u];
-    }
-#pragma unroll
-    for (int u = 0; u < kRowBatch; ++u) x[i + u] = fma(-tw, vv[u], xx[u]);
-  }
-  for (; i < m; ++i) x[i] = fma(-tw, v[i], x[i]);
-}
-
-__device__ void qr_cols_lane(const double* __restrict__ z, int m, int c, double* A, int lda, double* tau) {
-  const int lane = threadIdx.x & 31;
-  const int k = min(m, c);
-  for (int idx0 = 0; idx0 < m * c; idx0 += 32 * kRowBatch) {
-    double buf[kRowBatch];
-#pragma unroll
-    for (int u = 0; u < kRowBatch; ++u) {
-      const int idx = idx0 + 32 * u + lane;
-      buf[u] = idx < m * c ? __ldg(z + idx) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < kRowBatch; ++u) {
-      const int idx = idx0 + 32 * u + lane;
-      if (idx < m * c) A[(size_t)(idx / m) * lda + idx % m] = buf[u];
-    }
-  }
-  __syncwarp();
-  for (int j = 0; j < k; ++j) {
-    double* col = A + (size_t)j * lda;
-    double part = 0.0;
-    for (int i = j + 1 + lane; i < m; i += 32) part = fma(col[i], col[i], part);
-    const double ss = warp_sum(part);
-    const double alpha = col[j];
-    double tj = 0.0, scal = 0.0, beta = alpha;
-    if (ss != 0.0) {
-      const double nrm = sqrt(fma(alpha, alpha, ss));
-      beta = -copysign(nrm, alpha);
-      tj = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
-    }
-    if (tj != 0.0)
-      for (int i = j + 1 + lane; i < m; i += 32) col[i] *= scal;
-    __syncwarp();
-    if (tj != 0.0 && lane > j && lane < c) {  // lane l owns trailing column l
-      double* cl = A + (size_t)lane * lda;
-      reflector_update(col, cl, j, m, tj * reflector_dot(col, cl, j, m));
-    }
-    __syncwarp();
-    if (lane == 0) {
-      col[j] = beta;
-      tau[j] = tj;
-    }
-    __syncwarp();
-  }
-}
-
-// Y(:, 0:q) = Q [V(:, perm[0:q]); 0], q <= 32: lane `col` owns output
-// column col and applies the k reflectors in reverse order.
-__device__ void apply_cols_lane(const double* A, int lda, const double* tau, int m, int k, const double* V,
-                                int ldv, const int* perm, int q, double* Y, int ldy) {
-  const int lane = threadIdx.x & 31;
-  if (lane < q) {
-    double* y = Y + (size_t)lane * ldy;
-    const double* vc = V + (size_t)perm[lane] * ldv;
-    for (int i = 0; i < m; ++i) y[i] = i < k ? vc[i] : 0.0;
-    for (int j = k - 1; j >= 0; --j) {
-      const double tj = tau[j];
-      if (tj == 0.0) continue;
-      const double* v = A + (size_t)j * lda;
-      reflector_update(v, y, j, m, tj * reflector_dot(v, y, j, m));
-    }
-  }
-  __syncwarp();
-}
-
-// Variants (compile-time paths, so each instantiation gets its own register
-// budget): QRR = 1: lane-per-column QR / back-application (c <= 32), 0:
-// shared-memory QRCP with 4-lane column groups,
-// (JG, JE) = register Jacobi lane-group width / values per lane (JG = 0:
-// shared-memory Jacobi).
-template <int QRR, int JG, int JE>
+// One warp per target for wide sketches (32 < c <= 64, single block):
+// shared-memory QRCP with 4-lane column groups (pivoting preconditions the
+// Jacobi), 4-lane shared-memory Jacobi, warp back-application. Narrower
+// sketches take basis_cta_kernel.
 __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __restrict__ targets,
                                                          const int* __restrict__ list) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -892,11 +771,7 @@ __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __re
   SmallSmem s = carve_small(smem_raw, m, c, r);
   PROF_MARK(0);
   const double* z = T.lv[0].a;
-  // register-resident QR / back-application for small sketches
-  if constexpr (QRR > 0) {
-    qr_cols_lane(z, m, c, s.A, s.lda, s.tau);
-    PROF_MARK(1);
-  } else {
+  {
     for (int idx = lane; idx < m * c; idx += 32) {
       const int i = idx % m, j = idx / m;
       s.A[(size_t)j * s.lda + i] = z[idx];
@@ -1005,16 +880,10 @@ __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __re
     s.V[(size_t)j * s.ldv + i] = (i == j) ? 1.0 : 0.0;
   }
   __syncwarp();
-  // ---- one-sided Jacobi on rows: register-resident for k <= 32 (4-lane
-  // groups up to 16 rows, 2-lane groups up to 32), shared-memory otherwise
-  int sweeps;
-  if constexpr (JG > 0) {
-    sweeps = jacobi_rows_reg<JG, JE>(s.B, s.ldb, k, c, s.V, s.ldv);
-  } else {
-    build_pairs(pairs, (k + 1) & ~1);
-    __syncwarp();
-    sweeps = jacobi_rows_g4(s.B, s.ldb, k, c, s.V, s.ldv, pairs);
-  }
+  // ---- one-sided Jacobi on the rows of R (shared memory, 4-lane groups)
+  build_pairs(pairs, (k + 1) & ~1);
+  __syncwarp();
+  const int sweeps = jacobi_rows_g4(s.B, s.ldb, k, c, s.V, s.ldv, pairs);
   PROF_MARK(3);
   // ---- singular values, ordering, rank decision
   for (int i = lane; i < k; i += 32) {
@@ -1042,9 +911,7 @@ __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __re
     for (int i = lane; i < k; i += 32) T.sv[i] = s.sig[s.perm[i]];
   PROF_MARK(4);
   // ---- Y = Q [V(:, perm[:q]); 0]
-  if constexpr (QRR > 0) {
-    apply_cols_lane(s.A, s.lda, s.tau, m, k, s.V, s.ldv, s.perm, q, s.Y, s.lda);
-  } else {
+  {
     {
       const int grp = lane >> 2, gl = lane & 3;
       for (int cb = 0; cb < q; cb += 8) {
@@ -1124,13 +991,13 @@ __global__ void __launch_bounds__(32) basis_small_kernel(const BasisTarget* __re
 }
 
 // ---- CTA-wide small basis (c <= 32) ---------------------------------------
-// Same algorithm as basis_small_kernel<1, JG, JE> (Householder QR, register
-// Jacobi on the rows of R, back-application, Gaussian padding), but the QR
-// and the back-application are spread over the CTA's warps: warp w owns the
-// columns l = w (mod W); a reflector step is one warp reduction per owned
-// column plus one CTA barrier, and the owner of column j+1 builds reflector
-// j+1 right after updating that column (look-ahead), so a step costs about
-// two warp reductions of latency instead of a serial row loop per lane.
+// Householder QR, register-resident one-sided Jacobi on the rows of R (warp
+// 0), back-application and Gaussian padding. The QR and the
+// back-application are spread over the CTA's warps: warp w owns the columns
+// l = w (mod W); a reflector step is one warp reduction per owned column
+// plus one CTA barrier, and the owner of column j+1 builds reflector j+1
+// right after updating that column (look-ahead), so a step costs about two
+// warp reductions of latency instead of a serial row loop per lane.
 // columns per warp: OWN = 4 covers c <= 32 with 8 warps, OWN = 8 c <= 64
 
 // reflector j from column j (called by the owning warp): v below the
@@ -1368,8 +1235,8 @@ cudaError_t srtt_launch_basis_small(int variant, const BasisTarget* d_targets, c
       basis_cta_kernel<2, 12><<<n, kThreads, smem, stream>>>(d_targets, d_list);
       break;
     default:
-      SRTT_ENSURE_SMEM((basis_small_kernel<0, 0, 0>), smem);
-      basis_small_kernel<0, 0, 0><<<n, 32, smem, stream>>>(d_targets, d_list);
+      SRTT_ENSURE_SMEM(basis_small_kernel, smem);
+      basis_small_kernel<<<n, 32, smem, stream>>>(d_targets, d_list);
       break;
   }
   return cudaGetLastError();
