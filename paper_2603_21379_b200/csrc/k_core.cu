@@ -27,6 +27,11 @@
 // warp-private acc3 (r0 r1 r2) with U2[i2, :]. At the end of an item the
 // 8 warp partials are summed in a fixed order into the item's output slot,
 // so the core is bitwise reproducible run to run. X is read exactly once.
+//
+// core_flat_kernel (one row block, n0 <= 256) drops the items: every warp
+// streams an equal contiguous range of column tiles and its group records
+// are reduced in-kernel by the warp that completes each group (see below);
+// for short columns one unswizzled TMA box holds whole columns.
 #include <cuda.h>
 
 #include <algorithm>
