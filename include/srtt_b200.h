@@ -68,10 +68,24 @@ typedef struct srtt_options {
   int32_t reserved[6];
 } srtt_options;
 
-/* ExecPolicy (parallel.hpp:23-28). `workers` and `slice_mode` are accepted
- * for API parity (the GPU runs every mode / node concurrently and the core
- * pass over all SMs); index_partitions and emulate_serial_root keep their
- * reference meaning. slice_mode = -1 means auto. */
+/* ExecPolicy (parallel.hpp:23-28). The GPU schedule does not depend on
+ * `workers` / `slice_mode` (every mode / node runs concurrently, the core
+ * pass uses all SMs; the reference's results are bitwise independent of
+ * them too, parallel.hpp:18-21), but both are VALIDATED as the reference
+ * does, with its messages (SRTT_ERR_INVALID_ARGUMENT):
+ *   workers < 1      -> "run_independent_jobs: workers must be >= 1" (Tucker,
+ *                       parallel.hpp:88) / "tree_schedule: ..." (H-Tucker,
+ *                       parallel.hpp:206);
+ *   Tucker only (the reference then assembles the core with sliced_core):
+ *   slice_mode = -1 (auto) resolves through pick_slice_mode
+ *   (parallel.hpp:331-348; "pick_slice_mode: no mode can host N slices"),
+ *   an explicit mode outside [0, d) -> "sliced_core: slice mode out of
+ *   range", workers > extent of the slice mode -> "sliced_core: more workers
+ *   than slices along the slicing mode" (parallel.hpp:369-373). The
+ *   resolved slice mode is returned in srtt_report.slice_mode.
+ * index_partitions selects sample_indices_partitioned (sampling.hpp:41-66,
+ * bit-exact). emulate_serial_root makes the H-Tucker root pass wait for
+ * every basis job (parallel.hpp:168-170); results are unchanged. */
 typedef struct srtt_exec_policy {
   int64_t workers;
   int64_t slice_mode;
@@ -98,6 +112,14 @@ typedef struct srtt_report {
    * streaming kernel only, [3] K4 transfers */
   double kernel_seconds[4];
   int64_t launches; /* kernels launched by the call */
+  int64_t slice_mode; /* Tucker with a policy: the sliced_core slice mode the
+                         reference would use (-1: no policy / H-Tucker) */
+  /* optional, H-Tucker: node_bases[id] (id >= 1, non-NULL entries only)
+   * receives the basis U_S of node id that the decomposition used
+   * (n_S x r_S column-major, host or device memory as out_on_device). The
+   * reference keeps the internal node bases private (htucker.hpp:244); they
+   * are exported for parity checks of the internal nodes. */
+  double* const* node_bases;
 } srtt_report;
 
 /* Dimension tree (dimension_tree.hpp:9-17), heap/BFS node order, root = 0.
@@ -135,6 +157,10 @@ int srtt_sample_indices(uint64_t seed, uint64_t stream_id, int64_t m, int64_t s,
  * draws, normal index t0 on (the device generator, for parity tests). */
 int srtt_stream_normals(srtt_handle* h, uint64_t seed, uint64_t stream_id, uint64_t draw_offset,
                         uint64_t t0, int64_t n, double* out);
+/* pick_slice_mode (parallel.hpp:331-348): the mode whose extent needs the
+ * least padding to a multiple of `workers`; INVALID_ARGUMENT when no mode
+ * has at least `workers` slices. */
+int srtt_pick_slice_mode(int32_t d, const int64_t* dims, int64_t workers, int64_t* mode_out);
 /* DimensionTree::balanced (dimension_tree.hpp:36-64). Arrays sized
  * 2*order-1 (mode_begin: 2*order, modes: order*(depth+1) <= order*order). */
 int srtt_tree_balanced(int32_t order, int32_t* num_nodes, int32_t* mode_begin, int32_t* modes,

@@ -313,6 +313,15 @@ HTuckerDecomposition<Scalar> sub_r_rtl_ht(const DenseTensor<Scalar>& x, const Di
   return out;
 }
 
+/// pick_slice_mode (parallel.hpp:331-348).
+inline Index pick_slice_mode(const Shape& shape, Index workers) {
+  std::vector<std::int64_t> dims;
+  for (Index k = 0; k < shape.order(); ++k) dims.push_back(shape.dim(k));
+  std::int64_t m = -1;
+  detail::check(srtt_pick_slice_mode(static_cast<std::int32_t>(dims.size()), dims.data(), workers, &m));
+  return m;
+}
+
 inline NodeRanks uniform_node_ranks(const DimensionTree& tree, Index rank) {  // dimension_tree.hpp:159-163
   NodeRanks out(static_cast<std::size_t>(tree.num_nodes()), rank);
   out[0] = 1;

@@ -134,25 +134,28 @@ def as_tensor(data: np.ndarray, dims) -> np.ndarray:
     return np.reshape(np.asarray(data), tuple(int(n) for n in dims), order="F")
 
 
-def extract_fibers(x: np.ndarray, mode: int, cols) -> np.ndarray:
-    """unfolding.hpp:32-52: column j = fiber with base (c % g) + (c / g)*g*n_k,
-    stride g.  Pure copy (bitwise equal to the unfolding)."""
-    dims = x.shape
-    nk = dims[mode]
+def fiber_offsets(dims, mode: int, cols) -> np.ndarray:
+    """unfolding.hpp:32-52: flat offsets (n_k x s) of the sampled mode-k
+    fibres -- column j has base (c % g) + (c / g)*g*n_k and stride g."""
+    nk = int(dims[mode])
     g = strides_of(dims)[mode]
-    total = x.size // nk
+    total = int(np.prod(dims)) // nk
     cols = np.asarray(cols, np.int64)
     if np.any(cols < 0) or np.any(cols >= total):
         raise IndexError("extract_fibers: column index out of range")
     base = (cols % g) + (cols // g) * g * nk
-    offs = base[None, :] + np.arange(nk, dtype=np.int64)[:, None] * g
-    return flat(x)[offs]
+    return base[None, :] + np.arange(nk, dtype=np.int64)[:, None] * g
 
 
-def extract_group_fibers(x: np.ndarray, modes, cols) -> np.ndarray:
-    """unfolding.hpp:57-111: rows ordered by the linear map over S ascending
-    (first fastest), columns decoded over the complement modes ascending."""
-    dims = x.shape
+def extract_fibers(x: np.ndarray, mode: int, cols) -> np.ndarray:
+    """unfolding.hpp:32-52.  Pure copy (bitwise equal to the unfolding)."""
+    return flat(x)[fiber_offsets(x.shape, mode, cols)]
+
+
+def group_fiber_offsets(dims, modes, cols) -> np.ndarray:
+    """unfolding.hpp:57-111: flat offsets (n_S x w) of the sampled node
+    fibres; rows follow the linear map over S ascending (first fastest),
+    columns are decoded over the complement modes ascending."""
     d = len(dims)
     modes = sorted(int(m) for m in modes)
     if len(modes) >= d:
@@ -174,7 +177,12 @@ def extract_group_fibers(x: np.ndarray, modes, cols) -> np.ndarray:
     for k in modes:
         roff += (r % dims[k]) * st[k]
         r //= dims[k]
-    return flat(x)[roff[:, None] + base[None, :]]
+    return roff[:, None] + base[None, :]
+
+
+def extract_group_fibers(x: np.ndarray, modes, cols) -> np.ndarray:
+    """unfolding.hpp:57-111 (gather through group_fiber_offsets)."""
+    return flat(x)[group_fiber_offsets(x.shape, modes, cols)]
 
 
 def unfold(x: np.ndarray, mode: int) -> np.ndarray:
@@ -182,11 +190,28 @@ def unfold(x: np.ndarray, mode: int) -> np.ndarray:
 
 
 def ttm(x: np.ndarray, u: np.ndarray, mode: int) -> np.ndarray:
-    """tensor.hpp:255-289: contracts U (m x n_mode) with the mode fibers."""
-    if u.shape[1] != x.shape[mode]:
+    """tensor.hpp:255-289: contracts U (m x n_mode) with the mode fibers, as
+    the reference does it on the flat first-index-fastest data: X viewed as
+    g x n x post (g = prod n_<k); mode 0 is ONE GEMM (m x n)(n x post), the
+    last mode one GEMM (g x n)(n x m), middle modes one GEMM per trailing
+    block (post of them).  No copy of X when it is Fortran-contiguous."""
+    dims = x.shape
+    if u.shape[1] != dims[mode]:
         raise ValueError("ttm: matrix/mode extent mismatch")
-    y = np.tensordot(u, x, axes=([1], [mode]))
-    return np.moveaxis(y, 0, mode)
+    n = int(dims[mode])
+    g = int(np.prod(dims[:mode], dtype=np.int64))
+    post = int(np.prod(dims[mode + 1:], dtype=np.int64))
+    m = u.shape[0]
+    xf = np.ravel(x, order="F")
+    if g == 1:
+        out = xf.reshape(post, n) @ u.T           # C (post, m) == F (m, post)
+    elif post == 1:
+        out = u @ xf.reshape(n, g)                # C (m, g) == F (g, m)
+    else:
+        out = np.matmul(u, xf.reshape(post, n, g))  # C (post, m, g) == F (g, m, post)
+    nd = list(dims)
+    nd[mode] = m
+    return np.reshape(np.ravel(out), nd, order="F")
 
 
 def multi_ttm(x, factors):
@@ -399,10 +424,16 @@ def pick_slice_mode(dims, workers):
 
 
 def sliced_core(x, factors, policy: ExecPolicy):
-    """parallel.hpp:355-445: reduce contiguous slabs along the slice mode over
-    every other mode, then the final TTM along the slice mode."""
+    """parallel.hpp:355-445: `workers` jobs reduce contiguous slabs of slices
+    along the slice mode (bounds of :400-404), ONE SLICE AT A TIME over every
+    other mode in mode order (reduce_slice, :386-395) -- so the bits do not
+    depend on the worker count --, run concurrently on a thread pool
+    (run_independent_jobs, :87-129); the coordinator gathers the reduced
+    slabs and applies the final TTM along the slice mode (:424-441)."""
     dims = x.shape
     d = len(dims)
+    if len(factors) != d:
+        raise ValueError("sliced_core: need one factor per mode")
     sm = policy.slice_mode if policy.slice_mode is not None else pick_slice_mode(dims, policy.workers)
     if not 0 <= sm < d:
         raise ValueError("sliced_core: slice mode out of range")
@@ -410,17 +441,67 @@ def sliced_core(x, factors, policy: ExecPolicy):
         raise ValueError("sliced_core: more workers than slices along the slicing mode")
     nworkers = min(policy.workers, dims[sm])
     n = dims[sm]
-    slabs = []
-    for w in range(nworkers):
+    rdims = [n if k == sm else factors[k].shape[1] for k in range(d)]
+    reduced = np.zeros(rdims, order="F")
+    idx = [slice(None)] * d
+
+    def reduce_slab(w):
         lo = w * (n // nworkers) + min(w, n % nworkers)
         hi = lo + n // nworkers + (1 if w < n % nworkers else 0)
-        sl = np.take(x, np.arange(lo, hi), axis=sm)
-        for k in range(d):
-            if k != sm:
-                sl = ttm(sl, factors[k].T, k)
-        slabs.append(sl)
-    reduced = np.concatenate(slabs, axis=sm)
+        for i in range(lo, hi):
+            sl = np.take(x, [i], axis=sm)
+            for k in range(d):
+                if k != sm:
+                    sl = ttm(sl, factors[k].T, k)
+            j = list(idx)
+            j[sm] = slice(i, i + 1)
+            reduced[tuple(j)] = sl
+
+    if nworkers > 1:
+        with ThreadPoolExecutor(nworkers) as ex:
+            list(ex.map(reduce_slab, range(nworkers)))
+    else:
+        reduce_slab(0)
     return ttm(reduced, factors[sm].T, sm)
+
+
+def sliced_core_streamed(read_slab, dims, factors, slab=128):
+    """sliced_core's slab algebra (parallel.hpp:355-445) with the LAST mode as
+    the slice mode, for tensors that do not fit the host: ``read_slab(lo, hi)``
+    returns X[..., lo:hi) (an nd-array of dims[:-1] + [hi - lo]); each slab is
+    reduced over modes 0..d-2 in mode order, the reduced slabs are gathered
+    and the final TTM along mode d-1 is applied."""
+    d = len(dims)
+    n = int(dims[-1])
+    reduced = np.zeros([f.shape[1] for f in factors[:-1]] + [n], order="F")
+    for lo in range(0, n, slab):
+        hi = min(n, lo + slab)
+        sl = read_slab(lo, hi)
+        for k in range(d - 1):
+            sl = ttm(sl, factors[k].T, k)
+        reduced[..., lo:hi] = sl
+    return ttm(reduced, factors[-1].T, d - 1)
+
+
+def rel_error_streamed(read_slab, dims, core, factors, slab=128):
+    """rel_error(x, reconstruct(t)) (tensor.hpp:241-249, tucker.hpp:18-28)
+    slab by slab along the last mode: X-hat[..., lo:hi) =
+    (G x_0 U_0 ... x_{d-2} U_{d-2}) x_{d-1} U_{d-1}[lo:hi, :]."""
+    d = len(dims)
+    part = core
+    for k in range(d - 1):
+        part = ttm(part, factors[k], k)
+    num = den = 0.0
+    n = int(dims[-1])
+    for lo in range(0, n, slab):
+        hi = min(n, lo + slab)
+        xs = flat(read_slab(lo, hi))
+        xh = flat(ttm(part, factors[-1][lo:hi, :], d - 1))
+        num += float(np.dot(xs - xh, xs - xh))
+        den += float(np.dot(xs, xs))
+    if den == 0.0:
+        raise ValueError("rel_error: reference tensor has zero norm")
+    return math.sqrt(num) / math.sqrt(den)
 
 
 # --------------------------------------------------------------------------

@@ -265,14 +265,20 @@ struct srtt_handle {
   struct ParamSet {
     DevBuf d;
     HostBuf hst;
+    // per-target info (achieved rank, nrank, sweeps) + status flags: device
+    // memory written by the kernels of the call that owns this set, cleared
+    // in-stream at the start of that call and copied to `hinfo_buf` at its
+    // end (never touched by the host while a call may still run on it)
+    DevBuf info;
+    HostBuf hinfo_buf;
     cudaEvent_t done = nullptr;
     bool recorded = false;
+    int32_t* dinfo() { return reinterpret_cast<int32_t*>(info.p); }
+    int32_t* hinfo() { return reinterpret_cast<int32_t*>(hinfo_buf.p); }
   };
   ParamSet psets[2];
   int cur = 0;
   ParamSet& pset() { return psets[cur]; }
-  int32_t* hinfo = nullptr;   // mapped pinned: per-target info + flags, written by kernels
-  int32_t* dinfo = nullptr;   // device alias of hinfo
   DevBuf ones;
   int64_t launches = 0;
   // timing events (stage marks, per-kernel pairs) are recorded only for
@@ -1069,6 +1075,14 @@ double kernel_pair(srtt_handle* h, int i) {
   return ms * 1e-3;
 }
 
+// The device Gaussian generator is random-access (normal t = Box-Muller pair
+// t/2); the reference's stream retries a pair whose u1 == 0 (rng.hpp:71),
+// which shifts every later draw. The event has probability 2^-53 per pair;
+// when a kernel meets it the call reports it instead of failing silently.
+const char* const kU1ZeroWarning =
+    "Box-Muller u1 == 0 draw met (p = 2^-53): the reference would retry it and shift later Gaussian draws, "
+    "so Omega differs from the reference stream after that draw";
+
 // ==================================================================================
 // Sub-R-HOSVD
 // ==================================================================================
@@ -1079,7 +1093,7 @@ void finish_tucker(srtt_handle* h, Timer& tm, int d, const std::vector<int64_t>&
                    srtt_report* rep) {
   CK(cudaStreamSynchronize(h->stream));
   CK(cudaGetLastError());
-  const int32_t* hi = h->hinfo;
+  const int32_t* hi = h->pset().hinfo();
   for (int k = 0; k < d; ++k) {
     const int q = hi[4 * k];
     if (rep && rep->achieved_ranks) rep->achieved_ranks[k] = q;
@@ -1087,6 +1101,7 @@ void finish_tucker(srtt_handle* h, Timer& tm, int d, const std::vector<int64_t>&
       warnings.push_back("mode " + std::to_string(k) + ": sketch revealed rank " + std::to_string(q) +
                          " < target " + std::to_string(ranks[k]) + "; basis padded");
   }
+  if (hi[4 * d] & 1) warnings.push_back(kU1ZeroWarning);
   if (rep) {
     if (rep->sample_counts)
       for (int k = 0; k < d; ++k) rep->sample_counts[k] = samples[k];
@@ -1108,6 +1123,51 @@ void finish_tucker(srtt_handle* h, Timer& tm, int d, const std::vector<int64_t>&
     rep->launches = h->launches;
     write_warnings(rep, warnings);
   }
+}
+
+// ExecPolicy (parallel.hpp:23-28) semantics on the GPU path. The GPU runs
+// every mode / node concurrently and the core pass over all SMs whatever
+// `workers` says (the reference's results are bitwise independent of it,
+// parallel.hpp:18-21), but the policy is validated exactly as the
+// reference's engine does it, with the same messages:
+//   run_independent_jobs / tree_schedule: workers >= 1 (parallel.hpp:88, 206)
+//   sliced_core: slice mode given -> in range, else pick_slice_mode
+//   (parallel.hpp:331-348); workers <= slices along it (parallel.hpp:362-373).
+int64_t pick_slice_mode_impl(const std::vector<int64_t>& dims, int64_t workers) {
+  int64_t best = -1, best_score = INT64_MAX;
+  for (size_t k = 0; k < dims.size(); ++k) {
+    const int64_t nk = dims[k];
+    if (nk < workers) continue;
+    const int64_t rem = nk % workers;
+    const int64_t score = rem == 0 ? 0 : workers - rem;
+    if (score < best_score) {
+      best_score = score;
+      best = (int64_t)k;
+    }
+  }
+  if (best < 0) invalid("pick_slice_mode: no mode can host " + std::to_string(workers) + " slices");
+  return best;
+}
+
+// Limit of the streaming core engine (DMMA tile templates: 1, 2 or 4 rank
+// tiles of 8 in modes 0 and 1), checked before any work is issued.
+void check_core_ranks(int d, const int64_t* ranks, const char* who) {
+  if (d >= 2 && (ranks[0] > 32 || ranks[1] > 32))
+    invalid(std::string(who) + ": ranks above 32 in the first two core modes are not supported by the B200 "
+            "core kernel");
+}
+
+void check_workers(const srtt_exec_policy* exec, const char* who) {
+  if (exec && exec->workers < 1) invalid(std::string(who) + ": workers must be >= 1");
+}
+
+// sliced_core's slice-mode resolution (parallel.hpp:369-373); -1 = auto.
+int64_t resolve_slice_mode(const std::vector<int64_t>& dims, const srtt_exec_policy* exec) {
+  const int64_t d = (int64_t)dims.size();
+  const int64_t sm = exec->slice_mode == -1 ? pick_slice_mode_impl(dims, exec->workers) : exec->slice_mode;
+  if (sm < 0 || sm >= d) invalid("sliced_core: slice mode out of range");
+  if (exec->workers > dims[(size_t)sm]) invalid("sliced_core: more workers than slices along the slicing mode");
+  return sm;
 }
 
 void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d, const int64_t* dims_p,
@@ -1132,9 +1192,11 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   for (int k = 0; k < d; ++k)
     if (ranks[k] + p > SRTT_MAX_SKETCH_COLS)
       invalid("sub_r_hosvd: rank + oversampling above 64 is not supported by the B200 basis kernel");
+  check_core_ranks(d, ranks.data(), "sub_r_hosvd");
   std::vector<std::string> warnings;
   if (p < 4) warnings.push_back("oversampling below the recommended minimum of 4");
   const int64_t partitions = exec ? exec->index_partitions : 1;
+  check_workers(exec, "run_independent_jobs");  // parallel_factors (tucker.hpp:216)
 
   DeviceGuard guard(h->device);
   h->launches = 0;
@@ -1145,9 +1207,6 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     ~TimingReset() { h->timing = true; }
   } timing_reset{h};
   Timer tm{h};
-  tm.mark();  // 0
-  const double* x = stage_input(h, x_in, x_on_device, N);
-  tm.mark();  // 1 (after H2D)
 
   // --- host sampling: one stream per mode (tucker.hpp:145), JobError(k) on failure
   const double ts0 = now_s();
@@ -1167,6 +1226,14 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     state0[k] = srtt_host::stream_state0(seed, (uint64_t)k);
   }
   const double t_sampling = now_s() - ts0;
+  // with a policy the reference assembles the core through sliced_core
+  // (tucker.hpp:232-233), whose slice-mode checks come after the factor jobs
+  const int64_t slice_mode = exec ? resolve_slice_mode(dims, exec) : -1;
+  if (rep) rep->slice_mode = slice_mode;
+
+  tm.mark();  // 0
+  const double* x = stage_input(h, x_in, x_on_device, N);
+  tm.mark();  // 1 (after H2D)
 
   // --- fast path: a prepared call with the same signature only needs the
   // seed-dependent blob fields patched and its CUDA graph replayed
@@ -1202,7 +1269,6 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
         btp->state0 = state0[k];
         btp->draw_offset = draws[k];
       }
-      std::memset(h->hinfo, 0, sizeof(int32_t) * 4 * (d + 1));
       tm.n = 2;
       run_enqueue(h, pr.graph_key, [] { fail(SRTT_ERR_INTERNAL, "prepared graph missing"); });
       tm.n = 6;
@@ -1251,9 +1317,10 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
 
   // --- parameter blob (indices, target descriptors, basis lists): one H2D copy
   if (4 * (d + 1) > kInfoInts) invalid("sub_r_hosvd: too many modes");
-  int32_t* hi = h->hinfo;
-  std::memset(hi, 0, sizeof(int32_t) * 4 * (d + 1));
-  int32_t* d_flags = h->dinfo + 4 * d;
+  int32_t* const dinfo = h->pset().dinfo();
+  int32_t* const hinfo = h->pset().hinfo();
+  const size_t info_bytes = sizeof(int32_t) * 4 * (d + 1);
+  int32_t* d_flags = dinfo + 4 * d;
   Blob blob;
   std::vector<size_t> off_cols(d);
   for (int k = 0; k < d; ++k) off_cols[k] = blob.add(cols[k].data(), sizeof(int64_t) * cols[k].size());
@@ -1274,7 +1341,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     sk[k].cta_begin = ctas;
     sk[k].flags = d_flags;
     ctas += (sk[k].rows + sk[k].row_tile - 1) / sk[k].row_tile;
-    bt[k] = fill_basis(bp[k], bb[k], ws, sk[k].z, uptr[k], state0[k], draws[k], samples[k] * c, h->dinfo + 4 * k);
+    bt[k] = fill_basis(bp[k], bb[k], ws, sk[k].z, uptr[k], state0[k], draws[k], samples[k] * c, dinfo + 4 * k);
   }
   assign_basis_ctas(bt);
   const BasisLists lists = make_basis_lists(bt, blob);
@@ -1294,6 +1361,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
          (h->timing ? "|t" : "|n");
   run_enqueue(h, key, [&] {
     CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemsetAsync(dinfo, 0, info_bytes, h->stream));
     tm.n = 2;
     tm.mark();  // 2
     // --- K1: grouped gather + sketch over all modes
@@ -1323,6 +1391,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
       h->launches++;
     }
     tm.mark();  // 5
+    CK(cudaMemcpyAsync(hinfo, dinfo, info_bytes, cudaMemcpyDeviceToHost, h->stream));
   });
   tm.n = 6;
   // --- outputs (host destinations only; device outputs were written in place)
@@ -1380,8 +1449,11 @@ int srtt_create(const srtt_options* opts, srtt_handle** out) {
     h->stream = h->own_stream;
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
     for (auto& e : h->kev) CK(cudaEventCreate(&e));
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->hinfo), kInfoInts * sizeof(int32_t), cudaHostAllocMapped));
-    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dinfo), h->hinfo, 0));
+    for (auto& ps : h->psets) {
+      ps.info.ensure(kInfoInts * sizeof(int32_t));
+      ps.hinfo_buf.ensure(kInfoInts * sizeof(int32_t));
+      std::memset(ps.hinfo_buf.p, 0, kInfoInts * sizeof(int32_t));
+    }
     h->ones.ensure(sizeof(double));
     const double one = 1.0;
     CK(cudaMemcpy(h->ones.p, &one, sizeof(double), cudaMemcpyHostToDevice));
@@ -1401,7 +1473,6 @@ int srtt_destroy(srtt_handle* h) {
       cudaStreamDestroy(h->side);
       for (auto& e : h->fj) cudaEventDestroy(e);
       for (auto& ps : h->psets) cudaEventDestroy(ps.done);
-      if (h->hinfo) cudaFreeHost(h->hinfo);
     }
     delete h;
   });
@@ -1427,6 +1498,14 @@ int srtt_sample_indices(uint64_t seed, uint64_t stream_id, int64_t m, int64_t s,
       srtt_host::sample_indices(m, s, rng, out);
     std::memcpy(idx_out, out.data(), sizeof(int64_t) * out.size());
     if (draws_out) *draws_out = rng.draws;
+  });
+}
+
+int srtt_pick_slice_mode(int32_t d, const int64_t* dims, int64_t workers, int64_t* mode_out) {
+  return guarded([&] {
+    if (d < 1 || !dims) invalid("pick_slice_mode: empty shape");
+    const int64_t m = pick_slice_mode_impl(std::vector<int64_t>(dims, dims + d), workers);
+    if (mode_out) *mode_out = m;
   });
 }
 
@@ -1578,9 +1657,15 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   for (int i = 1; i < nn; ++i)
     if (ranks[i] + p > SRTT_MAX_SKETCH_COLS)
       invalid("sub_r_rtl_ht: rank + oversampling above 64 is not supported by the B200 basis kernel");
+  {
+    const int64_t rr[2] = {ranks[tr.left[0]], ranks[tr.right[0]]};
+    check_core_ranks(2, rr, "sub_r_rtl_ht");
+  }
   std::vector<std::string> warnings;
   if (p < 4) warnings.push_back("oversampling below the recommended minimum of 4");
   const int64_t partitions = exec ? exec->index_partitions : 1;
+  check_workers(exec, "tree_schedule");  // parallel.hpp:206
+  const bool serial_root = exec && exec->emulate_serial_root;
 
   DeviceGuard guard(h->device);
   h->launches = 0;
@@ -1594,6 +1679,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   tm.mark();  // 0
   const double* x = stage_input(h, x_in, x_on_device, N);
   tm.mark();  // 1
+  if (rep) rep->slice_mode = -1;
 
   const int nt = nn - 1;  // one basis target per non-root node (ids 1..nn-1)
   const double ts0 = now_s();
@@ -1635,9 +1721,10 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   }
   const size_t off_pad = L.take(sizeof(double) * max_n * nt);
   if (4 * (nt + 1) > kInfoInts) invalid("sub_r_rtl_ht: too many tree nodes");
-  int32_t* hi = h->hinfo;
-  std::memset(hi, 0, sizeof(int32_t) * 4 * (nt + 1));
-  int32_t* d_flags = h->dinfo + 4 * nt;
+  int32_t* const dinfo = h->pset().dinfo();
+  const int32_t* hi = h->pset().hinfo();
+  const size_t info_bytes = sizeof(int32_t) * 4 * (nt + 1);
+  int32_t* d_flags = dinfo + 4 * nt;
   // transfers of internal non-root nodes, and the root
   std::vector<int> internal;
   for (int i = 1; i < nn; ++i)
@@ -1683,7 +1770,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     sk[t].flags = d_flags;
     ctas += (sk[t].rows + sk[t].row_tile - 1) / sk[t].row_tile;
     bt[t] = fill_basis(bp[t], bb[t], ws, sk[t].z, ubasis(id), state0[t], draws[t], samples[id] * c,
-                       h->dinfo + 4 * t);
+                       dinfo + 4 * t);
   }
   assign_basis_ctas(bt);
   const BasisLists lists = make_basis_lists(bt, blob);
@@ -1721,7 +1808,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
            std::to_string(tr.modes[i].size());
   key += "|" + std::to_string(p) + "|" + ptr_key(x) + "|" + ptr_key(ws) + "|" + ptr_key(dp) + "|" + ptr_key(hp) + "|" +
          ptr_key(h->stream) + "|" + std::to_string(blob.lay.off) + "|" + std::to_string(out_on_device) +
-         (h->timing ? "|t" : "|n");
+         (serial_root ? "|s" : "|p") + (h->timing ? "|t" : "|n");
   if (out_on_device) {
     for (int k = 0; k < d; ++k) key += "|" + ptr_key(leaf_out[k]);
     if (transfers_out)
@@ -1732,12 +1819,15 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   // Small-node bases and the transfer tensors run on a side stream and
   // overlap the root pass, which only needs the root children's bases
   // (htucker.hpp:203-209: the root waits only for nodes 1 and 2).
-  bool root_needs_small = false;
+  // emulate_serial_root: the root also waits for every basis job
+  // (parallel.hpp:168-170), i.e. for the side stream's small bases too
+  bool root_needs_small = serial_root;
   for (int i : lists.small)
     if (i + 1 == tr.left[0] || i + 1 == tr.right[0]) root_needs_small = true;
   run_enqueue(h, key, [&] {
     tm.n = 2;
     CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemsetAsync(dinfo, 0, info_bytes, h->stream));
     tm.mark();  // 2
     CK(srtt_launch_sketch(reinterpret_cast<const SketchTarget*>(dp + off_sk), nt, ctas, cmax, h->stream));
     h->launches++;
@@ -1766,6 +1856,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     // join
     CK(cudaStreamWaitEvent(h->stream, h->fj[3], 0));
     tm.mark();  // 6
+    CK(cudaMemcpyAsync(const_cast<int32_t*>(hi), dinfo, info_bytes, cudaMemcpyDeviceToHost, h->stream));
   });
   tm.n = 7;
   if (!out_on_device) {
@@ -1782,6 +1873,10 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
       if (transfers_out[0]) copy_out(h, transfers_out[0], d_root, sizeof(double) * rl0 * rr0, 0);
     }
   }
+  if (rep && rep->node_bases)
+    for (int i = 1; i < nn; ++i)
+      if (rep->node_bases[i])
+        copy_out(h, rep->node_bases[i], ubasis(i), sizeof(double) * node_rows(i) * ranks[i], out_on_device);
   tm.mark();  // 7
   // device outputs and no report: stream-ordered, return without waiting
   // (the next call's host work overlaps this one's kernels)
@@ -1799,6 +1894,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
       warnings.push_back("node " + std::to_string(id) + ": sketch revealed rank " + std::to_string(q) +
                          " < target; basis padded");
   }
+  if (hi[4 * nt] & 1) warnings.push_back(kU1ZeroWarning);
   if (rep) {
     if (rep->achieved_ranks) rep->achieved_ranks[0] = 1;
     if (rep->sample_counts)

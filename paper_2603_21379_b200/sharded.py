@@ -59,8 +59,19 @@ class GpuShardPhases:
         lib.srtt_shard_core.argtypes = [vp, vp, i32, i32, vp, i64, i64, vp, vp, i32, vp, i32]
         self.lib = lib
 
+    def _bind(self):
+        """Run every phase on torch's CURRENT stream: the collectives between
+        the phases (torch.distributed / NCCL) and the torch ops that produce
+        x_local are ordered on that stream, so a phase bound to the handle's
+        own non-blocking stream could read sketches that are not reduced yet."""
+        import torch
+
+        self.h.set_stream(torch.cuda.current_stream().cuda_stream)
+
     def shard_sketches(self, x_local, dims, lo, hi, ranks, p, samples, seed):
         import torch
+
+        self._bind()
 
         d = len(dims)
         rows = [dims[k] if k < d - 1 else hi - lo for k in range(d)]
@@ -81,6 +92,7 @@ class GpuShardPhases:
     def bases_from_sketches(self, dims, ranks, p, samples, seed, zs):
         import torch
 
+        self._bind()
         d = len(dims)
         us = [torch.empty(dims[k] * ranks[k], dtype=torch.float64, device=zs[0].device) for k in range(d)]
         zp = (C.c_void_p * d)(*[z.data_ptr() for z in zs])
@@ -94,6 +106,7 @@ class GpuShardPhases:
     def shard_core(self, x_local, dims, lo, hi, ranks, factors):
         import torch
 
+        self._bind()
         d = len(dims)
         g = torch.empty(int(np.prod(ranks)), dtype=torch.float64, device=x_local.device)
         fp = (C.c_void_p * d)(*[u.data_ptr() for u in factors])

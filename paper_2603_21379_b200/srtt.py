@@ -105,7 +105,8 @@ class _Report(C.Structure):
     _fields_ = [("sample_counts", C.POINTER(C.c_int64)), ("achieved_ranks", C.POINTER(C.c_int64)),
                 ("warnings", C.c_char_p), ("warnings_capacity", C.c_int64), ("num_warnings", C.c_int64),
                 ("stage_seconds", C.c_double * len(STAGES)), ("flags", C.c_int32), ("reserved", C.c_int32),
-                ("kernel_seconds", C.c_double * 4), ("launches", C.c_int64)]
+                ("kernel_seconds", C.c_double * 4), ("launches", C.c_int64), ("slice_mode", C.c_int64),
+                ("node_bases", C.c_void_p)]
 
 
 class _Tree(C.Structure):
@@ -131,6 +132,7 @@ def _L():
         lib.srtt_sample_indices.argtypes = [u64, u64, i64, i64, i64, vp, vp]
         lib.srtt_stream_normals.argtypes = [vp, u64, u64, u64, u64, i64, vp]
         lib.srtt_tree_balanced.argtypes = [i32] + [vp] * 7
+        lib.srtt_pick_slice_mode.argtypes = [i32, vp, i64, vp]
         lib.srtt_sub_r_hosvd.argtypes = [vp, vp, i32, i32, vp, vp, i64, vp, u64, vp, vp, vp, i32, vp]
         lib.srtt_sub_r_rtl_ht.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, i64, u64, vp, vp, vp, i32, vp]
         lib.srtt_extract_fibers.argtypes = [vp, vp, i32, i32, vp, i32, vp, i64, vp, vp, i32]
@@ -256,6 +258,10 @@ class SubsampleReport:
     flags: int = 0
     launches: int = 0
     kernel_seconds: dict = field(default_factory=dict)
+    slice_mode: int | None = None
+    # H-Tucker: set want_node_bases to get every node's basis (id -> U_S)
+    want_node_bases: bool = False
+    node_bases: dict = field(default_factory=dict)
 
 
 HtSubsampleReport = SubsampleReport
@@ -396,6 +402,7 @@ def _report_from(crep, n, ach, samp, report, handle):
     report.flags = int(crep.flags)
     report.launches = int(crep.launches)
     report.jacobi_sweeps = int(crep.reserved)
+    report.slice_mode = None if int(crep.slice_mode) < 0 else int(crep.slice_mode)
     report.kernel_seconds = {"sketch": float(crep.kernel_seconds[0]), "basis": float(crep.kernel_seconds[1]),
                              "core": float(crep.kernel_seconds[2]), "transfer": float(crep.kernel_seconds[3])}
 
@@ -503,6 +510,13 @@ def sub_r_rtl_ht(x, tree, ranks, samples, oversampling, seed, exec_policy=None, 
     wbuf = C.create_string_buffer(8192)
     crep = _Report(sc.ctypes.data_as(C.POINTER(C.c_int64)), ach.ctypes.data_as(C.POINTER(C.c_int64)),
                    C.cast(wbuf, C.c_char_p), 8192, 0)
+    nb = None
+    if report is not None and getattr(report, "want_node_bases", False):
+        # every node's basis as used by the decomposition (internal nodes too)
+        nshape = {i: (tree.node_rows(i, dims), ranks[i]) for i in range(1, nn)}
+        nb = {i: _alloc_out([nshape[i]], device_out, xf)[0] for i in range(1, nn)}
+        nbp = (C.c_void_p * nn)(*([None] + [_ptr(nb[i])[0] for i in range(1, nn)]))
+        crep.node_bases = C.cast(nbp, C.c_void_p)
     ct = tree._c()
     ex = exec_policy._c() if exec_policy is not None else None
     # device outputs and no report: the call is stream-ordered (returns
@@ -513,6 +527,8 @@ def sub_r_rtl_ht(x, tree, ranks, samples, oversampling, seed, exec_policy=None, 
                                   C.byref(ex) if ex is not None else None, lp, tp, int(device_out), rep_arg))
     if rep_arg is not None:
         _report_from(crep, nn, ach, sc, report, h)
+        if nb is not None:
+            report.node_bases = {i: (b if device_out else b.reshape(nshape[i], order="F")) for i, b in nb.items()}
     if device_out:
         return HTuckerDecomposition(tree, leaf, [trs.get(i) for i in range(nn)])
     leaf_np = [leaf[m].reshape(leaf_shape[m], order="F") for m in range(d)]
@@ -543,18 +559,20 @@ def extract_fibers(x, mode, cols, *, handle=None):
     return extract_group_fibers(x, [mode], cols, handle=handle)
 
 
-def sketch(x, modes, cols, c, seed, stream_id, draw_offset, omega=None, *, handle=None):
-    """K1 alone: Z = Y(cols) * Omega, Omega from stream (seed, stream_id)."""
+def sketch(x, modes, cols, c, seed, stream_id, draw_offset, omega=None, *, dims=None, handle=None):
+    """K1 alone: Z = Y(cols) * Omega, Omega from stream (seed, stream_id).
+    ``x``: numpy nd-array, or a flat CUDA float64 tensor with ``dims``."""
     h = handle or default_handle()
-    dims = list(x.shape)
+    dims = list(x.shape) if dims is None else list(dims)
     xf = _flat_f64(x)
+    xp, xdev = _ptr(xf)
     modes_a = np.ascontiguousarray(np.asarray(modes, np.int32))
     cols_a = _i64(cols)
     rows = int(np.prod([dims[m] for m in modes]))
     z = np.zeros(rows * c)
     om = None if omega is None else np.ascontiguousarray(np.ravel(omega, order="F"), dtype=np.float64)
     dims_a = _i64(dims)
-    _check(_L().srtt_sketch(h._h, xf.ctypes.data, 0, len(dims), dims_a.ctypes.data, len(modes_a),
+    _check(_L().srtt_sketch(h._h, xp, xdev, len(dims), dims_a.ctypes.data, len(modes_a),
                             modes_a.ctypes.data, len(cols_a), cols_a.ctypes.data, c, seed, stream_id, draw_offset,
                             om.ctypes.data if om is not None else None, z.ctypes.data, 0))
     return z.reshape((rows, c), order="F")
@@ -599,10 +617,29 @@ def multi_ttm_core(x, factors, *, handle=None):
 core_from_factors = multi_ttm_core
 
 
+def pick_slice_mode(dims, workers):
+    """parallel.hpp:331-348."""
+    out = C.c_int64()
+    dims_a = _i64(dims)
+    _check(_L().srtt_pick_slice_mode(len(dims_a), dims_a.ctypes.data, int(workers), C.byref(out)))
+    return int(out.value)
+
+
 def sliced_core(x, factors, policy=None, *, handle=None):
-    """parallel.hpp:355-445: same numbers for every policy on the GPU."""
-    if policy is not None and policy.slice_mode is not None and not 0 <= policy.slice_mode < x.ndim:
+    """parallel.hpp:355-445: the policy is validated as the reference does
+    (slice mode, workers vs slices); the numbers are the same for every
+    policy (one streaming pass on the GPU)."""
+    if len(factors) != x.ndim:
+        raise InvalidArgument("sliced_core: need one factor per mode")
+    for k, f in enumerate(factors):
+        if np.shape(f)[0] != x.shape[k]:
+            raise InvalidArgument(f"sliced_core: factor rows mismatch in mode {k}")
+    policy = policy or ExecPolicy()
+    sm = policy.slice_mode if policy.slice_mode is not None else pick_slice_mode(x.shape, policy.workers)
+    if not 0 <= sm < x.ndim:
         raise InvalidArgument("sliced_core: slice mode out of range")
+    if policy.workers > x.shape[sm]:
+        raise InvalidArgument("sliced_core: more workers than slices along the slicing mode")
     return multi_ttm_core(x, factors, handle=handle)
 
 
