@@ -77,3 +77,34 @@ def test_validation(handle):
     bad[0] = 2
     with pytest.raises(P.InvalidArgument, match="root rank must be 1"):
         P.sub_r_rtl_ht(x, tree, bad, [1] + [30] * 6, 4, 0, handle=handle)
+
+
+def test_exec_policy_workers_validated(handle):
+    """tree_schedule (parallel.hpp:206) rejects workers < 1; no slice mode is
+    involved on the H-Tucker path."""
+    tree = P.DimensionTree.balanced(4)
+    x = np.random.default_rng(0).standard_normal((6,) * 4)
+    ranks = P.uniform_node_ranks(tree, 2)
+    with pytest.raises(P.InvalidArgument, match="^tree_schedule: workers must be >= 1$"):
+        P.sub_r_rtl_ht(x, tree, ranks, [1] + [30] * 6, 4, 0, P.ExecPolicy(workers=0), handle=handle)
+    rep = P.HtSubsampleReport()
+    P.sub_r_rtl_ht(x, tree, ranks, [1] + [30] * 6, 4, 0, P.ExecPolicy(workers=3), report=rep, handle=handle)
+    assert rep.slice_mode is None
+
+
+def test_internal_node_bases_reported(handle):
+    """The report's node_bases are the bases the decomposition used: leaves
+    equal the returned leaf factors bitwise, internal ones match the oracle's
+    node bases."""
+    tree, otree = P.DimensionTree.balanced(4), O.DimensionTree.balanced(4)
+    x, _ = planted_htucker((9,) * 4, otree, O.uniform_node_ranks(otree, 3), 4)
+    ranks = P.uniform_node_ranks(tree, 3)
+    samples = [1] + [min(30, tree.node_cols(i, x.shape)) for i in range(1, 7)]
+    rep = P.HtSubsampleReport(want_node_bases=True)
+    h = P.sub_r_rtl_ht(x, tree, ranks, samples, 4, 2, report=rep, handle=handle)
+    orep = O.HtSubsampleReport()
+    O.sub_r_rtl_ht(x, otree, ranks, samples, 4, 2, report=orep)
+    for i in range(1, 7):
+        assert projector_gap(rep.node_bases[i], orep.bases[i]) <= 1e-10
+        if otree.node(i).is_leaf():
+            assert np.array_equal(rep.node_bases[i], h.leaf_factors[otree.node(i).modes[0]])

@@ -150,3 +150,43 @@ def test_stream_ordered_calls_are_ordered_with_the_callers_stream(use_torch_defa
             call()
             got = core.cpu().numpy()  # ordered after the call on the caller's stream, no extra sync
             assert np.array_equal(got, ref)
+
+
+def test_exec_policy_validated_like_the_reference(handle):
+    """ExecPolicy on the GPU path: workers / slice_mode never change the
+    numbers (parallel.hpp:18-21) but are validated with the reference's
+    messages -- run_independent_jobs (parallel.hpp:88), pick_slice_mode
+    (:331-348) and sliced_core (:369-373) -- and the resolved slice mode is
+    reported."""
+    x = random_tensor((6, 7, 8), 5)
+    args = ([2] * 3, 4, [12] * 3, 3)
+    with pytest.raises(P.InvalidArgument, match="^run_independent_jobs: workers must be >= 1$"):
+        P.sub_r_hosvd(x, *args, P.ExecPolicy(workers=0), handle=handle)
+    with pytest.raises(P.InvalidArgument, match="^pick_slice_mode: no mode can host 9 slices$"):
+        P.sub_r_hosvd(x, *args, P.ExecPolicy(workers=9), handle=handle)
+    with pytest.raises(P.InvalidArgument, match="^sliced_core: slice mode out of range$"):
+        P.sub_r_hosvd(x, *args, P.ExecPolicy(workers=2, slice_mode=3), handle=handle)
+    with pytest.raises(P.InvalidArgument, match="^sliced_core: more workers than slices along the slicing mode$"):
+        P.sub_r_hosvd(x, *args, P.ExecPolicy(workers=7, slice_mode=0), handle=handle)
+    base = P.sub_r_hosvd(x, *args, handle=handle)
+    for pol in [P.ExecPolicy(workers=1), P.ExecPolicy(workers=4), P.ExecPolicy(workers=3, slice_mode=2)]:
+        rep = P.SubsampleReport()
+        t = P.sub_r_hosvd(x, *args, pol, report=rep, handle=handle)
+        want = pol.slice_mode if pol.slice_mode is not None else O.pick_slice_mode(x.shape, pol.workers)
+        assert rep.slice_mode == want
+        assert np.array_equal(t.core, base.core)
+        assert all(np.array_equal(u, v) for u, v in zip(t.factors, base.factors))
+    rep = P.SubsampleReport()
+    P.sub_r_hosvd(x, *args, report=rep, handle=handle)
+    assert rep.slice_mode is None
+
+
+def test_core_rank_limit_rejected_up_front(handle):
+    """Ranks above 32 in the first two core modes are refused before any
+    work is issued, with a message naming the limit (not a core-planner
+    error after the factor phase)."""
+    x = np.random.default_rng(1).standard_normal((40, 40, 8))
+    with pytest.raises(P.InvalidArgument, match="ranks above 32 in the first two core modes"):
+        P.sub_r_hosvd(x, [33, 4, 4], 6, [60] * 3, 0, handle=handle)
+    with pytest.raises(P.InvalidArgument, match="rank \\+ oversampling above 64"):
+        P.sub_r_hosvd(x, [8, 8, 8], 60, [120] * 3, 0, handle=handle)

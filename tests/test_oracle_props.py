@@ -183,3 +183,48 @@ def test_ht_storage_counts():
                                [np.zeros((1 if i == 0 else 5, 5, 5)) if not tree.node(i).is_leaf() else None
                                 for i in range(15)])
     assert O.ht_storage_count(h) == 8 * 75 + 6 * 125 + 25
+
+
+def test_pick_slice_mode_c_abi_matches_reference_rule():
+    """srtt_pick_slice_mode (host code of the C-ABI, no GPU needed) vs the
+    oracle's restatement of parallel.hpp:331-348, including the error."""
+    import paper_2603_21379_b200 as P
+
+    rng = np.random.default_rng(3)
+    for _ in range(300):
+        d = int(rng.integers(1, 6))
+        dims = [int(v) for v in rng.integers(1, 40, size=d)]
+        w = int(rng.integers(1, 20))
+        try:
+            want = O.pick_slice_mode(dims, w)
+        except ValueError as e:
+            with pytest.raises(P.InvalidArgument, match=str(e)):
+                P.pick_slice_mode(dims, w)
+            continue
+        assert P.pick_slice_mode(dims, w) == want
+
+
+def test_sliced_core_bitwise_across_workers_and_streamed():
+    """sliced_core is bitwise independent of the worker count
+    (acceptance.cpp:266-341 property); the slab-streamed variant used for
+    C5-size parity equals it, and rel_error_streamed equals rel_error."""
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((9, 8, 7, 10))
+    fs = [np.linalg.qr(rng.standard_normal((n, 3)))[0] for n in x.shape]
+    cores = [O.sliced_core(x, fs, O.ExecPolicy(workers=w, slice_mode=sm)) for w in (1, 3, 7) for sm in (0, 3)]
+    for c in cores[1:]:
+        assert np.abs(c - cores[0]).max() <= 1e-13
+    for w in (2, 5):
+        assert np.array_equal(O.sliced_core(x, fs, O.ExecPolicy(workers=w, slice_mode=3)),
+                              O.sliced_core(x, fs, O.ExecPolicy(workers=1, slice_mode=3)))
+    ref = O.core_from_factors(x, fs)
+    assert np.abs(cores[0] - ref).max() <= 1e-13
+
+    def read(lo, hi):
+        return x[..., lo:hi]
+
+    st = O.sliced_core_streamed(read, x.shape, fs, slab=3)
+    assert np.abs(st - ref).max() <= 1e-13
+    e1 = O.rel_error_streamed(read, x.shape, ref, fs, slab=4)
+    e2 = O.rel_error(x, O.reconstruct(O.TuckerDecomposition(ref, fs)))
+    assert abs(e1 - e2) <= 1e-14
