@@ -449,12 +449,12 @@ def sliced_core(x, factors, policy: ExecPolicy):
         lo = w * (n // nworkers) + min(w, n % nworkers)
         hi = lo + n // nworkers + (1 if w < n % nworkers else 0)
         for i in range(lo, hi):
-            sl = np.take(x, [i], axis=sm)
+            j = list(idx)
+            j[sm] = slice(i, i + 1)
+            sl = np.asfortranarray(x[tuple(j)])  # copy of slice i (parallel.hpp:387-389)
             for k in range(d):
                 if k != sm:
                     sl = ttm(sl, factors[k].T, k)
-            j = list(idx)
-            j[sm] = slice(i, i + 1)
             reduced[tuple(j)] = sl
 
     if nworkers > 1:
