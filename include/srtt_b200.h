@@ -308,6 +308,71 @@ int srtt_shard_core(srtt_handle* h, const double* x_local, int32_t x_on_device, 
                     const double* const* factors, int32_t factors_on_device, double* core_partial_out,
                     int32_t out_on_device);
 
+/* ---- multi-GPU: one process per GPU, NCCL over NVLink -------------------
+ * The handle owns an NCCL communicator (libnccl.so.2 is resolved at run
+ * time; SRTT_ERR_NCCL when it is missing). One rank creates the unique id
+ * (SRTT_UNIQUE_ID_BYTES opaque bytes) and the caller distributes it (MPI,
+ * torch.distributed, a file, ...); every rank then calls srtt_comm_init.
+ * The sharded decompositions below run their kernels and the NCCL
+ * collectives on the handle's stream, captured in one CUDA graph per call
+ * signature (use_graphs), and return identical outputs on every rank.
+ * Reference: sliced_core's slab algebra (parallel.hpp:355-445) and the
+ * H-Tucker job DAG (htucker.hpp:249-324, root_transfer :67-85) across GPUs;
+ * the reference's own engine is shared-memory threads only. */
+#define SRTT_UNIQUE_ID_BYTES 128
+int srtt_comm_unique_id(void* id_out);
+int srtt_comm_init(srtt_handle* h, int32_t world, int32_t rank, const void* unique_id);
+int srtt_comm_destroy(srtt_handle* h);
+/* world = 0 when the handle has no communicator. */
+int srtt_comm_info(srtt_handle* h, int32_t* world, int32_t* rank);
+/* [lo, hi) of part `rank` of n slices over `world` parts: the contiguous
+ * split of parallel.hpp:400-404 (sizes differ by at most one). */
+int srtt_split_bounds(int64_t n, int32_t world, int32_t rank, int64_t* lo, int64_t* hi);
+
+/* sub_r_hosvd (tucker.hpp:177-242) of a tensor split along its LAST mode:
+ * this rank passes X[..., slab_lo:slab_hi) (flat, first index fastest) and
+ * the GLOBAL dims. Exchanges: ONE allreduce of all sketches (sum_k
+ * dims[k] (r_k + p) doubles; the slab mode's rows are owned by one rank each)
+ * and ONE allreduce of the partial core (prod r_k doubles). Every slab must
+ * hold at least r_{d-1} slices. Outputs and report as srtt_sub_r_hosvd;
+ * report stage "gather" = the two exchanges. */
+int srtt_sub_r_hosvd_sharded(srtt_handle* h, const double* x_slab, int32_t x_on_device, int32_t d,
+                             const int64_t* dims, int64_t slab_lo, int64_t slab_hi, const int64_t* ranks,
+                             int64_t oversampling, const int64_t* samples, uint64_t seed,
+                             const srtt_exec_policy* exec, double* core_out, double* const* factors_out,
+                             int32_t out_on_device, srtt_report* rep);
+/* sub_r_rtl_ht (htucker.hpp:210-341) of a tensor split into column ranges
+ * of the root matricization M = n_left x n_right (n_left = prod of the
+ * root's left-child extents): this rank passes columns [col_lo, col_hi) of
+ * M, i.e. the flat range [col_lo n_left, col_hi n_left) of X. Exchanges:
+ * ONE allreduce of every node's partial sketch (sum_S n_S (r_S + p)
+ * doubles) and ONE allreduce of the partial root transfer (r_l r_r). */
+int srtt_sub_r_rtl_ht_sharded(srtt_handle* h, const double* x_cols, int32_t x_on_device, int32_t d,
+                              const int64_t* dims, int64_t col_lo, int64_t col_hi, const srtt_tree* tree,
+                              const int64_t* ranks, const int64_t* samples, int64_t oversampling, uint64_t seed,
+                              const srtt_exec_policy* exec, double* const* leaf_factors_out,
+                              double* const* transfers_out, int32_t out_on_device, srtt_report* rep);
+/* The H-Tucker split as synchronous phases (same plan and kernels as the
+ * fused entry; the caller exchanges between them, any transport):
+ *   1. srtt_ht_shard_sketches: z_out[id] (id >= 1, n_S x (r_S + p)) = this
+ *      range's PARTIAL sketch of node id                  -> allreduce(sum);
+ *   2. srtt_ht_bases_from_sketches: node bases (n_S x r_S, by node id) and
+ *      internal transfers (by node id) -- identical on every rank;
+ *   3. srtt_ht_shard_root: U_l^T M[:, c_lo:c_hi] U_r[c_lo:c_hi, :]
+ *      (r_l x r_r)                                         -> allreduce(sum). */
+int srtt_ht_shard_sketches(srtt_handle* h, const double* x_cols, int32_t x_on_device, int32_t d,
+                           const int64_t* dims, int64_t col_lo, int64_t col_hi, const srtt_tree* tree,
+                           const int64_t* ranks, const int64_t* samples, int64_t oversampling, uint64_t seed,
+                           const srtt_exec_policy* exec, double* const* z_out, int32_t out_on_device);
+int srtt_ht_bases_from_sketches(srtt_handle* h, int32_t d, const int64_t* dims, const srtt_tree* tree,
+                                const int64_t* ranks, const int64_t* samples, int64_t oversampling, uint64_t seed,
+                                const srtt_exec_policy* exec, const double* const* z, int32_t z_on_device,
+                                double* const* node_bases_out, double* const* transfers_out, int32_t out_on_device,
+                                int64_t* achieved_ranks);
+int srtt_ht_shard_root(srtt_handle* h, const double* x_cols, int32_t x_on_device, int64_t n_left, int64_t n_right,
+                       int64_t col_lo, int64_t col_hi, const double* u_left, int32_t r_left, const double* u_right,
+                       int32_t r_right, int32_t factors_on_device, double* b_out, int32_t out_on_device);
+
 #ifdef __cplusplus
 }
 #endif

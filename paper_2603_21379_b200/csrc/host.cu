@@ -301,6 +301,10 @@ struct srtt_handle {
     const double* d_core = nullptr;
   };
   std::map<std::string, Prepared> prepared;
+  // multi-GPU: the NCCL communicator this handle owns (srtt_comm_init);
+  // opaque here, see shard.cuh
+  void* comm = nullptr;
+  int world = 1, rank = 0;
   ~srtt_handle() {
     for (auto& g : graphs)
       if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
@@ -1418,6 +1422,8 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   if (end_call(h, rep || !out_on_device)) finish_tucker(h, tm, d, ranks, samples, t_sampling, warnings, rep);
 }
 
+void release_comm(srtt_handle* h);  // shard.cuh
+
 }  // namespace
 
 // ==================================================================================
@@ -1467,6 +1473,7 @@ int srtt_destroy(srtt_handle* h) {
     {
       DeviceGuard g(h->device);
       cudaStreamSynchronize(h->stream);
+      if (h->comm) release_comm(h);
       for (auto& e : h->ev) cudaEventDestroy(e);
       for (auto& e : h->kev) cudaEventDestroy(e);
       cudaStreamDestroy(h->own_stream);
@@ -2750,3 +2757,6 @@ int srtt_ht_rel_error(srtt_handle* h, const double* x, int32_t x_on_device, int3
 cudaStream_t srtt_internal_stream(srtt_handle* h) { return h->stream; }
 int srtt_internal_device(srtt_handle* h) { return h->device; }
 void srtt_internal_set_error(const std::string& msg) { g_last_error = msg; }
+
+// ---- multi-GPU (NCCL) entry points ----------------------------------------------
+#include "shard.cuh"

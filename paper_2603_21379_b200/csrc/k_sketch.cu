@@ -72,6 +72,9 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
   for (int cc = 0; cc < CMAX; ++cc) acc[cc] = 0.0;
 
   const double* __restrict__ x = T.x;
+  // flat-range sharding: only [flo, fhi) of the global flat index is local
+  const int64_t flo = T.flat_lo, fhi = T.flat_hi;
+  const bool ranged = fhi > 0;
   for (int64_t j0 = 0; j0 < T.w; j0 += kChunk) {
     const int jn = (int)srtt_dev::min64(kChunk, T.w - j0);
     __syncthreads();
@@ -99,7 +102,16 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
       base[jl] = b < 0 ? -1 : b;
     }
     __syncthreads();
-    if (active) {
+    if (active && ranged) {
+      for (int jl = js; jl < jn; jl += JS) {
+        const int64_t o = base[jl] + roff;
+        const double v = (o >= flo && o < fhi) ? __ldg(x + (o - flo)) : 0.0;
+        const double* om_j = om + jl * c;
+#pragma unroll
+        for (int cc = 0; cc < CMAX; ++cc)
+          if (cc < c) acc[cc] += v * om_j[cc];
+      }
+    } else if (active) {
       int jl = js;
       // 4 independent loads in flight per thread before the FMAs.
       for (; jl + 3 * JS < jn; jl += 4 * JS) {
@@ -134,13 +146,14 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
       if (cc < c) red[(js * RT + il) * c + cc] = acc[cc];
   }
   __syncthreads();
+  const int64_t ldz = T.ldz > 0 ? T.ldz : T.rows;
   for (int idx = tid; idx < RT * c; idx += kThreads) {
     const int rl = idx % RT, cc = idx / RT;
     const int64_t row = (int64_t)(blockIdx.x - T.cta_begin) * RT + rl;
     if (row >= T.rows) continue;
     double s = 0.0;
     for (int g = 0; g < JS; ++g) s += red[(g * RT + rl) * c + cc];
-    T.z[row + (int64_t)cc * T.rows] = s;
+    T.z[row + (int64_t)cc * ldz] = s;
   }
 }
 

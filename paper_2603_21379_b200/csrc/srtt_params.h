@@ -39,6 +39,13 @@ typedef struct SketchTarget {
   int32_t slab_digit;     // -1: no slab restriction
   int32_t pad0;
   int64_t slab_lo, slab_hi;
+  // flat-range sharding (H-Tucker, X split into column ranges of the root
+  // matricization): x holds only the flat range [flat_lo, flat_hi) of the
+  // global tensor; elements outside it contribute zero (flat_hi = 0: off)
+  int64_t flat_lo, flat_hi;
+  // leading dimension of z (0: rows); lets a rank write its rows of a
+  // row-distributed sketch into a zero-filled full-height buffer
+  int64_t ldz;
 } SketchTarget;
 
 // ---------------------------------------------------------------------------

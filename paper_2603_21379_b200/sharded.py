@@ -19,12 +19,25 @@ slab algebra holds with the slabs living on different devices:
                                                                -> all_reduce
 
 Only the sketches (sum n_k (r_k+p) doubles) and the core (prod r_k doubles)
-cross the interconnect; X never moves.  Work per rank is the slab, so the
-scaling is weak in the slab size.  The phase calls go through the C-ABI
-(``srtt_shard_sketches`` / ``srtt_bases_from_sketches`` / ``srtt_shard_core``)
-and the collectives through ``torch.distributed`` (NCCL on GPUs; any backend
-works because the phases are pluggable -- the CPU tests drive the same
-orchestration with gloo and a checker backend).
+cross the interconnect; X never moves.
+
+Two ways to run it:
+
+* ``sub_r_hosvd_nccl`` / ``sub_r_rtl_ht_nccl`` (the product path): ONE C-ABI
+  call per rank (``srtt_sub_r_hosvd_sharded`` / ``srtt_sub_r_rtl_ht_sharded``)
+  whose handle owns an NCCL communicator (``comm_init``); kernels and
+  collectives are captured in one CUDA graph per call signature.
+* ``sub_r_hosvd_sharded`` / ``sub_r_rtl_ht_sharded``: the same algebra as
+  separate synchronous phases (``srtt_shard_*`` / ``srtt_ht_shard_*``) with
+  the exchanges issued here through ``torch.distributed`` (any backend: the
+  CPU tests drive this orchestration with gloo and a checker backend).
+
+H-Tucker (htucker.hpp:210-341) splits X into column ranges of the root
+matricization M = n_left x n_right (a contiguous byte range of X): every
+node's sketch is a sum over its sampled fibre entries, so each rank forms
+PARTIAL sketches of every node from its range (allreduce), the bases and
+transfers follow identically on every rank, and the root transfer
+B_0 = sum_w U_l^T M_w U_r[c_lo:c_hi] is one more allreduce (htucker.hpp:67-85).
 """
 from __future__ import annotations
 
@@ -43,6 +56,141 @@ def slab_bounds(n: int, world: int, rank: int):
     lo = rank * (n // world) + min(rank, n % world)
     hi = lo + n // world + (1 if rank < n % world else 0)
     return lo, hi
+
+
+def _dist():
+    import torch.distributed as dist
+
+    return dist
+
+
+def comm_init(handle: _s.Handle, group=None):
+    """Give ``handle`` an NCCL communicator spanning the torch.distributed
+    group: rank 0 creates the NCCL unique id, the group broadcasts it, every
+    rank calls ``srtt_comm_init`` (the handle owns the communicator)."""
+    dist = _dist()
+    lib = _s._L()
+    world = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    uid = C.create_string_buffer(128)
+    if me == 0:
+        _s._check(lib.srtt_comm_unique_id(uid))
+    obj = [bytes(uid.raw) if me == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    uid = C.create_string_buffer(obj[0], 128)
+    _s._check(lib.srtt_comm_init(handle._h, world, me, uid))
+    return world, me
+
+
+def comm_init_local(handle: _s.Handle, world: int = 1, rank: int = 0, unique_id: bytes | None = None):
+    """``srtt_comm_init`` without torch.distributed: ``unique_id`` from
+    ``new_unique_id()`` distributed by any means (world 1 needs none)."""
+    lib = _s._L()
+    if unique_id is None:
+        unique_id = new_unique_id()
+    uid = C.create_string_buffer(bytes(unique_id), 128)
+    _s._check(lib.srtt_comm_init(handle._h, int(world), int(rank), uid))
+
+
+def new_unique_id() -> bytes:
+    uid = C.create_string_buffer(128)
+    _s._check(_s._L().srtt_comm_unique_id(uid))
+    return bytes(uid.raw)
+
+
+def comm_info(handle: _s.Handle):
+    w, r = C.c_int32(), C.c_int32()
+    _s._check(_s._L().srtt_comm_info(handle._h, C.byref(w), C.byref(r)))
+    return int(w.value), int(r.value)
+
+
+def column_bounds(tree, dims, world: int, rank: int):
+    """[c_lo, c_hi) of rank's columns of the root matricization
+    M = n_left x n_right, and (n_left, n_right)."""
+    nl = tree.node_rows(tree.node(0).left, dims)
+    nr = tree.node_rows(tree.node(0).right, dims)
+    lo, hi = slab_bounds(nr, world, rank)
+    return lo, hi, nl, nr
+
+
+def sub_r_hosvd_nccl(x_slab, dims, target, oversampling, samples, seed, *, handle, exec_policy=None,
+                     report=None, out=None):
+    """Fused slab-sharded sub_r_hosvd through ``srtt_sub_r_hosvd_sharded``
+    (the handle must own a communicator, see ``comm_init``). ``x_slab`` is
+    this rank's X[..., lo:hi) (flat CUDA float64, first index fastest) with
+    the bounds of ``slab_bounds``; returns identical device outputs on every
+    rank. Stream-ordered when no report is requested."""
+    import torch
+
+    world, me = comm_info(handle)
+    if world < 1:
+        raise _s.InvalidArgument("sharded: the handle has no communicator (comm_init)")
+    d = len(dims)
+    lo, hi = slab_bounds(dims[-1], world, me)
+    call = _s._CALLS.get(("sh",) + (tuple(dims), tuple(target), tuple(samples)))
+    if call is None:
+        call = _s._CALLS.setdefault(("sh",) + (tuple(dims), tuple(target), tuple(samples)),
+                                    _s._TuckerCall(dims, target, samples))
+    if out is None:
+        dev = x_slab.device
+        out = (torch.empty(int(np.prod(target)), dtype=torch.float64, device=dev),
+               [torch.empty(dims[k] * target[k], dtype=torch.float64, device=dev) for k in range(d)])
+    for k in range(d):
+        call.fptrs[k] = out[1][k].data_ptr()
+    ex = exec_policy._c() if exec_policy is not None else None
+    rep_arg = C.byref(call.rep) if report is not None else None
+    _s._check(_s._L().srtt_sub_r_hosvd_sharded(
+        handle._h, x_slab.data_ptr(), 1, d, call.dims_a.ctypes.data, lo, hi, call.ranks_a.ctypes.data,
+        int(oversampling), call.samp_a.ctypes.data, int(seed) & (2**64 - 1), C.byref(ex) if ex is not None else None,
+        out[0].data_ptr(), call.fptrs, 1, rep_arg))
+    if report is not None:
+        _s._report_from(call.rep, d, call.ach, call.sc, report, handle)
+    return ShardedTucker(core=out[0], factors=list(out[1]), achieved_ranks=list(getattr(report, "achieved_ranks", [])),
+                         slab=(lo, hi))
+
+
+def sub_r_rtl_ht_nccl(x_cols, dims, tree, ranks, samples, oversampling, seed, *, handle, exec_policy=None,
+                      report=None):
+    """Fused column-range-sharded sub_r_rtl_ht through
+    ``srtt_sub_r_rtl_ht_sharded``; ``x_cols`` holds this rank's columns
+    [c_lo, c_hi) of M = n_left x n_right (``column_bounds``). Returns device
+    leaf factors (by mode) and transfers (by node id), identical on every
+    rank."""
+    import torch
+
+    world, me = comm_info(handle)
+    if world < 1:
+        raise _s.InvalidArgument("sharded: the handle has no communicator (comm_init)")
+    d = len(dims)
+    lo, hi, nl, nr = column_bounds(tree, dims, world, me)
+    nn = tree.num_nodes
+    dev = x_cols.device
+    leaf = [None] * d
+    for i in tree.leaves():
+        m = tree.node(i).modes[0]
+        leaf[m] = torch.empty(dims[m] * ranks[i], dtype=torch.float64, device=dev)
+    trs = [None] * nn
+    for i in range(nn):
+        n = tree.node(i)
+        if not n.is_leaf():
+            trs[i] = torch.empty((1 if i == 0 else ranks[i]) * ranks[n.left] * ranks[n.right], dtype=torch.float64,
+                                 device=dev)
+    lp = (C.c_void_p * d)(*[u.data_ptr() for u in leaf])
+    tp = (C.c_void_p * nn)(*[None if t is None else t.data_ptr() for t in trs])
+    ranks_a, samp_a, dims_a = _s._i64(ranks), _s._i64(samples), _s._i64(dims)
+    ach, sc = np.zeros(nn, np.int64), np.zeros(nn, np.int64)
+    wbuf = C.create_string_buffer(8192)
+    crep = _s._Report(sc.ctypes.data_as(C.POINTER(C.c_int64)), ach.ctypes.data_as(C.POINTER(C.c_int64)),
+                      C.cast(wbuf, C.c_char_p), 8192, 0)
+    ct = tree._c()
+    ex = exec_policy._c() if exec_policy is not None else None
+    _s._check(_s._L().srtt_sub_r_rtl_ht_sharded(
+        handle._h, x_cols.data_ptr(), 1, d, dims_a.ctypes.data, lo, hi, C.byref(ct), ranks_a.ctypes.data,
+        samp_a.ctypes.data, int(oversampling), int(seed) & (2**64 - 1), C.byref(ex) if ex is not None else None,
+        lp, tp, 1, C.byref(crep) if report is not None else None))
+    if report is not None:
+        _s._report_from(crep, nn, ach, sc, report, handle)
+    return _s.HTuckerDecomposition(tree, leaf, trs)
 
 
 class GpuShardPhases:
@@ -185,3 +333,125 @@ def sub_r_hosvd_sharded(x_local, dims, target, oversampling, samples, seed, *, g
     core = ph.shard_core(x_local, dims, lo, hi, target, factors)
     dist.all_reduce(core, group=group)
     return ShardedTucker(core=core, factors=factors, achieved_ranks=achieved, slab=(lo, hi))
+
+
+# ---------------------------------------------------------------------------
+# H-Tucker: column-range sharding, phases + torch.distributed orchestration
+# ---------------------------------------------------------------------------
+class GpuHtShardPhases:
+    """srtt_ht_shard_sketches / srtt_ht_bases_from_sketches / srtt_ht_shard_root
+    on this process's GPU (run on torch's current stream)."""
+
+    def __init__(self, handle: _s.Handle | None = None):
+        self.h = handle or _s.default_handle()
+        lib = _s._L()
+        vp, i32, i64, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64
+        lib.srtt_ht_shard_sketches.argtypes = [vp, vp, i32, i32, vp, i64, i64, vp, vp, vp, i64, u64, vp, vp, i32]
+        lib.srtt_ht_bases_from_sketches.argtypes = [vp, i32, vp, vp, vp, vp, i64, u64, vp, vp, i32, vp, vp, i32, vp]
+        lib.srtt_ht_shard_root.argtypes = [vp, vp, i32, i64, i64, i64, i64, vp, i32, vp, i32, i32, vp, i32]
+        self.lib = lib
+
+    def _bind(self):
+        import torch
+
+        self.h.set_stream(torch.cuda.current_stream().cuda_stream)
+
+    def shard_sketches(self, x_cols, dims, tree, lo, hi, ranks, p, samples, seed):
+        """Partial sketch of every node (id -> flat n_S x (r_S+p) tensor)."""
+        import torch
+
+        self._bind()
+        nn = tree.num_nodes
+        zs = {i: torch.empty(tree.node_rows(i, dims) * (ranks[i] + p), dtype=torch.float64, device=x_cols.device)
+              for i in range(1, nn)}
+        zp = (C.c_void_p * nn)(*([None] + [zs[i].data_ptr() for i in range(1, nn)]))
+        ct = tree._c()
+        _s._check(self.lib.srtt_ht_shard_sketches(self.h._h, x_cols.data_ptr(), 1, len(dims), _s._i64(dims).ctypes.data,
+                                                  lo, hi, C.byref(ct), _s._i64(ranks).ctypes.data,
+                                                  _s._i64(samples).ctypes.data, p, seed, None, zp, 1))
+        return zs
+
+    def bases_from_sketches(self, dims, tree, ranks, p, samples, seed, zs):
+        """(node bases by id, transfers by id, achieved ranks)."""
+        import torch
+
+        self._bind()
+        nn = tree.num_nodes
+        dev = zs[1].device
+        us = {i: torch.empty(tree.node_rows(i, dims) * ranks[i], dtype=torch.float64, device=dev)
+              for i in range(1, nn)}
+        bs = {}
+        for i in range(1, nn):
+            n = tree.node(i)
+            if not n.is_leaf():
+                bs[i] = torch.empty(ranks[i] * ranks[n.left] * ranks[n.right], dtype=torch.float64, device=dev)
+        zp = (C.c_void_p * nn)(*([None] + [zs[i].data_ptr() for i in range(1, nn)]))
+        up = (C.c_void_p * nn)(*([None] + [us[i].data_ptr() for i in range(1, nn)]))
+        bp = (C.c_void_p * nn)(*[bs[i].data_ptr() if i in bs else None for i in range(nn)])
+        ach = np.zeros(nn, np.int64)
+        ct = tree._c()
+        _s._check(self.lib.srtt_ht_bases_from_sketches(self.h._h, len(dims), _s._i64(dims).ctypes.data, C.byref(ct),
+                                                       _s._i64(ranks).ctypes.data, _s._i64(samples).ctypes.data, p,
+                                                       seed, None, zp, 1, up, bp, 1, ach.ctypes.data))
+        return us, bs, [int(a) for a in ach]
+
+    def shard_root(self, x_cols, nl, nr, lo, hi, u_left, rl, u_right, rr):
+        import torch
+
+        self._bind()
+        b = torch.empty(rl * rr, dtype=torch.float64, device=x_cols.device)
+        _s._check(self.lib.srtt_ht_shard_root(self.h._h, x_cols.data_ptr(), 1, nl, nr, lo, hi, u_left.data_ptr(), rl,
+                                              u_right.data_ptr(), rr, 1, b.data_ptr(), 1))
+        return b
+
+
+@dataclass
+class ShardedHTucker:
+    leaf_factors: list    # by mode, flat n_m x r (identical on every rank)
+    transfers: list       # by node id (root: 1 x r_l x r_r), None for leaves
+    node_bases: dict      # id -> flat basis (identical on every rank)
+    achieved_ranks: list
+    columns: tuple        # this rank's [c_lo, c_hi) of the root matricization
+
+
+def sub_r_rtl_ht_sharded(x_cols, dims, tree, ranks, samples, oversampling, seed, *, group=None, phases=None):
+    """Sub-R-RtL-HT (htucker.hpp:210-341) of a tensor split into column
+    ranges of the root matricization over the process group, as three phases
+    with the exchanges issued here: allreduce of every node's partial sketch,
+    identical bases / transfers on every rank, allreduce of the partial root
+    transfer."""
+    dist = _dist()
+    nn = tree.num_nodes
+    d = len(dims)
+    if tree.order != d:
+        raise _s.InvalidArgument("sub_r_rtl_ht: tree and tensor order mismatch")
+    if len(ranks) != nn or len(samples) != nn:
+        raise _s.InvalidArgument("sub_r_rtl_ht: rank/sample vector must have one entry per node")
+    world = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    lo, hi, nl, nr = column_bounds(tree, dims, world, me)
+    if x_cols.numel() != (hi - lo) * nl:
+        raise _s.InvalidArgument("sharded sub_r_rtl_ht: local column range size mismatch")
+    ph = phases or GpuHtShardPhases()
+    zs = ph.shard_sketches(x_cols, dims, tree, lo, hi, ranks, oversampling, samples, seed)
+    import torch
+
+    flat = torch.cat([zs[i].reshape(-1) for i in range(1, nn)])   # ONE collective for all nodes
+    dist.all_reduce(flat, group=group)
+    off = 0
+    for i in range(1, nn):
+        n = zs[i].numel()
+        zs[i] = flat[off:off + n]
+        off += n
+    us, bs, ach = ph.bases_from_sketches(dims, tree, ranks, oversampling, samples, seed, zs)
+    root = tree.node(0)
+    b0 = ph.shard_root(x_cols, nl, nr, lo, hi, us[root.left], ranks[root.left], us[root.right], ranks[root.right])
+    dist.all_reduce(b0, group=group)
+    leaf = [None] * d
+    for i in tree.leaves():
+        leaf[tree.node(i).modes[0]] = us[i]
+    trs = [None] * nn
+    trs[0] = b0
+    for i, b in bs.items():
+        trs[i] = b
+    return ShardedHTucker(leaf_factors=leaf, transfers=trs, node_bases=us, achieved_ranks=ach, columns=(lo, hi))

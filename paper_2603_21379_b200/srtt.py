@@ -152,6 +152,15 @@ def _L():
         lib.srtt_tucker_rel_error.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, i32, vp]
         lib.srtt_ht_reconstruct.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, vp, i32]
         lib.srtt_ht_rel_error.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, vp, i32, vp]
+        lib.srtt_comm_unique_id.argtypes = [vp]
+        lib.srtt_comm_init.argtypes = [vp, i32, i32, vp]
+        lib.srtt_comm_destroy.argtypes = [vp]
+        lib.srtt_comm_info.argtypes = [vp, vp, vp]
+        lib.srtt_split_bounds.argtypes = [i64, i32, i32, vp, vp]
+        lib.srtt_sub_r_hosvd_sharded.argtypes = [vp, vp, i32, i32, vp, i64, i64, vp, i64, vp, u64, vp, vp, vp, i32,
+                                                 vp]
+        lib.srtt_sub_r_rtl_ht_sharded.argtypes = [vp, vp, i32, i32, vp, i64, i64, vp, vp, vp, i64, u64, vp, vp, vp,
+                                                  i32, vp]
         _LIB = lib
     return _LIB
 

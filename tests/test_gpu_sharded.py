@@ -138,3 +138,113 @@ def test_orchestrator_nccl_world1():
     env = dict(os.environ, ROOT=ROOT, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     r = subprocess.run([sys.executable, "-c", _NCCL_SCRIPT], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
+# ---------------------------------------------------------------------------
+# H-Tucker column-range sharding: phases emulated rank by rank on one GPU
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dims,r,p,w,seed,W", [((6, 5, 7, 4), 3, 4, 24, 1, 3), ((5, 4, 6, 3, 4, 5), 3, 4, 30, 2, 4),
+                                                ((12,) * 6, 4, 5, 40, 0, 5)])
+def test_ht_sharded_phases_match_oracle(dims, r, p, w, seed, W, O):
+    """Each rank's srtt_ht_shard_sketches / srtt_ht_shard_root on its column
+    range of M, the exchanges (sums) done here: the reduced sketches equal the
+    oracle's node sketches, and the bases / transfers / root give the
+    oracle's decomposition (htucker.hpp:210-341)."""
+    import torch
+
+    from paper_2603_21379_b200 import sharded
+    from parity import aligned_core_error
+
+    tree = O.DimensionTree.balanced(len(dims))
+    ranks = O.uniform_node_ranks(tree, r)
+    samples = [1] + [min(w, tree.node_cols(i, dims)) for i in range(1, tree.num_nodes)]
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(dims)
+    xf = torch.from_numpy(np.ravel(x, order="F").copy()).cuda()
+    ph = sharded.GpuHtShardPhases()
+    bounds = [sharded.column_bounds(tree, dims, W, g) for g in range(W)]
+    nl, nr = bounds[0][2], bounds[0][3]
+    parts = [ph.shard_sketches(xf[lo * nl:hi * nl].contiguous(), dims, tree, lo, hi, ranks, p, samples, seed)
+             for lo, hi, _, _ in bounds]
+    zs = {i: sum(pp[i] for pp in parts) for i in range(1, tree.num_nodes)}
+    orep = O.HtSubsampleReport()
+    ref = O.sub_r_rtl_ht(x, tree, ranks, samples, p, seed, report=orep)
+    for i in range(1, tree.num_nodes):
+        zr = orep.sketches[i]
+        zg = zs[i].cpu().numpy().reshape(zr.shape, order="F")
+        assert np.linalg.norm(zg - zr) <= 1e-13 * np.linalg.norm(zr), i
+    us, bs, ach = ph.bases_from_sketches(dims, tree, ranks, p, samples, seed, zs)
+    assert ach == orep.achieved_ranks
+    ub = {i: us[i].cpu().numpy().reshape(orep.bases[i].shape, order="F") for i in us}
+    for i in ub:
+        assert np.linalg.norm(ub[i] @ ub[i].T - orep.bases[i] @ orep.bases[i].T) <= 1e-10
+    root = tree.node(0)
+    b0 = sum(ph.shard_root(xf[lo * nl:hi * nl].contiguous(), nl, nr, lo, hi, us[root.left], r, us[root.right], r)
+             for lo, hi, _, _ in bounds)
+    b0 = b0.cpu().numpy().reshape((1, r, r), order="F")
+    one = np.ones((1, 1))
+    assert aligned_core_error(b0, [one, ub[root.left], ub[root.right]], ref.transfers[0],
+                              [one, orep.bases[root.left], orep.bases[root.right]]) <= 1e-10
+    for i, b in bs.items():
+        n = tree.node(i)
+        bt = b.cpu().numpy().reshape(ref.transfers[i].shape, order="F")
+        assert aligned_core_error(bt, [ub[i], ub[n.left], ub[n.right]], ref.transfers[i],
+                                  [orep.bases[i], orep.bases[n.left], orep.bases[n.right]]) <= 1e-10
+
+
+# ---------------------------------------------------------------------------
+# Fused NCCL entries (srtt_sub_r_hosvd_sharded / srtt_sub_r_rtl_ht_sharded)
+# ---------------------------------------------------------------------------
+def test_fused_nccl_world1_equals_single_gpu(O):
+    """World 1: the slab is the whole tensor and the allreduces are copies,
+    so the fused sharded decompositions (kernels + NCCL captured in one CUDA
+    graph) return BITWISE the single-GPU results; replays too."""
+    import torch
+
+    import paper_2603_21379_b200 as P
+    from paper_2603_21379_b200 import sharded
+
+    h = P.Handle(0, use_graphs=True)
+    sharded.comm_init_local(h)
+    assert sharded.comm_info(h) == (1, 0)
+    h.set_stream(torch.cuda.current_stream().cuda_stream)
+    dims, ranks, p, samples, seed = [40, 36, 30], [6, 5, 6], 5, [44, 40, 44], 3
+    x = torch.from_numpy(np.ravel(np.random.default_rng(2).standard_normal(dims), order="F").copy()).cuda()
+    single = P.sub_r_hosvd(x, ranks, p, samples, seed, dims=dims, device_out=True, handle=P.Handle(0))
+    rep = P.SubsampleReport()
+    t = sharded.sub_r_hosvd_nccl(x, dims, ranks, p, samples, seed, handle=h, report=rep)
+    assert rep.achieved_ranks == ranks and rep.timings["gather"] > 0
+    for _ in range(3):  # graph replays (stream-ordered)
+        t = sharded.sub_r_hosvd_nccl(x, dims, ranks, p, samples, seed, handle=h)
+    torch.cuda.synchronize()
+    assert torch.equal(t.core, single.core)
+    assert all(torch.equal(a, b) for a, b in zip(t.factors, single.factors))
+
+    tree = P.DimensionTree.balanced(4)
+    hd = [9, 8, 7, 6]
+    hr = P.uniform_node_ranks(tree, 3)
+    hs = [1] + [min(24, tree.node_cols(i, hd)) for i in range(1, tree.num_nodes)]
+    y = torch.from_numpy(np.ravel(np.random.default_rng(4).standard_normal(hd), order="F").copy()).cuda()
+    hs1 = P.sub_r_rtl_ht(y, tree, hr, hs, 4, 6, dims=hd, device_out=True, handle=P.Handle(0))
+    rep = P.HtSubsampleReport()
+    hs2 = sharded.sub_r_rtl_ht_nccl(y, hd, tree, hr, hs, 4, 6, handle=h, report=rep)
+    hs2 = sharded.sub_r_rtl_ht_nccl(y, hd, tree, hr, hs, 4, 6, handle=h)
+    torch.cuda.synchronize()
+    assert rep.achieved_ranks == [1] + [3] * 6
+    assert all(torch.equal(a, b) for a, b in zip(hs1.leaf_factors, hs2.leaf_factors))
+    assert all(torch.equal(a.reshape(-1), b) for a, b in zip(hs1.transfers, hs2.transfers) if a is not None)
+
+
+def test_fused_nccl_errors():
+    import torch
+
+    import paper_2603_21379_b200 as P
+    from paper_2603_21379_b200 import sharded
+
+    h = P.Handle(0)
+    x = torch.zeros(6 * 5 * 7, dtype=torch.float64, device="cuda")
+    with pytest.raises(P.InvalidArgument, match="no communicator"):
+        sharded.sub_r_hosvd_nccl(x, [6, 5, 7], [2, 2, 2], 2, [8, 8, 8], 0, handle=h)
+    sharded.comm_init_local(h)
+    with pytest.raises(P.InvalidArgument, match="more samples than fibers"):
+        sharded.sub_r_hosvd_nccl(x, [6, 5, 7], [2, 2, 2], 2, [99, 8, 8], 0, handle=h)

@@ -155,3 +155,137 @@ def test_slab_bounds_match_sliced_core():
             assert max(h - l for l, h in b) - min(h - l for l, h in b) <= 1
     with pytest.raises(ValueError):
         sharded.slab_bounds(3, 4, 0)
+
+
+# ---------------------------------------------------------------------------
+# H-Tucker: column ranges of the root matricization (htucker.hpp:210-341)
+# ---------------------------------------------------------------------------
+class OracleHtPhases:
+    """srtt_ht_shard_sketches / srtt_ht_bases_from_sketches /
+    srtt_ht_shard_root restated on the oracle (CPU torch tensors in/out):
+    sketch entries outside this rank's flat range contribute zero."""
+
+    def __init__(self):
+        import srtt_oracle as O
+
+        self.O = O
+
+    def _stream(self, dims, tree, i, w, c, seed):
+        O = self.O
+        rng = O.RngStream(seed, i)
+        cols = O.sample_indices(tree.node_cols(i, dims), w, rng)
+        return rng, cols, O.gaussian_matrix(w, c, rng)
+
+    def shard_sketches(self, x_cols, dims, tree, lo, hi, ranks, p, samples, seed):
+        O = self.O
+        nl = tree.node_rows(tree.node(0).left, dims)
+        flo, fhi = lo * nl, hi * nl
+        xl = x_cols.numpy()
+        zs = {}
+        for i in range(1, tree.num_nodes):
+            _, cols, omega = self._stream(dims, tree, i, samples[i], ranks[i] + p, seed)
+            offs = O.group_fiber_offsets(dims, tree.node(i).modes, cols)
+            inside = (offs >= flo) & (offs < fhi)
+            y = np.where(inside, xl[np.clip(offs - flo, 0, xl.size - 1)], 0.0)
+            zs[i] = torch.from_numpy(np.ravel(y @ omega, order="F").copy())
+        return zs
+
+    def bases_from_sketches(self, dims, tree, ranks, p, samples, seed, zs):
+        O = self.O
+        us, ach = {}, [1] + [0] * (tree.num_nodes - 1)
+        for i in range(1, tree.num_nodes):
+            c = ranks[i] + p
+            rng, _, _ = self._stream(dims, tree, i, samples[i], c, seed)
+            z = zs[i].numpy().reshape((tree.node_rows(i, dims), c), order="F")
+            b = O.range_basis_of_sketch(z, ranks[i], rng)
+            us[i] = b.q
+            ach[i] = b.numerical_rank
+        bs = {}
+        for i in range(1, tree.num_nodes):
+            n = tree.node(i)
+            if not n.is_leaf():
+                bs[i] = torch.from_numpy(np.ravel(O.transfer_tensor(us[i], us[n.left], us[n.right]), order="F").copy())
+        return {i: torch.from_numpy(np.ravel(u, order="F").copy()) for i, u in us.items()}, bs, ach
+
+    def shard_root(self, x_cols, nl, nr, lo, hi, u_left, rl, u_right, rr):
+        m = x_cols.numpy().reshape((nl, hi - lo), order="F")
+        ul = u_left.numpy().reshape((nl, rl), order="F")
+        ur = u_right.numpy().reshape((nr, rr), order="F")[lo:hi]
+        return torch.from_numpy(np.ravel(ul.T @ m @ ur, order="F").copy())
+
+
+def _ht_worker(rank, world, port, case, q):
+    try:
+        for p in (ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests")):
+            if p not in sys.path:
+                sys.path.insert(0, p)
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import srtt_oracle as O
+        from paper_2603_21379_b200 import sharded
+        from test_sharded_gloo import OracleHtPhases
+
+        dims, r, p, w, seed = case
+        tree = O.DimensionTree.balanced(len(dims))
+        ranks = O.uniform_node_ranks(tree, r)
+        samples = [1] + [min(w, tree.node_cols(i, dims)) for i in range(1, tree.num_nodes)]
+        x = np.random.default_rng(5).standard_normal(dims)
+        lo, hi, nl, nr = sharded.column_bounds(tree, dims, world, rank)
+        xc = torch.from_numpy(np.ravel(x, order="F")[lo * nl:hi * nl].copy())
+        h = sharded.sub_r_rtl_ht_sharded(xc, dims, tree, ranks, samples, p, seed, phases=OracleHtPhases())
+        q.put((rank, [u.numpy() for u in h.leaf_factors],
+               [None if t is None else t.numpy() for t in h.transfers], h.achieved_ranks, h.columns))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        import traceback
+
+        q.put((rank, traceback.format_exc(), None, None, None))
+
+
+HT_CASES = [
+    ((4, 5, 3, 6), 2, 2, 12, 3),        # n_right = 18 columns -> 9 | 9
+    ((3, 4, 2, 5, 3), 2, 2, 14, 8),     # order 5, n_right = 30 ... ragged tree
+]
+
+
+@pytest.mark.parametrize("case", HT_CASES)
+def test_htucker_sharded_matches_single_process(case, O):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ht_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=240)
+        res[r[0]] = r
+    for pr in procs:
+        pr.join(timeout=60)
+    for r in range(world):
+        assert not isinstance(res[r][1], str), res[r][1]
+    dims, rk, p, w, seed = case
+    tree = O.DimensionTree.balanced(len(dims))
+    ranks = O.uniform_node_ranks(tree, rk)
+    samples = [1] + [min(w, tree.node_cols(i, dims)) for i in range(1, tree.num_nodes)]
+    x = np.random.default_rng(5).standard_normal(dims)
+    orep = O.HtSubsampleReport()
+    ref = O.sub_r_rtl_ht(x, tree, ranks, samples, p, seed, report=orep)
+    for r in range(world):
+        _, leaf, trs, ach, cols = res[r]
+        assert ach == orep.achieved_ranks
+        for m in range(len(dims)):
+            u = leaf[m].reshape((dims[m], ranks[[i for i in tree.leaves() if tree.node(i).modes[0] == m][0]]),
+                                order="F")
+            assert np.linalg.norm(u @ u.T - ref.leaf_factors[m] @ ref.leaf_factors[m].T) < 1e-9
+        hd = O.HTuckerDecomposition(tree, [leaf[m].reshape(ref.leaf_factors[m].shape, order="F")
+                                           for m in range(len(dims))],
+                                    [None if t is None else t.reshape(ref.transfers[i].shape, order="F")
+                                     for i, t in enumerate(trs)])
+        e1 = O.rel_error(x, O.ht_reconstruct(hd))
+        e2 = O.rel_error(x, O.ht_reconstruct(ref))
+        assert abs(e1 - e2) <= 1e-10 * max(e2, 1.0)
+    np.testing.assert_array_equal(res[0][2][0], res[1][2][0])   # same root on both ranks
+    assert res[0][4][0] == 0 and res[0][4][1] == res[1][4][0]
