@@ -366,9 +366,10 @@ class GpuHtShardPhases:
               for i in range(1, nn)}
         zp = (C.c_void_p * nn)(*([None] + [zs[i].data_ptr() for i in range(1, nn)]))
         ct = tree._c()
-        _s._check(self.lib.srtt_ht_shard_sketches(self.h._h, x_cols.data_ptr(), 1, len(dims), _s._i64(dims).ctypes.data,
-                                                  lo, hi, C.byref(ct), _s._i64(ranks).ctypes.data,
-                                                  _s._i64(samples).ctypes.data, p, seed, None, zp, 1))
+        dims_a, ranks_a, samp_a = _s._i64(dims), _s._i64(ranks), _s._i64(samples)  # alive across the call
+        _s._check(self.lib.srtt_ht_shard_sketches(self.h._h, x_cols.data_ptr(), 1, len(dims), dims_a.ctypes.data,
+                                                  lo, hi, C.byref(ct), ranks_a.ctypes.data, samp_a.ctypes.data, p,
+                                                  seed, None, zp, 1))
         return zs
 
     def bases_from_sketches(self, dims, tree, ranks, p, samples, seed, zs):
@@ -390,9 +391,10 @@ class GpuHtShardPhases:
         bp = (C.c_void_p * nn)(*[bs[i].data_ptr() if i in bs else None for i in range(nn)])
         ach = np.zeros(nn, np.int64)
         ct = tree._c()
-        _s._check(self.lib.srtt_ht_bases_from_sketches(self.h._h, len(dims), _s._i64(dims).ctypes.data, C.byref(ct),
-                                                       _s._i64(ranks).ctypes.data, _s._i64(samples).ctypes.data, p,
-                                                       seed, None, zp, 1, up, bp, 1, ach.ctypes.data))
+        dims_a, ranks_a, samp_a = _s._i64(dims), _s._i64(ranks), _s._i64(samples)  # alive across the call
+        _s._check(self.lib.srtt_ht_bases_from_sketches(self.h._h, len(dims), dims_a.ctypes.data, C.byref(ct),
+                                                       ranks_a.ctypes.data, samp_a.ctypes.data, p, seed, None, zp, 1,
+                                                       up, bp, 1, ach.ctypes.data))
         return us, bs, [int(a) for a in ach]
 
     def shard_root(self, x_cols, nl, nr, lo, hi, u_left, rl, u_right, rr):

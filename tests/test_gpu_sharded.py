@@ -155,16 +155,19 @@ def test_ht_sharded_phases_match_oracle(dims, r, p, w, seed, W, O):
     from paper_2603_21379_b200 import sharded
     from parity import aligned_core_error
 
+    import paper_2603_21379_b200 as P
+
     tree = O.DimensionTree.balanced(len(dims))
+    ptree = P.DimensionTree.balanced(len(dims))
     ranks = O.uniform_node_ranks(tree, r)
     samples = [1] + [min(w, tree.node_cols(i, dims)) for i in range(1, tree.num_nodes)]
     rng = np.random.default_rng(seed)
     x = rng.standard_normal(dims)
     xf = torch.from_numpy(np.ravel(x, order="F").copy()).cuda()
     ph = sharded.GpuHtShardPhases()
-    bounds = [sharded.column_bounds(tree, dims, W, g) for g in range(W)]
+    bounds = [sharded.column_bounds(ptree, dims, W, g) for g in range(W)]
     nl, nr = bounds[0][2], bounds[0][3]
-    parts = [ph.shard_sketches(xf[lo * nl:hi * nl].contiguous(), dims, tree, lo, hi, ranks, p, samples, seed)
+    parts = [ph.shard_sketches(xf[lo * nl:hi * nl].contiguous(), dims, ptree, lo, hi, ranks, p, samples, seed)
              for lo, hi, _, _ in bounds]
     zs = {i: sum(pp[i] for pp in parts) for i in range(1, tree.num_nodes)}
     orep = O.HtSubsampleReport()
@@ -173,7 +176,7 @@ def test_ht_sharded_phases_match_oracle(dims, r, p, w, seed, W, O):
         zr = orep.sketches[i]
         zg = zs[i].cpu().numpy().reshape(zr.shape, order="F")
         assert np.linalg.norm(zg - zr) <= 1e-13 * np.linalg.norm(zr), i
-    us, bs, ach = ph.bases_from_sketches(dims, tree, ranks, p, samples, seed, zs)
+    us, bs, ach = ph.bases_from_sketches(dims, ptree, ranks, p, samples, seed, zs)
     assert ach == orep.achieved_ranks
     ub = {i: us[i].cpu().numpy().reshape(orep.bases[i].shape, order="F") for i in us}
     for i in ub:
