@@ -514,8 +514,27 @@ def run_product(args):
         torch.distributed.destroy_process_group()
 
 
+def _local_part(cfg, x_full, world, rank, P, sharded):
+    """This rank's part of the ONE global tensor: Tucker -> last-mode slab
+    X[..., lo:hi) (parallel.hpp:400-404 bounds); H-Tucker -> columns
+    [c_lo, c_hi) of the root matricization. Both are contiguous byte ranges."""
+    dims = list(cfg.dims)
+    if cfg.kind == "tucker":
+        lo, hi = sharded.slab_bounds(dims[-1], world, rank)
+        inner = cfg.entries // dims[-1]
+        return x_full[lo * inner:hi * inner].clone(), (lo, hi)
+    tree = P.DimensionTree.balanced(cfg.order)
+    lo, hi, nl, _ = sharded.column_bounds(tree, dims, world, rank)
+    return x_full[lo * nl:hi * nl].clone(), (lo, hi)
+
+
 def run_sharded(args):
-    """One slab-sharded decomposition per step (Tucker configs)."""
+    """ONE decomposition of the config's global tensor per step, split over
+    the ranks (strong scaling): each rank holds only its contiguous part
+    (Tucker: last-mode slab; H-Tucker: a column range of the root
+    matricization) and calls the fused C-ABI entry (srtt_sub_r_hosvd_sharded /
+    srtt_sub_r_rtl_ht_sharded) whose handle owns an NCCL communicator;
+    kernels and the two allreduces run in one CUDA graph per rank."""
     import torch
     import torch.distributed as dist
 
@@ -531,22 +550,47 @@ def run_sharded(args):
     from paper_2603_21379_b200 import sharded, synth
 
     cfg = synth.CONFIGS[args.config]
-    if cfg.kind != "tucker":
-        raise SystemExit("--mode sharded runs the Tucker configs (c1, c2, c3, c5)")
-    dims = list(cfg.dims[:-1]) + [cfg.dims[-1] * world]
-    x_local = synth.make_tensor(cfg, seed=rank, backend="torch", device=f"cuda:{local}")   # this rank's slab
-    h = P.Handle(local, use_graphs=False)
+    dims = list(cfg.dims)
+    # every rank generates the SAME global tensor (seed 0, deterministic
+    # generator) and keeps only its part
+    x_full = synth.make_tensor(cfg, seed=0, backend="torch", device=f"cuda:{local}")
+    x_loc, part = _local_part(cfg, x_full, world, rank, P, sharded)
+    del x_full
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    h = P.Handle(local, use_graphs=True)
     stream = torch.cuda.current_stream()
     h.set_stream(stream.cuda_stream)
-    ph = sharded.GpuShardPhases(h)
-    ranks = [cfg.rank] * cfg.order
-    samples = [min(4 * (cfg.rank + cfg.p), int(np.prod(dims)) // n) for n in dims]
+    sharded.comm_init(h)
+    if cfg.kind == "tucker":
+        ranks = [cfg.rank] * cfg.order
+        samples = cfg.samples()
+        out = (torch.empty(cfg.rank ** cfg.order, dtype=torch.float64, device=dev),
+               [torch.empty(n * cfg.rank, dtype=torch.float64, device=dev) for n in dims])
 
-    def step():
-        return sharded.sub_r_hosvd_sharded(x_local, dims, ranks, cfg.p, samples, 0, phases=ph)
+        def step(report=None, x=x_loc, device_out=True):
+            return sharded.sub_r_hosvd_nccl(x, dims, ranks, cfg.p, samples, 0, handle=h, report=report,
+                                            out=out if device_out else None, device_out=device_out)
 
+        def digest(res):
+            return torch.cat([res.core.reshape(-1)] + [f.reshape(-1) for f in res.factors]).cpu()
+    else:
+        tree = P.DimensionTree.balanced(cfg.order)
+        ranks = P.uniform_node_ranks(tree, cfg.rank)
+        samples = [1] + [min(4 * (cfg.rank + cfg.p), tree.node_cols(i, dims)) for i in range(1, tree.num_nodes)]
+
+        def step(report=None, x=x_loc, device_out=True):
+            return sharded.sub_r_rtl_ht_nccl(x, dims, tree, ranks, samples, cfg.p, 0, handle=h, report=report,
+                                             device_out=device_out)
+
+        def digest(res):
+            return torch.cat([u.reshape(-1) for u in res.leaf_factors] +
+                             [t.reshape(-1) for t in res.transfers if t is not None]).cpu()
+
+    rep = P.SubsampleReport()
     for _ in range(args.warmup):
-        step()
+        step(report=rep)
+    launches_per_step = rep.launches
     dist.barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
@@ -554,23 +598,92 @@ def run_sharded(args):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
-        step()
+        res = step()
     ev1.record(stream)
     ev1.synchronize()
+    timed_digest = digest(res)
+    t_extra = time.perf_counter()
+    while len(sampler.samples) < 3 and time.perf_counter() - t_extra < 10:
+        step()
+        torch.cuda.synchronize()
     sampler.stop()
     el = torch.tensor([ev0.elapsed_time(ev1) / 1e3], dtype=torch.float64, device=dev)
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
     elapsed = float(el.item())
-    total = int(np.prod(dims))
-    line = {"metric": METRIC, "value": total * args.steps / elapsed, "unit": UNIT, "n_gpus": world,
+    # outputs of the last timed call == a synchronous call's, bit for bit
+    core_t = []
+    for _ in range(5):
+        r = P.SubsampleReport()
+        ref = step(report=r)
+        core_t.append(r.kernel_seconds.get("core", 0.0))
+    verified = bool(torch.equal(timed_digest, digest(ref)))
+    ok = torch.tensor([1.0 if verified else 0.0], device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    verified = bool(ok.item() == 1.0)
+
+    # e2e: the same call with this rank's part in pinned HOST memory and the
+    # outputs copied back to the host inside the timed region
+    xh = x_loc.cpu().pin_memory().numpy()
+    if 2 * x_loc.numel() * 8 > 0.6 * torch.cuda.get_device_properties(dev).total_memory:
+        del x_loc
+        torch.cuda.empty_cache()
+    step(x=xh, device_out=False)
+    e2e_steps = max(1, min(args.steps, 10))
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        step(x=xh, device_out=False)
+    e1.record(stream)
+    e1.synchronize()
+    e2e_el = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device=dev)
+    dist.all_reduce(e2e_el, op=dist.ReduceOp.MAX)
+    if cfg.kind == "tucker":
+        d2h = 8 * (cfg.rank ** cfg.order + sum(n * cfg.rank for n in dims))
+    else:
+        d2h = 8 * (sum(n * cfg.rank for n in dims) + (cfg.order - 2) * cfg.rank ** 3 + cfg.rank ** 2)
+
+    # roofline of this rank's core / root pass over its part
+    peaks, peak_kind = _peaks()
+    core_med = statistics.median(core_t)
+    local_cfg = _local_cfg(cfg, world, rank, P, sharded)
+    roofline = core_roofline(local_cfg, core_med, peaks, peak_kind)
+    roofline["kernel_share_of_step"] = core_med / (elapsed / args.steps)
+    roofline["per_rank_part"] = list(local_cfg.dims)
+    if world > 1:
+        roofline["traffic"] = None  # the committed ncu capture is of the single-GPU launch
+    line = {"metric": METRIC, "value": cfg.entries * args.steps / elapsed, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": dict(_config_dict(cfg), dims=dims, entries=total, parallelism=f"slab-sharded x{world}"),
-            "clocks": sampler.summary()}
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config_dict(cfg),
+            "parallelism": (f"{'slab' if cfg.kind == 'tucker' else 'column-range'}-sharded x{world} "
+                            f"(one global tensor; fused C-ABI + NCCL allreduce of sketches and core, one CUDA "
+                            f"graph per rank)"),
+            "clocks": sampler.summary(), "gpu_launches": launches_per_step * args.steps,
+            "outputs_verified": verified,
+            "e2e": {"value": cfg.entries * e2e_steps / float(e2e_el.item()), "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * int(np.prod(local_cfg.dims)), "d2h_bytes_per_step": d2h,
+                    "steps": e2e_steps, "per_rank": True},
+            "roofline": roofline}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    sharded.comm_destroy(h)
     dist.destroy_process_group()
+
+
+def _local_cfg(cfg, world, rank, P, sharded):
+    """A Config describing this rank's part (for the per-rank roofline)."""
+    import dataclasses
+
+    dims = list(cfg.dims)
+    if cfg.kind == "tucker":
+        lo, hi = sharded.slab_bounds(dims[-1], world, rank)
+        return dataclasses.replace(cfg, dims=tuple(dims[:-1] + [hi - lo]))
+    tree = P.DimensionTree.balanced(cfg.order)
+    lo, hi, nl, _ = sharded.column_bounds(tree, dims, world, rank)
+    # the root pass streams n_left x (hi - lo) entries: model it as a 2-mode part
+    return dataclasses.replace(cfg, dims=(nl, hi - lo))
 
 
 def _traffic_from_profiles(cfg_name):
@@ -591,14 +704,16 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default="c5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mode", choices=["replicas", "sharded"], default="replicas",
-                    help="N>1: independent replicas (default) or one slab-sharded tensor")
+    ap.add_argument("--mode", choices=["auto", "replicas", "sharded"], default="auto",
+                    help="auto: N=1 single-GPU decomposition, N>1 ONE global tensor sharded over the ranks "
+                         "(strong scaling); replicas: independent decompositions per rank (weak scaling); "
+                         "sharded: force the NCCL-sharded path (also at N=1)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    elif args.mode == "sharded":
+    elif args.mode == "sharded" or (args.mode == "auto" and _dist_env()[1] > 1):
         run_sharded(args)
     else:
         run_product(args)

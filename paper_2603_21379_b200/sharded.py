@@ -98,6 +98,10 @@ def new_unique_id() -> bytes:
     return bytes(uid.raw)
 
 
+def comm_destroy(handle: _s.Handle):
+    _s._check(_s._L().srtt_comm_destroy(handle._h))
+
+
 def comm_info(handle: _s.Handle):
     w, r = C.c_int32(), C.c_int32()
     _s._check(_s._L().srtt_comm_info(handle._h, C.byref(w), C.byref(r)))
@@ -114,12 +118,14 @@ def column_bounds(tree, dims, world: int, rank: int):
 
 
 def sub_r_hosvd_nccl(x_slab, dims, target, oversampling, samples, seed, *, handle, exec_policy=None,
-                     report=None, out=None):
+                     report=None, out=None, device_out=True):
     """Fused slab-sharded sub_r_hosvd through ``srtt_sub_r_hosvd_sharded``
     (the handle must own a communicator, see ``comm_init``). ``x_slab`` is
-    this rank's X[..., lo:hi) (flat CUDA float64, first index fastest) with
-    the bounds of ``slab_bounds``; returns identical device outputs on every
-    rank. Stream-ordered when no report is requested."""
+    this rank's X[..., lo:hi) (flat, first index fastest: a CUDA float64
+    tensor, or a host numpy array staged by the library) with the bounds of
+    ``slab_bounds``; returns identical outputs on every rank (device tensors,
+    or numpy arrays with ``device_out=False``). Stream-ordered when the
+    outputs stay on the device and no report is requested."""
     import torch
 
     world, me = comm_info(handle)
@@ -131,18 +137,23 @@ def sub_r_hosvd_nccl(x_slab, dims, target, oversampling, samples, seed, *, handl
     if call is None:
         call = _s._CALLS.setdefault(("sh",) + (tuple(dims), tuple(target), tuple(samples)),
                                     _s._TuckerCall(dims, target, samples))
+    xf = _s._flat_f64(x_slab)
+    xp, xdev = _s._ptr(xf)
     if out is None:
-        dev = x_slab.device
-        out = (torch.empty(int(np.prod(target)), dtype=torch.float64, device=dev),
-               [torch.empty(dims[k] * target[k], dtype=torch.float64, device=dev) for k in range(d)])
+        if device_out:
+            dev = torch.device("cuda", handle.device)
+            out = (torch.empty(int(np.prod(target)), dtype=torch.float64, device=dev),
+                   [torch.empty(dims[k] * target[k], dtype=torch.float64, device=dev) for k in range(d)])
+        else:
+            out = (np.zeros(int(np.prod(target))), [np.zeros(dims[k] * target[k]) for k in range(d)])
     for k in range(d):
-        call.fptrs[k] = out[1][k].data_ptr()
+        call.fptrs[k] = _s._ptr(out[1][k])[0]
     ex = exec_policy._c() if exec_policy is not None else None
-    rep_arg = C.byref(call.rep) if report is not None else None
+    rep_arg = C.byref(call.rep) if (report is not None or not device_out) else None
     _s._check(_s._L().srtt_sub_r_hosvd_sharded(
-        handle._h, x_slab.data_ptr(), 1, d, call.dims_a.ctypes.data, lo, hi, call.ranks_a.ctypes.data,
+        handle._h, xp, xdev, d, call.dims_a.ctypes.data, lo, hi, call.ranks_a.ctypes.data,
         int(oversampling), call.samp_a.ctypes.data, int(seed) & (2**64 - 1), C.byref(ex) if ex is not None else None,
-        out[0].data_ptr(), call.fptrs, 1, rep_arg))
+        _s._ptr(out[0])[0], call.fptrs, int(device_out), rep_arg))
     if report is not None:
         _s._report_from(call.rep, d, call.ach, call.sc, report, handle)
     return ShardedTucker(core=out[0], factors=list(out[1]), achieved_ranks=list(getattr(report, "achieved_ranks", [])),
@@ -150,7 +161,7 @@ def sub_r_hosvd_nccl(x_slab, dims, target, oversampling, samples, seed, *, handl
 
 
 def sub_r_rtl_ht_nccl(x_cols, dims, tree, ranks, samples, oversampling, seed, *, handle, exec_policy=None,
-                      report=None):
+                      report=None, device_out=True):
     """Fused column-range-sharded sub_r_rtl_ht through
     ``srtt_sub_r_rtl_ht_sharded``; ``x_cols`` holds this rank's columns
     [c_lo, c_hi) of M = n_left x n_right (``column_bounds``). Returns device
@@ -164,19 +175,24 @@ def sub_r_rtl_ht_nccl(x_cols, dims, tree, ranks, samples, oversampling, seed, *,
     d = len(dims)
     lo, hi, nl, nr = column_bounds(tree, dims, world, me)
     nn = tree.num_nodes
-    dev = x_cols.device
+    dev = torch.device("cuda", handle.device)
+
+    def alloc(n):
+        return torch.empty(n, dtype=torch.float64, device=dev) if device_out else np.zeros(n)
+
     leaf = [None] * d
     for i in tree.leaves():
         m = tree.node(i).modes[0]
-        leaf[m] = torch.empty(dims[m] * ranks[i], dtype=torch.float64, device=dev)
+        leaf[m] = alloc(dims[m] * ranks[i])
     trs = [None] * nn
     for i in range(nn):
         n = tree.node(i)
         if not n.is_leaf():
-            trs[i] = torch.empty((1 if i == 0 else ranks[i]) * ranks[n.left] * ranks[n.right], dtype=torch.float64,
-                                 device=dev)
-    lp = (C.c_void_p * d)(*[u.data_ptr() for u in leaf])
-    tp = (C.c_void_p * nn)(*[None if t is None else t.data_ptr() for t in trs])
+            trs[i] = alloc((1 if i == 0 else ranks[i]) * ranks[n.left] * ranks[n.right])
+    lp = (C.c_void_p * d)(*[_s._ptr(u)[0] for u in leaf])
+    tp = (C.c_void_p * nn)(*[None if t is None else _s._ptr(t)[0] for t in trs])
+    xf = _s._flat_f64(x_cols)
+    xp, xdev = _s._ptr(xf)
     ranks_a, samp_a, dims_a = _s._i64(ranks), _s._i64(samples), _s._i64(dims)
     ach, sc = np.zeros(nn, np.int64), np.zeros(nn, np.int64)
     wbuf = C.create_string_buffer(8192)
@@ -185,9 +201,9 @@ def sub_r_rtl_ht_nccl(x_cols, dims, tree, ranks, samples, oversampling, seed, *,
     ct = tree._c()
     ex = exec_policy._c() if exec_policy is not None else None
     _s._check(_s._L().srtt_sub_r_rtl_ht_sharded(
-        handle._h, x_cols.data_ptr(), 1, d, dims_a.ctypes.data, lo, hi, C.byref(ct), ranks_a.ctypes.data,
+        handle._h, xp, xdev, d, dims_a.ctypes.data, lo, hi, C.byref(ct), ranks_a.ctypes.data,
         samp_a.ctypes.data, int(oversampling), int(seed) & (2**64 - 1), C.byref(ex) if ex is not None else None,
-        lp, tp, 1, C.byref(crep) if report is not None else None))
+        lp, tp, int(device_out), C.byref(crep) if (report is not None or not device_out) else None))
     if report is not None:
         _s._report_from(crep, nn, ach, sc, report, handle)
     return _s.HTuckerDecomposition(tree, leaf, trs)
