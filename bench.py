@@ -125,7 +125,7 @@ def _run_product(P, cfg, x, dims, seed, handle, device_out=True, report=None):
                              handle=handle, device_out=device_out, out=out)
     tree = P.DimensionTree.balanced(cfg.order)
     ranks = P.uniform_node_ranks(tree, cfg.rank)
-    samples = [1] + [min(4 * (cfg.rank + cfg.p), tree.node_cols(i, dims)) for i in range(1, tree.num_nodes)]
+    samples = cfg.node_samples(tree, dims)
     return P.sub_r_rtl_ht(x, tree, ranks, samples, cfg.p, seed, report=report, dims=dims, handle=handle,
                           device_out=device_out)
 
@@ -135,7 +135,7 @@ def _run_oracle(O, cfg, X, seed, policy=None):
         return O.sub_r_hosvd(X, [cfg.rank] * cfg.order, cfg.p, cfg.samples(), seed, exec_policy=policy)
     tree = O.DimensionTree.balanced(cfg.order)
     ranks = O.uniform_node_ranks(tree, cfg.rank)
-    samples = [1] + [min(4 * (cfg.rank + cfg.p), tree.node_cols(i, X.shape)) for i in range(1, tree.num_nodes)]
+    samples = cfg.node_samples(tree, X.shape)
     return O.sub_r_rtl_ht(X, tree, ranks, samples, cfg.p, seed, exec_policy=policy)
 
 
@@ -356,7 +356,8 @@ def core_roofline(cfg, core_s, peaks, peak_kind):
 
 def _config_dict(cfg):
     return {"workload": cfg.name, "description": cfg.description, "dims": list(cfg.dims), "rank": cfg.rank,
-            "oversampling": cfg.p, "samples_per_target": 4 * (cfg.rank + cfg.p), "entries": cfg.entries,
+            "oversampling": cfg.p,
+            "samples_per_target": (f"alpha={cfg.alpha} rule" if cfg.alpha else cfg.samples()[0]), "entries": cfg.entries,
             "bytes": cfg.entries * 8, "l2": "inputs larger than L2 (126 MB); no flush" if cfg.entries * 8 > 126e6
             else "input smaller than L2: 256 MB L2 flush between steps, inside the timed span"}
 
@@ -485,7 +486,8 @@ def run_product(args):
     if world > 1:
         torch.distributed.all_reduce(e2e_el, op=torch.distributed.ReduceOp.MAX)
     e2e_value = world * cfg.entries * e2e_steps / float(e2e_el.item())
-    samples_total = sum(4 * (cfg.rank + cfg.p) for _ in range(cfg.order))
+    samples_total = (sum(cfg.samples()) if cfg.kind == "tucker"
+                     else sum(cfg.node_samples(P.DimensionTree.balanced(cfg.order), dims)[1:]))
     if cfg.kind == "tucker":
         d2h = 8 * (cfg.rank ** cfg.order + sum(n * cfg.rank for n in dims))
     else:
@@ -577,7 +579,7 @@ def run_sharded(args):
     else:
         tree = P.DimensionTree.balanced(cfg.order)
         ranks = P.uniform_node_ranks(tree, cfg.rank)
-        samples = [1] + [min(4 * (cfg.rank + cfg.p), tree.node_cols(i, dims)) for i in range(1, tree.num_nodes)]
+        samples = cfg.node_samples(tree, dims)
 
         def step(report=None, x=x_loc, device_out=True):
             return sharded.sub_r_rtl_ht_nccl(x, dims, tree, ranks, samples, cfg.p, 0, handle=h, report=report,
@@ -702,7 +704,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default="c5")
+    ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5", "c4a20", "c5s64k"], default="c5",
+                    help="c1-c5: BASELINE.json configs; c4a20 / c5s64k: sketch-heavy variants ADDED for the K1 "
+                         "bandwidth measurement (not BASELINE configs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", choices=["auto", "replicas", "sharded"], default="auto",
                     help="auto: N=1 single-GPU decomposition, N>1 ONE global tensor sharded over the ranks "

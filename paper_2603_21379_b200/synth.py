@@ -23,6 +23,9 @@ class Config:
     rank: int
     p: int
     description: str
+    base: str = ""       # tensor family (added variants reuse a BASELINE config's generator)
+    fibres: int = 0      # Tucker: fibres per mode (0: the 4 (r + p) rule)
+    alpha: float = 0.0   # H-Tucker: node budgets w_S = min(ceil(alpha n_S), n_notS) (0: 4 (r + p))
 
     @property
     def order(self):
@@ -32,9 +35,26 @@ class Config:
     def entries(self):
         return int(np.prod(self.dims))
 
+    @property
+    def family(self):
+        return self.base or self.name
+
     def samples(self):
         """s = 4 (r + p) per mode (explicit for C1, assumed for the rest)."""
-        return [4 * (self.rank + self.p)] * self.order
+        return [self.fibres or 4 * (self.rank + self.p)] * self.order
+
+    def node_samples(self, tree, dims=None):
+        """H-Tucker node budgets: min(4 (r + p), n_notS), or the alpha rule
+        of node_sample_counts (dimension_tree.hpp:174-183); root entry 1."""
+        import math
+
+        dims = list(dims or self.dims)
+        out = [1]
+        for i in range(1, tree.num_nodes):
+            cols = tree.node_cols(i, dims)
+            want = math.ceil(self.alpha * tree.node_rows(i, dims)) if self.alpha else 4 * (self.rank + self.p)
+            out.append(min(want, cols))
+        return out
 
 
 CONFIGS = {
@@ -48,6 +68,14 @@ CONFIGS = {
                  "order-8 H-Tucker 12^8, sum of 10 rank-1 Gaussian terms + 1e-8 relative noise, r=10 p=5 w=60"),
     "c5": Config("c5", "tucker", (2048, 2048, 2048), 32, 10,
                  "order-3 Tucker 2048^3, rank-32 N(0,1) core + Gaussian-QR factors + 1e-6 relative noise, r=32 p=10 s=168"),
+    # ---- sketch-heavy variants ADDED for the K1 bandwidth measurement
+    # (SURVEY §8d); NOT BASELINE configs
+    "c4a20": Config("c4a20", "htucker", (12,) * 8, 10, 5,
+                    "ADDED variant of c4: node budgets by alpha = 20 (dimension_tree.hpp:174-183), so both "
+                    "level-1 nodes sample all 20736 columns", base="c4", alpha=20.0),
+    "c5s64k": Config("c5s64k", "tucker", (2048, 2048, 2048), 32, 10,
+                     "ADDED variant of c5: s = 65536 fibres per mode (1.07 GB gathered per mode)", base="c5",
+                     fibres=65536),
 }
 
 
@@ -163,16 +191,17 @@ def make_tensor(cfg: Config, seed: int = 0, backend: str = "torch", device: str 
     with smaller `dims` of the same family for tests)."""
     dims = tuple(dims or cfg.dims)
     d = len(dims)
-    if cfg.name == "c3":
+    fam = cfg.family
+    if fam == "c3":
         return _function_tensor(dims, backend, device)
     B = _backend(backend, seed, device)
     r = cfg.rank
-    if cfg.name in ("c1", "c5"):
+    if fam in ("c1", "c5"):
         core = B.randn(*([r] * d))
         factors = [B.qr_q(B.randn(n, r)) for n in dims]
         x = B.expand(core, factors)
-        return _add_relative_noise(B, x, 1e-8 if cfg.name == "c1" else 1e-6)
-    if cfg.name == "c2":
+        return _add_relative_noise(B, x, 1e-8 if fam == "c1" else 1e-6)
+    if fam == "c2":
         core = B.randn(*([r] * d))
         idx = np.indices([r] * d).sum(axis=0)
         scale = 10.0 ** (-idx / d)
@@ -187,7 +216,7 @@ def make_tensor(cfg: Config, seed: int = 0, backend: str = "torch", device: str 
         else:
             x.add_(B.randn(x.shape[0]), alpha=1e-10)
         return x
-    if cfg.name == "c4":
+    if fam == "c4":
         # sum of 10 rank-1 terms: core = superdiagonal of ones (10^d), factors a_t^(k)
         terms = 10
         vecs = [B.randn(n, terms) for n in dims]

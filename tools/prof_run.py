@@ -17,6 +17,6 @@ for i in range(reps):
     else:
         tree = P.DimensionTree.balanced(cfg.order)
         ranks = P.uniform_node_ranks(tree, cfg.rank)
-        samples = [1] + [min(4 * (cfg.rank + cfg.p), tree.node_cols(i, cfg.dims)) for i in range(1, tree.num_nodes)]
+        samples = cfg.node_samples(tree, cfg.dims)
         P.sub_r_rtl_ht(x, tree, ranks, samples, cfg.p, 0, report=rep, dims=list(cfg.dims), handle=h, device_out=True)
     print(i, {k: round(v * 1e6, 1) for k, v in rep.timings.items() if v}, {k: round(v * 1e6, 1) for k, v in rep.kernel_seconds.items()}, rep.launches, 'sweeps', getattr(rep, 'jacobi_sweeps', None))
