@@ -27,6 +27,7 @@
 // ---- kernel launchers (k_*.cu) ---------------------------------------------
 size_t srtt_sketch_smem_bytes(int cmax);
 cudaError_t srtt_launch_sketch(const SketchTarget*, int, int64_t, int, cudaStream_t);
+cudaError_t srtt_launch_sketch_reduce(const SketchTarget*, int, int64_t, cudaStream_t);
 size_t srtt_basis_top_smem(int m, int c, int r);
 size_t srtt_basis_level_smem(int mb, int c);
 cudaError_t srtt_launch_basis_top(int, const BasisTarget*, const int*, int, size_t, cudaStream_t);
@@ -930,6 +931,24 @@ void layout_core(Layout& L, CorePlan& cp, size_t& off_ufrag, std::vector<size_t>
 }
 
 // ---- sketch target construction ---------------------------------------------
+// Fibre chunks per K1 target: the grouped grid parallelises over rows only
+// when a target samples few fibres (BASELINE configs: w <= 168, one chunk,
+// direct write); a target with many fibres (sampling fractions of several
+// percent: c4a20, c5s64k) also splits its fibres over CTAs, >= 512 each,
+// until the target alone fills the GPU ~4 CTAs deep.
+int sketch_fsplit(int64_t rows, int64_t w) {
+  const int64_t rt = std::min<int64_t>(rows, 64);
+  const int64_t row_ctas = (rows + rt - 1) / rt;
+  const int64_t want = (4 * 148 + row_ctas - 1) / row_ctas;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(w / 512, want));
+}
+
+// Workspace for a target's fibre-chunk partials (0 when not split).
+size_t sketch_part_bytes(int64_t rows, int64_t w, int c) {
+  const int f = sketch_fsplit(rows, w);
+  return f > 1 ? sizeof(double) * (size_t)f * rows * c : 0;
+}
+
 SketchTarget make_sketch_target(const double* x, const std::vector<int64_t>& dims,
                                 const std::vector<int>& modes, int64_t w, int c) {
   SketchTarget T{};
@@ -960,7 +979,26 @@ SketchTarget make_sketch_target(const double* x, const std::vector<int64_t>& dim
   T.c = c;
   T.row_tile = (int)std::min<int64_t>(T.rows, 64);
   T.slab_digit = -1;
+  T.fsplit = sketch_fsplit(T.rows, w);
   return T;
+}
+
+// CTAs of one target in the grouped K1 grid.
+int64_t sketch_target_ctas(const SketchTarget& T) {
+  return (T.rows + T.row_tile - 1) / T.row_tile * T.fsplit;
+}
+
+// K1 over a group of targets (device array dT, host copy sk), plus the
+// fixed-order reduction of the fibre-chunk partials when any target is split.
+int launch_sketch_group(const SketchTarget* dT, const std::vector<SketchTarget>& sk, int64_t ctas, int cmax,
+                        cudaStream_t st) {
+  CK(srtt_launch_sketch(dT, (int)sk.size(), ctas, cmax, st));
+  int64_t split_elems = 0;
+  for (auto& t : sk)
+    if (t.fsplit > 1) split_elems = std::max<int64_t>(split_elems, t.rows * t.c);
+  if (!split_elems) return 1;
+  CK(srtt_launch_sketch_reduce(dT, (int)sk.size(), split_elems, st));
+  return 2;
 }
 
 // ---- report helpers ------------------------------------------------------------
@@ -1289,7 +1327,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   if (std::getenv("SRTT_DEBUG_CALLS")) std::fprintf(stderr, "tucker call: full path, set %d\n", h->cur);
   // --- workspace layout
   Layout L;
-  std::vector<size_t> off_z(d), off_u(d);
+  std::vector<size_t> off_z(d), off_u(d), off_zp(d);
   std::vector<BasisPlan> bp(d);
   std::vector<BasisBuffers> bb(d);
   int cmax = 0;
@@ -1297,6 +1335,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     const int c = (int)(ranks[k] + p);
     cmax = std::max(cmax, c);
     off_z[k] = L.take(sizeof(double) * dims[k] * c);
+    off_zp[k] = L.take(sketch_part_bytes(dims[k], samples[k], c));
     off_u[k] = out_on_device ? 0 : L.take(sizeof(double) * dims[k] * ranks[k]);
     bp[k] = plan_basis(dims[k], c, (int)ranks[k]);
     bb[k] = layout_basis(L, bp[k]);
@@ -1344,7 +1383,8 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     sk[k].draw_offset = draws[k];
     sk[k].cta_begin = ctas;
     sk[k].flags = d_flags;
-    ctas += (sk[k].rows + sk[k].row_tile - 1) / sk[k].row_tile;
+    sk[k].zpart = reinterpret_cast<double*>(ws + off_zp[k]);
+    ctas += sketch_target_ctas(sk[k]);
     bt[k] = fill_basis(bp[k], bb[k], ws, sk[k].z, uptr[k], state0[k], draws[k], samples[k] * c, dinfo + 4 * k);
   }
   assign_basis_ctas(bt);
@@ -1369,8 +1409,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     tm.n = 2;
     tm.mark();  // 2
     // --- K1: grouped gather + sketch over all modes
-    CK(srtt_launch_sketch(reinterpret_cast<const SketchTarget*>(dp + off_sk), d, ctas, cmax, h->stream));
-    h->launches++;
+    h->launches += launch_sketch_group(reinterpret_cast<const SketchTarget*>(dp + off_sk), sk, ctas, cmax, h->stream);
     tm.mark();  // 3
     // --- K2: basis of every sketch
     h->launches += launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt), lists, dp,
@@ -1710,7 +1749,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   const double t_sampling = now_s() - ts0;
 
   Layout L;
-  std::vector<size_t> off_z(nt), off_u(nt);
+  std::vector<size_t> off_z(nt), off_u(nt), off_zp(nt);
   std::vector<BasisPlan> bp(nt);
   std::vector<BasisBuffers> bb(nt);
   int cmax = 0;
@@ -1722,6 +1761,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     cmax = std::max(cmax, c);
     max_n = std::max(max_n, rows);
     off_z[t] = L.take(sizeof(double) * rows * c);
+    off_zp[t] = L.take(sketch_part_bytes(rows, samples[id], c));
     off_u[t] = L.take(sizeof(double) * rows * ranks[id]);
     bp[t] = plan_basis(rows, c, (int)ranks[id]);
     bb[t] = layout_basis(L, bp[t]);
@@ -1775,7 +1815,8 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     sk[t].draw_offset = draws[t];
     sk[t].cta_begin = ctas;
     sk[t].flags = d_flags;
-    ctas += (sk[t].rows + sk[t].row_tile - 1) / sk[t].row_tile;
+    sk[t].zpart = reinterpret_cast<double*>(ws + off_zp[t]);
+    ctas += sketch_target_ctas(sk[t]);
     bt[t] = fill_basis(bp[t], bb[t], ws, sk[t].z, ubasis(id), state0[t], draws[t], samples[id] * c,
                        dinfo + 4 * t);
   }
@@ -1836,8 +1877,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemsetAsync(dinfo, 0, info_bytes, h->stream));
     tm.mark();  // 2
-    CK(srtt_launch_sketch(reinterpret_cast<const SketchTarget*>(dp + off_sk), nt, ctas, cmax, h->stream));
-    h->launches++;
+    h->launches += launch_sketch_group(reinterpret_cast<const SketchTarget*>(dp + off_sk), sk, ctas, cmax, h->stream);
     tm.mark();  // 3
     // fork: side stream takes the small targets
     CK(cudaEventRecord(h->fj[0], h->stream));
@@ -2054,8 +2094,9 @@ int srtt_sketch(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d,
     CK(cudaMemcpyAsync(B.idx.p, cols, sizeof(int64_t) * ncols, cudaMemcpyHostToDevice, h->stream));
     T.cols = reinterpret_cast<const int64_t*>(B.idx.p);
     if (omega) T.omega = to_device(h, B.c, omega, ncols * c, 0);
-    B.b.ensure(sizeof(double) * T.rows * c);
+    B.b.ensure(sizeof(double) * T.rows * c + sketch_part_bytes(T.rows, ncols, c));
     T.z = reinterpret_cast<double*>(B.b.p);
+    T.zpart = T.z + T.rows * c;
     T.state0 = srtt_host::stream_state0(seed, stream_id);
     T.draw_offset = draw_offset;
     B.e.ensure(sizeof(int32_t) * 4 + sizeof(SketchTarget));
@@ -2066,8 +2107,7 @@ int srtt_sketch(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d,
     B.d.ensure(sizeof(SketchTarget));
     dT = reinterpret_cast<SketchTarget*>(B.d.p);
     CK(cudaMemcpyAsync(dT, &T, sizeof(T), cudaMemcpyHostToDevice, h->stream));
-    const int64_t ctas = (T.rows + T.row_tile - 1) / T.row_tile;
-    CK(srtt_launch_sketch(dT, 1, ctas, c, h->stream));
+    launch_sketch_group(dT, {T}, sketch_target_ctas(T), c, h->stream);
     copy_out(h, z_out, T.z, sizeof(double) * T.rows * c, out_on_device);
     CK(cudaStreamSynchronize(h->stream));
   });
@@ -2265,13 +2305,14 @@ int srtt_shard_sketches(srtt_handle* h, const double* x_local, int32_t x_on_devi
     const double* x = to_device(h, B.a, x_local, Nl, x_on_device);
     const SampledModes S = sample_all_modes(d, dims, samples, seed, exec ? exec->index_partitions : 1);
     Layout Lw;
-    std::vector<size_t> off_z(d), off_cols(d);
+    std::vector<size_t> off_z(d), off_cols(d), off_zp(d);
     int cmax = 0;
     for (int k = 0; k < d; ++k) {
       const int c = (int)(ranks[k] + p);
       cmax = std::max(cmax, c);
       off_z[k] = Lw.take(sizeof(double) * (k == L ? ldims[k] : dims[k]) * c);
       off_cols[k] = Lw.take(sizeof(int64_t) * samples[k]);
+      off_zp[k] = Lw.take(sketch_part_bytes(k == L ? ldims[k] : dims[k], samples[k], c));
     }
     const size_t off_t = Lw.take(sizeof(SketchTarget) * d);
     const size_t off_flags = Lw.take(sizeof(int32_t) * 4);
@@ -2295,13 +2336,14 @@ int srtt_shard_sketches(srtt_handle* h, const double* x_local, int32_t x_on_devi
       sk[k].draw_offset = S.draws[k];
       sk[k].cta_begin = ctas;
       sk[k].flags = reinterpret_cast<int32_t*>(ws + off_flags);
-      ctas += (sk[k].rows + sk[k].row_tile - 1) / sk[k].row_tile;
+      sk[k].zpart = reinterpret_cast<double*>(ws + off_zp[k]);
+      ctas += sketch_target_ctas(sk[k]);
       CK(cudaMemcpyAsync(ws + off_cols[k], S.cols[k].data(), sizeof(int64_t) * samples[k], cudaMemcpyHostToDevice,
                          h->stream));
     }
     CK(cudaMemsetAsync(ws + off_flags, 0, sizeof(int32_t) * 4, h->stream));
     CK(cudaMemcpyAsync(ws + off_t, sk.data(), sizeof(SketchTarget) * d, cudaMemcpyHostToDevice, h->stream));
-    CK(srtt_launch_sketch(reinterpret_cast<const SketchTarget*>(ws + off_t), d, ctas, cmax, h->stream));
+    launch_sketch_group(reinterpret_cast<const SketchTarget*>(ws + off_t), sk, ctas, cmax, h->stream);
     for (int k = 0; k < d; ++k)
       copy_out(h, z_out[k], ws + off_z[k], sizeof(double) * sk[k].rows * sk[k].c, out_on_device);
     CK(cudaStreamSynchronize(h->stream));

@@ -48,7 +48,15 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
   const int JS = kThreads / RT;
   const int il = tid % RT;
   const int js = tid / RT;
-  const int64_t i = (int64_t)(blockIdx.x - T.cta_begin) * RT + il;
+  // CTA -> (row tile, fibre chunk)
+  const int64_t local = (int64_t)blockIdx.x - T.cta_begin;
+  const int64_t row_ctas = (T.rows + RT - 1) / RT;
+  const int64_t rt = local % row_ctas;
+  const int fchunk = (int)(local / row_ctas);
+  const int64_t flen = (T.w + T.fsplit - 1) / T.fsplit;
+  const int64_t jbeg = (int64_t)fchunk * flen;
+  const int64_t jend = srtt_dev::min64(T.w, jbeg + flen);
+  const int64_t i = rt * RT + il;
   const bool active = (js < JS) && (i < T.rows);
 
   double* om = reinterpret_cast<double*>(smem_raw);         // kChunk x c
@@ -75,8 +83,8 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
   // flat-range sharding: only [flo, fhi) of the global flat index is local
   const int64_t flo = T.flat_lo, fhi = T.flat_hi;
   const bool ranged = fhi > 0;
-  for (int64_t j0 = 0; j0 < T.w; j0 += kChunk) {
-    const int jn = (int)srtt_dev::min64(kChunk, T.w - j0);
+  for (int64_t j0 = jbeg; j0 < jend; j0 += kChunk) {
+    const int jn = (int)srtt_dev::min64(kChunk, jend - j0);
     __syncthreads();
     // Omega(j, cc) is normal number t = j + cc * w of the stream
     // (column-major gaussian_matrix fill, sampling.hpp:74-75).
@@ -149,15 +157,42 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
   const int64_t ldz = T.ldz > 0 ? T.ldz : T.rows;
   for (int idx = tid; idx < RT * c; idx += kThreads) {
     const int rl = idx % RT, cc = idx / RT;
-    const int64_t row = (int64_t)(blockIdx.x - T.cta_begin) * RT + rl;
+    const int64_t row = rt * RT + rl;
     if (row >= T.rows) continue;
     double s = 0.0;
     for (int g = 0; g < JS; ++g) s += red[(g * RT + rl) * c + cc];
-    T.z[row + (int64_t)cc * ldz] = s;
+    if (T.fsplit > 1)
+      T.zpart[((int64_t)fchunk * c + cc) * T.rows + row] = s;
+    else
+      T.z[row + (int64_t)cc * ldz] = s;
+  }
+}
+
+// Fixed-order sum of the fibre-chunk partials of the split targets.
+__global__ void __launch_bounds__(256) sketch_reduce_kernel(const SketchTarget* __restrict__ targets,
+                                                            int ntargets) {
+  for (int t = 0; t < ntargets; ++t) {
+    const SketchTarget& T = targets[t];
+    if (T.fsplit <= 1) continue;
+    const int64_t n = T.rows * T.c;
+    const int64_t ldz = T.ldz > 0 ? T.ldz : T.rows;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t row = e % T.rows, cc = e / T.rows;
+      double s = 0.0;
+      for (int f = 0; f < T.fsplit; ++f) s += T.zpart[((int64_t)f * T.c + cc) * T.rows + row];
+      T.z[row + cc * ldz] = s;
+    }
   }
 }
 
 }  // namespace
+
+cudaError_t srtt_launch_sketch_reduce(const SketchTarget* d_targets, int ntargets, int64_t max_elems,
+                                      cudaStream_t stream) {
+  const int grid = (int)srtt_dev::min64(4 * 148, (max_elems + 255) / 256);
+  sketch_reduce_kernel<<<grid > 0 ? grid : 1, 256, 0, stream>>>(d_targets, ntargets);
+  return cudaGetLastError();
+}
 
 size_t srtt_sketch_smem_bytes(int cmax) {
   return (size_t)kChunk * cmax * sizeof(double) + kChunk * sizeof(int64_t) +

@@ -170,6 +170,9 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
     cmax = std::max<int>(cmax, (int)(ranks[k] + p));
   }
   const size_t off_zsum = W.take(sizeof(double) * zn);
+  std::vector<size_t> off_zp(d);
+  for (int k = 0; k < d; ++k)
+    off_zp[k] = W.take(sketch_part_bytes(k == L ? nl : dims[k], samples[k], (int)(ranks[k] + p)));
   std::vector<size_t> off_u(d);
   std::vector<BasisPlan> bp(d);
   std::vector<BasisBuffers> bb(d);
@@ -226,7 +229,8 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
     sk[k].draw_offset = S.draws[k];
     sk[k].cta_begin = ctas;
     sk[k].flags = dinfo + 4 * d;
-    ctas += (sk[k].rows + sk[k].row_tile - 1) / sk[k].row_tile;
+    sk[k].zpart = reinterpret_cast<double*>(ws + off_zp[k]);
+    ctas += sketch_target_ctas(sk[k]);
     bt[k] = fill_basis(bp[k], bb[k], ws, zsum + zoff[k], uptr[k], S.state0[k], S.draws[k], samples[k] * c,
                        dinfo + 4 * k);
   }
@@ -254,8 +258,7 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
     CK(cudaMemsetAsync(zsum + zoff[L], 0, sizeof(double) * zL, h->stream));
     tm.n = 2;
     tm.mark();  // 2
-    CK(srtt_launch_sketch(reinterpret_cast<const SketchTarget*>(dp + off_sk), d, ctas, cmax, h->stream));
-    h->launches++;
+    h->launches += launch_sketch_group(reinterpret_cast<const SketchTarget*>(dp + off_sk), sk, ctas, cmax, h->stream);
     tm.mark();  // 3
     allreduce_sum(h, zsum, (size_t)zn);
     tm.mark();  // 4
@@ -321,7 +324,7 @@ struct HtShard {
   int64_t zn = 0, max_n = 0;
   int cmax = 0;
   size_t off_zsum = 0, off_pad = 0, off_urs = 0, off_root = 0;
-  std::vector<size_t> off_u, off_b;
+  std::vector<size_t> off_u, off_b, off_zp;
   std::vector<BasisPlan> bp;
   std::vector<BasisBuffers> bb;
   std::vector<int> internal;
@@ -434,6 +437,8 @@ struct HtShard {
       max_n = std::max(max_n, rows[i]);
     }
     off_zsum = W.take(sizeof(double) * zn);
+    off_zp.assign(nn, 0);
+    for (int i = 1; i < nn; ++i) off_zp[i] = W.take(sketch_part_bytes(rows[i], samples[i], (int)(ranks[i] + p)));
     for (int i = 1; i < nn; ++i) {
       off_u[i] = W.take(sizeof(double) * rows[i] * ranks[i]);
       bp[i] = plan_basis(rows[i], (int)(ranks[i] + p), (int)ranks[i]);
@@ -479,7 +484,8 @@ struct HtShard {
       sk[t].draw_offset = draws[t];
       sk[t].cta_begin = ctas;
       sk[t].flags = dinfo + 4 * nt;
-      ctas += (sk[t].rows + sk[t].row_tile - 1) / sk[t].row_tile;
+      sk[t].zpart = reinterpret_cast<double*>(ws + off_zp[id]);
+      ctas += sketch_target_ctas(sk[t]);
       bt[t] = fill_basis(bp[id], bb[id], ws, zsum() + zoff[id], ubasis(id), state0[t], draws[t], samples[id] * c,
                          dinfo + 4 * t);
     }
@@ -518,8 +524,7 @@ struct HtShard {
   }
   // Phase 1: partial sketches of every node (K1, one grouped launch).
   int enqueue_sketches(srtt_handle* h) const {
-    CK(srtt_launch_sketch(reinterpret_cast<const SketchTarget*>(dp + off_sk), nt, ctas, cmax, h->stream));
-    return 1;
+    return launch_sketch_group(reinterpret_cast<const SketchTarget*>(dp + off_sk), sk, ctas, cmax, h->stream);
   }
   // Phase 2: bases of every node (K2) and the internal transfers (K4).
   int enqueue_bases(srtt_handle* h) {

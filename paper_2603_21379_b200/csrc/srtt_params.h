@@ -46,6 +46,13 @@ typedef struct SketchTarget {
   // leading dimension of z (0: rows); lets a rank write its rows of a
   // row-distributed sketch into a zero-filled full-height buffer
   int64_t ldz;
+  // fibre split: the w fibres are cut into fsplit contiguous chunks handled
+  // by different CTAs (grid = row tiles x fsplit); each chunk's partial Z
+  // goes to zpart[(f * c + cc) * rows + i] and a second kernel sums the
+  // chunks in a fixed order (deterministic). fsplit = 1: direct write.
+  int32_t fsplit;
+  int32_t pad1;
+  double* zpart;
 } SketchTarget;
 
 // ---------------------------------------------------------------------------

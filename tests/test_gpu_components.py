@@ -46,7 +46,10 @@ def test_fiber_gathers_bitwise(handle, dims):
 @pytest.mark.parametrize("dims,modes,w,c", [((128, 128, 128), [0], 52, 13), ((128, 128, 128), [2], 52, 13),
                                             ((40,) * 5, [3], 44, 11), ((12,) * 6, [0, 1, 2], 60, 15),
                                             ((12,) * 6, [3, 4], 60, 15), ((9, 8, 7, 6), [1, 3], 25, 20),
-                                            ((30, 20, 10), [1], 200, 42)])
+                                            ((30, 20, 10), [1], 200, 42),
+                                            # many fibres: split over CTAs (fixed-order partial sums)
+                                            ((64, 80, 90), [0], 6000, 42), ((64, 80, 90), [1], 5000, 13),
+                                            ((12,) * 6, [0, 1, 2], 1728, 15), ((12,) * 6, [3, 4, 5], 1728, 15)])
 def test_fused_sketch_matches_oracle(handle, dims, modes, w, c):
     """K1: Z = Y(cols) Omega with Omega from the reference stream; Z within 1e-13."""
     x = rng.standard_normal(dims)
