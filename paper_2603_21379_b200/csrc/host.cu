@@ -28,6 +28,7 @@
 size_t srtt_sketch_smem_bytes(int cmax);
 cudaError_t srtt_launch_sketch(const SketchTarget*, int, int64_t, int, cudaStream_t);
 cudaError_t srtt_launch_sketch_reduce(const SketchTarget*, int, int64_t, cudaStream_t);
+cudaError_t srtt_launch_omega(const SketchTarget*, int, int64_t, cudaStream_t);
 size_t srtt_basis_top_smem(int m, int c, int r);
 size_t srtt_basis_level_smem(int mb, int c);
 cudaError_t srtt_launch_basis_top(int, const BasisTarget*, const int*, int, size_t, cudaStream_t);
@@ -943,10 +944,17 @@ int sketch_fsplit(int64_t rows, int64_t w) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(w / 512, want));
 }
 
-// Workspace for a target's fibre-chunk partials (0 when not split).
+// Workspace for a target's fibre-chunk partials (when split) and its
+// once-generated Omega (when more than one CTA would generate it), appended.
+bool sketch_omega_once(int64_t rows, int64_t w) {
+  const int64_t rt = std::min<int64_t>(rows, 64);
+  return (rows + rt - 1) / rt * sketch_fsplit(rows, w) > 1;
+}
 size_t sketch_part_bytes(int64_t rows, int64_t w, int c) {
   const int f = sketch_fsplit(rows, w);
-  return f > 1 ? sizeof(double) * (size_t)f * rows * c : 0;
+  const size_t part = f > 1 ? sizeof(double) * (size_t)f * rows * c : 0;
+  const size_t om = sketch_omega_once(rows, w) ? sizeof(double) * (size_t)w * c : 0;
+  return (part + 255) / 256 * 256 + om;
 }
 
 SketchTarget make_sketch_target(const double* x, const std::vector<int64_t>& dims,
@@ -992,13 +1000,33 @@ int64_t sketch_target_ctas(const SketchTarget& T) {
 // fixed-order reduction of the fibre-chunk partials when any target is split.
 int launch_sketch_group(const SketchTarget* dT, const std::vector<SketchTarget>& sk, int64_t ctas, int cmax,
                         cudaStream_t st) {
+  int n = 0;
+  int64_t om_elems = 0;
+  for (auto& t : sk)
+    if (t.omega_gen) om_elems = std::max<int64_t>(om_elems, t.w * t.c);
+  if (om_elems) {
+    CK(srtt_launch_omega(dT, (int)sk.size(), om_elems, st));
+    ++n;
+  }
   CK(srtt_launch_sketch(dT, (int)sk.size(), ctas, cmax, st));
+  ++n;
   int64_t split_elems = 0;
   for (auto& t : sk)
     if (t.fsplit > 1) split_elems = std::max<int64_t>(split_elems, t.rows * t.c);
-  if (!split_elems) return 1;
+  if (!split_elems) return n;
   CK(srtt_launch_sketch_reduce(dT, (int)sk.size(), split_elems, st));
-  return 2;
+  return n + 1;
+}
+
+// Points a target at its scratch (see sketch_part_bytes): fibre-chunk
+// partials and, when Omega is to be generated once, its buffer.
+void attach_sketch_scratch(SketchTarget& T, char* scratch) {
+  T.zpart = reinterpret_cast<double*>(scratch);
+  if (!T.omega && sketch_omega_once(T.rows, T.w)) {
+    const size_t part = T.fsplit > 1 ? sizeof(double) * (size_t)T.fsplit * T.rows * T.c : 0;
+    T.omega_gen = reinterpret_cast<double*>(scratch + (part + 255) / 256 * 256);
+    T.omega = T.omega_gen;
+  }
 }
 
 // ---- report helpers ------------------------------------------------------------
@@ -1383,7 +1411,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     sk[k].draw_offset = draws[k];
     sk[k].cta_begin = ctas;
     sk[k].flags = d_flags;
-    sk[k].zpart = reinterpret_cast<double*>(ws + off_zp[k]);
+    attach_sketch_scratch(sk[k], ws + off_zp[k]);
     ctas += sketch_target_ctas(sk[k]);
     bt[k] = fill_basis(bp[k], bb[k], ws, sk[k].z, uptr[k], state0[k], draws[k], samples[k] * c, dinfo + 4 * k);
   }
@@ -1815,7 +1843,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     sk[t].draw_offset = draws[t];
     sk[t].cta_begin = ctas;
     sk[t].flags = d_flags;
-    sk[t].zpart = reinterpret_cast<double*>(ws + off_zp[t]);
+    attach_sketch_scratch(sk[t], ws + off_zp[t]);
     ctas += sketch_target_ctas(sk[t]);
     bt[t] = fill_basis(bp[t], bb[t], ws, sk[t].z, ubasis(id), state0[t], draws[t], samples[id] * c,
                        dinfo + 4 * t);
@@ -2094,11 +2122,11 @@ int srtt_sketch(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d,
     CK(cudaMemcpyAsync(B.idx.p, cols, sizeof(int64_t) * ncols, cudaMemcpyHostToDevice, h->stream));
     T.cols = reinterpret_cast<const int64_t*>(B.idx.p);
     if (omega) T.omega = to_device(h, B.c, omega, ncols * c, 0);
-    B.b.ensure(sizeof(double) * T.rows * c + sketch_part_bytes(T.rows, ncols, c));
+    B.b.ensure(sizeof(double) * T.rows * c + 256 + sketch_part_bytes(T.rows, ncols, c));
     T.z = reinterpret_cast<double*>(B.b.p);
-    T.zpart = T.z + T.rows * c;
     T.state0 = srtt_host::stream_state0(seed, stream_id);
     T.draw_offset = draw_offset;
+    attach_sketch_scratch(T, reinterpret_cast<char*>(B.b.p) + (sizeof(double) * T.rows * c + 255) / 256 * 256);
     B.e.ensure(sizeof(int32_t) * 4 + sizeof(SketchTarget));
     T.flags = reinterpret_cast<int32_t*>(B.e.p);
     CK(cudaMemsetAsync(T.flags, 0, sizeof(int32_t) * 4, h->stream));
@@ -2336,7 +2364,7 @@ int srtt_shard_sketches(srtt_handle* h, const double* x_local, int32_t x_on_devi
       sk[k].draw_offset = S.draws[k];
       sk[k].cta_begin = ctas;
       sk[k].flags = reinterpret_cast<int32_t*>(ws + off_flags);
-      sk[k].zpart = reinterpret_cast<double*>(ws + off_zp[k]);
+      attach_sketch_scratch(sk[k], ws + off_zp[k]);
       ctas += sketch_target_ctas(sk[k]);
       CK(cudaMemcpyAsync(ws + off_cols[k], S.cols[k].data(), sizeof(int64_t) * samples[k], cudaMemcpyHostToDevice,
                          h->stream));

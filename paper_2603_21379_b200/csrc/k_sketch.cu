@@ -168,6 +168,18 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
   }
 }
 
+// Omega of the targets with omega_gen set, generated once: normal number
+// t = j + cc * w of the target's stream after its sampling draws.
+__global__ void __launch_bounds__(256) omega_kernel(const SketchTarget* __restrict__ targets, int ntargets) {
+  for (int t = 0; t < ntargets; ++t) {
+    const SketchTarget& T = targets[t];
+    if (!T.omega_gen) continue;
+    const int64_t n = T.w * T.c;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+      T.omega_gen[e] = srtt_dev::normal_at(T.state0, T.draw_offset, (uint64_t)e, T.flags);
+  }
+}
+
 // Fixed-order sum of the fibre-chunk partials of the split targets.
 __global__ void __launch_bounds__(256) sketch_reduce_kernel(const SketchTarget* __restrict__ targets,
                                                             int ntargets) {
@@ -186,6 +198,12 @@ __global__ void __launch_bounds__(256) sketch_reduce_kernel(const SketchTarget* 
 }
 
 }  // namespace
+
+cudaError_t srtt_launch_omega(const SketchTarget* d_targets, int ntargets, int64_t max_elems, cudaStream_t stream) {
+  const int grid = (int)srtt_dev::min64(4 * 148, (max_elems + 255) / 256);
+  omega_kernel<<<grid > 0 ? grid : 1, 256, 0, stream>>>(d_targets, ntargets);
+  return cudaGetLastError();
+}
 
 cudaError_t srtt_launch_sketch_reduce(const SketchTarget* d_targets, int ntargets, int64_t max_elems,
                                       cudaStream_t stream) {

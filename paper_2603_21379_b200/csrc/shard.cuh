@@ -229,7 +229,7 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
     sk[k].draw_offset = S.draws[k];
     sk[k].cta_begin = ctas;
     sk[k].flags = dinfo + 4 * d;
-    sk[k].zpart = reinterpret_cast<double*>(ws + off_zp[k]);
+    attach_sketch_scratch(sk[k], ws + off_zp[k]);
     ctas += sketch_target_ctas(sk[k]);
     bt[k] = fill_basis(bp[k], bb[k], ws, zsum + zoff[k], uptr[k], S.state0[k], S.draws[k], samples[k] * c,
                        dinfo + 4 * k);
@@ -484,7 +484,7 @@ struct HtShard {
       sk[t].draw_offset = draws[t];
       sk[t].cta_begin = ctas;
       sk[t].flags = dinfo + 4 * nt;
-      sk[t].zpart = reinterpret_cast<double*>(ws + off_zp[id]);
+      attach_sketch_scratch(sk[t], ws + off_zp[id]);
       ctas += sketch_target_ctas(sk[t]);
       bt[t] = fill_basis(bp[id], bb[id], ws, zsum() + zoff[id], ubasis(id), state0[t], draws[t], samples[id] * c,
                          dinfo + 4 * t);
