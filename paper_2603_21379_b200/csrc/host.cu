@@ -29,6 +29,8 @@ size_t srtt_sketch_smem_bytes(int cmax);
 cudaError_t srtt_launch_sketch(const SketchTarget*, int, int64_t, int, cudaStream_t);
 cudaError_t srtt_launch_sketch_reduce(const SketchTarget*, int, int64_t, cudaStream_t);
 cudaError_t srtt_launch_omega(const SketchTarget*, int, int64_t, cudaStream_t);
+cudaError_t srtt_launch_scatter_block(const double*, double*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
+                                      int64_t, cudaStream_t);
 size_t srtt_basis_top_smem(int m, int c, int r);
 size_t srtt_basis_level_smem(int mb, int c);
 cudaError_t srtt_launch_basis_top(int, const BasisTarget*, const int*, int, size_t, cudaStream_t);
@@ -931,6 +933,72 @@ void layout_core(Layout& L, CorePlan& cp, size_t& off_ufrag, std::vector<size_t>
   off_tmp1 = L.take(sizeof(double) * big);
 }
 
+// The core pass of one call. The streaming kernel's DMMA tiles cover ranks
+// up to 32 in modes 0 and 1; larger ranks run one pass per (32-column block
+// of U_0) x (32-column block of U_1) -- core[a, b, ...] depends only on
+// column a of U_0 and column b of U_1 -- and each block's sub-core is
+// scattered into the core. X is then streamed once per block pair.
+struct CoreJob {
+  struct Piece {
+    CorePlan cp;
+    size_t off_ufrag = 0, off_part = 0, off_tmp0 = 0, off_tmp1 = 0;
+    std::vector<size_t> off_fu;
+    int64_t a0 = 0, ra = 0, b0 = 0, rb = 0;
+  };
+  std::vector<Piece> pieces;
+  std::vector<int64_t> dims, ranks;
+  size_t off_sub = 0;
+  bool blocked = false;
+
+  void plan(const std::vector<int64_t>& dims_, const std::vector<int64_t>& ranks_, int sms, Layout& L) {
+    dims = dims_;
+    ranks = ranks_;
+    const int d = (int)dims.size();
+    blocked = ranks[0] > 32 || (d >= 2 && ranks[1] > 32);
+    const int64_t r1 = d >= 2 ? ranks[1] : 1;
+    int64_t biggest = 0;
+    for (int64_t a0 = 0; a0 < ranks[0]; a0 += 32)
+      for (int64_t b0 = 0; b0 < r1; b0 += 32) {
+        Piece pc;
+        pc.a0 = a0;
+        pc.ra = std::min<int64_t>(32, ranks[0] - a0);
+        pc.b0 = b0;
+        pc.rb = std::min<int64_t>(32, r1 - b0);
+        std::vector<int64_t> pr = ranks;
+        pr[0] = pc.ra;
+        if (d >= 2) pr[1] = pc.rb;
+        pc.cp = plan_core(dims, pr, sms);
+        layout_core(L, pc.cp, pc.off_ufrag, pc.off_fu, pc.off_part, pc.off_tmp0, pc.off_tmp1);
+        biggest = std::max<int64_t>(biggest, prod(pr));
+        pieces.push_back(std::move(pc));
+        if (!blocked) break;
+      }
+    if (blocked) off_sub = L.take(sizeof(double) * biggest);
+  }
+
+  int launch(srtt_handle* h, const double* x, const std::vector<const double*>& u, double* out, char* ws) {
+    if (!blocked) {
+      Piece& pc = pieces[0];
+      return launch_core_pass(h, pc.cp, x, u, out, ws, pc.off_ufrag, pc.off_fu, pc.off_part, pc.off_tmp0, pc.off_tmp1);
+    }
+    const int d = (int)dims.size();
+    const int64_t r1 = d >= 2 ? ranks[1] : 1;
+    int64_t rest = 1;
+    for (int k = 2; k < d; ++k) rest *= ranks[k];
+    double* sub = reinterpret_cast<double*>(ws + off_sub);
+    int n = 0;
+    for (Piece& pc : pieces) {
+      std::vector<const double*> up = u;
+      up[0] = u[0] + pc.a0 * dims[0];
+      if (d >= 2) up[1] = u[1] + pc.b0 * dims[1];
+      n += launch_core_pass(h, pc.cp, x, up, sub, ws, pc.off_ufrag, pc.off_fu, pc.off_part, pc.off_tmp0, pc.off_tmp1);
+      CK(srtt_launch_scatter_block(sub, out, ranks[0], r1, pc.a0, pc.ra, pc.b0, pc.rb, rest, h->stream));
+      ++n;
+    }
+    return n;
+  }
+};
+
 // ---- sketch target construction ---------------------------------------------
 // Fibre chunks per K1 target: the grouped grid parallelises over rows only
 // when a target samples few fibres (BASELINE configs: w <= 168, one chunk,
@@ -1219,13 +1287,9 @@ int64_t pick_slice_mode_impl(const std::vector<int64_t>& dims, int64_t workers) 
   return best;
 }
 
-// Limit of the streaming core engine (DMMA tile templates: 1, 2 or 4 rank
-// tiles of 8 in modes 0 and 1), checked before any work is issued.
-void check_core_ranks(int d, const int64_t* ranks, const char* who) {
-  if (d >= 2 && (ranks[0] > 32 || ranks[1] > 32))
-    invalid(std::string(who) + ": ranks above 32 in the first two core modes are not supported by the B200 "
-            "core kernel");
-}
+// Ranks above 32 in the first two core modes run as rank blocks (CoreJob);
+// nothing to reject up front.
+void check_core_ranks(int, const int64_t*, const char*) {}
 
 void check_workers(const srtt_exec_policy* exec, const char* who) {
   if (exec && exec->workers < 1) invalid(std::string(who) + ": workers must be >= 1");
@@ -1372,13 +1436,8 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   int64_t max_n = 0;
   for (int k = 0; k < d; ++k) max_n = std::max(max_n, dims[k]);
   const size_t off_pad = L.take(sizeof(double) * max_n * d);
-  CorePlan cp;
-  size_t off_ufrag = 0, off_part = 0, off_tmp0 = 0, off_tmp1 = 0;
-  std::vector<size_t> off_fu;
-  if (d >= 2) {
-    cp = plan_core(dims, ranks, h->sms);
-    layout_core(L, cp, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
-  }
+  CoreJob core;
+  if (d >= 2) core.plan(dims, ranks, h->sms, L);
   h->ws.ensure(L.off);
   char* ws = reinterpret_cast<char*>(h->ws.p);
   std::vector<double*> uptr(d);
@@ -1446,7 +1505,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     // --- K3: core pass
     std::vector<const double*> ucp(uptr.begin(), uptr.end());
     if (d >= 2) {
-      h->launches += launch_core_pass(h, cp, x, ucp, d_core, ws, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+      h->launches += core.launch(h, x, ucp, d_core, ws);
     } else {
       TtmParams T{};
       T.in = x;
@@ -1811,10 +1870,8 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   off_b[0] = L.take(sizeof(double) * rl0 * rr0);
   const std::vector<int64_t> rdims = {node_rows(tr.left[0]), node_rows(tr.right[0])};
   const std::vector<int64_t> rranks = {rl0, rr0};
-  CorePlan cp = plan_core(rdims, rranks, h->sms);
-  size_t off_ufrag = 0, off_part = 0, off_tmp0 = 0, off_tmp1 = 0;
-  std::vector<size_t> off_fu;
-  layout_core(L, cp, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+  CoreJob core;
+  core.plan(rdims, rranks, h->sms, L);
   h->ws.ensure(L.off);
   char* ws = reinterpret_cast<char*>(h->ws.p);
 
@@ -1927,7 +1984,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     if (root_needs_small) CK(cudaStreamWaitEvent(h->stream, h->fj[1], 0));
     tm.mark();  // 5
     std::vector<const double*> ur = {ubasis(tr.left[0]), ubasis(tr.right[0])};
-    h->launches += launch_core_pass(h, cp, x, ur, d_root, ws, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+    h->launches += core.launch(h, x, ur, d_root, ws);
     // join
     CK(cudaStreamWaitEvent(h->stream, h->fj[3], 0));
     tm.mark();  // 6
@@ -2203,16 +2260,13 @@ int srtt_multi_ttm_core(srtt_handle* h, const double* x, int32_t x_on_device, in
     std::vector<DevBuf> ub(d);
     std::vector<const double*> u(d);
     for (int k = 0; k < d; ++k) u[k] = to_device(h, ub[k], factors[k], dv[k] * rv[k], factors_on_device);
-    CorePlan cp = plan_core(dv, rv, h->sms);
     Layout L;
-    size_t off_ufrag, off_part, off_tmp0, off_tmp1;
-    std::vector<size_t> off_fu;
-    layout_core(L, cp, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+    CoreJob core;
+    core.plan(dv, rv, h->sms, L);
     const size_t off_core = L.take(sizeof(double) * prod(rv));
     B.b.ensure(L.off);
     char* ws = reinterpret_cast<char*>(B.b.p);
-    launch_core_pass(h, cp, dx, u, reinterpret_cast<double*>(ws + off_core), ws, off_ufrag, off_fu, off_part,
-                     off_tmp0, off_tmp1);
+    core.launch(h, dx, u, reinterpret_cast<double*>(ws + off_core), ws);
     copy_out(h, core_out, ws + off_core, sizeof(double) * prod(rv), out_on_device);
     CK(cudaStreamSynchronize(h->stream));
   });

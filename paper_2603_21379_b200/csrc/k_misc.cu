@@ -3,6 +3,8 @@
 #include "srtt_device.cuh"
 #include "srtt_params.h"
 
+#include <algorithm>
+
 typedef struct TransferTarget {
   const double* us;   // node basis n_l*n_r x r_s (column-major)
   const double* ul;   // left child basis n_l x r_l
@@ -162,5 +164,28 @@ cudaError_t srtt_launch_normals(uint64_t state0, uint64_t draw_offset, uint64_t 
                                 cudaStream_t s) {
   const int blocks = (int)srtt_dev::min64(1024, (n + 255) / 256);
   normals_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(state0, draw_offset, t0, n, out);
+  return cudaGetLastError();
+}
+
+// Scatter of a (ra x rb x rest) sub-core into the (r0 x r1 x rest) core at
+// rows [a0, a0 + ra) of mode 0 and [b0, b0 + rb) of mode 1 (first index
+// fastest): the core pass for ranks above 32 in modes 0/1 runs one
+// streaming pass per rank block (host.cu CoreJob).
+namespace {
+__global__ void scatter_block_kernel(const double* __restrict__ sub, double* __restrict__ out, int64_t r0, int64_t r1,
+                                     int64_t a0, int64_t ra, int64_t b0, int64_t rb, int64_t rest) {
+  const int64_t n = ra * rb * rest;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = e % ra, b = (e / ra) % rb, q = e / (ra * rb);
+    out[(a0 + a) + r0 * ((b0 + b) + r1 * q)] = sub[e];
+  }
+}
+}  // namespace
+
+cudaError_t srtt_launch_scatter_block(const double* sub, double* out, int64_t r0, int64_t r1, int64_t a0, int64_t ra,
+                                      int64_t b0, int64_t rb, int64_t rest, cudaStream_t s) {
+  const int64_t n = ra * rb * rest;
+  const int grid = (int)std::min<int64_t>(1184, (n + 255) / 256);
+  scatter_block_kernel<<<grid > 0 ? grid : 1, 256, 0, s>>>(sub, out, r0, r1, a0, ra, b0, rb, rest);
   return cudaGetLastError();
 }

@@ -186,10 +186,8 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
   const size_t off_pad = W.take(sizeof(double) * max_n * d);
   const size_t off_uslab = W.take(sizeof(double) * nl * ranks[L]);
   const size_t off_core = W.take(sizeof(double) * prod(ranks));
-  CorePlan cp = plan_core(ldims, ranks, h->sms);
-  size_t off_ufrag = 0, off_part = 0, off_tmp0 = 0, off_tmp1 = 0;
-  std::vector<size_t> off_fu;
-  layout_core(W, cp, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+  CoreJob core;
+  core.plan(ldims, ranks, h->sms, W);
   h->ws.ensure(W.off);
   char* ws = reinterpret_cast<char*>(h->ws.p);
   double* zsum = reinterpret_cast<double*>(ws + off_zsum);
@@ -271,7 +269,7 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
                          ranks[L], cudaMemcpyDeviceToDevice, h->stream));
     std::vector<const double*> ucp(uptr.begin(), uptr.end());
     ucp[L] = uslab;
-    h->launches += launch_core_pass(h, cp, x, ucp, d_core, ws, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+    h->launches += core.launch(h, x, ucp, d_core, ws);
     tm.mark();  // 6
     allreduce_sum(h, d_core, (size_t)prod(ranks));
     tm.mark();  // 7
@@ -328,9 +326,7 @@ struct HtShard {
   std::vector<BasisPlan> bp;
   std::vector<BasisBuffers> bb;
   std::vector<int> internal;
-  CorePlan cp;
-  size_t off_ufrag = 0, off_part = 0, off_tmp0 = 0, off_tmp1 = 0;
-  std::vector<size_t> off_fu;
+  CoreJob core;
   // blob
   Blob blob;
   std::vector<size_t> off_cols;
@@ -453,8 +449,7 @@ struct HtShard {
     const int rl0 = (int)ranks[tr.left[0]], rr0 = (int)ranks[tr.right[0]];
     off_root = W.take(sizeof(double) * rl0 * rr0);
     off_urs = W.take(sizeof(double) * (chi - clo) * rr0);
-    cp = plan_core({nlr, chi - clo}, {rl0, rr0}, h->sms);
-    layout_core(W, cp, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+    core.plan({nlr, chi - clo}, {rl0, rr0}, h->sms, W);
     h->ws.ensure(W.off);
     ws = reinterpret_cast<char*>(h->ws.p);
     dinfo = h->pset().dinfo();
@@ -545,7 +540,7 @@ struct HtShard {
     CK(cudaMemcpy2DAsync(urs, sizeof(double) * nc, ur_full + col_lo, sizeof(double) * nrr, sizeof(double) * nc, rr0,
                          cudaMemcpyDeviceToDevice, h->stream));
     std::vector<const double*> u = {ul, urs};
-    return launch_core_pass(h, cp, x, u, out, ws, off_ufrag, off_fu, off_part, off_tmp0, off_tmp1);
+    return core.launch(h, x, u, out, ws);
   }
   std::string key(srtt_handle* h, const double* x) const {
     std::string k = "HS";
@@ -834,8 +829,6 @@ int srtt_ht_shard_root(srtt_handle* h, const double* x_cols, int32_t x_on_device
   return guarded([&] {
     if (!h) invalid("srtt: null handle");
     if (col_lo < 0 || col_hi > n_right || col_lo >= col_hi) invalid("sharded root: column range out of range");
-    if (r_left > 32 || r_right > 32)
-      invalid("root_transfer: ranks above 32 in the first two core modes are not supported by the B200 core kernel");
     DeviceGuard g(h->device);
     CompRef B = comp_bufs(h);
     const int64_t nc = col_hi - col_lo;

@@ -108,3 +108,21 @@ def test_internal_node_bases_reported(handle):
         assert projector_gap(rep.node_bases[i], orep.bases[i]) <= 1e-10
         if otree.node(i).is_leaf():
             assert np.array_equal(rep.node_bases[i], h.leaf_factors[otree.node(i).modes[0]])
+
+
+def test_root_children_ranks_above_32(handle):
+    """H-Tucker root pass with r_left, r_right = 40 (> the 32-wide DMMA tiles):
+    rank-block passes, parity with the oracle."""
+    tree, otree = P.DimensionTree.balanced(4), O.DimensionTree.balanced(4)
+    dims = (8, 8, 8, 8)
+    ranks = [1, 40, 40, 8, 8, 8, 8]
+    x = np.random.default_rng(6).standard_normal(dims)
+    samples = [1] + [min(56, tree.node_cols(i, dims)) for i in range(1, 7)]
+    rep = P.HtSubsampleReport()
+    h = P.sub_r_rtl_ht(x, tree, ranks, samples, 6, 2, report=rep, handle=handle)
+    orep = O.HtSubsampleReport()
+    ho = O.sub_r_rtl_ht(x, otree, ranks, samples, 6, 2, report=orep)
+    assert rep.achieved_ranks == orep.achieved_ranks
+    eg, ec = O.rel_error(x, O.ht_reconstruct(as_oracle(h, otree))), O.rel_error(x, O.ht_reconstruct(ho))
+    assert abs(eg - ec) <= 1e-10 * max(ec, 1.0)
+    assert h.transfers[0].shape == (1, 40, 40)

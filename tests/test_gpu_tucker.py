@@ -181,12 +181,29 @@ def test_exec_policy_validated_like_the_reference(handle):
     assert rep.slice_mode is None
 
 
-def test_core_rank_limit_rejected_up_front(handle):
-    """Ranks above 32 in the first two core modes are refused before any
-    work is issued, with a message naming the limit (not a core-planner
-    error after the factor phase)."""
-    x = np.random.default_rng(1).standard_normal((40, 40, 8))
-    with pytest.raises(P.InvalidArgument, match="ranks above 32 in the first two core modes"):
-        P.sub_r_hosvd(x, [33, 4, 4], 6, [60] * 3, 0, handle=handle)
+def test_ranks_above_32_match_oracle(handle):
+    """Ranks above the core kernel's 32-wide DMMA tiles (modes 0/1) run as
+    rank blocks scattered into the core; parity with the oracle as usual.
+    r + p above 64 (the basis kernels) is refused up front."""
+    dims, ranks, p, s = (64, 56, 40), [48, 40, 20], 10, [70, 60, 40]
+    x, _, _ = planted_tucker(dims, (44, 36, 16), 9)
+    x = x + 1e-10 * np.random.default_rng(3).standard_normal(dims)
+    rep = P.SubsampleReport()
+    t = P.sub_r_hosvd(x, ranks, p, s, 4, report=rep, handle=handle)
+    orep = O.SubsampleReport()
+    to = O.sub_r_hosvd(x, ranks, p, s, 4, report=orep)
+    assert rep.achieved_ranks == orep.achieved_ranks
+    for k in range(3):
+        q = rep.achieved_ranks[k]
+        assert projector_gap(t.factors[k][:, :q], to.factors[k][:, :q]) <= 1e-9
+    assert aligned_core_error(t.core, t.factors, to.core, to.factors) <= 1e-9
+    eg, ec = tucker_rel_error(x, t.core, t.factors), tucker_rel_error(x, to.core, to.factors)
+    assert abs(eg - ec) <= 1e-10 * max(ec, 1.0)
+    # the component: multi_ttm with ranks (40, 36, 5)
+    fs = [np.linalg.qr(np.random.default_rng(k).standard_normal((n, r)))[0] for k, (n, r) in
+          enumerate(zip(dims, (40, 36, 5)))]
+    g = P.multi_ttm_core(x, fs, handle=handle)
+    assert np.abs(g - O.core_from_factors(x, fs)).max() <= 1e-12 * np.abs(x).max() * 64
     with pytest.raises(P.InvalidArgument, match="rank \\+ oversampling above 64"):
-        P.sub_r_hosvd(x, [8, 8, 8], 60, [120] * 3, 0, handle=handle)
+        P.sub_r_hosvd(np.random.default_rng(1).standard_normal((40, 40, 8)), [8, 8, 8], 60, [120] * 3, 0,
+                      handle=handle)
