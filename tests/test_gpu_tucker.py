@@ -186,7 +186,7 @@ def test_ranks_above_32_match_oracle(handle):
     rank blocks scattered into the core; parity with the oracle as usual.
     r + p above 64 (the basis kernels) is refused up front."""
     dims, ranks, p, s = (64, 56, 40), [48, 40, 20], 10, [70, 60, 40]
-    x, _, _ = planted_tucker(dims, (44, 36, 16), 9)
+    x, _, _ = planted_tucker(dims, (48, 40, 20), 9)
     x = x + 1e-10 * np.random.default_rng(3).standard_normal(dims)
     rep = P.SubsampleReport()
     t = P.sub_r_hosvd(x, ranks, p, s, 4, report=rep, handle=handle)
