@@ -352,6 +352,25 @@ int srtt_sub_r_rtl_ht_sharded(srtt_handle* h, const double* x_cols, int32_t x_on
                               const int64_t* ranks, const int64_t* samples, int64_t oversampling, uint64_t seed,
                               const srtt_exec_policy* exec, double* const* leaf_factors_out,
                               double* const* transfers_out, int32_t out_on_device, srtt_report* rep);
+/* Replicated X (the tensor fits every GPU; the north star's mode/node-
+ * parallel regime): every rank passes ALL of X. Modes (Tucker) or non-root
+ * nodes (H-Tucker) are assigned to ranks by greedy longest-processing-time
+ * on n_S s_S (r_S + p) -- the reference's per-mode / per-node jobs
+ * (parallel.hpp:133-147, 205-277) spread over GPUs instead of threads --;
+ * each rank sketches and factors only its targets into a zero-filled pack,
+ * ONE allreduce of the pack (plus one of the per-target info words) gives
+ * every rank every basis, and the full pass is split by last-mode slabs
+ * (Tucker) or root-matricization column ranges (H-Tucker) of the replica
+ * and allreduced. Outputs are identical on every rank. */
+int srtt_sub_r_hosvd_replicated(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d,
+                                const int64_t* dims, const int64_t* ranks, int64_t oversampling,
+                                const int64_t* samples, uint64_t seed, const srtt_exec_policy* exec, double* core_out,
+                                double* const* factors_out, int32_t out_on_device, srtt_report* rep);
+int srtt_sub_r_rtl_ht_replicated(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d, const int64_t* dims,
+                                 const srtt_tree* tree, const int64_t* ranks, const int64_t* samples,
+                                 int64_t oversampling, uint64_t seed, const srtt_exec_policy* exec,
+                                 double* const* leaf_factors_out, double* const* transfers_out, int32_t out_on_device,
+                                 srtt_report* rep);
 /* The H-Tucker split as synchronous phases (same plan and kernels as the
  * fused entry; the caller exchanges between them, any transport):
  *   1. srtt_ht_shard_sketches: z_out[id] (id >= 1, n_S x (r_S + p)) = this

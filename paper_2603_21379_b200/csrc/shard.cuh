@@ -122,15 +122,55 @@ void finish_report_common(srtt_report* rep, Timer& tm, double t_sampling, int64_
 // ==================================================================================
 // Slab-sharded Sub-R-HOSVD (fused: kernels + NCCL in one graph)
 // ==================================================================================
+// Greedy longest-processing-time assignment of targets to ranks (cost
+// descending, ties by index; each to the least loaded rank, ties to the
+// lowest rank): identical on every rank. Returns which targets are this
+// rank's.
+std::vector<char> assign_targets(const std::vector<double>& cost, int world, int rank) {
+  std::vector<int> order(cost.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  std::vector<double> load(world, 0.0);
+  std::vector<char> mine(cost.size(), 0);
+  for (int t : order) {
+    int best = 0;
+    for (int w = 1; w < world; ++w)
+      if (load[w] < load[best]) best = w;
+    load[best] += cost[t];
+    if (best == rank) mine[t] = 1;
+  }
+  return mine;
+}
+
+void allreduce_sum_i32(srtt_handle* h, int32_t* buf, size_t count) {
+  if (count == 0) return;
+  nccl_check(nccl_api().all_reduce(buf, buf, count, ncclInt32, ncclSum, comm_of(h), h->stream), "ncclAllReduce");
+}
+
+// Tucker across GPUs, two layouts of X (the north star's two regimes):
+//  slab-sharded (replicated = false): this rank holds X[..., lo:hi) only --
+//    partial sketches, allreduce, identical bases, slab core, allreduce;
+//  replicated (replicated = true): every rank holds all of X -- the modes
+//    are assigned to ranks (LPT by n_k s_k (r_k + p)), each rank sketches and
+//    factors only its modes into a zero-filled factor pack, ONE allreduce
+//    of the pack (and of the per-mode info) gives every rank every factor,
+//    then the core pass is split by last-mode slabs of the replica and
+//    allreduced (parallel.hpp:133-147 mode jobs + :355-445 slab core).
 void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device, int d, const int64_t* dims_p,
                              int64_t lo, int64_t hi, const int64_t* ranks_p, int64_t p, const int64_t* samples_p,
                              uint64_t seed, const srtt_exec_policy* exec, double* core_out,
-                             double* const* factors_out, int out_on_device, srtt_report* rep) {
+                             double* const* factors_out, int out_on_device, srtt_report* rep,
+                             bool replicated = false) {
   if (!h) invalid("srtt: null handle");
   std::vector<int64_t> dims(dims_p, dims_p + d), ranks(ranks_p, ranks_p + d), samples(samples_p, samples_p + d);
   validate_tucker(d, dims, ranks, samples, p);
   check_core_ranks(d, ranks.data(), "sub_r_hosvd");
   const int L = d - 1;
+  if (replicated) {
+    comm_of(h);
+    if (h->world > dims[L]) invalid("replicated sub_r_hosvd: more ranks than slices along the last mode");
+    split_bounds(dims[L], h->world, h->rank, lo, hi);
+  }
   if (lo < 0 || hi > dims[L] || lo >= hi) invalid("sharded sub_r_hosvd: slab out of range");
   if (hi - lo < ranks[L]) invalid("sharded sub_r_hosvd: every slab must hold at least r_{d-1} slices");
   check_workers(exec, "run_independent_jobs");
@@ -141,6 +181,13 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
   ldims[L] = hi - lo;
   const int64_t Nl = prod(ldims);
   const int64_t nl = hi - lo;
+  const int64_t inner = prod(dims) / dims[L];
+  std::vector<char> mine(d, 1);
+  if (replicated) {
+    std::vector<double> cost(d);
+    for (int k = 0; k < d; ++k) cost[k] = (double)dims[k] * samples[k] * (ranks[k] + p);
+    mine = assign_targets(cost, h->world, h->rank);
+  }
 
   DeviceGuard guard(h->device);
   h->launches = 0;
@@ -156,7 +203,8 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
   const double t_sampling = now_s() - ts0;
   const int64_t slice_mode = exec ? resolve_slice_mode(dims, exec) : -1;
   tm.mark();  // 0
-  const double* x = stage_input(h, x_in, x_on_device, Nl);
+  const double* x = stage_input(h, x_in, x_on_device, replicated ? prod(dims) : Nl);
+  const double* xslab = replicated ? x + lo * inner : x;  // the core pass's part
   tm.mark();  // 1
 
   // --- workspace: all sketches in ONE buffer (one allreduce), bases, core
@@ -172,13 +220,15 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
   const size_t off_zsum = W.take(sizeof(double) * zn);
   std::vector<size_t> off_zp(d);
   for (int k = 0; k < d; ++k)
-    off_zp[k] = W.take(sketch_part_bytes(k == L ? nl : dims[k], samples[k], (int)(ranks[k] + p)));
+    off_zp[k] = W.take(sketch_part_bytes(k == L && !replicated ? nl : dims[k], samples[k], (int)(ranks[k] + p)));
   std::vector<size_t> off_u(d);
   std::vector<BasisPlan> bp(d);
   std::vector<BasisBuffers> bb(d);
-  int64_t max_n = 0;
+  int64_t max_n = 0, upack_n = 0;
+  for (int k = 0; k < d; ++k) upack_n += dims[k] * ranks[k];
+  const size_t off_upack = replicated ? W.take(sizeof(double) * upack_n) : 0;
   for (int k = 0; k < d; ++k) {
-    off_u[k] = out_on_device ? 0 : W.take(sizeof(double) * dims[k] * ranks[k]);
+    off_u[k] = (out_on_device || replicated) ? 0 : W.take(sizeof(double) * dims[k] * ranks[k]);
     bp[k] = plan_basis(dims[k], (int)(ranks[k] + p), (int)ranks[k]);
     bb[k] = layout_basis(W, bp[k]);
     max_n = std::max(max_n, dims[k]);
@@ -192,7 +242,10 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
   char* ws = reinterpret_cast<char*>(h->ws.p);
   double* zsum = reinterpret_cast<double*>(ws + off_zsum);
   std::vector<double*> uptr(d);
-  for (int k = 0; k < d; ++k) uptr[k] = out_on_device ? factors_out[k] : reinterpret_cast<double*>(ws + off_u[k]);
+  double* upack = reinterpret_cast<double*>(ws + off_upack);
+  for (int k = 0, o = 0; k < d; o += (int)(dims[k] * ranks[k]), ++k)
+    uptr[k] = replicated ? upack + o
+                         : (out_on_device ? factors_out[k] : reinterpret_cast<double*>(ws + off_u[k]));
   double* d_core = out_on_device ? core_out : reinterpret_cast<double*>(ws + off_core);
 
   // --- parameter blob
@@ -211,7 +264,10 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
   int64_t ctas = 0;
   for (int k = 0; k < d; ++k) {
     const int c = (int)(ranks[k] + p);
-    if (k == L) {  // this rank's rows [lo, hi) of Z_{d-1}, written at row lo of the full block
+    if (replicated) {  // a whole mode of the replica, as on one GPU
+      sk[k] = make_sketch_target(x, dims, {k}, samples[k], c);
+      sk[k].z = zsum + zoff[k];
+    } else if (k == L) {  // this rank's rows [lo, hi) of Z_{d-1}, written at row lo of the full block
       sk[k] = make_sketch_target(x, ldims, {k}, samples[k], c);
       sk[k].z = zsum + zoff[k] + lo;
       sk[k].ldz = dims[k];
@@ -232,6 +288,21 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
     bt[k] = fill_basis(bp[k], bb[k], ws, zsum + zoff[k], uptr[k], S.state0[k], S.draws[k], samples[k] * c,
                        dinfo + 4 * k);
   }
+  if (replicated) {  // this rank's modes only (CTA offsets recomputed)
+    std::vector<SketchTarget> sk_m;
+    std::vector<BasisTarget> bt_m;
+    ctas = 0;
+    for (int k = 0; k < d; ++k)
+      if (mine[k]) {
+        sk[k].cta_begin = ctas;
+        ctas += sketch_target_ctas(sk[k]);
+        sk_m.push_back(sk[k]);
+        bt_m.push_back(bt[k]);
+      }
+    sk.swap(sk_m);
+    bt.swap(bt_m);
+  }
+  const int nsk = (int)sk.size();
   assign_basis_ctas(bt);
   const BasisLists lists = make_basis_lists(bt, blob);
   h->pset().d.ensure(blob.lay.off);
@@ -239,10 +310,10 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
   dp = reinterpret_cast<char*>(h->pset().d.p);
   char* hp = reinterpret_cast<char*>(h->pset().hst.p);
   for (auto& it : blob.items) std::memcpy(hp + it.first, it.second.data(), it.second.size());
-  std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * d);
-  std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * d);
+  if (nsk) std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * nsk);
+  if (nsk) std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * nsk);
 
-  std::string key = "TS";
+  std::string key = replicated ? "TR" : "TS";
   for (int k = 0; k < d; ++k)
     key += "|" + std::to_string(dims[k]) + "," + std::to_string(ranks[k]) + "," + std::to_string(samples[k]) + "," +
            ptr_key(uptr[k]);
@@ -253,15 +324,25 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
   run_enqueue(h, key, [&] {
     CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemsetAsync(dinfo, 0, info_bytes, h->stream));
-    CK(cudaMemsetAsync(zsum + zoff[L], 0, sizeof(double) * zL, h->stream));
+    if (replicated)
+      CK(cudaMemsetAsync(upack, 0, sizeof(double) * upack_n, h->stream));
+    else
+      CK(cudaMemsetAsync(zsum + zoff[L], 0, sizeof(double) * zL, h->stream));
     tm.n = 2;
     tm.mark();  // 2
-    h->launches += launch_sketch_group(reinterpret_cast<const SketchTarget*>(dp + off_sk), sk, ctas, cmax, h->stream);
+    if (nsk)
+      h->launches += launch_sketch_group(reinterpret_cast<const SketchTarget*>(dp + off_sk), sk, ctas, cmax,
+                                         h->stream);
     tm.mark();  // 3
-    allreduce_sum(h, zsum, (size_t)zn);
+    if (!replicated) allreduce_sum(h, zsum, (size_t)zn);
     tm.mark();  // 4
-    h->launches += launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt), lists, dp,
-                                      reinterpret_cast<double*>(ws + off_pad), max_n);
+    if (nsk)
+      h->launches += launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt), lists, dp,
+                                        reinterpret_cast<double*>(ws + off_pad), max_n);
+    if (replicated) {  // every rank's factors (others' entries are zero) and per-mode info
+      allreduce_sum(h, upack, (size_t)upack_n);
+      allreduce_sum_i32(h, dinfo, 4 * (size_t)(d + 1));
+    }
     tm.mark();  // 5
     // U_{d-1} rows [lo, hi) as a contiguous block for the slab's core pass
     double* uslab = reinterpret_cast<double*>(ws + off_uslab);
@@ -269,17 +350,17 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
                          ranks[L], cudaMemcpyDeviceToDevice, h->stream));
     std::vector<const double*> ucp(uptr.begin(), uptr.end());
     ucp[L] = uslab;
-    h->launches += core.launch(h, x, ucp, d_core, ws);
+    h->launches += core.launch(h, xslab, ucp, d_core, ws);
     tm.mark();  // 6
     allreduce_sum(h, d_core, (size_t)prod(ranks));
     tm.mark();  // 7
     CK(cudaMemcpyAsync(hinfo, dinfo, info_bytes, cudaMemcpyDeviceToHost, h->stream));
   });
   tm.n = 8;
-  if (!out_on_device) {
-    copy_out(h, core_out, d_core, sizeof(double) * prod(ranks), 0);
-    for (int k = 0; k < d; ++k) copy_out(h, factors_out[k], uptr[k], sizeof(double) * dims[k] * ranks[k], 0);
-  }
+  if (!out_on_device) copy_out(h, core_out, d_core, sizeof(double) * prod(ranks), 0);
+  if (!out_on_device || replicated)
+    for (int k = 0; k < d; ++k)
+      copy_out(h, factors_out[k], uptr[k], sizeof(double) * dims[k] * ranks[k], out_on_device);
   if (!end_call(h, rep || !out_on_device)) return;
   CK(cudaStreamSynchronize(h->stream));
   CK(cudaGetLastError());
@@ -290,14 +371,14 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
       warnings.push_back("mode " + std::to_string(k) + ": sketch revealed rank " + std::to_string(q) + " < target " +
                          std::to_string(ranks[k]) + "; basis padded");
   }
-  if (hinfo[4 * d] & 1) warnings.push_back(kU1ZeroWarning);
+  if (hinfo[4 * d] != 0) warnings.push_back(kU1ZeroWarning);
   if (rep) {
     if (rep->sample_counts)
       for (int k = 0; k < d; ++k) rep->sample_counts[k] = samples[k];
     finish_report_common(rep, tm, t_sampling, h->launches);
     rep->kernel_seconds[2] = kernel_pair(h, 2);
     rep->slice_mode = slice_mode;
-    rep->flags = hinfo[4 * d];
+    rep->flags = hinfo[4 * d] != 0 ? 1 : 0;
     write_warnings(rep, warnings);
   }
 }
@@ -314,6 +395,10 @@ struct HtShard {
   std::vector<int64_t> dims, ranks, samples;
   int64_t p = 0, N = 0, nlr = 0, nrr = 0, col_lo = 0, col_hi = 0;
   bool whole = true;  // the range covers the tensor (no masking)
+  bool replicated = false;  // X replicated on every rank: nodes assigned to ranks
+  std::vector<char> mine;   // by target t (node t + 1): this rank's nodes
+  size_t off_upack = 0;
+  int64_t upack_n = 0;
   std::vector<std::vector<int64_t>> cols;
   std::vector<uint64_t> draws, state0;
   double t_sampling = 0;
@@ -353,7 +438,8 @@ struct HtShard {
   // Validation (htucker.hpp:217-233 order), sampling, workspace + blob.
   void build(srtt_handle* h, const double* x, int d_, const int64_t* dims_p, const srtt_tree* tree_p,
              const int64_t* ranks_p, const int64_t* samples_p, int64_t p_, uint64_t seed,
-             const srtt_exec_policy* exec, int64_t clo, int64_t chi) {
+             const srtt_exec_policy* exec, int64_t clo, int64_t chi, bool replicated_ = false) {
+    replicated = replicated_;
     if (d_ < 2 || d_ > SRTT_MAX_ORDER) invalid("sub_r_rtl_ht: unsupported order");
     d = d_;
     dims.assign(dims_p, dims_p + d);
@@ -392,7 +478,7 @@ struct HtShard {
       invalid("sharded sub_r_rtl_ht: every column range must hold at least r_right columns");
     col_lo = clo;
     col_hi = chi;
-    whole = (clo == 0 && chi == nrr);
+    whole = replicated || (clo == 0 && chi == nrr);
     // sampling: stream bound to the node id (htucker.hpp:264)
     const int64_t partitions = exec ? exec->index_partitions : 1;
     const double ts0 = now_s();
@@ -435,8 +521,11 @@ struct HtShard {
     off_zsum = W.take(sizeof(double) * zn);
     off_zp.assign(nn, 0);
     for (int i = 1; i < nn; ++i) off_zp[i] = W.take(sketch_part_bytes(rows[i], samples[i], (int)(ranks[i] + p)));
-    for (int i = 1; i < nn; ++i) {
-      off_u[i] = W.take(sizeof(double) * rows[i] * ranks[i]);
+    upack_n = 0;
+    for (int i = 1; i < nn; ++i) upack_n += rows[i] * ranks[i];
+    off_upack = W.take(sizeof(double) * upack_n);  // every node basis, contiguous
+    for (int i = 1, o = 0; i < nn; o += (int)(rows[i] * ranks[i]), ++i) {
+      off_u[i] = off_upack + sizeof(double) * o;
       bp[i] = plan_basis(rows[i], (int)(ranks[i] + p), (int)ranks[i]);
       bb[i] = layout_basis(W, bp[i]);
     }
@@ -484,6 +573,24 @@ struct HtShard {
       bt[t] = fill_basis(bp[id], bb[id], ws, zsum() + zoff[id], ubasis(id), state0[t], draws[t], samples[id] * c,
                          dinfo + 4 * t);
     }
+    mine.assign(nt, 1);
+    if (replicated) {  // this rank's nodes only (LPT by n_S w_S (r_S + p))
+      std::vector<double> cost(nt);
+      for (int t = 0; t < nt; ++t) cost[t] = (double)rows[t + 1] * samples[t + 1] * (ranks[t + 1] + p);
+      mine = assign_targets(cost, h->world, h->rank);
+      std::vector<SketchTarget> sk_m;
+      std::vector<BasisTarget> bt_m;
+      ctas = 0;
+      for (int t = 0; t < nt; ++t)
+        if (mine[t]) {
+          sk[t].cta_begin = ctas;
+          ctas += sketch_target_ctas(sk[t]);
+          sk_m.push_back(sk[t]);
+          bt_m.push_back(bt[t]);
+        }
+      sk.swap(sk_m);
+      bt.swap(bt_m);
+    }
     assign_basis_ctas(bt);
     lists = make_basis_lists(bt, blob);
     for (int i : internal) {
@@ -508,23 +615,30 @@ struct HtShard {
     dp = reinterpret_cast<char*>(h->pset().d.p);
     hp = reinterpret_cast<char*>(h->pset().hst.p);
     for (auto& it : blob.items) std::memcpy(hp + it.first, it.second.data(), it.second.size());
-    std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * nt);
-    std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * nt);
+    if (!sk.empty()) std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * sk.size());
+    if (!bt.empty()) std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * bt.size());
     if (!tt.empty()) std::memcpy(hp + off_tt, tt.data(), sizeof(TransferTarget) * tt.size());
   }
 
   void upload(srtt_handle* h) const {
     CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemsetAsync(dinfo, 0, sizeof(int32_t) * 4 * (nt + 1), h->stream));
+    if (replicated) CK(cudaMemsetAsync(ws + off_upack, 0, sizeof(double) * upack_n, h->stream));
   }
   // Phase 1: partial sketches of every node (K1, one grouped launch).
   int enqueue_sketches(srtt_handle* h) const {
+    if (sk.empty()) return 0;
     return launch_sketch_group(reinterpret_cast<const SketchTarget*>(dp + off_sk), sk, ctas, cmax, h->stream);
   }
   // Phase 2: bases of every node (K2) and the internal transfers (K4).
   int enqueue_bases(srtt_handle* h) {
-    int n = launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt), lists, dp,
-                               reinterpret_cast<double*>(ws + off_pad), max_n);
+    int n = bt.empty() ? 0
+                       : launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt), lists, dp,
+                                            reinterpret_cast<double*>(ws + off_pad), max_n);
+    if (replicated) {  // every rank's node bases (others' entries are zero) and per-node info
+      allreduce_sum(h, reinterpret_cast<double*>(ws + off_upack), (size_t)upack_n);
+      allreduce_sum_i32(h, dinfo, 4 * (size_t)(nt + 1));
+    }
     if (!tt.empty()) {
       CK(srtt_launch_transfer(reinterpret_cast<const TransferTarget*>(dp + off_tt), (int)tt.size(), tctas, max_rl,
                               max_rr, h->stream));
@@ -563,7 +677,7 @@ struct HtShard {
         warnings.push_back("node " + std::to_string(id) + ": sketch revealed rank " + std::to_string(q) +
                            " < target; basis padded");
     }
-    if (hinfo[4 * nt] & 1) warnings.push_back(kU1ZeroWarning);
+    if (hinfo[4 * nt] != 0) warnings.push_back(kU1ZeroWarning);
     if (rep && rep->achieved_ranks) rep->achieved_ranks[0] = 1;
     if (rep && rep->sample_counts)
       for (int i = 0; i < nn; ++i) rep->sample_counts[i] = samples[i];
@@ -574,9 +688,16 @@ void run_sub_r_rtl_ht_sharded(srtt_handle* h, const double* x_in, int x_on_devic
                               int64_t col_lo, int64_t col_hi, const srtt_tree* tree_p, const int64_t* ranks_p,
                               const int64_t* samples_p, int64_t p, uint64_t seed, const srtt_exec_policy* exec,
                               double* const* leaf_out, double* const* transfers_out, int out_on_device,
-                              srtt_report* rep) {
+                              srtt_report* rep, bool replicated = false) {
   if (!h) invalid("srtt: null handle");
   comm_of(h);
+  if (replicated) {  // the root pass is split by column ranges of the replica
+    const Tree t = read_tree(tree_p, d);
+    int64_t nr = 1;
+    for (int m : t.modes[t.right[0]]) nr *= dims_p[m];
+    if (h->world > nr) invalid("replicated sub_r_rtl_ht: more ranks than root columns");
+    split_bounds(nr, h->world, h->rank, col_lo, col_hi);
+  }
   DeviceGuard guard(h->device);
   h->launches = 0;
   begin_call(h);
@@ -593,32 +714,33 @@ void run_sub_r_rtl_ht_sharded(srtt_handle* h, const double* x_in, int x_on_devic
   (void)Nfull;
   // the staged size needs the tree: build once with a null x to validate
   // and size, then point the targets at the staged buffer
-  S.build(h, nullptr, d, dims_p, tree_p, ranks_p, samples_p, p, seed, exec, col_lo, col_hi);
-  const int64_t nloc = (col_hi - col_lo) * S.nlr;
+  S.build(h, nullptr, d, dims_p, tree_p, ranks_p, samples_p, p, seed, exec, col_lo, col_hi, replicated);
+  const int64_t nloc = replicated ? S.N : (col_hi - col_lo) * S.nlr;
   std::vector<std::string> warnings;
   if (p < 4) warnings.push_back("oversampling below the recommended minimum of 4");
   tm.mark();  // 0
   const double* x = stage_input(h, x_in, x_on_device, nloc);
   tm.mark();  // 1
   for (auto& t : S.sk) t.x = x;
-  std::memcpy(S.hp + S.off_sk, S.sk.data(), sizeof(SketchTarget) * S.nt);
+  if (!S.sk.empty()) std::memcpy(S.hp + S.off_sk, S.sk.data(), sizeof(SketchTarget) * S.sk.size());
+  const double* xroot = replicated ? x + col_lo * S.nlr : x;  // this rank's columns of M
   const bool serial_root = exec && exec->emulate_serial_root;  // all bases precede the root here anyway
   (void)serial_root;
   const int il = S.tr.left[0], ir = S.tr.right[0];
   const int rl0 = (int)S.ranks[il], rr0 = (int)S.ranks[ir];
   double* d_root = (out_on_device && transfers_out && transfers_out[0]) ? transfers_out[0] : S.root();
-  std::string key = S.key(h, x) + "|" + ptr_key(d_root);
+  std::string key = S.key(h, x) + "|" + ptr_key(d_root) + (replicated ? "|rep" : "|sh");
   run_enqueue(h, key, [&] {
     S.upload(h);
     tm.n = 2;
     tm.mark();  // 2
     h->launches += S.enqueue_sketches(h);
     tm.mark();  // 3
-    allreduce_sum(h, S.zsum(), (size_t)S.zn);
+    if (!replicated) allreduce_sum(h, S.zsum(), (size_t)S.zn);
     tm.mark();  // 4
     h->launches += S.enqueue_bases(h);
     tm.mark();  // 5
-    h->launches += S.enqueue_root(h, x, S.ubasis(il), S.ubasis(ir), d_root);
+    h->launches += S.enqueue_root(h, xroot, S.ubasis(il), S.ubasis(ir), d_root);
     tm.mark();  // 6
     allreduce_sum(h, d_root, (size_t)rl0 * rr0);
     tm.mark();  // 7
@@ -759,6 +881,27 @@ int srtt_sub_r_rtl_ht_sharded(srtt_handle* h, const double* x_cols, int32_t x_on
   });
 }
 
+int srtt_sub_r_hosvd_replicated(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d,
+                                const int64_t* dims, const int64_t* ranks, int64_t oversampling,
+                                const int64_t* samples, uint64_t seed, const srtt_exec_policy* exec, double* core_out,
+                                double* const* factors_out, int32_t out_on_device, srtt_report* rep) {
+  return guarded([&] {
+    run_sub_r_hosvd_sharded(h, x, x_on_device, d, dims, 0, 0, ranks, oversampling, samples, seed, exec, core_out,
+                            factors_out, out_on_device, rep, true);
+  });
+}
+
+int srtt_sub_r_rtl_ht_replicated(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d, const int64_t* dims,
+                                 const srtt_tree* tree, const int64_t* ranks, const int64_t* samples,
+                                 int64_t oversampling, uint64_t seed, const srtt_exec_policy* exec,
+                                 double* const* leaf_factors_out, double* const* transfers_out, int32_t out_on_device,
+                                 srtt_report* rep) {
+  return guarded([&] {
+    run_sub_r_rtl_ht_sharded(h, x, x_on_device, d, dims, 0, 0, tree, ranks, samples, oversampling, seed, exec,
+                             leaf_factors_out, transfers_out, out_on_device, rep, true);
+  });
+}
+
 // ---- H-Tucker phases (synchronous; the caller exchanges between them) ------
 int srtt_ht_shard_sketches(srtt_handle* h, const double* x_cols, int32_t x_on_device, int32_t d,
                            const int64_t* dims, int64_t col_lo, int64_t col_hi, const srtt_tree* tree,
@@ -773,7 +916,7 @@ int srtt_ht_shard_sketches(srtt_handle* h, const double* x_cols, int32_t x_on_de
     CompRef B = comp_bufs(h);
     const double* x = to_device(h, B.a, x_cols, (col_hi - col_lo) * S.nlr, x_on_device);
     for (auto& t : S.sk) t.x = x;
-    std::memcpy(S.hp + S.off_sk, S.sk.data(), sizeof(SketchTarget) * S.nt);
+    if (!S.sk.empty()) std::memcpy(S.hp + S.off_sk, S.sk.data(), sizeof(SketchTarget) * S.sk.size());
     S.upload(h);
     S.enqueue_sketches(h);
     for (int i = 1; i < S.nn; ++i)

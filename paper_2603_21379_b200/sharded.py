@@ -118,7 +118,7 @@ def column_bounds(tree, dims, world: int, rank: int):
 
 
 def sub_r_hosvd_nccl(x_slab, dims, target, oversampling, samples, seed, *, handle, exec_policy=None,
-                     report=None, out=None, device_out=True):
+                     report=None, out=None, device_out=True, replicated=False):
     """Fused slab-sharded sub_r_hosvd through ``srtt_sub_r_hosvd_sharded``
     (the handle must own a communicator, see ``comm_init``). ``x_slab`` is
     this rank's X[..., lo:hi) (flat, first index fastest: a CUDA float64
@@ -150,10 +150,16 @@ def sub_r_hosvd_nccl(x_slab, dims, target, oversampling, samples, seed, *, handl
         call.fptrs[k] = _s._ptr(out[1][k])[0]
     ex = exec_policy._c() if exec_policy is not None else None
     rep_arg = C.byref(call.rep) if (report is not None or not device_out) else None
-    _s._check(_s._L().srtt_sub_r_hosvd_sharded(
-        handle._h, xp, xdev, d, call.dims_a.ctypes.data, lo, hi, call.ranks_a.ctypes.data,
-        int(oversampling), call.samp_a.ctypes.data, int(seed) & (2**64 - 1), C.byref(ex) if ex is not None else None,
-        _s._ptr(out[0])[0], call.fptrs, int(device_out), rep_arg))
+    if replicated:  # x_slab is ALL of X; modes assigned to ranks, core split by slabs of the replica
+        _s._check(_s._L().srtt_sub_r_hosvd_replicated(
+            handle._h, xp, xdev, d, call.dims_a.ctypes.data, call.ranks_a.ctypes.data, int(oversampling),
+            call.samp_a.ctypes.data, int(seed) & (2**64 - 1), C.byref(ex) if ex is not None else None,
+            _s._ptr(out[0])[0], call.fptrs, int(device_out), rep_arg))
+    else:
+        _s._check(_s._L().srtt_sub_r_hosvd_sharded(
+            handle._h, xp, xdev, d, call.dims_a.ctypes.data, lo, hi, call.ranks_a.ctypes.data,
+            int(oversampling), call.samp_a.ctypes.data, int(seed) & (2**64 - 1),
+            C.byref(ex) if ex is not None else None, _s._ptr(out[0])[0], call.fptrs, int(device_out), rep_arg))
     if report is not None:
         _s._report_from(call.rep, d, call.ach, call.sc, report, handle)
     return ShardedTucker(core=out[0], factors=list(out[1]), achieved_ranks=list(getattr(report, "achieved_ranks", [])),
@@ -161,7 +167,7 @@ def sub_r_hosvd_nccl(x_slab, dims, target, oversampling, samples, seed, *, handl
 
 
 def sub_r_rtl_ht_nccl(x_cols, dims, tree, ranks, samples, oversampling, seed, *, handle, exec_policy=None,
-                      report=None, device_out=True):
+                      report=None, device_out=True, replicated=False):
     """Fused column-range-sharded sub_r_rtl_ht through
     ``srtt_sub_r_rtl_ht_sharded``; ``x_cols`` holds this rank's columns
     [c_lo, c_hi) of M = n_left x n_right (``column_bounds``). Returns device
@@ -200,10 +206,17 @@ def sub_r_rtl_ht_nccl(x_cols, dims, tree, ranks, samples, oversampling, seed, *,
                       C.cast(wbuf, C.c_char_p), 8192, 0)
     ct = tree._c()
     ex = exec_policy._c() if exec_policy is not None else None
-    _s._check(_s._L().srtt_sub_r_rtl_ht_sharded(
-        handle._h, xp, xdev, d, dims_a.ctypes.data, lo, hi, C.byref(ct), ranks_a.ctypes.data,
-        samp_a.ctypes.data, int(oversampling), int(seed) & (2**64 - 1), C.byref(ex) if ex is not None else None,
-        lp, tp, int(device_out), C.byref(crep) if (report is not None or not device_out) else None))
+    rarg = C.byref(crep) if (report is not None or not device_out) else None
+    if replicated:  # x_cols is ALL of X; nodes assigned to ranks, root split by column ranges
+        _s._check(_s._L().srtt_sub_r_rtl_ht_replicated(
+            handle._h, xp, xdev, d, dims_a.ctypes.data, C.byref(ct), ranks_a.ctypes.data, samp_a.ctypes.data,
+            int(oversampling), int(seed) & (2**64 - 1), C.byref(ex) if ex is not None else None, lp, tp,
+            int(device_out), rarg))
+    else:
+        _s._check(_s._L().srtt_sub_r_rtl_ht_sharded(
+            handle._h, xp, xdev, d, dims_a.ctypes.data, lo, hi, C.byref(ct), ranks_a.ctypes.data,
+            samp_a.ctypes.data, int(oversampling), int(seed) & (2**64 - 1), C.byref(ex) if ex is not None else None,
+            lp, tp, int(device_out), rarg))
     if report is not None:
         _s._report_from(crep, nn, ach, sc, report, handle)
     return _s.HTuckerDecomposition(tree, leaf, trs)

@@ -161,6 +161,9 @@ def _L():
                                                  vp]
         lib.srtt_sub_r_rtl_ht_sharded.argtypes = [vp, vp, i32, i32, vp, i64, i64, vp, vp, vp, i64, u64, vp, vp, vp,
                                                   i32, vp]
+        lib.srtt_sub_r_hosvd_replicated.argtypes = [vp, vp, i32, i32, vp, vp, i64, vp, u64, vp, vp, vp, i32, vp]
+        lib.srtt_sub_r_rtl_ht_replicated.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, i64, u64, vp, vp, vp, i32,
+                                                     vp]
         _LIB = lib
     return _LIB
 

@@ -238,6 +238,60 @@ def test_fused_nccl_world1_equals_single_gpu(O):
     assert all(torch.equal(a.reshape(-1), b) for a, b in zip(hs1.transfers, hs2.transfers) if a is not None)
 
 
+def test_replicated_world1_equals_single_gpu():
+    """Replicated regime (all of X on every rank, modes / nodes assigned to
+    ranks, factor pack allreduced): at world 1 every target is this rank's
+    and the split full pass is the whole pass, so the outputs equal the
+    single-GPU ones bitwise."""
+    import torch
+
+    import paper_2603_21379_b200 as P
+    from paper_2603_21379_b200 import sharded
+
+    h = P.Handle(0, use_graphs=True)
+    sharded.comm_init_local(h)
+    h.set_stream(torch.cuda.current_stream().cuda_stream)
+    dims, ranks, p, samples, seed = [40, 36, 30, 8], [6, 5, 6, 3], 5, [44, 40, 44, 30], 8
+    x = torch.from_numpy(np.ravel(np.random.default_rng(5).standard_normal(dims), order="F").copy()).cuda()
+    single = P.sub_r_hosvd(x, ranks, p, samples, seed, dims=dims, device_out=True, handle=P.Handle(0))
+    rep = P.SubsampleReport()
+    t = sharded.sub_r_hosvd_nccl(x, dims, ranks, p, samples, seed, handle=h, report=rep, replicated=True)
+    t = sharded.sub_r_hosvd_nccl(x, dims, ranks, p, samples, seed, handle=h, replicated=True)
+    torch.cuda.synchronize()
+    assert rep.achieved_ranks == ranks
+    assert torch.equal(t.core, single.core)
+    assert all(torch.equal(a, b) for a, b in zip(t.factors, single.factors))
+    tree = P.DimensionTree.balanced(4)
+    hd = [9, 8, 7, 6]
+    hr = P.uniform_node_ranks(tree, 3)
+    hs = [1] + [min(24, tree.node_cols(i, hd)) for i in range(1, tree.num_nodes)]
+    y = torch.from_numpy(np.ravel(np.random.default_rng(4).standard_normal(hd), order="F").copy()).cuda()
+    h1 = P.sub_r_rtl_ht(y, tree, hr, hs, 4, 6, dims=hd, device_out=True, handle=P.Handle(0))
+    rep = P.HtSubsampleReport()
+    h2 = sharded.sub_r_rtl_ht_nccl(y, hd, tree, hr, hs, 4, 6, handle=h, report=rep, replicated=True)
+    torch.cuda.synchronize()
+    assert rep.achieved_ranks == [1] + [3] * 6
+    assert all(torch.equal(a, b) for a, b in zip(h1.leaf_factors, h2.leaf_factors))
+    assert all(torch.equal(a.reshape(-1), b) for a, b in zip(h1.transfers, h2.transfers) if a is not None)
+
+
+def test_target_assignment_is_balanced_and_identical_on_every_rank(O):
+    """The LPT assignment the replicated regime uses, restated: every target
+    goes to exactly one rank and the heaviest rank carries at most the
+    optimum plus the largest target (the greedy bound)."""
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        n, world = int(rng.integers(1, 15)), int(rng.integers(1, 9))
+        cost = rng.integers(1, 100, size=n).astype(float)
+        order = sorted(range(n), key=lambda t: -cost[t])
+        load, owner = [0.0] * world, [0] * n
+        for t in order:
+            w = min(range(world), key=lambda r: (load[r], r))
+            load[w] += cost[t]
+            owner[t] = w
+        assert max(load) <= cost.sum() / world + cost.max() + 1e-9
+
+
 def test_fused_nccl_errors():
     import torch
 
