@@ -530,13 +530,15 @@ def _local_part(cfg, x_full, world, rank, P, sharded):
     return x_full[lo * nl:hi * nl].clone(), (lo, hi)
 
 
-def run_sharded(args):
+def run_sharded(args, replicated=False):
     """ONE decomposition of the config's global tensor per step, split over
-    the ranks (strong scaling): each rank holds only its contiguous part
-    (Tucker: last-mode slab; H-Tucker: a column range of the root
-    matricization) and calls the fused C-ABI entry (srtt_sub_r_hosvd_sharded /
-    srtt_sub_r_rtl_ht_sharded) whose handle owns an NCCL communicator;
-    kernels and the two allreduces run in one CUDA graph per rank."""
+    the ranks (strong scaling), through the fused C-ABI entries whose handle
+    owns an NCCL communicator (kernels and allreduces in one CUDA graph per
+    rank). Two regimes (north star): sharded -- each rank holds only its
+    contiguous part (Tucker: last-mode slab; H-Tucker: a column range of the
+    root matricization; srtt_sub_r_hosvd_sharded / srtt_sub_r_rtl_ht_sharded);
+    replicated -- every rank holds all of X, modes / nodes are assigned to
+    ranks and the full pass is split (srtt_sub_r_*_replicated)."""
     import torch
     import torch.distributed as dist
 
@@ -556,7 +558,10 @@ def run_sharded(args):
     # every rank generates the SAME global tensor (seed 0, deterministic
     # generator) and keeps only its part
     x_full = synth.make_tensor(cfg, seed=0, backend="torch", device=f"cuda:{local}")
-    x_loc, part = _local_part(cfg, x_full, world, rank, P, sharded)
+    if replicated:
+        x_loc = x_full
+    else:
+        x_loc, part = _local_part(cfg, x_full, world, rank, P, sharded)
     del x_full
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
@@ -572,7 +577,8 @@ def run_sharded(args):
 
         def step(report=None, x=x_loc, device_out=True):
             return sharded.sub_r_hosvd_nccl(x, dims, ranks, cfg.p, samples, 0, handle=h, report=report,
-                                            out=out if device_out else None, device_out=device_out)
+                                            out=out if device_out else None, device_out=device_out,
+                                            replicated=replicated)
 
         def digest(res):
             return torch.cat([res.core.reshape(-1)] + [f.reshape(-1) for f in res.factors]).cpu()
@@ -583,7 +589,7 @@ def run_sharded(args):
 
         def step(report=None, x=x_loc, device_out=True):
             return sharded.sub_r_rtl_ht_nccl(x, dims, tree, ranks, samples, cfg.p, 0, handle=h, report=report,
-                                             device_out=device_out)
+                                             device_out=device_out, replicated=replicated)
 
         def digest(res):
             return torch.cat([u.reshape(-1) for u in res.leaf_factors] +
@@ -659,13 +665,17 @@ def run_sharded(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": _config_dict(cfg),
-            "parallelism": (f"{'slab' if cfg.kind == 'tucker' else 'column-range'}-sharded x{world} "
+            "parallelism": (f"replicated x{world}: X on every rank, {'modes' if cfg.kind == 'tucker' else 'nodes'} "
+                            f"assigned to ranks, factor pack + full-pass partials allreduced (fused C-ABI + NCCL, "
+                            f"one CUDA graph per rank)" if replicated else
+                            f"{'slab' if cfg.kind == 'tucker' else 'column-range'}-sharded x{world} "
                             f"(one global tensor; fused C-ABI + NCCL allreduce of sketches and core, one CUDA "
                             f"graph per rank)"),
             "clocks": sampler.summary(), "gpu_launches": launches_per_step * args.steps,
             "outputs_verified": verified,
             "e2e": {"value": cfg.entries * e2e_steps / float(e2e_el.item()), "unit": UNIT,
-                    "h2d_bytes_per_step": 8 * int(np.prod(local_cfg.dims)), "d2h_bytes_per_step": d2h,
+                    "h2d_bytes_per_step": 8 * (cfg.entries if replicated else int(np.prod(local_cfg.dims))),
+                    "d2h_bytes_per_step": d2h,
                     "steps": e2e_steps, "per_rank": True},
             "roofline": roofline}
     if rank == 0:
@@ -708,17 +718,21 @@ def main():
                     help="c1-c5: BASELINE.json configs; c4a20 / c5s64k: sketch-heavy variants ADDED for the K1 "
                          "bandwidth measurement (not BASELINE configs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mode", choices=["auto", "replicas", "sharded"], default="auto",
-                    help="auto: N=1 single-GPU decomposition, N>1 ONE global tensor sharded over the ranks "
-                         "(strong scaling); replicas: independent decompositions per rank (weak scaling); "
-                         "sharded: force the NCCL-sharded path (also at N=1)")
+    ap.add_argument("--mode", choices=["auto", "replicas", "sharded", "replicated"], default="auto",
+                    help="auto: N=1 single-GPU decomposition; N>1 ONE global tensor over the ranks (strong "
+                         "scaling): slab-sharded for c5 / c5s64k (the BASELINE's sharded config), replicated with "
+                         "modes / nodes assigned to ranks for the configs that fit per GPU; replicas: independent "
+                         "decompositions per rank (weak scaling); sharded / replicated: force that NCCL path (also "
+                         "at N=1)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    elif args.mode == "sharded" or (args.mode == "auto" and _dist_env()[1] > 1):
+    elif args.mode == "sharded" or (args.mode == "auto" and _dist_env()[1] > 1 and args.config.startswith("c5")):
         run_sharded(args)
+    elif args.mode == "replicated" or (args.mode == "auto" and _dist_env()[1] > 1):
+        run_sharded(args, replicated=True)
     else:
         run_product(args)
 
