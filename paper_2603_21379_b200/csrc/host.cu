@@ -29,6 +29,7 @@ size_t srtt_sketch_smem_bytes(int cmax);
 cudaError_t srtt_launch_sketch(const SketchTarget*, int, int64_t, int, cudaStream_t);
 cudaError_t srtt_launch_sketch_reduce(const SketchTarget*, int, int64_t, cudaStream_t);
 cudaError_t srtt_launch_omega(const SketchTarget*, int, int64_t, cudaStream_t);
+cudaError_t srtt_launch_sketch_contig(const SketchTarget*, int, int64_t, int, cudaStream_t);
 cudaError_t srtt_launch_scatter_block(const double*, double*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                                       int64_t, cudaStream_t);
 size_t srtt_basis_top_smem(int m, int c, int r);
@@ -1056,12 +1057,32 @@ SketchTarget make_sketch_target(const double* x, const std::vector<int64_t>& dim
   T.row_tile = (int)std::min<int64_t>(T.rows, 64);
   T.slab_digit = -1;
   T.fsplit = sketch_fsplit(T.rows, w);
+  // contiguous fibres (S = the leading modes 0..m-1, so fibre j starts at
+  // cols[j] * rows) with many fibres: staged DMMA kernel (K1c)
+  bool leading = !modes.empty();
+  std::vector<int> ms(modes.begin(), modes.end());
+  std::sort(ms.begin(), ms.end());
+  for (size_t i = 0; i < ms.size(); ++i) leading = leading && ms[i] == (int)i;
+  T.contig = (leading && w >= 512 && c <= 64 && !std::getenv("SRTT_NO_K1C")) ? 1 : 0;
   return T;
 }
 
-// CTAs of one target in the grouped K1 grid.
+// CTAs of one target in the grouped scalar K1 grid (0 for K1c targets).
 int64_t sketch_target_ctas(const SketchTarget& T) {
+  if (T.contig) return 0;
   return (T.rows + T.row_tile - 1) / T.row_tile * T.fsplit;
+}
+
+// K1c index space (contig targets need Omega in memory and no sharding
+// masks; others fall back to the scalar kernel); returns its CTA count.
+int64_t assign_contig_ctas(std::vector<SketchTarget>& sk) {
+  int64_t n = 0;
+  for (auto& t : sk) {
+    if (t.contig && (!t.omega || t.slab_digit >= 0 || t.flat_hi > 0)) t.contig = 0;
+    t.cta_begin_c = n;
+    if (t.contig) n += (t.rows + 63) / 64 * t.fsplit;
+  }
+  return n;
 }
 
 // K1 over a group of targets (device array dT, host copy sk), plus the
@@ -1076,8 +1097,21 @@ int launch_sketch_group(const SketchTarget* dT, const std::vector<SketchTarget>&
     CK(srtt_launch_omega(dT, (int)sk.size(), om_elems, st));
     ++n;
   }
-  CK(srtt_launch_sketch(dT, (int)sk.size(), ctas, cmax, st));
-  ++n;
+  if (ctas > 0) {
+    CK(srtt_launch_sketch(dT, (int)sk.size(), ctas, cmax, st));
+    ++n;
+  }
+  int64_t ctas_c = 0;
+  int cmax_c = 0;
+  for (auto& t : sk)
+    if (t.contig) {
+      ctas_c += (t.rows + 63) / 64 * t.fsplit;
+      cmax_c = std::max(cmax_c, t.c);
+    }
+  if (ctas_c > 0) {
+    CK(srtt_launch_sketch_contig(dT, (int)sk.size(), ctas_c, cmax_c, st));
+    ++n;
+  }
   int64_t split_elems = 0;
   for (auto& t : sk)
     if (t.fsplit > 1) split_elems = std::max<int64_t>(split_elems, t.rows * t.c);
@@ -1095,6 +1129,8 @@ void attach_sketch_scratch(SketchTarget& T, char* scratch) {
     T.omega_gen = reinterpret_cast<double*>(scratch + (part + 255) / 256 * 256);
     T.omega = T.omega_gen;
   }
+  // K1c needs Omega in memory and no sharding masks (set before this call)
+  if (T.contig && (!T.omega || T.slab_digit >= 0 || T.flat_hi > 0)) T.contig = 0;
 }
 
 // ---- report helpers ------------------------------------------------------------
@@ -1481,6 +1517,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   dp = reinterpret_cast<char*>(h->pset().d.p);
   char* hp = reinterpret_cast<char*>(h->pset().hst.p);
   for (auto& it : blob.items) std::memcpy(hp + it.first, it.second.data(), it.second.size());
+  assign_contig_ctas(sk);
   std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * d);
   std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * d);
   std::string key = "T";
@@ -1931,6 +1968,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     max_rr = std::max(max_rr, T.rr);
     tt.push_back(T);
   }
+  assign_contig_ctas(sk);
   std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * nt);
   std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * nt);
   if (!tt.empty()) std::memcpy(hp + off_tt, tt.data(), sizeof(TransferTarget) * tt.size());
@@ -2191,6 +2229,11 @@ int srtt_sketch(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d,
     SketchTarget* dT = reinterpret_cast<SketchTarget*>(reinterpret_cast<char*>(B.e.p) + 64);
     B.d.ensure(sizeof(SketchTarget));
     dT = reinterpret_cast<SketchTarget*>(B.d.p);
+    {
+      std::vector<SketchTarget> one = {T};
+      assign_contig_ctas(one);
+      T = one[0];
+    }
     CK(cudaMemcpyAsync(dT, &T, sizeof(T), cudaMemcpyHostToDevice, h->stream));
     launch_sketch_group(dT, {T}, sketch_target_ctas(T), c, h->stream);
     copy_out(h, z_out, T.z, sizeof(double) * T.rows * c, out_on_device);
@@ -2424,6 +2467,7 @@ int srtt_shard_sketches(srtt_handle* h, const double* x_local, int32_t x_on_devi
                          h->stream));
     }
     CK(cudaMemsetAsync(ws + off_flags, 0, sizeof(int32_t) * 4, h->stream));
+    assign_contig_ctas(sk);
     CK(cudaMemcpyAsync(ws + off_t, sk.data(), sizeof(SketchTarget) * d, cudaMemcpyHostToDevice, h->stream));
     launch_sketch_group(reinterpret_cast<const SketchTarget*>(ws + off_t), sk, ctas, cmax, h->stream);
     for (int k = 0; k < d; ++k)

@@ -168,6 +168,137 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
   }
 }
 
+// ---------------------------------------------------------------------------
+// Staged DMMA sketch for contiguous fibres with many fibres (K1c).
+// Z(i, :) = sum_j X[cols[j] * rows + i] Omega(j, :): a GEMM whose A operand
+// (rows x fibres) is gathered column by column. A CTA owns 64 rows and one
+// fibre chunk; each stage brings 32 fibre segments (64 rows, coalesced
+// 8-byte cp.async, any alignment; rows / fibres beyond the ends zero-fill)
+// and the matching 32 rows of Omega into shared memory, kCStages deep, and
+// the 8 warps (8 rows each) accumulate Z tiles with DMMA m8n8k4 (A = the
+// fibre values, B = Omega, c padded to multiples of 8). Fixed k order:
+// deterministic. Partials per fibre chunk as in sketch_kernel.
+// ---------------------------------------------------------------------------
+constexpr int kCRows = 64, kCFib = 32, kCStages = 4;
+constexpr int kCYld = kCRows + 4;  // = 4 (mod 16): conflict-free A fragment reads
+
+__device__ __forceinline__ void cp_async8z(void* smem, const double* g, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(srtt_dev::smem_u32(smem)), "l"(g),
+               "r"(ok ? 8u : 0u)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int CT>  // 8-column tiles of c
+__global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTarget* __restrict__ targets,
+                                                                 int ntargets) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ SketchTarget T;
+  __shared__ int tsel;
+  constexpr int CP = 8 * CT + ((4 - (8 * CT) % 16) + 16) % 16;  // Omega row pitch = 4 (mod 16)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  if (tid == 0) {
+    int lo = 0, hi = ntargets - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (targets[mid].cta_begin_c <= (int64_t)blockIdx.x) lo = mid; else hi = mid - 1;
+    }
+    tsel = lo;
+  }
+  __syncthreads();
+  {
+    const int* src = reinterpret_cast<const int*>(&targets[tsel]);
+    int* dst = reinterpret_cast<int*>(&T);
+    for (int k = tid; k < (int)(sizeof(SketchTarget) / sizeof(int)); k += kThreads) dst[k] = src[k];
+  }
+  __syncthreads();
+  const int c = T.c;
+  const int64_t rows = T.rows;
+  const int64_t local = (int64_t)blockIdx.x - T.cta_begin_c;
+  const int64_t row_ctas = (rows + kCRows - 1) / kCRows;
+  const int64_t rt = local % row_ctas;
+  const int fchunk = (int)(local / row_ctas);
+  const int64_t flen = (T.w + T.fsplit - 1) / T.fsplit;
+  const int64_t jbeg = (int64_t)fchunk * flen;
+  const int64_t jend = srtt_dev::min64(T.w, jbeg + flen);
+  const int64_t row0 = rt * kCRows;
+  double* Ys = reinterpret_cast<double*>(smem_raw);     // kCStages x kCFib x kCYld
+  double* Os = Ys + kCStages * kCFib * kCYld;           // kCStages x kCFib x CP
+  const double* __restrict__ x = T.x;
+  const double* __restrict__ om = T.omega;
+
+  // stage s <- fibres [j0, j0 + kCFib)
+  auto load = [&](int s, int64_t j0) {
+    double* ys = Ys + s * kCFib * kCYld;
+    double* os = Os + s * kCFib * CP;
+    const int r = tid % kCRows;
+    const int64_t row = row0 + r;
+    for (int f = tid / kCRows; f < kCFib; f += kThreads / kCRows) {
+      const int64_t j = j0 + f;
+      const bool ok = j < jend && row < rows;
+      const double* src = ok ? x + T.cols[j] * rows + row : x;
+      cp_async8z(ys + f * kCYld + r, src, ok);
+    }
+    for (int e = tid; e < kCFib * CP; e += kThreads) {
+      const int f = e / CP, cc = e % CP;
+      const int64_t j = j0 + f;
+      const bool ok = j < jend && cc < c;
+      cp_async8z(os + e, ok ? om + j + (int64_t)cc * T.w : om, ok);
+    }
+  };
+
+  double acc[CT][2];
+#pragma unroll
+  for (int ct = 0; ct < CT; ++ct) acc[ct][0] = acc[ct][1] = 0.0;
+  const int64_t nst = (jend - jbeg + kCFib - 1) / kCFib;
+#pragma unroll
+  for (int s = 0; s < kCStages - 1; ++s) {
+    if (s < nst) load(s, jbeg + (int64_t)s * kCFib);
+    cp_async_commit();
+  }
+  for (int64_t st = 0; st < nst; ++st) {
+    cp_async_wait<kCStages - 2>();
+    __syncthreads();
+    {  // refill the stage freed by the previous iteration
+      const int64_t nx = st + kCStages - 1;
+      if (nx < nst) load((int)(nx % kCStages), jbeg + nx * kCFib);
+      cp_async_commit();
+    }
+    const int s = (int)(st % kCStages);
+    const double* ys = Ys + s * kCFib * kCYld + 8 * warp + g;
+    const double* os = Os + s * kCFib * CP + g;
+#pragma unroll
+    for (int kk = 0; kk < kCFib / 4; ++kk) {
+      const int f = 4 * kk + tq;
+      const double a = ys[f * kCYld];
+#pragma unroll
+      for (int ct = 0; ct < CT; ++ct) srtt_dev::dmma_8x8x4(acc[ct][0], acc[ct][1], a, os[f * CP + 8 * ct]);
+    }
+  }
+  cp_async_wait<0>();
+  // D fragment: row 8 warp + g, columns 8 ct + 2 tq + {0, 1}
+  const int64_t row = row0 + 8 * warp + g;
+  if (row < rows) {
+    const int64_t ldz = T.ldz > 0 ? T.ldz : rows;
+#pragma unroll
+    for (int ct = 0; ct < CT; ++ct)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int cc = 8 * ct + 2 * tq + v;
+        if (cc >= c) continue;
+        if (T.fsplit > 1)
+          T.zpart[((int64_t)fchunk * c + cc) * rows + row] = acc[ct][v];
+        else
+          T.z[row + (int64_t)cc * ldz] = acc[ct][v];
+      }
+  }
+}
+
 // Omega of the targets with omega_gen set, generated once: normal number
 // t = j + cc * w of the target's stream after its sampling draws.
 __global__ void __launch_bounds__(256) omega_kernel(const SketchTarget* __restrict__ targets, int ntargets) {
@@ -198,6 +329,37 @@ __global__ void __launch_bounds__(256) sketch_reduce_kernel(const SketchTarget* 
 }
 
 }  // namespace
+
+size_t srtt_sketch_contig_smem(int ct) {
+  const int CP = 8 * ct + ((4 - (8 * ct) % 16) + 16) % 16;
+  return sizeof(double) * (size_t)kCStages * kCFib * (kCYld + CP);
+}
+
+cudaError_t srtt_launch_sketch_contig(const SketchTarget* d_targets, int ntargets, int64_t total_ctas, int cmax,
+                                      cudaStream_t stream) {
+  if (total_ctas <= 0) return cudaSuccess;
+  const int ct = (cmax + 7) / 8;
+  const size_t smem = srtt_sketch_contig_smem(ct);
+#define SRTT_CONTIG_CASE(N)                                                                         \
+  case N:                                                                                           \
+    SRTT_ENSURE_SMEM((sketch_contig_kernel<N>), smem);                                              \
+    sketch_contig_kernel<N><<<(unsigned)total_ctas, kThreads, smem, stream>>>(d_targets, ntargets); \
+    break;
+  switch (ct) {
+    SRTT_CONTIG_CASE(1)
+    SRTT_CONTIG_CASE(2)
+    SRTT_CONTIG_CASE(3)
+    SRTT_CONTIG_CASE(4)
+    SRTT_CONTIG_CASE(5)
+    SRTT_CONTIG_CASE(6)
+    SRTT_CONTIG_CASE(7)
+    SRTT_CONTIG_CASE(8)
+    default:
+      return cudaErrorInvalidValue;
+  }
+#undef SRTT_CONTIG_CASE
+  return cudaGetLastError();
+}
 
 cudaError_t srtt_launch_omega(const SketchTarget* d_targets, int ntargets, int64_t max_elems, cudaStream_t stream) {
   const int grid = (int)srtt_dev::min64(4 * 148, (max_elems + 255) / 256);

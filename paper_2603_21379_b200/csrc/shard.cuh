@@ -310,6 +310,7 @@ void run_sub_r_hosvd_sharded(srtt_handle* h, const double* x_in, int x_on_device
   dp = reinterpret_cast<char*>(h->pset().d.p);
   char* hp = reinterpret_cast<char*>(h->pset().hst.p);
   for (auto& it : blob.items) std::memcpy(hp + it.first, it.second.data(), it.second.size());
+  assign_contig_ctas(sk);
   if (nsk) std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * nsk);
   if (nsk) std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * nsk);
 
@@ -615,6 +616,7 @@ struct HtShard {
     dp = reinterpret_cast<char*>(h->pset().d.p);
     hp = reinterpret_cast<char*>(h->pset().hst.p);
     for (auto& it : blob.items) std::memcpy(hp + it.first, it.second.data(), it.second.size());
+    assign_contig_ctas(sk);
     if (!sk.empty()) std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * sk.size());
     if (!bt.empty()) std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * bt.size());
     if (!tt.empty()) std::memcpy(hp + off_tt, tt.data(), sizeof(TransferTarget) * tt.size());
