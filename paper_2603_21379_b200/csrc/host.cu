@@ -1016,8 +1016,10 @@ int sketch_fsplit(int64_t rows, int64_t w) {
 // Workspace for a target's fibre-chunk partials (when split) and its
 // once-generated Omega (when more than one CTA would generate it), appended.
 bool sketch_omega_once(int64_t rows, int64_t w) {
+  // only where regenerating it per CTA costs more than one extra launch:
+  // many CTAs AND a large Omega (C4's 324 CTAs x 900 normals do not pay)
   const int64_t rt = std::min<int64_t>(rows, 64);
-  return (rows + rt - 1) / rt * sketch_fsplit(rows, w) > 1;
+  return (rows + rt - 1) / rt * sketch_fsplit(rows, w) >= 8 && w >= 512;
 }
 size_t sketch_part_bytes(int64_t rows, int64_t w, int c) {
   const int f = sketch_fsplit(rows, w);
@@ -1422,7 +1424,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     }
     pkey += std::to_string(p) + "|" + ptr_key(x) + "|" + (out_on_device ? ptr_key(core_out) : "h") + "|" +
             ptr_key(h->stream) + "|" + std::to_string(partitions) + "|" + std::to_string(h->cur) +
-            (h->timing ? "|t" : "|n");
+            (h->timing ? "|t" : "|n") + ((rep || !out_on_device) ? "|i" : "|o");
     auto pit = h->prepared.find(pkey);
     if (pit != h->prepared.end() && pit->second.ws == h->ws.p && pit->second.dp == h->pset().d.p &&
         pit->second.hp == h->pset().hst.p && h->graphs.count(pit->second.graph_key)) {
@@ -1483,11 +1485,14 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
 
   // --- parameter blob (indices, target descriptors, basis lists): one H2D copy
   if (4 * (d + 1) > kInfoInts) invalid("sub_r_hosvd: too many modes");
-  int32_t* const dinfo = h->pset().dinfo();
+  // per-target info words + status flags live at the head of the parameter
+  // blob: its H2D copy zeroes them every call (no separate memset), they
+  // are copied back only for calls that synchronise
   int32_t* const hinfo = h->pset().hinfo();
   const size_t info_bytes = sizeof(int32_t) * 4 * (d + 1);
-  int32_t* d_flags = dinfo + 4 * d;
+  const bool need_info = rep || !out_on_device;
   Blob blob;
+  const size_t off_info = blob.reserve(info_bytes);
   std::vector<size_t> off_cols(d);
   for (int k = 0; k < d; ++k) off_cols[k] = blob.add(cols[k].data(), sizeof(int64_t) * cols[k].size());
   const size_t off_sk = blob.reserve(sizeof(SketchTarget) * d);
@@ -1497,6 +1502,8 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   int64_t ctas = 0;
   h->pset().d.ensure(blob.lay.off + 4096);
   char* dp = reinterpret_cast<char*>(h->pset().d.p);
+  int32_t* const dinfo = reinterpret_cast<int32_t*>(dp + off_info);
+  int32_t* d_flags = dinfo + 4 * d;
   for (int k = 0; k < d; ++k) {
     const int c = (int)(ranks[k] + p);
     sk[k] = make_sketch_target(x, dims, {k}, samples[k], c);
@@ -1517,6 +1524,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   dp = reinterpret_cast<char*>(h->pset().d.p);
   char* hp = reinterpret_cast<char*>(h->pset().hst.p);
   for (auto& it : blob.items) std::memcpy(hp + it.first, it.second.data(), it.second.size());
+  std::memset(hp + off_info, 0, info_bytes);
   assign_contig_ctas(sk);
   std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * d);
   std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * d);
@@ -1526,10 +1534,9 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
            ptr_key(uptr[k]);
   key += "|" + std::to_string(p) + "|" + ptr_key(x) + "|" + ptr_key(d_core) + "|" + ptr_key(ws) + "|" + ptr_key(dp) +
          "|" + ptr_key(hp) + "|" + ptr_key(h->stream) + "|" + std::to_string(blob.lay.off) +
-         (h->timing ? "|t" : "|n");
+         (h->timing ? "|t" : "|n") + (need_info ? "|i" : "|o");
   run_enqueue(h, key, [&] {
     CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
-    CK(cudaMemsetAsync(dinfo, 0, info_bytes, h->stream));
     tm.n = 2;
     tm.mark();  // 2
     // --- K1: grouped gather + sketch over all modes
@@ -1558,7 +1565,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
       h->launches++;
     }
     tm.mark();  // 5
-    CK(cudaMemcpyAsync(hinfo, dinfo, info_bytes, cudaMemcpyDeviceToHost, h->stream));
+    if (need_info) CK(cudaMemcpyAsync(hinfo, dinfo, info_bytes, cudaMemcpyDeviceToHost, h->stream));
   });
   tm.n = 6;
   // --- outputs (host destinations only; device outputs were written in place)
@@ -1892,10 +1899,9 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   }
   const size_t off_pad = L.take(sizeof(double) * max_n * nt);
   if (4 * (nt + 1) > kInfoInts) invalid("sub_r_rtl_ht: too many tree nodes");
-  int32_t* const dinfo = h->pset().dinfo();
   const int32_t* hi = h->pset().hinfo();
   const size_t info_bytes = sizeof(int32_t) * 4 * (nt + 1);
-  int32_t* d_flags = dinfo + 4 * nt;
+  const bool need_info = rep || !out_on_device;
   // transfers of internal non-root nodes, and the root
   std::vector<int> internal;
   for (int i = 1; i < nn; ++i)
@@ -1913,6 +1919,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   char* ws = reinterpret_cast<char*>(h->ws.p);
 
   Blob blob;
+  const size_t off_info = blob.reserve(info_bytes);  // zeroed by the blob copy (see sub_r_hosvd)
   std::vector<size_t> off_cols(nt);
   for (int t = 0; t < nt; ++t) off_cols[t] = blob.add(cols[t].data(), sizeof(int64_t) * cols[t].size());
   const size_t off_sk = blob.reserve(sizeof(SketchTarget) * nt);
@@ -1920,6 +1927,8 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   const size_t off_tt = blob.reserve(sizeof(TransferTarget) * std::max<size_t>(1, internal.size()));
   h->pset().d.ensure(blob.lay.off + 4096);
   char* dp = reinterpret_cast<char*>(h->pset().d.p);
+  int32_t* const dinfo = reinterpret_cast<int32_t*>(dp + off_info);
+  int32_t* d_flags = dinfo + 4 * nt;
   std::vector<SketchTarget> sk(nt);
   std::vector<BasisTarget> bt(nt);
   int64_t ctas = 0;
@@ -1968,6 +1977,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     max_rr = std::max(max_rr, T.rr);
     tt.push_back(T);
   }
+  std::memset(hp + off_info, 0, info_bytes);
   assign_contig_ctas(sk);
   std::memcpy(hp + off_sk, sk.data(), sizeof(SketchTarget) * nt);
   std::memcpy(hp + off_bt, bt.data(), sizeof(BasisTarget) * nt);
@@ -1979,7 +1989,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
            std::to_string(tr.modes[i].size());
   key += "|" + std::to_string(p) + "|" + ptr_key(x) + "|" + ptr_key(ws) + "|" + ptr_key(dp) + "|" + ptr_key(hp) + "|" +
          ptr_key(h->stream) + "|" + std::to_string(blob.lay.off) + "|" + std::to_string(out_on_device) +
-         (serial_root ? "|s" : "|p") + (h->timing ? "|t" : "|n");
+         (serial_root ? "|s" : "|p") + (h->timing ? "|t" : "|n") + (need_info ? "|i" : "|o");
   if (out_on_device) {
     for (int k = 0; k < d; ++k) key += "|" + ptr_key(leaf_out[k]);
     if (transfers_out)
@@ -1998,7 +2008,6 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   run_enqueue(h, key, [&] {
     tm.n = 2;
     CK(cudaMemcpyAsync(dp, hp, blob.lay.off, cudaMemcpyHostToDevice, h->stream));
-    CK(cudaMemsetAsync(dinfo, 0, info_bytes, h->stream));
     tm.mark();  // 2
     h->launches += launch_sketch_group(reinterpret_cast<const SketchTarget*>(dp + off_sk), sk, ctas, cmax, h->stream);
     tm.mark();  // 3
@@ -2026,7 +2035,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     // join
     CK(cudaStreamWaitEvent(h->stream, h->fj[3], 0));
     tm.mark();  // 6
-    CK(cudaMemcpyAsync(const_cast<int32_t*>(hi), dinfo, info_bytes, cudaMemcpyDeviceToHost, h->stream));
+    if (need_info) CK(cudaMemcpyAsync(const_cast<int32_t*>(hi), dinfo, info_bytes, cudaMemcpyDeviceToHost, h->stream));
   });
   tm.n = 7;
   if (!out_on_device) {
