@@ -232,17 +232,30 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
   const double* __restrict__ x = T.x;
   const double* __restrict__ om = T.omega;
 
-  // stage s <- fibres [j0, j0 + kCFib)
+  // Fibre base offsets of the stages are read one stage ahead of their
+  // copies (register-held), so the cols[] load latency never sits in front
+  // of a cp.async issue: this thread copies fibres f = tid / 64 + 4 i.
+  constexpr int kFPT = kCFib / (kThreads / kCRows);  // fibres per thread per stage
+  const int r_me = tid % kCRows, f_me = tid / kCRows;
+  const int64_t* __restrict__ cols = T.cols;
+  int64_t cbase[kFPT];
+  auto fetch_bases = [&](int64_t j0) {
+#pragma unroll
+    for (int i = 0; i < kFPT; ++i) {
+      const int64_t j = j0 + f_me + (kThreads / kCRows) * i;
+      cbase[i] = j < jend ? __ldg(cols + j) * rows : -1;
+    }
+  };
+  // stage s <- fibres [j0, j0 + kCFib) (bases already in cbase)
   auto load = [&](int s, int64_t j0) {
     double* ys = Ys + s * kCFib * kCYld;
     double* os = Os + s * kCFib * CP;
-    const int r = tid % kCRows;
-    const int64_t row = row0 + r;
-    for (int f = tid / kCRows; f < kCFib; f += kThreads / kCRows) {
-      const int64_t j = j0 + f;
-      const bool ok = j < jend && row < rows;
-      const double* src = ok ? x + T.cols[j] * rows + row : x;
-      cp_async8z(ys + f * kCYld + r, src, ok);
+    const int64_t row = row0 + r_me;
+#pragma unroll
+    for (int i = 0; i < kFPT; ++i) {
+      const int f = f_me + (kThreads / kCRows) * i;
+      const bool ok = cbase[i] >= 0 && row < rows;
+      cp_async8z(ys + f * kCYld + r_me, ok ? x + cbase[i] + row : x, ok);
     }
     for (int e = tid; e < kCFib * CP; e += kThreads) {
       const int f = e / CP, cc = e % CP;
@@ -258,16 +271,21 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
   const int64_t nst = (jend - jbeg + kCFib - 1) / kCFib;
 #pragma unroll
   for (int s = 0; s < kCStages - 1; ++s) {
-    if (s < nst) load(s, jbeg + (int64_t)s * kCFib);
+    if (s < nst) {
+      fetch_bases(jbeg + (int64_t)s * kCFib);
+      load(s, jbeg + (int64_t)s * kCFib);
+    }
     cp_async_commit();
   }
+  fetch_bases(jbeg + (int64_t)(kCStages - 1) * kCFib);
   for (int64_t st = 0; st < nst; ++st) {
     cp_async_wait<kCStages - 2>();
     __syncthreads();
-    {  // refill the stage freed by the previous iteration
+    {  // refill the stage freed by the previous iteration; bases one stage ahead
       const int64_t nx = st + kCStages - 1;
       if (nx < nst) load((int)(nx % kCStages), jbeg + nx * kCFib);
       cp_async_commit();
+      fetch_bases(jbeg + (nx + 1) * kCFib);
     }
     const int s = (int)(st % kCStages);
     const double* ys = Ys + s * kCFib * kCYld + 8 * warp + g;
