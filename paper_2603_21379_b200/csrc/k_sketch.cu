@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
 // ---------------------------------------------------------------------------
 constexpr int kCRows = 64, kCFib = 32, kCStages = 4;
 constexpr int kCYld = kCRows + 4;  // = 4 (mod 16): conflict-free A fragment reads
+constexpr int kCOld = kCFib + 4;   // Omega stored transposed (column cc, fibre f), pitch = 4 (mod 16)
 
 __device__ __forceinline__ void cp_async8z(void* smem, const double* g, bool ok) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(srtt_dev::smem_u32(smem)), "l"(g),
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SketchTarget T;
   __shared__ int tsel;
-  constexpr int CP = 8 * CT + ((4 - (8 * CT) % 16) + 16) % 16;  // Omega row pitch = 4 (mod 16)
+  constexpr int CP = 8 * CT;  // Omega columns (c padded to the 8-wide tiles)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;
   if (tid == 0) {
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
   const int64_t jend = srtt_dev::min64(T.w, jbeg + flen);
   const int64_t row0 = rt * kCRows;
   double* Ys = reinterpret_cast<double*>(smem_raw);     // kCStages x kCFib x kCYld
-  double* Os = Ys + kCStages * kCFib * kCYld;           // kCStages x kCFib x CP
+  double* Os = Ys + kCStages * kCFib * kCYld;           // kCStages x CP x kCOld (transposed)
   const double* __restrict__ x = T.x;
   const double* __restrict__ om = T.omega;
 
@@ -243,25 +244,27 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
 #pragma unroll
     for (int i = 0; i < kFPT; ++i) {
       const int64_t j = j0 + f_me + (kThreads / kCRows) * i;
-      cbase[i] = j < jend ? __ldg(cols + j) * rows : -1;
+      cbase[i] = j < jend ? __ldg(cols + j) : -1;  // scaled by rows at use (latency off the issue path)
     }
   };
   // stage s <- fibres [j0, j0 + kCFib) (bases already in cbase)
   auto load = [&](int s, int64_t j0) {
     double* ys = Ys + s * kCFib * kCYld;
-    double* os = Os + s * kCFib * CP;
+    double* os = Os + s * CP * kCOld;
     const int64_t row = row0 + r_me;
 #pragma unroll
     for (int i = 0; i < kFPT; ++i) {
       const int f = f_me + (kThreads / kCRows) * i;
       const bool ok = cbase[i] >= 0 && row < rows;
-      cp_async8z(ys + f * kCYld + r_me, ok ? x + cbase[i] + row : x, ok);
+      cp_async8z(ys + f * kCYld + r_me, ok ? x + cbase[i] * rows + row : x, ok);
     }
+    // Omega(j, cc) column-major (ld w): a warp copies 32 consecutive fibres
+    // of one column (coalesced), stored transposed
     for (int e = tid; e < kCFib * CP; e += kThreads) {
-      const int f = e / CP, cc = e % CP;
+      const int cc = e / kCFib, f = e % kCFib;
       const int64_t j = j0 + f;
       const bool ok = j < jend && cc < c;
-      cp_async8z(os + e, ok ? om + j + (int64_t)cc * T.w : om, ok);
+      cp_async8z(os + cc * kCOld + f, ok ? om + j + (int64_t)cc * T.w : om, ok);
     }
   };
 
@@ -289,13 +292,13 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
     }
     const int s = (int)(st % kCStages);
     const double* ys = Ys + s * kCFib * kCYld + 8 * warp + g;
-    const double* os = Os + s * kCFib * CP + g;
+    const double* os = Os + s * CP * kCOld + g * kCOld + tq;  // B(k = tq, n = g) = Omega(f, 8 ct + g)
 #pragma unroll
     for (int kk = 0; kk < kCFib / 4; ++kk) {
-      const int f = 4 * kk + tq;
-      const double a = ys[f * kCYld];
+      const double a = ys[(4 * kk + tq) * kCYld];
 #pragma unroll
-      for (int ct = 0; ct < CT; ++ct) srtt_dev::dmma_8x8x4(acc[ct][0], acc[ct][1], a, os[f * CP + 8 * ct]);
+      for (int ct = 0; ct < CT; ++ct)
+        srtt_dev::dmma_8x8x4(acc[ct][0], acc[ct][1], a, os[8 * ct * kCOld + 4 * kk]);
     }
   }
   cp_async_wait<0>();
@@ -349,8 +352,7 @@ __global__ void __launch_bounds__(256) sketch_reduce_kernel(const SketchTarget* 
 }  // namespace
 
 size_t srtt_sketch_contig_smem(int ct) {
-  const int CP = 8 * ct + ((4 - (8 * ct) % 16) + 16) % 16;
-  return sizeof(double) * (size_t)kCStages * kCFib * (kCYld + CP);
+  return sizeof(double) * (size_t)kCStages * ((size_t)kCFib * kCYld + (size_t)8 * ct * kCOld);
 }
 
 cudaError_t srtt_launch_sketch_contig(const SketchTarget* d_targets, int ntargets, int64_t total_ctas, int cmax,
