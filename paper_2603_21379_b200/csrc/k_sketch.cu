@@ -189,6 +189,11 @@ __device__ __forceinline__ void cp_async8z(void* smem, const double* g, bool ok)
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async16z(void* smem, const double* g, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(srtt_dev::smem_u32(smem)), "l"(g),
+               "r"(ok ? 16u : 0u)
+               : "memory");
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
@@ -236,15 +241,22 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
   // Fibre base offsets of the stages are read one stage ahead of their
   // copies (register-held), so the cols[] load latency never sits in front
   // of a cp.async issue: this thread copies fibres f = tid / 64 + 4 i.
-  constexpr int kFPT = kCFib / (kThreads / kCRows);  // fibres per thread per stage
-  const int r_me = tid % kCRows, f_me = tid / kCRows;
+  // even `rows` (fibre starts 16-byte aligned): each thread copies 2 rows
+  // per 16-byte cp.async, else 1 row per 8-byte cp.async
+  const bool pairs = (rows & 1) == 0;
+  const int rpt = pairs ? 2 : 1;                               // rows per copy
+  const int tpf = kCRows / rpt;                                // threads per fibre segment
+  const int fstep = kThreads / tpf;                            // fibres per pass
+  constexpr int kFPT = kCFib / (kThreads / kCRows) ;           // max passes (8-byte case)
+  const int npass = kCFib / fstep;
+  const int r_me = (tid % tpf) * rpt, f_me = tid / tpf;
   const int64_t* __restrict__ cols = T.cols;
   int64_t cbase[kFPT];
   auto fetch_bases = [&](int64_t j0) {
 #pragma unroll
     for (int i = 0; i < kFPT; ++i) {
-      const int64_t j = j0 + f_me + (kThreads / kCRows) * i;
-      cbase[i] = j < jend ? __ldg(cols + j) : -1;  // scaled by rows at use (latency off the issue path)
+      const int64_t j = j0 + f_me + fstep * i;
+      cbase[i] = (i < npass && j < jend) ? __ldg(cols + j) : -1;  // scaled by rows at use (latency off the issue path)
     }
   };
   // stage s <- fibres [j0, j0 + kCFib) (bases already in cbase)
@@ -254,9 +266,13 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
     const int64_t row = row0 + r_me;
 #pragma unroll
     for (int i = 0; i < kFPT; ++i) {
-      const int f = f_me + (kThreads / kCRows) * i;
-      const bool ok = cbase[i] >= 0 && row < rows;
-      cp_async8z(ys + f * kCYld + r_me, ok ? x + cbase[i] * rows + row : x, ok);
+      if (i >= npass) break;
+      const int f = f_me + fstep * i;
+      const bool ok = cbase[i] >= 0 && row < rows;  // rows even: row + 1 < rows too
+      if (pairs)
+        cp_async16z(ys + f * kCYld + r_me, ok ? x + cbase[i] * rows + row : x, ok);
+      else
+        cp_async8z(ys + f * kCYld + r_me, ok ? x + cbase[i] * rows + row : x, ok);
     }
     // Omega(j, cc) column-major (ld w): a warp copies 32 consecutive fibres
     // of one column (coalesced), stored transposed
