@@ -284,9 +284,14 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
     }
   };
 
-  double acc[CT][2];
+  // KS interleaved accumulator sets (k steps kk = s mod KS) keep >= 4
+  // independent DMMA chains per warp; summed in a fixed order at the end
+  constexpr int KS = CT >= 4 ? 1 : 4 / CT;
+  double acc[KS][CT][2];
 #pragma unroll
-  for (int ct = 0; ct < CT; ++ct) acc[ct][0] = acc[ct][1] = 0.0;
+  for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+    for (int ct = 0; ct < CT; ++ct) acc[ks][ct][0] = acc[ks][ct][1] = 0.0;
   const int64_t nst = (jend - jbeg + kCFib - 1) / kCFib;
 #pragma unroll
   for (int s = 0; s < kCStages - 1; ++s) {
@@ -314,10 +319,17 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
       const double a = ys[(4 * kk + tq) * kCYld];
 #pragma unroll
       for (int ct = 0; ct < CT; ++ct)
-        srtt_dev::dmma_8x8x4(acc[ct][0], acc[ct][1], a, os[8 * ct * kCOld + 4 * kk]);
+        srtt_dev::dmma_8x8x4(acc[kk % KS][ct][0], acc[kk % KS][ct][1], a, os[8 * ct * kCOld + 4 * kk]);
     }
   }
   cp_async_wait<0>();
+#pragma unroll
+  for (int ks = 1; ks < KS; ++ks)
+#pragma unroll
+    for (int ct = 0; ct < CT; ++ct) {
+      acc[0][ct][0] += acc[ks][ct][0];
+      acc[0][ct][1] += acc[ks][ct][1];
+    }
   // D fragment: row 8 warp + g, columns 8 ct + 2 tq + {0, 1}
   const int64_t row = row0 + 8 * warp + g;
   if (row < rows) {
@@ -329,9 +341,9 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
         const int cc = 8 * ct + 2 * tq + v;
         if (cc >= c) continue;
         if (T.fsplit > 1)
-          T.zpart[((int64_t)fchunk * c + cc) * rows + row] = acc[ct][v];
+          T.zpart[((int64_t)fchunk * c + cc) * rows + row] = acc[0][ct][v];
         else
-          T.z[row + (int64_t)cc * ldz] = acc[ct][v];
+          T.z[row + (int64_t)cc * ldz] = acc[0][ct][v];
       }
   }
 }
