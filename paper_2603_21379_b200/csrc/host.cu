@@ -1013,6 +1013,13 @@ int sketch_fsplit(int64_t rows, int64_t w) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(w / 512, want));
 }
 
+// Fibre chunks of a K1c target (128-row CTAs): about 4 CTAs per SM overall.
+int sketch_fsplit_contig(int64_t rows, int64_t w) {
+  const int64_t row_ctas = (rows + 127) / 128;
+  const int64_t want = (4 * 148 + row_ctas / 2) / row_ctas;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(w / 256, want));
+}
+
 // Workspace for a target's fibre-chunk partials (when split) and its
 // once-generated Omega (when more than one CTA would generate it), appended.
 bool sketch_omega_once(int64_t rows, int64_t w) {
@@ -1022,7 +1029,8 @@ bool sketch_omega_once(int64_t rows, int64_t w) {
   return (rows + rt - 1) / rt * sketch_fsplit(rows, w) >= 8 && w >= 512;
 }
 size_t sketch_part_bytes(int64_t rows, int64_t w, int c) {
-  const int f = sketch_fsplit(rows, w);
+  // upper bound over the scalar and the K1c split (the kernel is chosen later)
+  const int f = std::max(sketch_fsplit(rows, w), sketch_fsplit_contig(rows, w));
   const size_t part = f > 1 ? sizeof(double) * (size_t)f * rows * c : 0;
   const size_t om = sketch_omega_once(rows, w) ? sizeof(double) * (size_t)w * c : 0;
   return (part + 255) / 256 * 256 + om;
@@ -1066,6 +1074,7 @@ SketchTarget make_sketch_target(const double* x, const std::vector<int64_t>& dim
   std::sort(ms.begin(), ms.end());
   for (size_t i = 0; i < ms.size(); ++i) leading = leading && ms[i] == (int)i;
   T.contig = (leading && w >= 512 && c <= 64 && !std::getenv("SRTT_NO_K1C")) ? 1 : 0;
+  if (T.contig) T.fsplit = sketch_fsplit_contig(T.rows, w);
   return T;
 }
 
@@ -1082,7 +1091,7 @@ int64_t assign_contig_ctas(std::vector<SketchTarget>& sk) {
   for (auto& t : sk) {
     if (t.contig && (!t.omega || t.slab_digit >= 0 || t.flat_hi > 0)) t.contig = 0;
     t.cta_begin_c = n;
-    if (t.contig) n += (t.rows + 63) / 64 * t.fsplit;
+    if (t.contig) n += (t.rows + 127) / 128 * t.fsplit;
   }
   return n;
 }
@@ -1107,7 +1116,7 @@ int launch_sketch_group(const SketchTarget* dT, const std::vector<SketchTarget>&
   int cmax_c = 0;
   for (auto& t : sk)
     if (t.contig) {
-      ctas_c += (t.rows + 63) / 64 * t.fsplit;
+      ctas_c += (t.rows + 127) / 128 * t.fsplit;
       cmax_c = std::max(cmax_c, t.c);
     }
   if (ctas_c > 0) {

@@ -179,9 +179,11 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
 // fibre values, B = Omega, c padded to multiples of 8). Fixed k order:
 // deterministic. Partials per fibre chunk as in sketch_kernel.
 // ---------------------------------------------------------------------------
-constexpr int kCRows = 64, kCFib = 32, kCStages = 4;
+constexpr int kCRows = 128, kCFib = 28, kCStages = 3;  // ~101 KB: two CTAs per SM
+constexpr int kCMW = kCRows / (8 * (kThreads / 32));  // 8-row tiles per warp (2: 16 rows)
 constexpr int kCYld = kCRows + 4;  // = 4 (mod 16): conflict-free A fragment reads
-constexpr int kCOld = kCFib + 4;   // Omega stored transposed (column cc, fibre f), pitch = 4 (mod 16)
+constexpr int kCOld = 36;          // Omega stored transposed (column cc, fibre f), pitch = 4 (mod 16)
+static_assert(kCFib % 4 == 0 && kCOld >= kCFib && kCOld % 16 == 4, "K1c stage geometry");
 
 __device__ __forceinline__ void cp_async8z(void* smem, const double* g, bool ok) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(srtt_dev::smem_u32(smem)), "l"(g),
@@ -286,12 +288,14 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
 
   // KS interleaved accumulator sets (k steps kk = s mod KS) keep >= 4
   // independent DMMA chains per warp; summed in a fixed order at the end
-  constexpr int KS = CT >= 4 ? 1 : 4 / CT;
-  double acc[KS][CT][2];
+  constexpr int KS = kCMW * CT >= 4 ? 1 : 4 / (kCMW * CT);
+  double acc[KS][kCMW][CT][2];
 #pragma unroll
   for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-    for (int ct = 0; ct < CT; ++ct) acc[ks][ct][0] = acc[ks][ct][1] = 0.0;
+    for (int m = 0; m < kCMW; ++m)
+#pragma unroll
+      for (int ct = 0; ct < CT; ++ct) acc[ks][m][ct][0] = acc[ks][m][ct][1] = 0.0;
   const int64_t nst = (jend - jbeg + kCFib - 1) / kCFib;
 #pragma unroll
   for (int s = 0; s < kCStages - 1; ++s) {
@@ -312,28 +316,38 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
       fetch_bases(jbeg + (nx + 1) * kCFib);
     }
     const int s = (int)(st % kCStages);
-    const double* ys = Ys + s * kCFib * kCYld + 8 * warp + g;
+    const double* ys = Ys + s * kCFib * kCYld + 8 * kCMW * warp + g;
     const double* os = Os + s * CP * kCOld + g * kCOld + tq;  // B(k = tq, n = g) = Omega(f, 8 ct + g)
 #pragma unroll
     for (int kk = 0; kk < kCFib / 4; ++kk) {
-      const double a = ys[(4 * kk + tq) * kCYld];
+      double a[kCMW];
 #pragma unroll
-      for (int ct = 0; ct < CT; ++ct)
-        srtt_dev::dmma_8x8x4(acc[kk % KS][ct][0], acc[kk % KS][ct][1], a, os[8 * ct * kCOld + 4 * kk]);
+      for (int m = 0; m < kCMW; ++m) a[m] = ys[(4 * kk + tq) * kCYld + 8 * m];
+#pragma unroll
+      for (int ct = 0; ct < CT; ++ct) {
+        const double b = os[8 * ct * kCOld + 4 * kk];
+#pragma unroll
+        for (int m = 0; m < kCMW; ++m)
+          srtt_dev::dmma_8x8x4(acc[kk % KS][m][ct][0], acc[kk % KS][m][ct][1], a[m], b);
+      }
     }
   }
   cp_async_wait<0>();
 #pragma unroll
   for (int ks = 1; ks < KS; ++ks)
 #pragma unroll
-    for (int ct = 0; ct < CT; ++ct) {
-      acc[0][ct][0] += acc[ks][ct][0];
-      acc[0][ct][1] += acc[ks][ct][1];
-    }
-  // D fragment: row 8 warp + g, columns 8 ct + 2 tq + {0, 1}
-  const int64_t row = row0 + 8 * warp + g;
-  if (row < rows) {
-    const int64_t ldz = T.ldz > 0 ? T.ldz : rows;
+    for (int m = 0; m < kCMW; ++m)
+#pragma unroll
+      for (int ct = 0; ct < CT; ++ct) {
+        acc[0][m][ct][0] += acc[ks][m][ct][0];
+        acc[0][m][ct][1] += acc[ks][m][ct][1];
+      }
+  // D fragment: row 16 warp + 8 m + g, columns 8 ct + 2 tq + {0, 1}
+  const int64_t ldz = T.ldz > 0 ? T.ldz : rows;
+#pragma unroll
+  for (int m = 0; m < kCMW; ++m) {
+    const int64_t row = row0 + 8 * kCMW * warp + 8 * m + g;
+    if (row >= rows) continue;
 #pragma unroll
     for (int ct = 0; ct < CT; ++ct)
 #pragma unroll
@@ -341,9 +355,9 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
         const int cc = 8 * ct + 2 * tq + v;
         if (cc >= c) continue;
         if (T.fsplit > 1)
-          T.zpart[((int64_t)fchunk * c + cc) * rows + row] = acc[0][ct][v];
+          T.zpart[((int64_t)fchunk * c + cc) * rows + row] = acc[0][m][ct][v];
         else
-          T.z[row + (int64_t)cc * ldz] = acc[0][ct][v];
+          T.z[row + (int64_t)cc * ldz] = acc[0][m][ct][v];
       }
   }
 }
