@@ -240,49 +240,52 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
   const double* __restrict__ x = T.x;
   const double* __restrict__ om = T.omega;
 
-  // Fibre base offsets of the stages are read one stage ahead of their
-  // copies (register-held), so the cols[] load latency never sits in front
-  // of a cp.async issue: this thread copies fibres f = tid / 64 + 4 i.
-  // even `rows` (fibre starts 16-byte aligned): each thread copies 2 rows
-  // per 16-byte cp.async, else 1 row per 8-byte cp.async
+  // Fibre start offsets (cols[j] * rows) live in a small per-stage table in
+  // shared memory, written by warp 0 one iteration ahead of the copies that
+  // use them (its cols[] loads are issued another iteration earlier), so no
+  // copy waits on a cols[] load and the 64-bit products are formed once.
+  // Even `rows` (fibre starts 16-byte aligned): 2 rows per 16-byte
+  // cp.async, else 1 row per 8-byte cp.async.
+  __shared__ int64_t sbase[kCStages][kCFib];
   const bool pairs = (rows & 1) == 0;
-  const int rpt = pairs ? 2 : 1;                               // rows per copy
-  const int tpf = kCRows / rpt;                                // threads per fibre segment
-  const int fstep = kThreads / tpf;                            // fibres per pass
-  constexpr int kFPT = kCFib / (kThreads / kCRows) ;           // max passes (8-byte case)
+  const int rpt = pairs ? 2 : 1;            // rows per copy
+  const int tpf = kCRows / rpt;             // threads per fibre segment
+  const int fstep = kThreads / tpf;         // fibres per pass
   const int npass = kCFib / fstep;
   const int r_me = (tid % tpf) * rpt, f_me = tid / tpf;
   const int64_t* __restrict__ cols = T.cols;
-  int64_t cbase[kFPT];
-  auto fetch_bases = [&](int64_t j0) {
-#pragma unroll
-    for (int i = 0; i < kFPT; ++i) {
-      const int64_t j = j0 + f_me + fstep * i;
-      cbase[i] = (i < npass && j < jend) ? __ldg(cols + j) : -1;  // scaled by rows at use (latency off the issue path)
+  int64_t creg = -1;                        // warp 0, lane < kCFib: cols[] of the stage after next
+  auto fetch_cols = [&](int64_t j0) {
+    if (warp == 0 && lane < kCFib) {
+      const int64_t j = j0 + lane;
+      creg = j < jend ? __ldg(cols + j) : -1;
     }
   };
-  // stage s <- fibres [j0, j0 + kCFib) (bases already in cbase)
+  auto put_bases = [&](int s) {
+    if (warp == 0 && lane < kCFib) sbase[s][lane] = creg >= 0 ? creg * rows : -1;
+  };
+  // stage s <- fibres [j0, j0 + kCFib) (table sbase[s] already written)
   auto load = [&](int s, int64_t j0) {
     double* ys = Ys + s * kCFib * kCYld;
     double* os = Os + s * CP * kCOld;
     const int64_t row = row0 + r_me;
-#pragma unroll
-    for (int i = 0; i < kFPT; ++i) {
-      if (i >= npass) break;
+    for (int i = 0; i < npass; ++i) {
       const int f = f_me + fstep * i;
-      const bool ok = cbase[i] >= 0 && row < rows;  // rows even: row + 1 < rows too
+      const int64_t b = sbase[s][f];
+      const bool ok = b >= 0 && row < rows;  // rows even: row + 1 < rows too
       if (pairs)
-        cp_async16z(ys + f * kCYld + r_me, ok ? x + cbase[i] * rows + row : x, ok);
+        cp_async16z(ys + f * kCYld + r_me, ok ? x + b + row : x, ok);
       else
-        cp_async8z(ys + f * kCYld + r_me, ok ? x + cbase[i] * rows + row : x, ok);
+        cp_async8z(ys + f * kCYld + r_me, ok ? x + b + row : x, ok);
     }
-    // Omega(j, cc) column-major (ld w): a warp copies 32 consecutive fibres
-    // of one column (coalesced), stored transposed
-    for (int e = tid; e < kCFib * CP; e += kThreads) {
-      const int cc = e / kCFib, f = e % kCFib;
-      const int64_t j = j0 + f;
-      const bool ok = j < jend && cc < c;
-      cp_async8z(os + cc * kCOld + f, ok ? om + j + (int64_t)cc * T.w : om, ok);
+    // Omega(j, cc) column-major (ld w): warp w copies columns w, w + 8, ...
+    // with one fibre per lane (coalesced), stored transposed
+    if (lane < kCFib) {
+      const int64_t j = j0 + lane;
+      for (int cc = warp; cc < CP; cc += kThreads / 32) {
+        const bool ok = j < jend && cc < c;
+        cp_async8z(os + cc * kCOld + lane, ok ? om + j + (int64_t)cc * T.w : om, ok);
+      }
     }
   };
 
@@ -297,23 +300,28 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
 #pragma unroll
       for (int ct = 0; ct < CT; ++ct) acc[ks][m][ct][0] = acc[ks][m][ct][1] = 0.0;
   const int64_t nst = (jend - jbeg + kCFib - 1) / kCFib;
+  // prologue: tables of stages 0 .. NST-1, copies of stages 0 .. NST-2
+  for (int s = 0; s < kCStages; ++s) {
+    fetch_cols(jbeg + (int64_t)s * kCFib);
+    put_bases(s);
+  }
+  __syncthreads();
 #pragma unroll
   for (int s = 0; s < kCStages - 1; ++s) {
-    if (s < nst) {
-      fetch_bases(jbeg + (int64_t)s * kCFib);
-      load(s, jbeg + (int64_t)s * kCFib);
-    }
+    if (s < nst) load(s, jbeg + (int64_t)s * kCFib);
     cp_async_commit();
   }
-  fetch_bases(jbeg + (int64_t)(kCStages - 1) * kCFib);
+  fetch_cols(jbeg + (int64_t)kCStages * kCFib);  // table of stage NST, written at iteration 0
   for (int64_t st = 0; st < nst; ++st) {
     cp_async_wait<kCStages - 2>();
     __syncthreads();
-    {  // refill the stage freed by the previous iteration; bases one stage ahead
+    {  // refill the stage freed by the previous iteration (its table was
+       // written before the barrier); then the table of the stage after it
       const int64_t nx = st + kCStages - 1;
       if (nx < nst) load((int)(nx % kCStages), jbeg + nx * kCFib);
       cp_async_commit();
-      fetch_bases(jbeg + (nx + 1) * kCFib);
+      put_bases((int)((nx + 1) % kCStages));
+      fetch_cols(jbeg + (nx + 2) * kCFib);
     }
     const int s = (int)(st % kCStages);
     const double* ys = Ys + s * kCFib * kCYld + 8 * kCMW * warp + g;
