@@ -29,7 +29,7 @@ size_t srtt_sketch_smem_bytes(int cmax);
 cudaError_t srtt_launch_sketch(const SketchTarget*, int, int64_t, int, cudaStream_t);
 cudaError_t srtt_launch_sketch_reduce(const SketchTarget*, int, int64_t, cudaStream_t);
 cudaError_t srtt_launch_omega(const SketchTarget*, int, int64_t, cudaStream_t);
-cudaError_t srtt_launch_sketch_contig(const SketchTarget*, int, int64_t, int, cudaStream_t);
+cudaError_t srtt_launch_sketch_contig(const SketchTarget*, int, int64_t, int, int, cudaStream_t);
 cudaError_t srtt_launch_scatter_block(const double*, double*, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
                                       int64_t, cudaStream_t);
 size_t srtt_basis_top_smem(int m, int c, int r);
@@ -1084,16 +1084,53 @@ int64_t sketch_target_ctas(const SketchTarget& T) {
   return (T.rows + T.row_tile - 1) / T.row_tile * T.fsplit;
 }
 
-// K1c index space (contig targets need Omega in memory and no sharding
-// masks; others fall back to the scalar kernel); returns its CTA count.
+// K1c / K1t index spaces (contig targets need Omega in memory and no
+// sharding masks; K1c ones fall back to the scalar kernel otherwise).
 int64_t assign_contig_ctas(std::vector<SketchTarget>& sk) {
-  int64_t n = 0;
+  int64_t n = 0, nt = 0;
   for (auto& t : sk) {
-    if (t.contig && (!t.omega || t.slab_digit >= 0 || t.flat_hi > 0)) t.contig = 0;
+    if (t.contig == 1 && (!t.omega || t.slab_digit >= 0 || t.flat_hi > 0)) t.contig = 0;
     t.cta_begin_c = n;
-    if (t.contig) n += (t.rows + 127) / 128 * t.fsplit;
+    t.cta_begin_t = nt;
+    if (t.contig == 1) n += (t.rows + 127) / 128 * t.fsplit;
+    if (t.contig == 2) nt += (t.rows + 127) / 128 * t.fsplit;
   }
   return n;
+}
+
+// K1t opt-in (single-GPU paths): a target whose row modes are the TRAILING
+// modes and whose columns are densely sampled (>= 1/4 of them, >= 512) has
+// its sampled columns sorted ascending here -- cols is reordered in place and
+// perm[k] = the sampled position of sorted column k -- so neighbouring fibres
+// of a K1t stage are neighbouring addresses. Z is a sum over the fibres, so
+// the order only changes rounding. Returns whether it did.
+bool sketch_trans_prepare(const std::vector<int64_t>& dims, std::vector<int> modes, int64_t w, int c,
+                          std::vector<int64_t>& cols, std::vector<int64_t>& perm) {
+  if (std::getenv("SRTT_NO_K1C") || c > 64 || w < 512 || modes.empty()) return false;
+  std::sort(modes.begin(), modes.end());
+  const int d = (int)dims.size();
+  for (size_t i = 0; i < modes.size(); ++i)
+    if (modes[i] != d - (int)modes.size() + (int)i) return false;
+  int64_t rows = 1;
+  for (int m : modes) rows *= dims[m];
+  const int64_t ncols = prod(dims) / rows;
+  if (4 * w < ncols || !sketch_omega_once(rows, w)) return false;
+  perm.resize(w);
+  for (int64_t k = 0; k < w; ++k) perm[k] = k;
+  std::sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) { return cols[a] < cols[b]; });
+  std::vector<int64_t> sorted(w);
+  for (int64_t k = 0; k < w; ++k) sorted[k] = cols[perm[k]];
+  cols.swap(sorted);
+  return true;
+}
+
+// Marks a prepared K1t target (after make_sketch_target).
+void mark_sketch_trans(SketchTarget& T, const int64_t* dperm) {
+  T.contig = 2;
+  T.perm = dperm;
+  T.ncols = 1;
+  for (int mm = 0; mm < T.ncol_modes; ++mm) T.ncols *= T.col_dim[mm];
+  T.fsplit = sketch_fsplit_contig(T.rows, T.w);
 }
 
 // K1 over a group of targets (device array dT, host copy sk), plus the
@@ -1112,16 +1149,18 @@ int launch_sketch_group(const SketchTarget* dT, const std::vector<SketchTarget>&
     CK(srtt_launch_sketch(dT, (int)sk.size(), ctas, cmax, st));
     ++n;
   }
-  int64_t ctas_c = 0;
-  int cmax_c = 0;
-  for (auto& t : sk)
-    if (t.contig) {
-      ctas_c += (t.rows + 127) / 128 * t.fsplit;
-      cmax_c = std::max(cmax_c, t.c);
+  for (int kind = 1; kind <= 2; ++kind) {  // K1c, then K1t
+    int64_t ctas_c = 0;
+    int cmax_c = 0;
+    for (auto& t : sk)
+      if (t.contig == kind) {
+        ctas_c += (t.rows + 127) / 128 * t.fsplit;
+        cmax_c = std::max(cmax_c, t.c);
+      }
+    if (ctas_c > 0) {
+      CK(srtt_launch_sketch_contig(dT, (int)sk.size(), ctas_c, cmax_c, kind == 2, st));
+      ++n;
     }
-  if (ctas_c > 0) {
-    CK(srtt_launch_sketch_contig(dT, (int)sk.size(), ctas_c, cmax_c, st));
-    ++n;
   }
   int64_t split_elems = 0;
   for (auto& t : sk)
@@ -1140,8 +1179,11 @@ void attach_sketch_scratch(SketchTarget& T, char* scratch) {
     T.omega_gen = reinterpret_cast<double*>(scratch + (part + 255) / 256 * 256);
     T.omega = T.omega_gen;
   }
-  // K1c needs Omega in memory and no sharding masks (set before this call)
-  if (T.contig && (!T.omega || T.slab_digit >= 0 || T.flat_hi > 0)) T.contig = 0;
+  // K1c needs Omega in memory and no sharding masks (set before this call);
+  // a K1t target's columns are sorted, so it can never fall back
+  if (T.contig == 1 && (!T.omega || T.slab_digit >= 0 || T.flat_hi > 0)) T.contig = 0;
+  if (T.contig == 2 && (!T.omega_gen || T.slab_digit >= 0 || T.flat_hi > 0))
+    fail(SRTT_ERR_INTERNAL, "K1t target without a generated Omega");
 }
 
 // ---- report helpers ------------------------------------------------------------
@@ -1503,7 +1545,15 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   Blob blob;
   const size_t off_info = blob.reserve(info_bytes);
   std::vector<size_t> off_cols(d);
+  // dense trailing-mode targets: sorted columns for K1t (changes cols[k])
+  std::vector<std::vector<int64_t>> perms(d);
+  std::vector<size_t> off_perm(d, 0);
+  bool any_trans = false;
+  for (int k = 0; k < d; ++k)
+    if (sketch_trans_prepare(dims, {k}, samples[k], (int)(ranks[k] + p), cols[k], perms[k])) any_trans = true;
   for (int k = 0; k < d; ++k) off_cols[k] = blob.add(cols[k].data(), sizeof(int64_t) * cols[k].size());
+  for (int k = 0; k < d; ++k)
+    if (!perms[k].empty()) off_perm[k] = blob.add(perms[k].data(), sizeof(int64_t) * perms[k].size());
   const size_t off_sk = blob.reserve(sizeof(SketchTarget) * d);
   const size_t off_bt = blob.reserve(sizeof(BasisTarget) * d);
   std::vector<SketchTarget> sk(d);
@@ -1516,6 +1566,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   for (int k = 0; k < d; ++k) {
     const int c = (int)(ranks[k] + p);
     sk[k] = make_sketch_target(x, dims, {k}, samples[k], c);
+    if (!perms[k].empty()) mark_sketch_trans(sk[k], reinterpret_cast<const int64_t*>(dp + off_perm[k]));
     sk[k].cols = reinterpret_cast<const int64_t*>(dp + off_cols[k]);
     sk[k].z = reinterpret_cast<double*>(ws + off_z[k]);
     sk[k].state0 = state0[k];
@@ -1583,7 +1634,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
     for (int k = 0; k < d; ++k) copy_out(h, factors_out[k], uptr[k], sizeof(double) * dims[k] * ranks[k], 0);
   }
   tm.mark();  // 6
-  if (h->use_graphs) {
+  if (h->use_graphs && !any_trans) {  // K1t signatures re-sort per seed: no fast path
     srtt_handle::Prepared pr;
     pr.image.assign(hp, hp + blob.lay.off);
     pr.off_cols = off_cols;
@@ -1930,7 +1981,13 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   Blob blob;
   const size_t off_info = blob.reserve(info_bytes);  // zeroed by the blob copy (see sub_r_hosvd)
   std::vector<size_t> off_cols(nt);
+  std::vector<std::vector<int64_t>> perms(nt);
+  std::vector<size_t> off_perm(nt, 0);
+  for (int t = 0; t < nt; ++t)
+    sketch_trans_prepare(dims, tr.modes[t + 1], samples[t + 1], (int)(ranks[t + 1] + p), cols[t], perms[t]);
   for (int t = 0; t < nt; ++t) off_cols[t] = blob.add(cols[t].data(), sizeof(int64_t) * cols[t].size());
+  for (int t = 0; t < nt; ++t)
+    if (!perms[t].empty()) off_perm[t] = blob.add(perms[t].data(), sizeof(int64_t) * perms[t].size());
   const size_t off_sk = blob.reserve(sizeof(SketchTarget) * nt);
   const size_t off_bt = blob.reserve(sizeof(BasisTarget) * nt);
   const size_t off_tt = blob.reserve(sizeof(TransferTarget) * std::max<size_t>(1, internal.size()));
@@ -1949,6 +2006,7 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
     const int id = t + 1;
     const int c = (int)(ranks[id] + p);
     sk[t] = make_sketch_target(x, dims, tr.modes[id], samples[id], c);
+    if (!perms[t].empty()) mark_sketch_trans(sk[t], reinterpret_cast<const int64_t*>(dp + off_perm[t]));
     sk[t].cols = reinterpret_cast<const int64_t*>(dp + off_cols[t]);
     sk[t].z = reinterpret_cast<double*>(ws + off_z[t]);
     sk[t].state0 = state0[t];
@@ -2231,9 +2289,16 @@ int srtt_sketch(srtt_handle* h, const double* x, int32_t x_on_device, int32_t d,
     SketchTarget T = make_sketch_target(dx, dv, mv, ncols, c);
     for (int64_t j = 0; j < ncols; ++j)
       if (cols[j] < 0 || cols[j] >= N / T.rows) throw std::out_of_range("extract_fibers: column index out of range");
-    B.idx.ensure(sizeof(int64_t) * std::max<int64_t>(ncols, 1));
-    CK(cudaMemcpyAsync(B.idx.p, cols, sizeof(int64_t) * ncols, cudaMemcpyHostToDevice, h->stream));
+    std::vector<int64_t> cv(cols, cols + ncols), perm;
+    const bool trans = !omega && sketch_trans_prepare(dv, mv, ncols, c, cv, perm);
+    B.idx.ensure(sizeof(int64_t) * std::max<int64_t>(2 * ncols, 1));
+    CK(cudaMemcpyAsync(B.idx.p, cv.data(), sizeof(int64_t) * ncols, cudaMemcpyHostToDevice, h->stream));
     T.cols = reinterpret_cast<const int64_t*>(B.idx.p);
+    if (trans) {
+      CK(cudaMemcpyAsync(reinterpret_cast<int64_t*>(B.idx.p) + ncols, perm.data(), sizeof(int64_t) * ncols,
+                         cudaMemcpyHostToDevice, h->stream));
+      mark_sketch_trans(T, reinterpret_cast<const int64_t*>(B.idx.p) + ncols);
+    }
     if (omega) T.omega = to_device(h, B.c, omega, ncols * c, 0);
     B.b.ensure(sizeof(double) * T.rows * c + 256 + sketch_part_bytes(T.rows, ncols, c));
     T.z = reinterpret_cast<double*>(B.b.p);

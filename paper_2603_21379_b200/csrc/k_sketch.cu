@@ -201,7 +201,13 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <int CT>  // 8-column tiles of c
+constexpr int kTYld = kCFib + 8;  // K1t: Y stored [row][fibre], pitch = 4 (mod 16)
+static_assert(kTYld % 16 == 4, "K1t stage geometry");
+
+// CT: 8-column tiles of c. TR = false: K1c (fibres contiguous, Y stored
+// [fibre][row]); TR = true: K1t (sorted columns of a trailing-mode target,
+// neighbouring fibres are neighbouring addresses; Y stored [row][fibre]).
+template <int CT, bool TR>
 __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTarget* __restrict__ targets,
                                                                  int ntargets) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -214,7 +220,8 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
     int lo = 0, hi = ntargets - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (targets[mid].cta_begin_c <= (int64_t)blockIdx.x) lo = mid; else hi = mid - 1;
+      if ((TR ? targets[mid].cta_begin_t : targets[mid].cta_begin_c) <= (int64_t)blockIdx.x) lo = mid;
+      else hi = mid - 1;
     }
     tsel = lo;
   }
@@ -227,7 +234,7 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
   __syncthreads();
   const int c = T.c;
   const int64_t rows = T.rows;
-  const int64_t local = (int64_t)blockIdx.x - T.cta_begin_c;
+  const int64_t local = (int64_t)blockIdx.x - (TR ? T.cta_begin_t : T.cta_begin_c);
   const int64_t row_ctas = (rows + kCRows - 1) / kCRows;
   const int64_t rt = local % row_ctas;
   const int fchunk = (int)(local / row_ctas);
@@ -235,8 +242,9 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
   const int64_t jbeg = (int64_t)fchunk * flen;
   const int64_t jend = srtt_dev::min64(T.w, jbeg + flen);
   const int64_t row0 = rt * kCRows;
-  double* Ys = reinterpret_cast<double*>(smem_raw);     // kCStages x kCFib x kCYld
-  double* Os = Ys + kCStages * kCFib * kCYld;           // kCStages x CP x kCOld (transposed)
+  constexpr int kYst = TR ? kCRows * kTYld : kCFib * kCYld;  // Y doubles per stage
+  double* Ys = reinterpret_cast<double*>(smem_raw);     // kCStages x (K1c: kCFib x kCYld, K1t: kCRows x kTYld)
+  double* Os = Ys + kCStages * kYst;                    // kCStages x CP x kCOld (transposed)
   const double* __restrict__ x = T.x;
   const double* __restrict__ om = T.omega;
 
@@ -262,12 +270,22 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
     }
   };
   auto put_bases = [&](int s) {
-    if (warp == 0 && lane < kCFib) sbase[s][lane] = creg >= 0 ? creg * rows : -1;
+    if (warp == 0 && lane < kCFib) sbase[s][lane] = creg >= 0 ? (TR ? creg : creg * rows) : -1;
   };
   // stage s <- fibres [j0, j0 + kCFib) (table sbase[s] already written)
   auto load = [&](int s, int64_t j0) {
-    double* ys = Ys + s * kCFib * kCYld;
+    double* ys = Ys + s * kYst;
     double* os = Os + s * CP * kCOld;
+    if constexpr (TR) {  // element (row i, fibre f) = X[cols_sorted[f] + ncols * i]: lanes = fibres
+      if (lane < kCFib) {
+        const int64_t b = sbase[s][lane];
+        for (int i = warp; i < kCRows; i += kThreads / 32) {
+          const int64_t row = row0 + i;
+          const bool ok = b >= 0 && row < rows;
+          cp_async8z(ys + i * kTYld + lane, ok ? x + b + T.ncols * row : x, ok);
+        }
+      }
+    } else {
     const int64_t row = row0 + r_me;
     for (int i = 0; i < npass; ++i) {
       const int f = f_me + fstep * i;
@@ -277,6 +295,7 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
         cp_async16z(ys + f * kCYld + r_me, ok ? x + b + row : x, ok);
       else
         cp_async8z(ys + f * kCYld + r_me, ok ? x + b + row : x, ok);
+    }
     }
     // Omega(j, cc) column-major (ld w): warp w copies columns w, w + 8, ...
     // with one fibre per lane (coalesced), stored transposed
@@ -324,13 +343,14 @@ __global__ void __launch_bounds__(kThreads) sketch_contig_kernel(const SketchTar
       fetch_cols(jbeg + (nx + 2) * kCFib);
     }
     const int s = (int)(st % kCStages);
-    const double* ys = Ys + s * kCFib * kCYld + 8 * kCMW * warp + g;
+    const double* ys = TR ? Ys + s * kYst + (8 * kCMW * warp + g) * kTYld + tq
+                          : Ys + s * kYst + 8 * kCMW * warp + g;
     const double* os = Os + s * CP * kCOld + g * kCOld + tq;  // B(k = tq, n = g) = Omega(f, 8 ct + g)
 #pragma unroll
     for (int kk = 0; kk < kCFib / 4; ++kk) {
       double a[kCMW];
 #pragma unroll
-      for (int m = 0; m < kCMW; ++m) a[m] = ys[(4 * kk + tq) * kCYld + 8 * m];
+      for (int m = 0; m < kCMW; ++m) a[m] = TR ? ys[8 * m * kTYld + 4 * kk] : ys[(4 * kk + tq) * kCYld + 8 * m];
 #pragma unroll
       for (int ct = 0; ct < CT; ++ct) {
         const double b = os[8 * ct * kCOld + 4 * kk];
@@ -377,8 +397,12 @@ __global__ void __launch_bounds__(256) omega_kernel(const SketchTarget* __restri
     const SketchTarget& T = targets[t];
     if (!T.omega_gen) continue;
     const int64_t n = T.w * T.c;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
-      T.omega_gen[e] = srtt_dev::normal_at(T.state0, T.draw_offset, (uint64_t)e, T.flags);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+      // K1t targets: row k of Omega is the sorted column's sampled position
+      const int64_t k = e % T.w, cc = e / T.w;
+      const int64_t t = T.perm ? T.perm[k] + cc * T.w : e;
+      T.omega_gen[e] = srtt_dev::normal_at(T.state0, T.draw_offset, (uint64_t)t, T.flags);
+    }
   }
 }
 
@@ -401,19 +425,25 @@ __global__ void __launch_bounds__(256) sketch_reduce_kernel(const SketchTarget* 
 
 }  // namespace
 
-size_t srtt_sketch_contig_smem(int ct) {
-  return sizeof(double) * (size_t)kCStages * ((size_t)kCFib * kCYld + (size_t)8 * ct * kCOld);
+size_t srtt_sketch_contig_smem(int ct, bool tr) {
+  const size_t y = tr ? (size_t)kCRows * kTYld : (size_t)kCFib * kCYld;
+  return sizeof(double) * (size_t)kCStages * (y + (size_t)8 * ct * kCOld);
 }
 
 cudaError_t srtt_launch_sketch_contig(const SketchTarget* d_targets, int ntargets, int64_t total_ctas, int cmax,
-                                      cudaStream_t stream) {
+                                      int trans, cudaStream_t stream) {
   if (total_ctas <= 0) return cudaSuccess;
   const int ct = (cmax + 7) / 8;
-  const size_t smem = srtt_sketch_contig_smem(ct);
-#define SRTT_CONTIG_CASE(N)                                                                         \
-  case N:                                                                                           \
-    SRTT_ENSURE_SMEM((sketch_contig_kernel<N>), smem);                                              \
-    sketch_contig_kernel<N><<<(unsigned)total_ctas, kThreads, smem, stream>>>(d_targets, ntargets); \
+  const size_t smem = srtt_sketch_contig_smem(ct, trans != 0);
+#define SRTT_CONTIG_CASE(N)                                                                                   \
+  case N:                                                                                                     \
+    if (trans) {                                                                                              \
+      SRTT_ENSURE_SMEM((sketch_contig_kernel<N, true>), smem);                                                \
+      sketch_contig_kernel<N, true><<<(unsigned)total_ctas, kThreads, smem, stream>>>(d_targets, ntargets);  \
+    } else {                                                                                                  \
+      SRTT_ENSURE_SMEM((sketch_contig_kernel<N, false>), smem);                                               \
+      sketch_contig_kernel<N, false><<<(unsigned)total_ctas, kThreads, smem, stream>>>(d_targets, ntargets); \
+    }                                                                                                         \
     break;
   switch (ct) {
     SRTT_CONTIG_CASE(1)

@@ -166,3 +166,28 @@ def test_c5_matches_oracle():
     ec = O.rel_error_streamed(read, dims, core_c, factors_c)
     assert abs(eg - ec) <= 1e-10 * max(ec, 1.0), (eg, ec)
     assert ec <= 1e-5  # rank-32 signal + 1e-6 relative noise
+
+
+def test_c4a20_sketch_heavy_variant_matches_oracle():
+    """The ADDED sketch-heavy variant c4a20 (alpha = 20: both level-1 nodes
+    sample all 20736 columns): node 1 runs the staged K1c kernel, node 2 the
+    sorted-column K1t kernel; every node basis and the error against the
+    oracle on the same bits."""
+    cfg, xd = gen("c4a20")
+    dims = list(cfg.dims)
+    tree, otree = P.DimensionTree.balanced(8), O.DimensionTree.balanced(8)
+    ranks = P.uniform_node_ranks(tree, cfg.rank)
+    samples = cfg.node_samples(tree, dims)
+    assert samples[1] == samples[2] == 20736
+    rep = P.HtSubsampleReport(want_node_bases=True)
+    h = P.sub_r_rtl_ht(xd, tree, ranks, samples, cfg.p, 0, report=rep, dims=dims)
+    eg = P.ht_rel_error(xd, h, dims=dims)
+    X = O.as_tensor(xd.cpu().numpy(), dims)
+    del xd
+    orep = O.HtSubsampleReport()
+    ho = O.sub_r_rtl_ht(X, otree, ranks, samples, cfg.p, 0, report=orep)
+    assert rep.achieved_ranks == orep.achieved_ranks
+    for i in range(1, 15):
+        assert projector_gap(rep.node_bases[i], orep.bases[i]) <= 1e-10, i
+    ec = O.rel_error(X, O.ht_reconstruct(ho))
+    assert abs(eg - ec) <= 1e-10 * max(ec, 1.0), (eg, ec)
