@@ -49,7 +49,7 @@ def test_fiber_gathers_bitwise(handle, dims):
                                             ((30, 20, 10), [1], 200, 42),
                                             # many fibres: split over CTAs (fixed-order partial sums)
                                             ((64, 80, 90), [0], 6000, 42), ((64, 80, 90), [1], 5000, 13),
-                                            ((63, 81, 90), [0], 6000, 21), ((7, 9, 5, 300), [0, 1, 2], 1500, 15),
+                                            ((63, 81, 90), [0], 6000, 21), ((7, 9, 5, 2000), [0, 1, 2], 1500, 15),
                                             ((12,) * 6, [0, 1, 2], 1728, 15), ((12,) * 6, [3, 4, 5], 1728, 15)])
 def test_fused_sketch_matches_oracle(handle, dims, modes, w, c):
     """K1: Z = Y(cols) Omega with Omega from the reference stream; Z within 1e-13."""
