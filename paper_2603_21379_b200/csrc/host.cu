@@ -40,6 +40,16 @@ size_t srtt_basis_small_smem(int m, int c, int r);
 cudaError_t srtt_launch_basis_small(int, const BasisTarget*, const int*, int, size_t, cudaStream_t);
 int srtt_basis_small_variant(int m, int c);
 constexpr int kSmallVariants = 5;
+int srtt_wtree_cp(int c);
+int srtt_wtree_chunk(int cp);
+int srtt_wtree_factor_threads();
+size_t srtt_wtree_top_smem(int n0, int c, bool pad);
+int64_t srtt_wtree_persist_doubles(int rows, int c);
+size_t srtt_wtree_factor_smem(int rows, int c);
+size_t srtt_wtree_apply_smem(int rows, int c);
+cudaError_t srtt_launch_wtree_top(int, const BasisTarget*, const int*, int, size_t, cudaStream_t);
+cudaError_t srtt_launch_wtree_factor(int, const BasisTarget*, const int2*, int, size_t, cudaStream_t);
+cudaError_t srtt_launch_wtree_apply(int, const BasisTarget*, const int2*, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_tsqr_factor(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_tsqr_apply(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_pad(const BasisTarget*, int, double*, int64_t, cudaStream_t);
@@ -365,17 +375,63 @@ int level_block_rows(int c) {
 struct BasisPlan {
   int64_t n;
   int c, r;
+  int kind;  // 0: shared-memory QR kernels; 1: register-tree path (c <= 32)
   int nlevels;
   int64_t lv_n[SRTT_MAX_QR_LEVELS + 1];
   int lv_nblk[SRTT_MAX_QR_LEVELS + 1];
   int lv_blk[SRTT_MAX_QR_LEVELS + 1];
 };
 
+// Register-tree path (k_basis.cu): sketches with c <= 32 columns whose top
+// fits one CTA. Single-CTA targets keep their level-0 reflectors in shared
+// memory; taller ones are cut into CTAs of rpc rows (a multiple of the warp
+// block, 4 warps per CTA) whose R factors one top CTA combines.
+// SRTT_BASIS_SMEMQR=1 (development) forces the shared-memory kernels.
+constexpr size_t kWtreeSmemBudget = 220 * 1024;
+
+bool plan_basis_wtree(BasisPlan& b) {
+  static const bool off = [] {
+    const char* e = std::getenv("SRTT_BASIS_SMEMQR");
+    return e && *e == '1';
+  }();
+  const int cp = srtt_wtree_cp(b.c);
+  if (off || cp == 0 || b.n < 1) return false;
+  b.kind = 1;
+  if (b.n <= 4096 && srtt_wtree_top_smem((int)b.n, b.c, true) <= kWtreeSmemBudget) {
+    b.nlevels = 0;
+    b.lv_n[0] = b.n;
+    b.lv_nblk[0] = 1;
+    b.lv_blk[0] = (int)b.n;
+    return true;
+  }
+  const int chunk = srtt_wtree_chunk(cp);
+  const int warps = srtt_wtree_factor_threads() / 32;
+  for (int bpw = 1; bpw <= 16; ++bpw) {
+    const int64_t rpc = (int64_t)warps * chunk * bpw;
+    const int64_t ncta = (b.n + rpc - 1) / rpc;
+    const int64_t rem = b.n - (ncta - 1) * rpc;
+    const int64_t top = (ncta - 1) * b.c + std::min<int64_t>(rem, b.c);
+    if (top > 4096 || srtt_wtree_top_smem((int)top, b.c, false) > kWtreeSmemBudget) continue;
+    if (srtt_wtree_apply_smem((int)rpc, b.c) > kWtreeSmemBudget) break;
+    b.nlevels = 1;
+    b.lv_n[0] = b.n;
+    b.lv_nblk[0] = (int)ncta;
+    b.lv_blk[0] = (int)rpc;
+    b.lv_n[1] = top;
+    b.lv_nblk[1] = 1;
+    b.lv_blk[1] = (int)top;
+    return true;
+  }
+  b.kind = 0;
+  return false;
+}
+
 BasisPlan plan_basis(int64_t n, int c, int r) {
   BasisPlan b{};
   b.n = n;
   b.c = c;
   b.r = r;
+  if (plan_basis_wtree(b)) return b;
   int tmax = top_max_rows(c, r);
   int blk = level_block_rows(c);
   if (tmax < c) invalid("range_basis_of_sketch: sketch too wide for the B200 basis kernel");
@@ -415,6 +471,8 @@ BasisPlan plan_basis(int64_t n, int c, int r) {
 struct BasisBuffers {  // offsets into the workspace
   size_t a[SRTT_MAX_QR_LEVELS + 1], tau[SRTT_MAX_QR_LEVELS + 1], y[SRTT_MAX_QR_LEVELS + 1];
   size_t info, sv, pad;
+  size_t vup;
+  int64_t vup_stride;
 };
 
 // z (level-0 matrix) and u (final basis) are supplied by the caller.
@@ -428,6 +486,10 @@ BasisBuffers layout_basis(Layout& L, const BasisPlan& p) {
   B.info = L.take(4 * sizeof(int32_t));
   B.sv = L.take(sizeof(double) * p.c);
   B.pad = 0;
+  if (p.kind == 1 && p.nlevels == 1) {
+    B.vup_stride = srtt_wtree_persist_doubles(p.lv_blk[0], p.c);
+    B.vup = L.take(sizeof(double) * (size_t)B.vup_stride * p.lv_nblk[0]);
+  }
   return B;
 }
 
@@ -454,11 +516,17 @@ BasisTarget fill_basis(const BasisPlan& p, const BasisBuffers& B, char* ws, doub
   T.state0 = state0;
   T.draw_offset = draw_offset;
   T.normal_base = normal_base;
+  T.kind = p.kind;
+  if (p.kind == 1 && p.nlevels == 1) {
+    T.vup = reinterpret_cast<double*>(ws + B.vup);
+    T.vup_stride = B.vup_stride;
+  }
   return T;
 }
 
 // Which targets take the one-warp small path (single block, fits 96 KB).
 bool basis_is_small(const BasisTarget& t) {
+  if (t.kind == 1) return t.nlevels == 0;
   return t.nlevels == 0 && t.n <= 1024 && srtt_basis_small_smem((int)t.n, t.c, t.r) <= 96 * 1024;
 }
 
@@ -470,25 +538,51 @@ struct BasisLists {
   size_t off_small = 0, off_big = 0;  // blob offsets
   size_t off_small_v[kSmallVariants] = {};
   size_t off_map[SRTT_MAX_QR_LEVELS] = {};  // per TSQR level: CTA -> (target, block)
+  // register-tree targets by column padding (16 / 32): single-CTA ones, the
+  // tops of tall ones, and the (target, CTA) map of the tall ones
+  std::vector<int> w_small[2], w_tall[2];
+  size_t off_w_small[2] = {}, off_w_tall[2] = {}, off_w_map[2] = {};
+  int w_ctas[2] = {};
 };
 
 BasisLists make_basis_lists(const std::vector<BasisTarget>& targets, Blob& blob) {
   BasisLists L;
   for (int i = 0; i < (int)targets.size(); ++i) (basis_is_small(targets[i]) ? L.small : L.big).push_back(i);
+  for (int v = 0; v < 2; ++v) {
+    std::vector<int2> map;
+    for (int i = 0; i < (int)targets.size(); ++i) {
+      const BasisTarget& t = targets[i];
+      if (t.kind != 1 || srtt_wtree_cp(t.c) != (v ? 32 : 16)) continue;
+      if (t.nlevels == 0) {
+        L.w_small[v].push_back(i);
+      } else {
+        L.w_tall[v].push_back(i);
+        for (int b = 0; b < t.lv[0].nblk; ++b) map.push_back(make_int2(i, b));
+      }
+    }
+    if (!L.w_small[v].empty()) L.off_w_small[v] = blob.add(L.w_small[v].data(), sizeof(int) * L.w_small[v].size());
+    if (!L.w_tall[v].empty()) {
+      L.off_w_tall[v] = blob.add(L.w_tall[v].data(), sizeof(int) * L.w_tall[v].size());
+      L.off_w_map[v] = blob.add(map.data(), sizeof(int2) * map.size());
+      L.w_ctas[v] = (int)map.size();
+    }
+  }
   for (int l = 0; l < SRTT_MAX_QR_LEVELS; ++l) {
     std::vector<int2> map;
     for (int i = 0; i < (int)targets.size(); ++i)
-      if (targets[i].nlevels > l)
+      if (targets[i].kind == 0 && targets[i].nlevels > l)
         for (int b = 0; b < targets[i].lv[l].nblk; ++b) map.push_back(make_int2(i, b));
     if (map.empty()) break;
     L.off_map[l] = blob.add(map.data(), sizeof(int2) * map.size());
   }
   const int zero = 0;
   L.off_small = blob.add(L.small.empty() ? &zero : L.small.data(), sizeof(int) * std::max<size_t>(1, L.small.size()));
-  for (int i : L.small) L.small_v[srtt_basis_small_variant((int)targets[i].n, targets[i].c)].push_back(i);
+  for (int i : L.small)
+    if (targets[i].kind == 0) L.small_v[srtt_basis_small_variant((int)targets[i].n, targets[i].c)].push_back(i);
   for (int v = 0; v < kSmallVariants; ++v)
     if (!L.small_v[v].empty()) L.off_small_v[v] = blob.add(L.small_v[v].data(), sizeof(int) * L.small_v[v].size());
-  for (int i : L.big) L.big_v[srtt_basis_top_variant(targets[i].c)].push_back(i);
+  for (int i : L.big)
+    if (targets[i].kind == 0) L.big_v[srtt_basis_top_variant(targets[i].c)].push_back(i);
   for (int v = 0; v < 3; ++v)
     if (!L.big_v[v].empty()) L.off_big_v[v] = blob.add(L.big_v[v].data(), sizeof(int) * L.big_v[v].size());
   L.off_big = blob.add(L.big.empty() ? &zero : L.big.data(), sizeof(int) * std::max<size_t>(1, L.big.size()));
@@ -501,8 +595,41 @@ int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const 
                        cudaStream_t small_stream = nullptr) {
   int launches = 0;
   int maxlev = 0;
-  for (auto& t : targets) maxlev = std::max(maxlev, t.nlevels);
+  bool any_tall = false;
+  for (auto& t : targets) {
+    if (t.kind == 0) maxlev = std::max(maxlev, t.nlevels);
+    any_tall = any_tall || t.nlevels > 0;
+  }
   const int nt = (int)targets.size();
+  // register-tree targets: single-CTA ones on the side stream, tall ones as
+  // factor -> top -> apply on the main stream
+  for (int v = 0; v < 2; ++v) {
+    const int cp = v ? 32 : 16;
+    if (!lists.w_small[v].empty()) {
+      size_t smem = 0;
+      for (int i : lists.w_small[v]) smem = std::max(smem, srtt_wtree_top_smem((int)targets[i].n, targets[i].c, true));
+      CK(srtt_launch_wtree_top(cp, dT, reinterpret_cast<const int*>(dblob + lists.off_w_small[v]),
+                               (int)lists.w_small[v].size(), smem, small_stream ? small_stream : h->stream));
+      ++launches;
+    }
+  }
+  for (int v = 0; v < 2; ++v) {
+    const int cp = v ? 32 : 16;
+    if (lists.w_tall[v].empty()) continue;
+    size_t sf = 0, st = 0, sa = 0;
+    for (int i : lists.w_tall[v]) {
+      const BasisTarget& t = targets[i];
+      sf = std::max(sf, srtt_wtree_factor_smem(t.lv[0].blk_rows, t.c));
+      sa = std::max(sa, srtt_wtree_apply_smem(t.lv[0].blk_rows, t.c));
+      st = std::max(st, srtt_wtree_top_smem((int)t.lv[1].n, t.c, false));
+    }
+    const int2* map = reinterpret_cast<const int2*>(dblob + lists.off_w_map[v]);
+    CK(srtt_launch_wtree_factor(cp, dT, map, lists.w_ctas[v], sf, h->stream));
+    CK(srtt_launch_wtree_top(cp, dT, reinterpret_cast<const int*>(dblob + lists.off_w_tall[v]),
+                             (int)lists.w_tall[v].size(), st, h->stream));
+    CK(srtt_launch_wtree_apply(cp, dT, map, lists.w_ctas[v], sa, h->stream));
+    launches += 3;
+  }
   for (int v = 0; v < kSmallVariants; ++v) {
     if (lists.small_v[v].empty()) continue;
     size_t smem = 0;
@@ -517,7 +644,7 @@ int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const 
     int nctas = 0;
     size_t smem = 0;
     for (auto& t : targets)
-      if (t.nlevels > l) {
+      if (t.kind == 0 && t.nlevels > l) {
         nctas += t.lv[l].nblk;
         smem = std::max(smem, srtt_basis_level_smem(t.lv[l].blk_rows, t.c));
       }
@@ -538,7 +665,7 @@ int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const 
     int nctas = 0;
     size_t sm = 0;
     for (auto& t : targets)
-      if (t.nlevels > l) {
+      if (t.kind == 0 && t.nlevels > l) {
         nctas += t.lv[l].nblk;
         sm = std::max(sm, srtt_basis_level_smem(t.lv[l].blk_rows, t.c));
       }
@@ -546,7 +673,7 @@ int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const 
                               h->stream));
     ++launches;
   }
-  if (maxlev > 0) {
+  if (any_tall) {
     CK(srtt_launch_pad(dT, nt, pad_scratch, pad_stride, h->stream));
     ++launches;
   }
@@ -558,7 +685,7 @@ void assign_basis_ctas(std::vector<BasisTarget>& targets) {
     int c = 0;
     for (auto& t : targets) {
       t.cta_begin[l] = c;
-      if (t.nlevels > l) c += t.lv[l].nblk;
+      if (t.kind == 0 && t.nlevels > l) c += t.lv[l].nblk;
     }
   }
 }

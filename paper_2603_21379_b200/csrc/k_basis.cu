@@ -1183,6 +1183,664 @@ __global__ void __launch_bounds__(kThreads) basis_cta_kernel(const BasisTarget* 
   PROF_MARK_CTA(7);
 }
 
+
+// ===========================================================================
+// Register-resident TSQR tree (sketches with c <= 32 columns).
+//
+// The shared-memory QR above pays one CTA barrier and two dependent warp
+// reductions per reflector, with all 8 warps working on one column pair at
+// a time. Here a WARP owns a whole row block: lane l holds rows
+// {l, l + 32, ...} of the block in registers (RT rows x CP columns, RT * CP
+// = 64 doubles), so a reflector step is one lane-local dot-product pass, one
+// reduce-scatter through a conflict-free shared-memory transpose and one
+// lane-local update; the live columns shift one register to the left per
+// step, so the rolled step loop only ever touches statically indexed
+// registers. Row blocks are combined as a tree inside the CTA (warp R
+// factors stacked in shared memory and factored again) and, for tall
+// sketches, across CTAs through one stacked-R level in global memory.
+//
+// Reflector convention of this path: H_j = I - g_j u_j u_j^T with u_j stored
+// whole (zeros above the diagonal, u_jj = alpha - beta on it, the column
+// tail below), g_j = 2 / (u_j^T u_j) computed from the stored u_j.
+//
+// The small SVD: R^T = Q_1 R_1 (a second register QR), one-sided Jacobi on
+// the rows of R_1 without accumulating the rotations: R_1 = J S W^T, and
+// the left singular vectors of R (= those of Z up to Q) are the normalised
+// rows of the rotated matrix, W = (J^T R_1)^T S^-1.
+// ===========================================================================
+constexpr int kTreeMaxLevels = 12;
+
+// development: per-segment clocks of the QR step (tools/microbench/wqr.cu)
+#ifdef SRTT_WQR_PROF
+__device__ long long g_wqr_clk[8];
+#define WQR_CLK_DECL long long wq_t[6], wq_acc[6] = {0, 0, 0, 0, 0, 0}
+#define WQR_CLK(i)                                        \
+  do {                                                    \
+    wq_t[i] = clock64();                                  \
+    if (i > 0) wq_acc[i] += wq_t[i] - wq_t[i - 1];        \
+  } while (0)
+#define WQR_CLK_OUT                                                   \
+  do {                                                                \
+    if (threadIdx.x == 0 && blockIdx.x == 0)                          \
+      for (int i = 0; i < 6; ++i) g_wqr_clk[i] = wq_acc[i];           \
+  } while (0)
+#else
+#define WQR_CLK_DECL
+#define WQR_CLK(i)
+#define WQR_CLK_OUT
+#endif
+
+struct WTree {
+  int L;                           // QR levels; the final R is S[L]
+  int rows[kTreeMaxLevels + 1];    // rows entering level l
+  int nblk[kTreeMaxLevels];
+  int soff[kTreeMaxLevels + 1];    // S_l, l >= 1: stacked R entering level l (then V_l in place), ld = rows | 1
+  int goff[kTreeMaxLevels];        // g_l: nblk x c
+  int yoff[kTreeMaxLevels + 1];    // Y_l, l >= 1 (back-application), ld = rows | 1
+  int persist;                     // doubles of the S + g part (kept for the apply kernel)
+  int total;
+};
+
+__host__ __device__ inline WTree wtree_plan(int n0, int c, int chunk) {
+  WTree t;
+  int rows = n0, l = 0;
+  t.rows[0] = n0;
+  for (;;) {
+    const int nb = (rows + chunk - 1) / chunk;
+    const int rem = rows - (nb - 1) * chunk;
+    t.nblk[l] = nb;
+    rows = (nb - 1) * c + (rem < c ? rem : c);
+    ++l;
+    t.rows[l] = rows;
+    if (nb == 1 || l >= kTreeMaxLevels) break;
+  }
+  t.L = l;
+  int off = 0;
+  for (int i = 1; i <= l; ++i) { t.soff[i] = off; off += (t.rows[i] | 1) * c; }
+  for (int i = 0; i < l; ++i) { t.goff[i] = off; off += t.nblk[i] * c; }
+  t.persist = off;
+  for (int i = 1; i <= l; ++i) { t.yoff[i] = off; off += (t.rows[i] | 1) * c; }
+  t.total = off;
+  return t;
+}
+
+template <int CP> struct WTile {
+  static constexpr int RT = 64 / CP;      // rows per lane
+  static constexpr int CHUNK = 32 * RT;   // rows per warp block
+  static constexpr int WSCR = 32 * (CP + 2) + 2 * CP;  // per-warp scratch doubles
+};
+
+// Sum D[p] over the 32 lanes; afterwards the lanes [col * 32 / CP, ...)
+// hold the total of column col (fixed summation order). The scratch rows
+// are CP + 2 doubles apart: 16-byte vector stores, and both the stores and
+// the column reads are bank-conflict free. The caller must pass a warp
+// barrier before the next call (every user below does: the coefficient
+// broadcast follows each reduction).
+template <int CP>
+__device__ __forceinline__ double reduce_scatter_sm(const double (&D)[CP], double* red, int lane) {
+  constexpr int LPC = 32 / CP, SPL = 32 / LPC, LD = CP + 2;
+  double2* row = reinterpret_cast<double2*>(red + lane * LD);
+#pragma unroll
+  for (int p = 0; p < CP; p += 2) row[p / 2] = make_double2(D[p], D[p + 1]);
+  __syncwarp();
+  const int col = lane / LPC, part = lane % LPC;
+  const double* q = red + (size_t)(part * SPL) * LD + col;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+  for (int i = 0; i < SPL; i += 4) {
+    s0 += q[(i + 0) * LD];
+    s1 += q[(i + 1) * LD];
+    s2 += q[(i + 2) * LD];
+    s3 += q[(i + 3) * LD];
+  }
+  double s = (s0 + s1) + (s2 + s3);
+  if (LPC == 2) s += __shfl_xor_sync(0xffffffffu, s, 1);
+  return s;
+}
+
+// Shared-memory accesses by 32-bit shared-window address: the reflector,
+// g and R destinations of the step loops are always shared memory, and a
+// generic store there costs a few hundred cycles at the next warp barrier.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void sts_f64(uint32_t addr, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+// Householder QR of the warp's register block a (nr rows, c columns; rows
+// beyond nr and columns beyond c are zero). Reflector j goes to
+// vout[row + j * ldv] (STOREV), g_j to gout[j], row j of R to
+// rout[j * rs + col * cs] (entries on and right of the diagonal only).
+template <int CP, bool STOREV>
+__device__ void wqr_factor(double (&a)[WTile<CP>::RT][CP], int nr, int c, double* vout, int ldv, double* gout,
+                           double* rout, int rs, int cs, double* wsm) {
+  constexpr int RT = WTile<CP>::RT, LPC = 32 / CP;
+  const int lane = threadIdx.x & 31;
+  const int mycol = lane / LPC;
+  double* red = wsm;
+  double* prow = wsm + 32 * (CP + 2);
+  double* csm = prow + CP;
+  const int kb = nr < c ? nr : c;
+  // all destinations are shared memory (see smem_addr)
+  uint32_t va = STOREV ? smem_addr(vout) + 8u * lane : 0u;   // element (lane, j = 0)
+  uint32_t ga = STOREV ? smem_addr(gout) : 0u;
+  uint32_t ra = smem_addr(rout) + 8u * (uint32_t)(mycol * cs);  // element (j = 0, col = mycol)
+  const uint32_t vstep = 8u * (uint32_t)ldv, rstep = 8u * (uint32_t)(rs + cs);
+  WQR_CLK_DECL;
+  for (int j = 0; j < kb; ++j) {
+    const int lj = j & 31, tj = j >> 5;
+    WQR_CLK(0);
+#pragma unroll
+    for (int t = 0; t < RT; ++t)
+      if (tj == t) {
+        if (lane == lj) {
+#pragma unroll
+          for (int p = 0; p < CP; p += 2) reinterpret_cast<double2*>(prow)[p / 2] = make_double2(a[t][p], a[t][p + 1]);
+        }
+      }
+    double xm[RT];
+#pragma unroll
+    for (int t = 0; t < RT; ++t) xm[t] = (t * 32 + lane > j) ? a[t][0] : 0.0;
+    double D[CP];
+#pragma unroll
+    for (int p = 0; p < CP; ++p) {
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) s = fma(xm[t], a[t][p], s);
+      D[p] = s;
+    }
+    WQR_CLK(1);
+    const double dtot = reduce_scatter_sm<CP>(D, red, lane);  // (its barrier also publishes prow)
+    WQR_CLK(2);
+    const double ss = __shfl_sync(0xffffffffu, dtot, 0);
+    const double alpha = prow[0];
+    double beta = alpha, ujj = 0.0, g = 0.0;
+    if (ss != 0.0) {
+      // g = 2 / (ss + u_jj^2) = 1 / (nrm |u_jj|), from one reciprocal square
+      // root and one reciprocal (the chain is the step's critical path)
+      const double n2 = fma(alpha, alpha, ss);
+      const double rn = rsqrt(n2);
+      const double nrm = n2 * rn;
+      beta = -copysign(nrm, alpha);
+      ujj = alpha - beta;
+      g = rn * __drcp_rn(fabs(ujj));
+    }
+    const double arow = prow[mycol];
+    const double cl = g * fma(ujj, arow, dtot);
+    WQR_CLK(3);
+    if (lane % LPC == 0) {
+      csm[mycol] = cl;
+      if (j + mycol < c) sts_f64(ra, mycol == 0 ? beta : arow - cl * ujj);
+    }
+    ra += rstep;
+    if (STOREV) {
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int row = t * 32 + lane;
+        if (row < nr) sts_f64(va + 256u * t, row > j ? xm[t] : (row == j ? ujj : 0.0));
+      }
+      if (lane == 0) sts_f64(ga + 8u * j, g);
+      va += vstep;
+    }
+    __syncwarp();
+    WQR_CLK(4);
+#pragma unroll
+    for (int p = 0; p < CP; p += 2) {
+      const double2 e = reinterpret_cast<const double2*>(csm)[p / 2];
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        if (p > 0) a[t][p - 1] = fma(-e.x, xm[t], a[t][p]);
+        a[t][p] = fma(-e.y, xm[t], a[t][p + 1 < CP ? p + 1 : p]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < RT; ++t) a[t][CP - 1] = 0.0;
+    __syncwarp();
+    WQR_CLK(5);
+  }
+  WQR_CLK_OUT;
+}
+
+// y <- H_0 ... H_{kb-1} y for the warp's register block y (nr rows).
+template <int CP>
+__device__ void wqr_apply(double (&y)[WTile<CP>::RT][CP], int nr, int kb, const double* v, int ldv, const double* g,
+                          double* wsm) {
+  constexpr int RT = WTile<CP>::RT, LPC = 32 / CP;
+  const int lane = threadIdx.x & 31;
+  const int mycol = lane / LPC;
+  double* red = wsm;
+  double* esm = wsm + 32 * (CP + 2);
+  // v and g are shared memory (see smem_addr)
+  const uint32_t vstep = 8u * (uint32_t)ldv;
+  uint32_t va = smem_addr(v) + 8u * lane + vstep * (uint32_t)(kb > 0 ? kb - 1 : 0);
+  const uint32_t ga = smem_addr(g);
+  double vt[RT];
+#pragma unroll
+  for (int t = 0; t < RT; ++t) vt[t] = (kb > 0 && t * 32 + lane < nr) ? lds_f64(va + 256u * t) : 0.0;
+  for (int j = kb - 1; j >= 0; --j) {
+    va -= vstep;
+    double vn[RT];
+#pragma unroll
+    for (int t = 0; t < RT; ++t) vn[t] = (j > 0 && t * 32 + lane < nr) ? lds_f64(va + 256u * t) : 0.0;
+    const double gj = lds_f64(ga + 8u * j);
+    double D[CP];
+#pragma unroll
+    for (int p = 0; p < CP; ++p) {
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) s = fma(vt[t], y[t][p], s);
+      D[p] = s;
+    }
+    const double dtot = reduce_scatter_sm<CP>(D, red, lane);
+    if (lane % LPC == 0) esm[mycol] = gj * dtot;
+    __syncwarp();
+#pragma unroll
+    for (int p = 0; p < CP; p += 2) {
+      const double2 e = reinterpret_cast<const double2*>(esm)[p / 2];
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        y[t][p] = fma(-e.x, vt[t], y[t][p]);
+        y[t][p + 1] = fma(-e.y, vt[t], y[t][p + 1]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < RT; ++t) vt[t] = vn[t];
+  }
+}
+
+// One-sided Jacobi on the rows of B (k x k, row-major, ld ldb) by one warp,
+// rows resident in registers (circle method as jacobi_rows_reg), rotations
+// not accumulated. A sweep whose largest rotated pair had
+// |cos(angle)| <= 3e-7 is the last one (quadratic convergence: the
+// remaining couplings are below 1e-13 relative).
+template <int G, int E>
+__device__ int jacobi_rows_nov(double* B, int ldb, int k) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane / G, gl = lane % G;
+  const int kk = (k + 1) & ~1;
+  const int np = kk / 2;
+  const bool live = g < np;
+  const double tol2 = 4.0 * DBL_EPSILON * DBL_EPSILON;
+  int tp = g, bp = kk - 1 - g;
+  double tb[E], bb[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int j = gl + G * e;
+    tb[e] = (live && tp < k && j < k) ? B[(size_t)tp * ldb + j] : 0.0;
+    bb[e] = (live && bp < k && j < k) ? B[(size_t)bp * ldb + j] : 0.0;
+  }
+  const int src_prev = (lane - G) & 31, src_next = (lane + G) & 31;
+  int sweep = 0;
+  if (k >= 2) {
+    for (; sweep < 80; ++sweep) {
+      int rotated = 0, big = 0;
+      for (int rd = 0; rd < kk - 1; ++rd) {
+        double app = 0.0, aqq = 0.0, apq = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          app = fma(tb[e], tb[e], app);
+          aqq = fma(bb[e], bb[e], aqq);
+          apq = fma(tb[e], bb[e], apq);
+        }
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) {
+          app += __shfl_xor_sync(0xffffffffu, app, o);
+          aqq += __shfl_xor_sync(0xffffffffu, aqq, o);
+          apq += __shfl_xor_sync(0xffffffffu, apq, o);
+        }
+        const double a2 = apq * apq, pq = app * aqq;
+        if (live && apq != 0.0 && a2 > tol2 * pq) {
+          double cs, sn;
+          jacobi_rotation(app, aqq, apq, &cs, &sn);
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const double x = tb[e], y = bb[e];
+            tb[e] = cs * x - sn * y;
+            bb[e] = sn * x + cs * y;
+          }
+          rotated = 1;
+          if (a2 > 1e-13 * pq) big = 1;
+        }
+        if (np > 1) {
+          // advance: top[0] stays, top[1] <- bot[0], top[g] <- top[g-1],
+          // bot[g] <- bot[g+1], bot[np-1] <- top[np-1]
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const double send = g == 0 ? bb[e] : tb[e];
+            const double fp = __shfl_sync(0xffffffffu, send, src_prev);
+            const double fn = __shfl_sync(0xffffffffu, bb[e], src_next);
+            const double otb = tb[e];
+            if (g >= 1) tb[e] = fp;
+            bb[e] = g == np - 1 ? otb : fn;
+          }
+          const int sendp = g == 0 ? bp : tp;
+          const int fpp = __shfl_sync(0xffffffffu, sendp, src_prev);
+          const int fnp = __shfl_sync(0xffffffffu, bp, src_next);
+          const int otp = tp;
+          if (g >= 1) tp = fpp;
+          bp = g == np - 1 ? otp : fnp;
+        }
+      }
+      if (!__any_sync(0xffffffffu, rotated)) break;
+      if (!__any_sync(0xffffffffu, big)) { ++sweep; break; }
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int j = gl + G * e;
+    if (live && tp < k && j < k) B[(size_t)tp * ldb + j] = tb[e];
+    if (live && bp < k && j < k) B[(size_t)bp * ldb + j] = bb[e];
+  }
+  __syncwarp();
+  return sweep;
+}
+
+// Factor levels lo..L-1 of a CTA's tree. Level 0 reads in0 (ld ld0) and
+// writes its reflectors to v0 (ld ldv0; may alias in0); upper levels live in
+// the arena. All warps of the CTA take row blocks round-robin.
+template <int CP>
+__device__ void wtree_factor(const WTree& tr, int c, const double* in0, int64_t ld0, double* v0, int64_t ldv0,
+                             double* arena, double* wscr_all, double* stage0 = nullptr) {
+  constexpr int RT = WTile<CP>::RT, CHUNK = WTile<CP>::CHUNK;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double* wsm = wscr_all + (size_t)warp * WTile<CP>::WSCR;
+  for (int l = 0; l < tr.L; ++l) {
+    const int rows = tr.rows[l];
+    const double* src = l == 0 ? in0 : arena + tr.soff[l];
+    const int64_t lds = l == 0 ? ld0 : (rows | 1);
+    double* vdst = l == 0 ? v0 : arena + tr.soff[l];
+    const int64_t ldv = l == 0 ? ldv0 : (rows | 1);
+    double* rnext = arena + tr.soff[l + 1];
+    const int64_t ldr = tr.rows[l + 1] | 1;
+    for (int b = warp; b < tr.nblk[l]; b += nw) {
+      const int r0 = b * CHUNK;
+      const int nr = min(CHUNK, rows - r0);
+      double a[RT][CP];
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int row = t * 32 + lane;
+#pragma unroll
+        for (int p = 0; p < CP; ++p) a[t][p] = (row < nr && p < c) ? src[r0 + row + (int64_t)p * lds] : 0.0;
+      }
+      __syncwarp();
+      if (l == 0 && stage0) {
+        // v0 is global memory: a store there inside the step loop would make
+        // every warp barrier of the step wait for its acknowledgement, so
+        // the reflectors are staged in shared memory and copied out after
+        double* st = stage0 + (size_t)warp * (CHUNK + 1) * c;
+        wqr_factor<CP, true>(a, nr, c, st, CHUNK + 1, arena + tr.goff[l] + b * c, rnext + b * c, 1, ldr, wsm);
+        __syncwarp();
+        const int kb = min(nr, c);
+        for (int j = 0; j < kb; ++j)
+#pragma unroll
+          for (int t = 0; t < RT; ++t) {
+            const int row = t * 32 + lane;
+            if (row < nr) vdst[r0 + row + (int64_t)j * ldv] = st[row + j * (CHUNK + 1)];
+          }
+        __syncwarp();
+      } else {
+        wqr_factor<CP, true>(a, nr, c, vdst + r0, ldv, arena + tr.goff[l] + b * c, rnext + b * c, 1, ldr, wsm);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Back-application through levels L-1..0: Y_L (arena) holds the kb_top x q
+// input; the level-0 result goes to out0 (ld ldo). v0 as in wtree_factor;
+// when stage0 is set the level-0 reflector block is first copied into the
+// warp's staging area (it lives in global memory).
+template <int CP>
+__device__ void wtree_apply(const WTree& tr, int c, int q, const double* v0, int64_t ldv0, double* arena,
+                            double* wscr_all, double* out0, int64_t ldo, double* stage0) {
+  constexpr int RT = WTile<CP>::RT, CHUNK = WTile<CP>::CHUNK;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double* wsm = wscr_all + (size_t)warp * WTile<CP>::WSCR;
+  for (int l = tr.L - 1; l >= 0; --l) {
+    const int rows = tr.rows[l];
+    const double* vsrc = l == 0 ? v0 : arena + tr.soff[l];
+    const int64_t ldv = l == 0 ? ldv0 : (rows | 1);
+    const double* yin = arena + tr.yoff[l + 1];
+    const int64_t ldyi = tr.rows[l + 1] | 1;
+    double* yout = l == 0 ? out0 : arena + tr.yoff[l];
+    const int64_t ldyo = l == 0 ? ldo : (rows | 1);
+    for (int b = warp; b < tr.nblk[l]; b += nw) {
+      const int r0 = b * CHUNK;
+      const int nr = min(CHUNK, rows - r0);
+      const int kb = min(nr, c);
+      const double* vb = vsrc + r0;
+      int64_t ldvb = ldv;
+      if (l == 0 && stage0) {
+        double* st = stage0 + (size_t)warp * (CHUNK + 1) * c;
+        // batches of 8 loads in flight per lane (the block sits in L2)
+        const int tot = kb * nr;
+        for (int i0 = lane; i0 < tot; i0 += 32 * 8) {
+          double tmp[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int idx = i0 + 32 * u;
+            tmp[u] = idx < tot ? vb[idx % nr + (int64_t)(idx / nr) * ldv] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int idx = i0 + 32 * u;
+            if (idx < tot) st[idx % nr + (idx / nr) * (CHUNK + 1)] = tmp[u];
+          }
+        }
+        __syncwarp();
+        vb = st;
+        ldvb = CHUNK + 1;
+      }
+      double y[RT][CP];
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int row = t * 32 + lane;
+#pragma unroll
+        for (int p = 0; p < CP; ++p) y[t][p] = (row < kb && p < q) ? yin[b * c + row + (int64_t)p * ldyi] : 0.0;
+      }
+      wqr_apply<CP>(y, nr, kb, vb, ldvb, arena + tr.goff[l] + b * c, wsm);
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int row = t * 32 + lane;
+#pragma unroll
+        for (int p = 0; p < CP; ++p)
+          if (row < nr && p < q) yout[r0 + row + (int64_t)p * ldyo] = y[t][p];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+struct WTopSmem {
+  double* v0;     // (n0 | 1) x c level-0 reflectors
+  double* arena;  // tree arena
+  double* wscr;   // per-warp scratch
+  double* B;      // CP x (CP + 1) Jacobi rows
+  double* sig;
+  double* dots;
+  double* red;
+  double* vpad;   // n0 (padding scratch, single-CTA targets)
+  int* perm;
+};
+
+__host__ __device__ inline size_t wtop_doubles(int n0, int c, int CP, int nwarps, int chunk, bool pad) {
+  const WTree tr = wtree_plan(n0, c, chunk);
+  return (size_t)(n0 | 1) * c + tr.total + 4 + (size_t)nwarps * (32 * (CP + 2) + 2 * CP) + (size_t)CP * (CP + 1) + CP + CP +
+         64 + (pad ? n0 : 0) + CP / 2 + 2;
+}
+
+// Whole basis of a single-CTA target (nlevels == 0), or the top of a tall
+// one (nlevels == 1: input = the stacked R of the factor kernel, output =
+// the stacked Y for the apply kernel).
+template <int CP>
+__global__ void __launch_bounds__(kThreads) basis_wtree_kernel(const BasisTarget* __restrict__ targets,
+                                                              const int* __restrict__ list) {
+  constexpr int RT = WTile<CP>::RT, CHUNK = WTile<CP>::CHUNK;
+  constexpr int LDB = CP + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ BasisTarget T;
+  stage_target(&T, &targets[list[blockIdx.x]]);
+  __syncthreads();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool tall = T.nlevels > 0;
+  const QrLevel L = T.lv[T.nlevels];
+  const int n0 = (int)L.n, c = T.c, r = T.r;
+  const WTree tr = wtree_plan(n0, c, CHUNK);
+  WTopSmem s;
+  {
+    double* p = reinterpret_cast<double*>(smem_raw);
+    s.v0 = p; p += ((size_t)(n0 | 1) * c + 1) & ~(size_t)1;
+    s.arena = p; p += (tr.total + 1) & ~1;
+    s.wscr = p; p += (size_t)kWarps * WTile<CP>::WSCR;  // 16-byte aligned (vector accesses)
+    s.B = p; p += CP * LDB;
+    s.sig = p; p += CP;
+    s.dots = p; p += CP;
+    s.red = p; p += 64;
+    s.vpad = p; p += tall ? 0 : n0;
+    s.perm = reinterpret_cast<int*>(p);
+  }
+  PROF_MARK_CTA(0);
+  for (int i = tid; i < tr.persist; i += blockDim.x) s.arena[i] = 0.0;
+  for (int i = tid; i < CP * LDB; i += blockDim.x) s.B[i] = 0.0;
+  __syncthreads();
+  wtree_factor<CP>(tr, c, L.a, L.n, s.v0, n0 | 1, s.arena, s.wscr);
+  PROF_MARK_CTA(1);
+  // R^T = Q_1 R_1, then Jacobi on the rows of R_1 (warp 0)
+  const int k = tr.rows[tr.L];
+  int sweeps = 0;
+  if (warp == 0) {
+    const double* Rf = s.arena + tr.soff[tr.L];
+    const int ldr = k | 1;
+    double a[RT][CP];
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+      const int row = t * 32 + lane;  // column index of R
+#pragma unroll
+      for (int p = 0; p < CP; ++p) a[t][p] = (row < c && p < k) ? Rf[p + (size_t)row * ldr] : 0.0;
+    }
+    wqr_factor<CP, false>(a, c, k, nullptr, 0, nullptr, s.B, LDB, 1, s.wscr);
+    __syncwarp();
+    PROF_MARK(2);
+    if (CP == 16) sweeps = jacobi_rows_nov<4, 4>(s.B, LDB, k);
+    else sweeps = jacobi_rows_nov<2, 16>(s.B, LDB, k);
+  }
+  __syncthreads();
+  PROF_MARK_CTA(3);
+  for (int i = tid; i < k; i += blockDim.x) {
+    const double* bi = s.B + (size_t)i * LDB;
+    s.sig[i] = sqrt(dot4(bi, bi, 0, k));
+  }
+  __syncthreads();
+  for (int i = tid; i < k; i += blockDim.x) {
+    int rank = 0;
+    for (int j = 0; j < k; ++j) rank += (s.sig[j] > s.sig[i]) || (s.sig[j] == s.sig[i] && j < i);
+    s.perm[rank] = i;
+  }
+  __syncthreads();
+  const double smax = k > 0 ? s.sig[s.perm[0]] : 0.0;
+  const double tol_rank = (double)srtt_dev::max64(T.n, (int64_t)c) * DBL_EPSILON * smax;
+  int nrank = 0;
+  for (int i = 0; i < k; ++i) nrank += s.sig[i] > tol_rank;
+  const int q = min(nrank, r);
+  if (tid == 0) {
+    T.info[0] = q;
+    T.info[1] = nrank;
+    T.info[2] = sweeps;
+  }
+  if (T.sv)
+    for (int i = tid; i < k; i += blockDim.x) T.sv[i] = s.sig[s.perm[i]];
+  // Y_L = W(:, perm[:q]): normalised rows of the rotated R_1
+  {
+    double* yt = s.arena + tr.yoff[tr.L];
+    const int ldy = k | 1;
+    for (int idx = tid; idx < k * q; idx += blockDim.x) {
+      const int i = idx % k, col = idx / k;
+      const int src = s.perm[col];
+      yt[i + (size_t)col * ldy] = s.B[(size_t)src * LDB + i] / s.sig[src];
+    }
+  }
+  __syncthreads();
+  PROF_MARK_CTA(4);
+  wtree_apply<CP>(tr, c, q, s.v0, n0 | 1, s.arena, s.wscr, tall ? L.y : T.u, tall ? L.n : T.n, nullptr);
+  PROF_MARK_CTA(5);
+  if (!tall && q < r)
+    pad_columns(T.u, n0, n0, q, r, T.state0, T.draw_offset, (uint64_t)T.normal_base, s.vpad, s.dots, s.red);
+  PROF_MARK_CTA(6);
+  PROF_MARK_CTA(7);
+}
+
+constexpr int kWfThreads = 128;  // factor / apply CTAs of tall targets: one warp per SM sub-partition
+
+// Tall targets, level 0: CTA (target, i) factors rows [i * rpc, ...) of Z in
+// place, keeps its upper tree levels in T.vup and stacks its R.
+template <int CP>
+__global__ void __launch_bounds__(kWfThreads) basis_wfactor_kernel(const BasisTarget* __restrict__ targets,
+                                                                  const int2* __restrict__ map) {
+  constexpr int CHUNK = WTile<CP>::CHUNK;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ BasisTarget T;
+  const int2 tb = map[blockIdx.x];
+  stage_target(&T, &targets[tb.x]);
+  __syncthreads();
+  const QrLevel L = T.lv[0];
+  const QrLevel P = T.lv[1];
+  const int c = T.c;
+  const int64_t r0 = (int64_t)tb.y * L.blk_rows;
+  const int nrows = (int)srtt_dev::min64(L.blk_rows, L.n - r0);
+  const WTree tr = wtree_plan(nrows, c, CHUNK);
+  double* arena = reinterpret_cast<double*>(smem_raw);
+  double* wscr = arena + ((tr.persist + 1) & ~1);
+  double* stage = wscr + (size_t)(kWfThreads / 32) * WTile<CP>::WSCR;
+  for (int i = threadIdx.x; i < tr.persist; i += blockDim.x) arena[i] = 0.0;
+  __syncthreads();
+  wtree_factor<CP>(tr, c, L.a + r0, L.n, L.a + r0, L.n, arena, wscr, stage);
+  const int k = tr.rows[tr.L];
+  const double* Rf = arena + tr.soff[tr.L];
+  for (int idx = threadIdx.x; idx < k * c; idx += blockDim.x) {
+    const int i = idx % k, j = idx / k;
+    P.a[(int64_t)j * P.n + (int64_t)tb.y * c + i] = Rf[i + (size_t)j * (k | 1)];
+  }
+  double* up = T.vup + (int64_t)tb.y * T.vup_stride;
+  for (int i = threadIdx.x; i < tr.persist; i += blockDim.x) up[i] = arena[i];
+}
+
+template <int CP>
+__global__ void __launch_bounds__(kWfThreads) basis_wapply_kernel(const BasisTarget* __restrict__ targets,
+                                                                 const int2* __restrict__ map) {
+  constexpr int CHUNK = WTile<CP>::CHUNK;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ BasisTarget T;
+  const int2 tb = map[blockIdx.x];
+  stage_target(&T, &targets[tb.x]);
+  __syncthreads();
+  const QrLevel L = T.lv[0];
+  const QrLevel P = T.lv[1];
+  const int c = T.c;
+  const int q = T.info[0];
+  const int64_t r0 = (int64_t)tb.y * L.blk_rows;
+  const int nrows = (int)srtt_dev::min64(L.blk_rows, L.n - r0);
+  const WTree tr = wtree_plan(nrows, c, CHUNK);
+  double* arena = reinterpret_cast<double*>(smem_raw);
+  double* wscr = arena + ((tr.total + 1) & ~1);
+  double* stage = wscr + (size_t)(kWfThreads / 32) * WTile<CP>::WSCR;
+  const double* up = T.vup + (int64_t)tb.y * T.vup_stride;
+  for (int i = threadIdx.x; i < tr.persist; i += blockDim.x) arena[i] = up[i];
+  const int k = tr.rows[tr.L];
+  double* yt = arena + tr.yoff[tr.L];
+  for (int idx = threadIdx.x; idx < k * q; idx += blockDim.x) {
+    const int i = idx % k, col = idx / k;
+    yt[i + (size_t)col * (k | 1)] = P.y[(int64_t)col * P.n + (int64_t)tb.y * c + i];
+  }
+  __syncthreads();
+  wtree_apply<CP>(tr, c, q, L.a + r0, L.n, arena, wscr, L.y + r0, L.n, stage);
+}
+
 }  // namespace
 
 size_t srtt_basis_top_smem(int m, int c, int r) {
@@ -1284,6 +1942,75 @@ cudaError_t srtt_launch_pad(const BasisTarget* d_targets, int ntargets, double* 
                             int64_t scratch_stride, cudaStream_t stream) {
   if (ntargets <= 0) return cudaSuccess;
   pad_kernel<<<ntargets, kThreads, 0, stream>>>(d_targets, scratch, scratch_stride);
+  return cudaGetLastError();
+}
+
+
+// ---- register-tree path (c <= 32): planning helpers and launchers ----------
+int srtt_wtree_cp(int c) { return c <= 16 ? 16 : (c <= 32 ? 32 : 0); }
+int srtt_wtree_chunk(int cp) { return cp == 16 ? WTile<16>::CHUNK : WTile<32>::CHUNK; }
+int srtt_wtree_factor_threads() { return kWfThreads; }
+
+size_t srtt_wtree_top_smem(int n0, int c, bool pad) {
+  const int cp = srtt_wtree_cp(c);
+  return wtop_doubles(n0, c, cp, kWarps, srtt_wtree_chunk(cp), pad) * sizeof(double) + 64;
+}
+
+int64_t srtt_wtree_persist_doubles(int rows, int c) {
+  const int cp = srtt_wtree_cp(c);
+  return wtree_plan(rows, c, srtt_wtree_chunk(cp)).persist;
+}
+
+size_t srtt_wtree_factor_smem(int rows, int c) {
+  const int cp = srtt_wtree_cp(c);
+  const WTree tr = wtree_plan(rows, c, srtt_wtree_chunk(cp));
+  return ((size_t)tr.persist + 2 + (size_t)(kWfThreads / 32) * ((32 * (cp + 2) + 2 * cp) + (size_t)(srtt_wtree_chunk(cp) + 1) * c)) * sizeof(double);
+}
+
+size_t srtt_wtree_apply_smem(int rows, int c) {
+  const int cp = srtt_wtree_cp(c);
+  const int chunk = srtt_wtree_chunk(cp);
+  const WTree tr = wtree_plan(rows, c, chunk);
+  return ((size_t)tr.total + 2 + (size_t)(kWfThreads / 32) * ((32 * (cp + 2) + 2 * cp) + (size_t)(chunk + 1) * c)) *
+         sizeof(double);
+}
+
+cudaError_t srtt_launch_wtree_top(int cp, const BasisTarget* d_targets, const int* d_list, int n, size_t smem,
+                                  cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  if (cp == 16) {
+    SRTT_ENSURE_SMEM((basis_wtree_kernel<16>), smem);
+    basis_wtree_kernel<16><<<n, kThreads, smem, stream>>>(d_targets, d_list);
+  } else {
+    SRTT_ENSURE_SMEM((basis_wtree_kernel<32>), smem);
+    basis_wtree_kernel<32><<<n, kThreads, smem, stream>>>(d_targets, d_list);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t srtt_launch_wtree_factor(int cp, const BasisTarget* d_targets, const int2* d_map, int nctas, size_t smem,
+                                     cudaStream_t stream) {
+  if (nctas <= 0) return cudaSuccess;
+  if (cp == 16) {
+    SRTT_ENSURE_SMEM((basis_wfactor_kernel<16>), smem);
+    basis_wfactor_kernel<16><<<nctas, kWfThreads, smem, stream>>>(d_targets, d_map);
+  } else {
+    SRTT_ENSURE_SMEM((basis_wfactor_kernel<32>), smem);
+    basis_wfactor_kernel<32><<<nctas, kWfThreads, smem, stream>>>(d_targets, d_map);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t srtt_launch_wtree_apply(int cp, const BasisTarget* d_targets, const int2* d_map, int nctas, size_t smem,
+                                    cudaStream_t stream) {
+  if (nctas <= 0) return cudaSuccess;
+  if (cp == 16) {
+    SRTT_ENSURE_SMEM((basis_wapply_kernel<16>), smem);
+    basis_wapply_kernel<16><<<nctas, kWfThreads, smem, stream>>>(d_targets, d_map);
+  } else {
+    SRTT_ENSURE_SMEM((basis_wapply_kernel<32>), smem);
+    basis_wapply_kernel<32><<<nctas, kWfThreads, smem, stream>>>(d_targets, d_map);
+  }
   return cudaGetLastError();
 }
 
