@@ -50,6 +50,12 @@ size_t srtt_wtree_apply_smem(int rows, int c);
 cudaError_t srtt_launch_wtree_top(int, const BasisTarget*, const int*, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_wtree_factor(int, const BasisTarget*, const int2*, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_wtree_apply(int, const BasisTarget*, const int2*, int, size_t, cudaStream_t);
+int srtt_wide_block_rows();
+size_t srtt_wide_top_smem(int m, int c, int r, bool pad);
+size_t srtt_wide_level_smem(int mb, int c);
+cudaError_t srtt_launch_wide_top(const BasisTarget*, const int*, int, size_t, cudaStream_t);
+cudaError_t srtt_launch_wide_factor(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
+cudaError_t srtt_launch_wide_apply(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_tsqr_factor(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_tsqr_apply(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_pad(const BasisTarget*, int, double*, int64_t, cudaStream_t);
@@ -426,12 +432,53 @@ bool plan_basis_wtree(BasisPlan& b) {
   return false;
 }
 
+// Wide register path (k_basis.cu): 32 < c <= 64, 8-warp teams on 256-row
+// blocks, the level structure of the shared-memory path (one launch per
+// level, stacked R of c rows per block).
+bool plan_basis_wide(BasisPlan& b) {
+  static const bool off = [] {
+    const char* e = std::getenv("SRTT_BASIS_SMEMQR");
+    return e && *e == '1';
+  }();
+  if (off || b.c <= 32 || b.c > 64 || b.n < 1) return false;
+  const int blk = srtt_wide_block_rows();
+  int tmax = blk;
+  while (tmax > b.c && srtt_wide_top_smem(tmax, b.c, b.r, false) > kWtreeSmemBudget) tmax -= 32;
+  if (tmax < b.c || srtt_wide_top_smem(tmax, b.c, b.r, false) > kWtreeSmemBudget) return false;
+  if (srtt_wide_level_smem(blk, b.c) > kWtreeSmemBudget) return false;
+  b.kind = 2;
+  if (b.n <= tmax && srtt_wide_top_smem((int)b.n, b.c, b.r, true) <= kWtreeSmemBudget) {
+    b.nlevels = 0;
+    b.lv_n[0] = b.n;
+    b.lv_nblk[0] = 1;
+    b.lv_blk[0] = (int)b.n;
+    return true;
+  }
+  int64_t nl = b.n;
+  int l = 0;
+  while (nl > tmax || l == 0) {
+    if (l >= SRTT_MAX_QR_LEVELS) { b.kind = 0; return false; }
+    const int nblk = (int)((nl + blk - 1) / blk);
+    b.lv_n[l] = nl;
+    b.lv_nblk[l] = nblk;
+    b.lv_blk[l] = blk;
+    nl = (int64_t)nblk * b.c;
+    ++l;
+  }
+  b.lv_n[l] = nl;
+  b.lv_nblk[l] = 1;
+  b.lv_blk[l] = (int)nl;
+  b.nlevels = l;
+  return true;
+}
+
 BasisPlan plan_basis(int64_t n, int c, int r) {
   BasisPlan b{};
   b.n = n;
   b.c = c;
   b.r = r;
   if (plan_basis_wtree(b)) return b;
+  if (plan_basis_wide(b)) return b;
   int tmax = top_max_rows(c, r);
   int blk = level_block_rows(c);
   if (tmax < c) invalid("range_basis_of_sketch: sketch too wide for the B200 basis kernel");
@@ -526,7 +573,7 @@ BasisTarget fill_basis(const BasisPlan& p, const BasisBuffers& B, char* ws, doub
 
 // Which targets take the one-warp small path (single block, fits 96 KB).
 bool basis_is_small(const BasisTarget& t) {
-  if (t.kind == 1) return t.nlevels == 0;
+  if (t.kind != 0) return t.nlevels == 0;
   return t.nlevels == 0 && t.n <= 1024 && srtt_basis_small_smem((int)t.n, t.c, t.r) <= 96 * 1024;
 }
 
@@ -543,6 +590,12 @@ struct BasisLists {
   std::vector<int> w_small[2], w_tall[2];
   size_t off_w_small[2] = {}, off_w_tall[2] = {}, off_w_map[2] = {};
   int w_ctas[2] = {};
+  // wide register path (kind 2): single-block targets, tall ones, and the
+  // per-level (target, block) maps of the tall ones
+  std::vector<int> x_small, x_tall;
+  size_t off_x_small = 0, off_x_tall = 0, off_x_map[SRTT_MAX_QR_LEVELS] = {};
+  int x_ctas[SRTT_MAX_QR_LEVELS] = {};
+  int x_levels = 0;
 };
 
 BasisLists make_basis_lists(const std::vector<BasisTarget>& targets, Blob& blob) {
@@ -565,6 +618,22 @@ BasisLists make_basis_lists(const std::vector<BasisTarget>& targets, Blob& blob)
       L.off_w_tall[v] = blob.add(L.w_tall[v].data(), sizeof(int) * L.w_tall[v].size());
       L.off_w_map[v] = blob.add(map.data(), sizeof(int2) * map.size());
       L.w_ctas[v] = (int)map.size();
+    }
+  }
+  for (int i = 0; i < (int)targets.size(); ++i)
+    if (targets[i].kind == 2) (targets[i].nlevels == 0 ? L.x_small : L.x_tall).push_back(i);
+  if (!L.x_small.empty()) L.off_x_small = blob.add(L.x_small.data(), sizeof(int) * L.x_small.size());
+  if (!L.x_tall.empty()) {
+    L.off_x_tall = blob.add(L.x_tall.data(), sizeof(int) * L.x_tall.size());
+    for (int l = 0; l < SRTT_MAX_QR_LEVELS; ++l) {
+      std::vector<int2> map;
+      for (int i : L.x_tall)
+        if (targets[i].nlevels > l)
+          for (int b = 0; b < targets[i].lv[l].nblk; ++b) map.push_back(make_int2(i, b));
+      if (map.empty()) break;
+      L.off_x_map[l] = blob.add(map.data(), sizeof(int2) * map.size());
+      L.x_ctas[l] = (int)map.size();
+      L.x_levels = l + 1;
     }
   }
   for (int l = 0; l < SRTT_MAX_QR_LEVELS; ++l) {
@@ -638,6 +707,35 @@ int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const 
     CK(srtt_launch_basis_small(v, dT, reinterpret_cast<const int*>(dblob + lists.off_small_v[v]),
                                (int)lists.small_v[v].size(), smem, small_stream ? small_stream : h->stream));
     ++launches;
+  }
+  if (!lists.x_small.empty()) {
+    size_t smem = 0;
+    for (int i : lists.x_small)
+      smem = std::max(smem, srtt_wide_top_smem((int)targets[i].n, targets[i].c, targets[i].r, true));
+    CK(srtt_launch_wide_top(dT, reinterpret_cast<const int*>(dblob + lists.off_x_small), (int)lists.x_small.size(), smem,
+                            small_stream ? small_stream : h->stream));
+    ++launches;
+  }
+  if (!lists.x_tall.empty()) {
+    size_t sl = 0, st = 0;
+    for (int i : lists.x_tall) {
+      const BasisTarget& t = targets[i];
+      sl = std::max(sl, srtt_wide_level_smem(t.lv[0].blk_rows, t.c));
+      st = std::max(st, srtt_wide_top_smem((int)t.lv[t.nlevels].n, t.c, t.r, false));
+    }
+    for (int l = 0; l < lists.x_levels; ++l) {
+      CK(srtt_launch_wide_factor(dT, reinterpret_cast<const int2*>(dblob + lists.off_x_map[l]), l, lists.x_ctas[l], sl,
+                                 h->stream));
+      ++launches;
+    }
+    CK(srtt_launch_wide_top(dT, reinterpret_cast<const int*>(dblob + lists.off_x_tall), (int)lists.x_tall.size(), st,
+                            h->stream));
+    ++launches;
+    for (int l = lists.x_levels - 1; l >= 0; --l) {
+      CK(srtt_launch_wide_apply(dT, reinterpret_cast<const int2*>(dblob + lists.off_x_map[l]), l, lists.x_ctas[l], sl,
+                                h->stream));
+      ++launches;
+    }
   }
   if (lists.big.empty()) return launches;
   for (int l = 0; l < maxlev; ++l) {

@@ -1267,7 +1267,10 @@ __host__ __device__ inline WTree wtree_plan(int n0, int c, int chunk) {
 template <int CP> struct WTile {
   static constexpr int RT = 64 / CP;      // rows per lane
   static constexpr int CHUNK = 32 * RT;   // rows per warp block
-  static constexpr int WSCR = 32 * (CP + 2) + 2 * CP;  // per-warp scratch doubles
+  static constexpr int LPC = 32 / CP;     // lanes sharing a column after the reduce-scatter
+  static constexpr int PADG = LPC == 1 ? 0 : 16 / LPC;  // pad between the source-lane groups (bank spread)
+  static constexpr int RED = 32 * (CP + 2) + (LPC - 1) * PADG;  // reduce-scatter transpose area
+  static constexpr int WSCR = RED + 3 * CP;  // per-warp scratch doubles (+ pivot row, coefficients, dump row)
 };
 
 // Sum D[p] over the 32 lanes; afterwards the lanes [col * 32 / CP, ...)
@@ -1278,13 +1281,13 @@ template <int CP> struct WTile {
 // broadcast follows each reduction).
 template <int CP>
 __device__ __forceinline__ double reduce_scatter_sm(const double (&D)[CP], double* red, int lane) {
-  constexpr int LPC = 32 / CP, SPL = 32 / LPC, LD = CP + 2;
-  double2* row = reinterpret_cast<double2*>(red + lane * LD);
+  constexpr int LPC = 32 / CP, SPL = 32 / LPC, LD = CP + 2, PADG = WTile<CP>::PADG;
+  double2* row = reinterpret_cast<double2*>(red + lane * LD + (lane / SPL) * PADG);
 #pragma unroll
   for (int p = 0; p < CP; p += 2) row[p / 2] = make_double2(D[p], D[p + 1]);
   __syncwarp();
   const int col = lane / LPC, part = lane % LPC;
-  const double* q = red + (size_t)(part * SPL) * LD + col;
+  const double* q = red + (size_t)(part * SPL) * LD + part * PADG + col;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
   for (int i = 0; i < SPL; i += 4) {
@@ -1294,7 +1297,8 @@ __device__ __forceinline__ double reduce_scatter_sm(const double (&D)[CP], doubl
     s3 += q[(i + 3) * LD];
   }
   double s = (s0 + s1) + (s2 + s3);
-  if (LPC == 2) s += __shfl_xor_sync(0xffffffffu, s, 1);
+#pragma unroll
+  for (int o = 1; o < LPC; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   return s;
 }
 
@@ -1322,7 +1326,7 @@ __device__ void wqr_factor(double (&a)[WTile<CP>::RT][CP], int nr, int c, double
   const int lane = threadIdx.x & 31;
   const int mycol = lane / LPC;
   double* red = wsm;
-  double* prow = wsm + 32 * (CP + 2);
+  double* prow = wsm + WTile<CP>::RED;
   double* csm = prow + CP;
   const int kb = nr < c ? nr : c;
   // all destinations are shared memory (see smem_addr)
@@ -1334,14 +1338,17 @@ __device__ void wqr_factor(double (&a)[WTile<CP>::RT][CP], int nr, int c, double
   for (int j = 0; j < kb; ++j) {
     const int lj = j & 31, tj = j >> 5;
     WQR_CLK(0);
+    {
+      // pivot row to shared memory without a divergent branch: the owner
+      // lane stores to prow, every other lane to the dump row behind csm
+      double2* pdst = reinterpret_cast<double2*>(lane == lj ? prow : csm + CP);
 #pragma unroll
-    for (int t = 0; t < RT; ++t)
-      if (tj == t) {
-        if (lane == lj) {
+      for (int t = 0; t < RT; ++t)
+        if (tj == t) {
 #pragma unroll
-          for (int p = 0; p < CP; p += 2) reinterpret_cast<double2*>(prow)[p / 2] = make_double2(a[t][p], a[t][p + 1]);
+          for (int p = 0; p < CP; p += 2) pdst[p / 2] = make_double2(a[t][p], a[t][p + 1]);
         }
-      }
+    }
     double xm[RT];
 #pragma unroll
     for (int t = 0; t < RT; ++t) xm[t] = (t * 32 + lane > j) ? a[t][0] : 0.0;
@@ -1413,7 +1420,7 @@ __device__ void wqr_apply(double (&y)[WTile<CP>::RT][CP], int nr, int kb, const 
   const int lane = threadIdx.x & 31;
   const int mycol = lane / LPC;
   double* red = wsm;
-  double* esm = wsm + 32 * (CP + 2);
+  double* esm = wsm + WTile<CP>::RED;
   // v and g are shared memory (see smem_addr)
   const uint32_t vstep = 8u * (uint32_t)ldv;
   uint32_t va = smem_addr(v) + 8u * lane + vstep * (uint32_t)(kb > 0 ? kb - 1 : 0);
@@ -1671,7 +1678,7 @@ struct WTopSmem {
 
 __host__ __device__ inline size_t wtop_doubles(int n0, int c, int CP, int nwarps, int chunk, bool pad) {
   const WTree tr = wtree_plan(n0, c, chunk);
-  return (size_t)(n0 | 1) * c + tr.total + 4 + (size_t)nwarps * (32 * (CP + 2) + 2 * CP) + (size_t)CP * (CP + 1) + CP + CP +
+  return (size_t)(n0 | 1) * c + tr.total + 4 + (size_t)nwarps * (CP == 16 ? WTile<16>::WSCR : WTile<32>::WSCR) + (size_t)CP * (CP + 1) + CP + CP +
          64 + (pad ? n0 : 0) + CP / 2 + 2;
 }
 
@@ -1773,6 +1780,452 @@ __global__ void __launch_bounds__(kThreads) basis_wtree_kernel(const BasisTarget
     pad_columns(T.u, n0, n0, q, r, T.state0, T.draw_offset, (uint64_t)T.normal_base, s.vpad, s.dots, s.red);
   PROF_MARK_CTA(6);
   PROF_MARK_CTA(7);
+}
+
+// ===========================================================================
+// Wide sketches (32 < c <= 64): a TEAM of 8 warps (one CTA) owns a row block
+// of 256 rows. Lane l of every warp holds rows {l, l + 32, ...} (8 rows);
+// the columns are dealt cyclically over the warps (warp w holds columns
+// w, w + 8, ...: 8 local columns, 64 doubles per lane). In step j the owner
+// warp of column j reduces its norm, publishes the masked column and
+// (ss, alpha) through shared memory (double-buffered: one CTA barrier per
+// step); then every warp forms its own dot products, reduce-scatters them
+// inside the warp and updates its own columns; only the owner shifts its
+// live columns one register to the left. The back-application needs no
+// team communication at all: warp w applies all reflectors to its own 8
+// columns of Y (wqr_apply<8>).
+// ===========================================================================
+constexpr int kTeamWarps = 8, kTeamCP = 8, kTeamRT = 8, kTeamRows = 256;
+
+struct TeamScratch {
+  double* xs;    // 2 x 256 masked pivot column
+  double* hdr;   // 2 x 2 (ss, alpha)
+  double* wscr;  // kTeamWarps x WTile<8>::WSCR
+};
+constexpr int kTeamScratchDoubles = 2 * kTeamRows + 4 + kTeamWarps * WTile<kTeamCP>::WSCR;
+
+__device__ __forceinline__ TeamScratch team_scratch(double* p) {
+  TeamScratch t;
+  t.xs = p;
+  t.hdr = p + 2 * kTeamRows;
+  t.wscr = t.hdr + 4;
+  return t;
+}
+
+// Team Householder QR of the block in registers (nr rows, c columns; warp w
+// local column p = global column 8 p + w). All destinations are shared
+// memory: reflector j to vout[row + j * ldv] (STOREV), g_j to gout[j], row j
+// of R to rout[j * rs + col * cs].
+template <bool STOREV>
+__device__ void tqr_factor(double (&a)[kTeamRT][kTeamCP], int nr, int c, double* vout, int ldv, double* gout,
+                           double* rout, int rs, int cs, const TeamScratch& ts) {
+  constexpr int RT = kTeamRT, CP = kTeamCP, NW = kTeamWarps, LPC = 32 / CP;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int mycol = lane / LPC;
+  double* wsm = ts.wscr + (size_t)warp * WTile<CP>::WSCR;
+  double* red = wsm;
+  double* prow = wsm + WTile<CP>::RED;
+  double* csm = prow + CP;
+  const int kb = nr < c ? nr : c;
+  const uint32_t ra0 = smem_addr(rout);
+  const uint32_t va0 = STOREV ? smem_addr(vout) + 8u * lane : 0u;
+  const uint32_t ga0 = STOREV ? smem_addr(gout) : 0u;
+  int sh = 0;  // live columns of this warp start at global column NW * sh + warp
+  for (int j = 0; j < kb; ++j) {
+    const int wj = j % NW, lj = j & 31, tj = j >> 5;
+    double* xsb = ts.xs + (j & 1) * kTeamRows;
+    double* hb = ts.hdr + (j & 1) * 2;
+    double xm[RT];
+    if (warp == wj) {
+      double part = 0.0, al = 0.0;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        xm[t] = (t * 32 + lane > j) ? a[t][0] : 0.0;
+        part = fma(xm[t], xm[t], part);
+        if (tj == t) al = a[t][0];
+        xsb[t * 32 + lane] = xm[t];
+      }
+      part = warp_sum(part);
+      al = __shfl_sync(0xffffffffu, al, lj);
+      if (lane == 0) {
+        hb[0] = part;
+        hb[1] = al;
+      }
+    }
+    __syncthreads();
+    if (warp != wj) {
+#pragma unroll
+      for (int t = 0; t < RT; ++t) xm[t] = xsb[t * 32 + lane];
+    }
+    const double ss = hb[0], alpha = hb[1];
+    {
+      double2* pdst = reinterpret_cast<double2*>(lane == lj ? prow : csm + CP);
+#pragma unroll
+      for (int t = 0; t < 2; ++t)  // j < 64: the pivot row is one of the first 64
+        if (tj == t) {
+#pragma unroll
+          for (int p = 0; p < CP; p += 2) pdst[p / 2] = make_double2(a[t][p], a[t][p + 1]);
+        }
+    }
+    double D[CP];
+#pragma unroll
+    for (int p = 0; p < CP; ++p) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int t = 0; t < RT; t += 2) {
+        s0 = fma(xm[t], a[t][p], s0);
+        s1 = fma(xm[t + 1], a[t + 1][p], s1);
+      }
+      D[p] = s0 + s1;
+    }
+    const double dtot = reduce_scatter_sm<CP>(D, red, lane);
+    double beta = alpha, ujj = 0.0, g = 0.0;
+    if (ss != 0.0) {
+      const double n2 = fma(alpha, alpha, ss);
+      const double rn = rsqrt(n2);
+      const double nrm = n2 * rn;
+      beta = -copysign(nrm, alpha);
+      ujj = alpha - beta;
+      g = rn * __drcp_rn(fabs(ujj));
+    }
+    const double arow = prow[mycol];
+    const double cl = g * fma(ujj, arow, dtot);
+    if (lane % LPC == 0) {
+      csm[mycol] = cl;
+      const int col = NW * (mycol + sh) + warp;
+      if (col < c) sts_f64(ra0 + 8u * (uint32_t)(j * rs + col * cs), col == j ? beta : arow - cl * ujj);
+    }
+    if (STOREV && warp == wj) {
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int row = t * 32 + lane;
+        if (row < nr) sts_f64(va0 + 8u * (uint32_t)(j * ldv) + 256u * t, row > j ? xm[t] : (row == j ? ujj : 0.0));
+      }
+      if (lane == 0) sts_f64(ga0 + 8u * j, g);
+    }
+    __syncwarp();
+    if (warp == wj) {
+#pragma unroll
+      for (int p = 0; p < CP; p += 2) {
+        const double2 e = reinterpret_cast<const double2*>(csm)[p / 2];
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+          if (p > 0) a[t][p - 1] = fma(-e.x, xm[t], a[t][p]);
+          a[t][p] = fma(-e.y, xm[t], a[t][p + 1]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < RT; ++t) a[t][CP - 1] = 0.0;
+      ++sh;
+    } else {
+#pragma unroll
+      for (int p = 0; p < CP; p += 2) {
+        const double2 e = reinterpret_cast<const double2*>(csm)[p / 2];
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+          a[t][p] = fma(-e.x, xm[t], a[t][p]);
+          a[t][p + 1] = fma(-e.y, xm[t], a[t][p + 1]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+// Register block of the team: element (row, global column NW p + w) from
+// src[row * rstride + col * cstride].
+__device__ __forceinline__ void team_load(double (&a)[kTeamRT][kTeamCP], const double* src, int64_t rstride,
+                                          int64_t cstride, int nr, int c) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int t = 0; t < kTeamRT; ++t) {
+    const int row = t * 32 + lane;
+#pragma unroll
+    for (int p = 0; p < kTeamCP; ++p) {
+      const int col = kTeamWarps * p + warp;
+      a[t][p] = (row < nr && col < c) ? src[row * rstride + col * cstride] : 0.0;
+    }
+  }
+}
+
+// Back-application of one team block: warp w applies the kb reflectors (vst,
+// ld ldv, shared memory) to columns [8 w, 8 w + 8) of Y. Input: the kb x q
+// matrix yin (ld ldyi), zero below; output rows to yout (ld ldyo).
+__device__ void team_apply(int nr, int kb, int q, const double* vst, int ldv, const double* gst, const double* yin,
+                           int64_t ldyi, double* yout, int64_t ldyo, const TeamScratch& ts) {
+  constexpr int RT = kTeamRT, CP = kTeamCP;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c0 = warp * CP;
+  if (c0 < q) {
+    double y[RT][CP];
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+      const int row = t * 32 + lane;
+#pragma unroll
+      for (int p = 0; p < CP; ++p) y[t][p] = (row < kb && c0 + p < q) ? yin[row + (int64_t)(c0 + p) * ldyi] : 0.0;
+    }
+    wqr_apply<CP>(y, nr, kb, vst, ldv, gst, ts.wscr + (size_t)warp * WTile<CP>::WSCR);
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+      const int row = t * 32 + lane;
+#pragma unroll
+      for (int p = 0; p < CP; ++p)
+        if (row < nr && c0 + p < q) yout[row + (int64_t)(c0 + p) * ldyo] = y[t][p];
+    }
+  }
+}
+
+// One-sided Jacobi on the rows of B (k x k, row-major, ld ldb, shared
+// memory), rotations not accumulated, all warps of the CTA: 4-lane groups
+// take the round-robin pairs of a round, one CTA barrier per round.
+template <int E>
+__device__ int jacobi_rows_cta(double* B, int ldb, int k, const unsigned short* pairs) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gid = warp * 8 + (lane >> 2), gl = lane & 3;
+  const int kk = (k + 1) & ~1;
+  const int npairs = kk / 2;
+  const double tol2 = 4.0 * DBL_EPSILON * DBL_EPSILON;
+  if (k < 2) return 0;
+  int sweep = 0;
+  for (; sweep < 80; ++sweep) {
+    int rotated = 0, big = 0;
+    for (int rd = 0; rd < kk - 1; ++rd) {
+      int p = 0, q = 0;
+      bool valid = gid < npairs;
+      if (valid) {
+        const unsigned short e = pairs[rd * npairs + gid];
+        p = e & 0xff;
+        q = e >> 8;
+        valid = q < k;
+      }
+      double* bp = B + (size_t)p * ldb;
+      double* bq = B + (size_t)q * ldb;
+      double x[E], y[E];
+      double app = 0.0, aqq = 0.0, apq = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int j = gl + 4 * e;
+        const bool in = valid && j < k;
+        x[e] = in ? bp[j] : 0.0;
+        y[e] = in ? bq[j] : 0.0;
+        app = fma(x[e], x[e], app);
+        aqq = fma(y[e], y[e], aqq);
+        apq = fma(x[e], y[e], apq);
+      }
+      app += __shfl_xor_sync(0xffffffffu, app, 1);
+      aqq += __shfl_xor_sync(0xffffffffu, aqq, 1);
+      apq += __shfl_xor_sync(0xffffffffu, apq, 1);
+      app += __shfl_xor_sync(0xffffffffu, app, 2);
+      aqq += __shfl_xor_sync(0xffffffffu, aqq, 2);
+      apq += __shfl_xor_sync(0xffffffffu, apq, 2);
+      const double a2 = apq * apq, pq = app * aqq;
+      if (valid && apq != 0.0 && a2 > tol2 * pq) {
+        double cs, sn;
+        jacobi_rotation(app, aqq, apq, &cs, &sn);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int j = gl + 4 * e;
+          if (j < k) {
+            bp[j] = cs * x[e] - sn * y[e];
+            bq[j] = sn * x[e] + cs * y[e];
+          }
+        }
+        rotated = 1;
+        if (a2 > 1e-13 * pq) big = 1;
+      }
+      __syncthreads();
+    }
+    const int any = __syncthreads_or(rotated);
+    if (!any) break;
+    if (!__syncthreads_or(big)) { ++sweep; break; }
+  }
+  __syncthreads();
+  return sweep;
+}
+
+struct WideTopSmem {
+  double* v;      // (m | 1) x c reflectors of the top block
+  double* g;      // c
+  double* rb;     // c x (c | 1): R (column-major), then R_1 / the Jacobi rows (row-major)
+  double* ytop;   // (c | 1) x r
+  double* scr;    // team scratch
+  double* sig;
+  double* dots;
+  double* red;
+  double* vpad;   // m (padding scratch, single-block targets)
+  int* perm;
+};
+
+__host__ __device__ inline size_t wide_top_doubles(int m, int c, int r, bool pad) {
+  return (size_t)(m | 1) * c + 1 + (c + 2) + (size_t)c * (c | 1) + 1 + (size_t)(c | 1) * r + 1 + kTeamScratchDoubles + c + c +
+         64 + (pad ? m : 0) + c / 2 + 4;
+}
+
+// Top of a wide target (or all of a single-block one): team QR of the top
+// block, R^T = Q_1 R_1, CTA Jacobi on the rows of R_1, rank decision,
+// back-application through the top block.
+__global__ void __launch_bounds__(kThreads) basis_wide_top_kernel(const BasisTarget* __restrict__ targets,
+                                                                 const int* __restrict__ list) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ BasisTarget T;
+  __shared__ unsigned short pairs[64 * 32];
+  stage_target(&T, &targets[list[blockIdx.x]]);
+  __syncthreads();
+  const int tid = threadIdx.x;
+  const int top = T.nlevels;
+  const QrLevel L = T.lv[top];
+  const int m = (int)L.n, c = T.c, r = T.r;
+  const int k = min(m, c);
+  const int ldv = m | 1, ldr = c | 1;
+  WideTopSmem s;
+  {
+    double* p = reinterpret_cast<double*>(smem_raw);
+    s.v = p; p += ((size_t)ldv * c + 1) & ~(size_t)1;
+    s.g = p; p += (c + 2) & ~1;
+    s.rb = p; p += ((size_t)c * ldr + 1) & ~(size_t)1;
+    s.ytop = p; p += ((size_t)ldr * r + 1) & ~(size_t)1;
+    s.scr = p; p += kTeamScratchDoubles;
+    s.sig = p; p += c;
+    s.dots = p; p += c;
+    s.red = p; p += 64;
+    s.vpad = p; p += top == 0 ? m : 0;
+    s.perm = reinterpret_cast<int*>(p);
+  }
+  const TeamScratch ts = team_scratch(s.scr);
+  PROF_MARK_CTA(8);
+  for (int i = tid; i < c * ldr; i += blockDim.x) s.rb[i] = 0.0;
+  build_pairs(pairs, (k + 1) & ~1);
+  __syncthreads();
+  {
+    double a[kTeamRT][kTeamCP];
+    team_load(a, L.a, 1, L.n, m, c);
+    tqr_factor<true>(a, m, c, s.v, ldv, s.g, s.rb, 1, ldr, ts);  // R(j, col) at rb[j + col * ldr]
+  }
+  PROF_MARK_CTA(9);
+  {
+    // second QR on R^T (c x k): element (row, col) = R(col, row); R_1 (k x k) row-major over the same storage
+    double a[kTeamRT][kTeamCP];
+    team_load(a, s.rb, ldr, 1, c, k);
+    __syncthreads();
+    for (int i = tid; i < c * ldr; i += blockDim.x) s.rb[i] = 0.0;
+    __syncthreads();
+    tqr_factor<false>(a, c, k, nullptr, 0, nullptr, s.rb, ldr, 1, ts);  // R_1(j, col) at rb[j * ldr + col]
+  }
+  const int sweeps = jacobi_rows_cta<16>(s.rb, ldr, k, pairs);
+  PROF_MARK_CTA(10);
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int i = warp; i < k; i += kWarps) {
+    double ss = 0.0;
+    for (int j = lane; j < k; j += 32) ss += s.rb[(size_t)i * ldr + j] * s.rb[(size_t)i * ldr + j];
+    ss = warp_sum(ss);
+    if (lane == 0) s.sig[i] = sqrt(ss);
+  }
+  __syncthreads();
+  for (int i = tid; i < k; i += blockDim.x) {
+    int rank = 0;
+    for (int j = 0; j < k; ++j) rank += (s.sig[j] > s.sig[i]) || (s.sig[j] == s.sig[i] && j < i);
+    s.perm[rank] = i;
+  }
+  __syncthreads();
+  const double smax = k > 0 ? s.sig[s.perm[0]] : 0.0;
+  const double tol = (double)srtt_dev::max64(T.n, (int64_t)c) * DBL_EPSILON * smax;
+  int nrank = 0;
+  for (int i = 0; i < k; ++i) nrank += s.sig[i] > tol;
+  const int q = min(nrank, r);
+  if (tid == 0) {
+    T.info[0] = q;
+    T.info[1] = nrank;
+    T.info[2] = sweeps;
+  }
+  if (T.sv)
+    for (int i = tid; i < k; i += blockDim.x) T.sv[i] = s.sig[s.perm[i]];
+  for (int idx = tid; idx < k * q; idx += blockDim.x) {
+    const int i = idx % k, col = idx / k;
+    const int src = s.perm[col];
+    s.ytop[i + (size_t)col * ldr] = s.rb[(size_t)src * ldr + i] / s.sig[src];
+  }
+  __syncthreads();
+  PROF_MARK_CTA(11);
+  team_apply(m, k, q, s.v, ldv, s.g, s.ytop, ldr, top == 0 ? T.u : L.y, top == 0 ? T.n : L.n, ts);
+  __syncthreads();
+  PROF_MARK_CTA(12);
+  if (top == 0 && q < r)
+    pad_columns(T.u, m, m, q, r, T.state0, T.draw_offset, (uint64_t)T.normal_base, s.vpad, s.dots, s.red);
+  PROF_MARK_CTA(13);
+}
+
+__host__ __device__ inline size_t wide_level_doubles(int mb, int c) {
+  return (size_t)(mb | 1) * c + 1 + (c + 2) + (size_t)c * (c | 1) + 1 + kTeamScratchDoubles + 4;
+}
+
+// One level below the top of a wide target: CTA (target, b) factors row
+// block b in place (reflectors u_j whole, g in L.tau) and stacks its R.
+__global__ void __launch_bounds__(kThreads) basis_wide_factor_kernel(const BasisTarget* __restrict__ targets,
+                                                                    const int2* __restrict__ map, int level) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ BasisTarget T;
+  const int2 tb = map[blockIdx.x];
+  stage_target(&T, &targets[tb.x]);
+  __syncthreads();
+  const QrLevel L = T.lv[level];
+  const QrLevel P = T.lv[level + 1];
+  const int b = tb.y, c = T.c;
+  const int64_t r0 = (int64_t)b * L.blk_rows;
+  const int mb = (int)srtt_dev::min64(L.blk_rows, L.n - r0);
+  const int kb = min(mb, c);
+  const int ldv = mb | 1, ldr = c | 1;
+  double* p = reinterpret_cast<double*>(smem_raw);
+  double* vst = p; p += ((size_t)ldv * c + 1) & ~(size_t)1;
+  double* gst = p; p += (c + 2) & ~1;
+  double* rst = p; p += ((size_t)c * ldr + 1) & ~(size_t)1;
+  const TeamScratch ts = team_scratch(p);
+  for (int i = threadIdx.x; i < c * ldr; i += blockDim.x) rst[i] = 0.0;
+  for (int i = threadIdx.x; i < c; i += blockDim.x) gst[i] = 0.0;
+  __syncthreads();
+  {
+    double a[kTeamRT][kTeamCP];
+    team_load(a, L.a + r0, 1, L.n, mb, c);
+    tqr_factor<true>(a, mb, c, vst, ldv, gst, rst, 1, ldr, ts);
+  }
+  for (int idx = threadIdx.x; idx < mb * kb; idx += blockDim.x) {
+    const int i = idx % mb, j = idx / mb;
+    L.a[(int64_t)j * L.n + r0 + i] = vst[i + (size_t)j * ldv];
+  }
+  for (int j = threadIdx.x; j < c; j += blockDim.x) L.tau[(int64_t)b * c + j] = gst[j];
+  for (int idx = threadIdx.x; idx < c * c; idx += blockDim.x) {
+    const int i = idx % c, j = idx / c;
+    P.a[(int64_t)j * P.n + (int64_t)b * c + i] = i < kb ? rst[i + (size_t)j * ldr] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) basis_wide_apply_kernel(const BasisTarget* __restrict__ targets,
+                                                                   const int2* __restrict__ map, int level) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ BasisTarget T;
+  const int2 tb = map[blockIdx.x];
+  stage_target(&T, &targets[tb.x]);
+  __syncthreads();
+  const QrLevel L = T.lv[level];
+  const QrLevel P = T.lv[level + 1];
+  const int b = tb.y, c = T.c;
+  const int q = T.info[0];
+  const int64_t r0 = (int64_t)b * L.blk_rows;
+  const int mb = (int)srtt_dev::min64(L.blk_rows, L.n - r0);
+  const int kb = min(mb, c);
+  const int ldv = mb | 1;
+  double* p = reinterpret_cast<double*>(smem_raw);
+  double* vst = p; p += ((size_t)ldv * c + 1) & ~(size_t)1;
+  double* gst = p; p += (c + 2) & ~1;
+  p += ((size_t)c * (c | 1) + 1) & ~(size_t)1;
+  const TeamScratch ts = team_scratch(p);
+  for (int idx = threadIdx.x; idx < mb * kb; idx += blockDim.x) {
+    const int i = idx % mb, j = idx / mb;
+    vst[i + (size_t)j * ldv] = L.a[(int64_t)j * L.n + r0 + i];
+  }
+  for (int j = threadIdx.x; j < c; j += blockDim.x) gst[j] = L.tau[(int64_t)b * c + j];
+  __syncthreads();
+  team_apply(mb, kb, q, vst, ldv, gst, P.y + (int64_t)b * c, P.n, L.y + r0, L.n, ts);
 }
 
 constexpr int kWfThreads = 128;  // factor / apply CTAs of tall targets: one warp per SM sub-partition
@@ -1964,14 +2417,14 @@ int64_t srtt_wtree_persist_doubles(int rows, int c) {
 size_t srtt_wtree_factor_smem(int rows, int c) {
   const int cp = srtt_wtree_cp(c);
   const WTree tr = wtree_plan(rows, c, srtt_wtree_chunk(cp));
-  return ((size_t)tr.persist + 2 + (size_t)(kWfThreads / 32) * ((32 * (cp + 2) + 2 * cp) + (size_t)(srtt_wtree_chunk(cp) + 1) * c)) * sizeof(double);
+  return ((size_t)tr.persist + 2 + (size_t)(kWfThreads / 32) * ((cp == 16 ? WTile<16>::WSCR : WTile<32>::WSCR) + (size_t)(srtt_wtree_chunk(cp) + 1) * c)) * sizeof(double);
 }
 
 size_t srtt_wtree_apply_smem(int rows, int c) {
   const int cp = srtt_wtree_cp(c);
   const int chunk = srtt_wtree_chunk(cp);
   const WTree tr = wtree_plan(rows, c, chunk);
-  return ((size_t)tr.total + 2 + (size_t)(kWfThreads / 32) * ((32 * (cp + 2) + 2 * cp) + (size_t)(chunk + 1) * c)) *
+  return ((size_t)tr.total + 2 + (size_t)(kWfThreads / 32) * ((cp == 16 ? WTile<16>::WSCR : WTile<32>::WSCR) + (size_t)(chunk + 1) * c)) *
          sizeof(double);
 }
 
@@ -2011,6 +2464,36 @@ cudaError_t srtt_launch_wtree_apply(int cp, const BasisTarget* d_targets, const 
     SRTT_ENSURE_SMEM((basis_wapply_kernel<32>), smem);
     basis_wapply_kernel<32><<<nctas, kWfThreads, smem, stream>>>(d_targets, d_map);
   }
+  return cudaGetLastError();
+}
+
+
+// ---- wide register path (32 < c <= 64) ---------------------------------------
+int srtt_wide_block_rows() { return kTeamRows; }
+size_t srtt_wide_top_smem(int m, int c, int r, bool pad) { return wide_top_doubles(m, c, r, pad) * sizeof(double) + 64; }
+size_t srtt_wide_level_smem(int mb, int c) { return wide_level_doubles(mb, c) * sizeof(double) + 64; }
+
+cudaError_t srtt_launch_wide_top(const BasisTarget* d_targets, const int* d_list, int n, size_t smem,
+                                 cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  SRTT_ENSURE_SMEM(basis_wide_top_kernel, smem);
+  basis_wide_top_kernel<<<n, kThreads, smem, stream>>>(d_targets, d_list);
+  return cudaGetLastError();
+}
+
+cudaError_t srtt_launch_wide_factor(const BasisTarget* d_targets, const int2* d_map, int level, int nctas, size_t smem,
+                                    cudaStream_t stream) {
+  if (nctas <= 0) return cudaSuccess;
+  SRTT_ENSURE_SMEM(basis_wide_factor_kernel, smem);
+  basis_wide_factor_kernel<<<nctas, kThreads, smem, stream>>>(d_targets, d_map, level);
+  return cudaGetLastError();
+}
+
+cudaError_t srtt_launch_wide_apply(const BasisTarget* d_targets, const int2* d_map, int level, int nctas, size_t smem,
+                                   cudaStream_t stream) {
+  if (nctas <= 0) return cudaSuccess;
+  SRTT_ENSURE_SMEM(basis_wide_apply_kernel, smem);
+  basis_wide_apply_kernel<<<nctas, kThreads, smem, stream>>>(d_targets, d_map, level);
   return cudaGetLastError();
 }
 
