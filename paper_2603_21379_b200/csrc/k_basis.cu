@@ -1462,9 +1462,12 @@ __device__ void wqr_apply(double (&y)[WTile<CP>::RT][CP], int nr, int kb, const 
 
 // One-sided Jacobi on the rows of B (k x k, row-major, ld ldb) by one warp,
 // rows resident in registers (circle method as jacobi_rows_reg), rotations
-// not accumulated. A sweep whose largest rotated pair had
-// |cos(angle)| <= 3e-7 is the last one (quadratic convergence: the
-// remaining couplings are below 1e-13 relative).
+// not accumulated. A sweep in which every rotated pair had
+// |cos(angle between the rows)| <= 3e-7 AND a rotation angle below 1e-6 is
+// the last one (the couplings left behind are products of two such small
+// numbers; pairs inside a cluster of equal singular values rotate by large
+// angles whatever their coupling, so they keep the sweeps going until no
+// pair exceeds the 2 eps threshold).
 template <int G, int E>
 __device__ int jacobi_rows_nov(double* B, int ldb, int k) {
   const int lane = threadIdx.x & 31;
@@ -1511,7 +1514,7 @@ __device__ int jacobi_rows_nov(double* B, int ldb, int k) {
             bb[e] = sn * x + cs * y;
           }
           rotated = 1;
-          if (a2 > 1e-13 * pq) big = 1;
+          if (a2 > 1e-13 * pq || fabs(sn) > 1e-6) big = 1;
         }
         if (np > 1) {
           // advance: top[0] stays, top[1] <- bot[0], top[g] <- top[g-1],
@@ -2032,7 +2035,7 @@ __device__ int jacobi_rows_cta(double* B, int ldb, int k, const unsigned short* 
           }
         }
         rotated = 1;
-        if (a2 > 1e-13 * pq) big = 1;
+        if (a2 > 1e-13 * pq || fabs(sn) > 1e-6) big = 1;
       }
       __syncthreads();
     }
