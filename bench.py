@@ -5,19 +5,21 @@ One "step" = one full Sub-R-HOSVD (or Sub-R-RtL-HT for c4) of the config's
 synthetic tensor: host index sampling + K1 sketch + K2 basis + K3 core pass,
 X resident in HBM (``value``); ``e2e`` times the same call through the C-ABI
 with X in pinned HOST memory (H2D of X and D2H of the factors/core inside
-the timed region).  Default workload: BASELINE.json configs[1] (order-5
-Tucker 40^5, 1.02e8 entries, 819 MB > L2, so no L2 flush is needed).
+the timed region).  Default workload: BASELINE.json configs[4] (C5, order-3
+Tucker 2048^3, 8.6e9 entries, 68.7 GB: the largest configuration that fits
+one 180 GB B200; inputs far larger than L2, so no flush is needed).
+``--config`` selects c1-c5 (or the added sketch-heavy variants).
 
 ``--impl reference`` times the CPU restatement of the reference (oracle/,
-numpy + OpenBLAS on all host cores; the reference itself needs Eigen, absent
-in this image) on the same config.
+numpy + OpenBLAS on the host cores under the reference's own policies; the
+reference itself needs Eigen, absent in this image) on the same config and
+the same X bits (a bounded leading slab for c5).
 
-Multi-GPU (torchrun): by default each rank decomposes its own replica
-(seed = rank), weak scaling, no data-path collective; time = max over ranks.
-``--mode sharded`` instead decomposes ONE tensor whose last mode is split
-into per-rank slabs of the config's size (global last extent = N x the
-config's), through paper_2603_21379_b200.sharded (partial sketches ->
-NCCL allreduce/allgather -> bases -> partial core -> allreduce).
+Multi-GPU (torchrun, ``--mode auto``): ONE global tensor per step over the
+ranks (strong scaling) through the fused NCCL C-ABI: slab-sharded for c5
+(each rank holds its last-mode slab), replicated with modes / nodes assigned
+to ranks for the configs that fit per GPU. ``--mode replicas`` runs
+independent decompositions per rank instead (weak scaling).
 """
 from __future__ import annotations
 
