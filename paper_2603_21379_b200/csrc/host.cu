@@ -56,6 +56,9 @@ size_t srtt_wide_level_smem(int mb, int c);
 cudaError_t srtt_launch_wide_top(const BasisTarget*, const int*, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_wide_factor(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_wide_apply(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
+size_t srtt_basis_generic_smem(int c, int r);
+int64_t srtt_basis_generic_doubles(int64_t n, int c);
+cudaError_t srtt_launch_basis_generic(const BasisTarget*, const int*, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_tsqr_factor(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_tsqr_apply(const BasisTarget*, const int2*, int, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_pad(const BasisTarget*, int, double*, int64_t, cudaStream_t);
@@ -479,6 +482,16 @@ BasisPlan plan_basis(int64_t n, int c, int r) {
   b.r = r;
   if (plan_basis_wtree(b)) return b;
   if (plan_basis_wide(b)) return b;
+  if (c > 64) {
+    // generic kernel (k_basis.cu): one CTA per target on global memory
+    if (c > SRTT_MAX_SKETCH_COLS) invalid("range_basis_of_sketch: sketch too wide for the B200 basis kernels");
+    b.kind = 3;
+    b.nlevels = 0;
+    b.lv_n[0] = n;
+    b.lv_nblk[0] = 1;
+    b.lv_blk[0] = (int)std::min<int64_t>(n, INT32_MAX);
+    return b;
+  }
   int tmax = top_max_rows(c, r);
   int blk = level_block_rows(c);
   if (tmax < c) invalid("range_basis_of_sketch: sketch too wide for the B200 basis kernel");
@@ -537,6 +550,10 @@ BasisBuffers layout_basis(Layout& L, const BasisPlan& p) {
     B.vup_stride = srtt_wtree_persist_doubles(p.lv_blk[0], p.c);
     B.vup = L.take(sizeof(double) * (size_t)B.vup_stride * p.lv_nblk[0]);
   }
+  if (p.kind == 3) {
+    B.vup_stride = srtt_basis_generic_doubles(p.n, p.c);
+    B.vup = L.take(sizeof(double) * (size_t)B.vup_stride);
+  }
   return B;
 }
 
@@ -564,7 +581,7 @@ BasisTarget fill_basis(const BasisPlan& p, const BasisBuffers& B, char* ws, doub
   T.draw_offset = draw_offset;
   T.normal_base = normal_base;
   T.kind = p.kind;
-  if (p.kind == 1 && p.nlevels == 1) {
+  if ((p.kind == 1 && p.nlevels == 1) || p.kind == 3) {
     T.vup = reinterpret_cast<double*>(ws + B.vup);
     T.vup_stride = B.vup_stride;
   }
@@ -592,6 +609,8 @@ struct BasisLists {
   int w_ctas[2] = {};
   // wide register path (kind 2): single-block targets, tall ones, and the
   // per-level (target, block) maps of the tall ones
+  std::vector<int> generic;  // kind 3 (c > 64): one CTA each, global memory
+  size_t off_generic = 0;
   std::vector<int> x_small, x_tall;
   size_t off_x_small = 0, off_x_tall = 0, off_x_map[SRTT_MAX_QR_LEVELS] = {};
   int x_ctas[SRTT_MAX_QR_LEVELS] = {};
@@ -620,6 +639,9 @@ BasisLists make_basis_lists(const std::vector<BasisTarget>& targets, Blob& blob)
       L.w_ctas[v] = (int)map.size();
     }
   }
+  for (int i = 0; i < (int)targets.size(); ++i)
+    if (targets[i].kind == 3) L.generic.push_back(i);
+  if (!L.generic.empty()) L.off_generic = blob.add(L.generic.data(), sizeof(int) * L.generic.size());
   for (int i = 0; i < (int)targets.size(); ++i)
     if (targets[i].kind == 2) (targets[i].nlevels == 0 ? L.x_small : L.x_tall).push_back(i);
   if (!L.x_small.empty()) L.off_x_small = blob.add(L.x_small.data(), sizeof(int) * L.x_small.size());
@@ -706,6 +728,13 @@ int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const 
       smem = std::max(smem, srtt_basis_small_smem((int)targets[i].n, targets[i].c, targets[i].r));
     CK(srtt_launch_basis_small(v, dT, reinterpret_cast<const int*>(dblob + lists.off_small_v[v]),
                                (int)lists.small_v[v].size(), smem, small_stream ? small_stream : h->stream));
+    ++launches;
+  }
+  if (!lists.generic.empty()) {
+    size_t smem = 0;
+    for (int i : lists.generic) smem = std::max(smem, srtt_basis_generic_smem(targets[i].c, targets[i].r));
+    CK(srtt_launch_basis_generic(dT, reinterpret_cast<const int*>(dblob + lists.off_generic), (int)lists.generic.size(),
+                                 smem, small_stream ? small_stream : h->stream));
     ++launches;
   }
   if (!lists.x_small.empty()) {
@@ -1639,7 +1668,7 @@ void run_sub_r_hosvd(srtt_handle* h, const double* x_in, int x_on_device, int d,
   }
   for (int k = 0; k < d; ++k)
     if (ranks[k] + p > SRTT_MAX_SKETCH_COLS)
-      invalid("sub_r_hosvd: rank + oversampling above 64 is not supported by the B200 basis kernel");
+      invalid("sub_r_hosvd: rank + oversampling above 256 is not supported by the B200 basis kernels");
   check_core_ranks(d, ranks.data(), "sub_r_hosvd");
   std::vector<std::string> warnings;
   if (p < 4) warnings.push_back("oversampling below the recommended minimum of 4");
@@ -2118,7 +2147,9 @@ void run_sub_r_rtl_ht(srtt_handle* h, const double* x_in, int x_on_device, int d
   }
   for (int i = 1; i < nn; ++i)
     if (ranks[i] + p > SRTT_MAX_SKETCH_COLS)
-      invalid("sub_r_rtl_ht: rank + oversampling above 64 is not supported by the B200 basis kernel");
+      invalid("sub_r_rtl_ht: rank + oversampling above 256 is not supported by the B200 basis kernels");
+  for (int i = 1; i < nn; ++i)
+    if (ranks[i] > 64) invalid("sub_r_rtl_ht: node ranks above 64 are not supported by the B200 transfer kernel");
   {
     const int64_t rr[2] = {ranks[tr.left[0]], ranks[tr.right[0]]};
     check_core_ranks(2, rr, "sub_r_rtl_ht");
@@ -2555,7 +2586,7 @@ int srtt_range_basis_of_sketch(srtt_handle* h, const double* z, int32_t z_on_dev
                                int32_t out_on_device) {
   return guarded([&] {
     if (rank < 1 || rank > c) invalid("range_basis_of_sketch: rank out of range");
-    if (c > SRTT_MAX_SKETCH_COLS) invalid("range_basis_of_sketch: more than 64 sketch columns unsupported");
+    if (c > SRTT_MAX_SKETCH_COLS) invalid("range_basis_of_sketch: more than 256 sketch columns unsupported");
     if (n < 1) invalid("range_basis_of_sketch: empty sketch");
     DeviceGuard g(h->device);
     CompBufs B;
@@ -2713,7 +2744,7 @@ void validate_tucker(int d, const std::vector<int64_t>& dims, const std::vector<
       invalid("sub_r_hosvd: samples below rank + oversampling in mode " + std::to_string(k));
     if (samples[k] > N / dims[k]) invalid("sub_r_hosvd: more samples than fibers in mode " + std::to_string(k));
     if (ranks[k] + p > SRTT_MAX_SKETCH_COLS)
-      invalid("sub_r_hosvd: rank + oversampling above 64 is not supported by the B200 basis kernel");
+      invalid("sub_r_hosvd: rank + oversampling above 256 is not supported by the B200 basis kernels");
   }
 }
 

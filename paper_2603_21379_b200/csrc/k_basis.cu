@@ -2231,6 +2231,84 @@ __global__ void __launch_bounds__(kThreads) basis_wide_apply_kernel(const BasisT
   team_apply(mb, kb, q, vst, ldv, gst, P.y + (int64_t)b * c, P.n, L.y + r0, L.n, ts);
 }
 
+// ===========================================================================
+// Generic basis kernel (c > 64, up to SRTT_MAX_SKETCH_COLS): the reference
+// bounds ranks only by the extents (tucker.hpp:184-197), so sketches wider
+// than the register kernels cover still get a basis: one CTA per target,
+// everything in global memory (Z factored in place; R rows, the rotation
+// accumulator and tau in T.vup), the shared-memory algorithms of the top
+// kernel (QRCP Householder, 4-lane Jacobi with accumulated rotations, warp
+// back-application). Slow (no TSQR, no registers) but exact to the same
+// tolerances; it exists for contract parity, not for the BASELINE configs.
+// ===========================================================================
+__global__ void __launch_bounds__(kThreads) basis_generic_kernel(const BasisTarget* __restrict__ targets,
+                                                                const int* __restrict__ list) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ BasisTarget T;
+  stage_target(&T, &targets[list[blockIdx.x]]);
+  __syncthreads();
+  const int64_t n = T.n;
+  const int m = (int)n, c = T.c, r = T.r;
+  const int k = min(m, c);
+  const int kk = (k + 1) & ~1;
+  double* vn = reinterpret_cast<double*>(smem_raw);
+  double* sig = vn + c;
+  double* dots = sig + c;
+  double* red = dots + c;
+  double* scal_beta = red + 64;
+  int* perm = reinterpret_cast<int*>(scal_beta + 2);
+  unsigned short* pairs = reinterpret_cast<unsigned short*>(perm + c + (c & 1));
+  double* A = T.lv[0].a;
+  double* B = T.vup;
+  double* V = B + (size_t)k * c;
+  double* tau = V + (size_t)k * k;
+  double* vpad = tau + c;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  householder_qr(A, m, c, m, tau, scal_beta, vn);
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < k * c; idx += blockDim.x) {
+    const int i = idx / c, j = idx % c;
+    B[idx] = (j >= i) ? A[(size_t)j * n + i] : 0.0;
+  }
+  for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) V[idx] = (idx % k == idx / k) ? 1.0 : 0.0;
+  build_pairs(pairs, kk);
+  __syncthreads();
+  const int sweeps = jacobi_rows_g4(B, c, k, c, V, k, pairs);
+  for (int i = warp; i < k; i += kWarps) {
+    double ss = 0.0;
+    for (int j = lane; j < c; j += 32) ss += B[(size_t)i * c + j] * B[(size_t)i * c + j];
+    ss = warp_sum(ss);
+    if (lane == 0) sig[i] = sqrt(ss);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    int rank = 0;
+    for (int j = 0; j < k; ++j) rank += (sig[j] > sig[i]) || (sig[j] == sig[i] && j < i);
+    perm[rank] = i;
+  }
+  __syncthreads();
+  const double smax = k > 0 ? sig[perm[0]] : 0.0;
+  const double tol = (double)srtt_dev::max64(n, (int64_t)c) * DBL_EPSILON * smax;
+  int nrank = 0;
+  for (int i = 0; i < k; ++i) nrank += sig[i] > tol;
+  const int q = min(nrank, r);
+  if (threadIdx.x == 0) {
+    T.info[0] = q;
+    T.info[1] = nrank;
+    T.info[2] = sweeps;
+  }
+  if (T.sv)
+    for (int i = threadIdx.x; i < k; i += blockDim.x) T.sv[i] = sig[perm[i]];
+  for (int64_t idx = threadIdx.x; idx < n * q; idx += blockDim.x) {
+    const int64_t i = idx % n, col = idx / n;
+    T.u[idx] = (i < k) ? V[(size_t)perm[col] * k + i] : 0.0;
+  }
+  __syncthreads();
+  for (int col = warp; col < q; col += kWarps) apply_q_warp(A, m, k, m, tau, T.u + (size_t)col * n);
+  __syncthreads();
+  if (q < r) pad_columns(T.u, n, n, q, r, T.state0, T.draw_offset, (uint64_t)T.normal_base, vpad, dots, red);
+}
+
 constexpr int kWfThreads = 128;  // factor / apply CTAs of tall targets: one warp per SM sub-partition
 
 // Tall targets, level 0: CTA (target, i) factors rows [i * rpc, ...) of Z in
@@ -2470,6 +2548,27 @@ cudaError_t srtt_launch_wtree_apply(int cp, const BasisTarget* d_targets, const 
   return cudaGetLastError();
 }
 
+
+// ---- generic kernel (c > 64) ----------------------------------------------------
+size_t srtt_basis_generic_smem(int c, int r) {
+  (void)r;
+  const int kk = (c + 1) & ~1;
+  return (size_t)(3 * c + 64 + 2) * sizeof(double) + (size_t)(c + 2) * sizeof(int) +
+         (size_t)(kk - 1) * (kk / 2) * sizeof(unsigned short) + 64;
+}
+
+int64_t srtt_basis_generic_doubles(int64_t n, int c) {
+  const int64_t k = n < c ? n : c;
+  return k * c + k * k + c + n + 8;
+}
+
+cudaError_t srtt_launch_basis_generic(const BasisTarget* d_targets, const int* d_list, int n, size_t smem,
+                                      cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  SRTT_ENSURE_SMEM(basis_generic_kernel, smem);
+  basis_generic_kernel<<<n, kThreads, smem, stream>>>(d_targets, d_list);
+  return cudaGetLastError();
+}
 
 // ---- wide register path (32 < c <= 64) ---------------------------------------
 int srtt_wide_block_rows() { return kTeamRows; }

@@ -43,7 +43,8 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
   }
   __syncthreads();
 
-  const int c = T.c;
+  const int ctot = T.c;
+  const int cw = ctot < CMAX ? ctot : CMAX;  // columns per pass (more than CMAX columns: several passes)
   const int RT = T.row_tile;
   const int JS = kThreads / RT;
   const int il = tid % RT;
@@ -59,9 +60,9 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
   const int64_t i = rt * RT + il;
   const bool active = (js < JS) && (i < T.rows);
 
-  double* om = reinterpret_cast<double*>(smem_raw);         // kChunk x c
-  int64_t* base = reinterpret_cast<int64_t*>(om + kChunk * c);  // kChunk
-  double* red = reinterpret_cast<double*>(base + kChunk);    // kThreads x c
+  double* om = reinterpret_cast<double*>(smem_raw);         // kChunk x cw
+  int64_t* base = reinterpret_cast<int64_t*>(om + kChunk * cw);  // kChunk
+  double* red = reinterpret_cast<double*>(base + kChunk);    // kThreads x cw
 
   // Row offset of row i in the flat tensor: mixed-radix decode over S's
   // modes, first mode fastest (unfolding.hpp:81-108 row odometer).
@@ -75,14 +76,17 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
     }
   }
 
-  double acc[CMAX];
-#pragma unroll
-  for (int cc = 0; cc < CMAX; ++cc) acc[cc] = 0.0;
-
   const double* __restrict__ x = T.x;
   // flat-range sharding: only [flo, fhi) of the global flat index is local
   const int64_t flo = T.flat_lo, fhi = T.flat_hi;
   const bool ranged = fhi > 0;
+  // Sketches wider than CMAX columns (r + p > 64) take one pass over the
+  // sampled fibres per window of CMAX columns [c0, c0 + c).
+  for (int c0 = 0; c0 < ctot; c0 += CMAX) {
+  const int c = ctot - c0 < CMAX ? ctot - c0 : CMAX;
+  double acc[CMAX];
+#pragma unroll
+  for (int cc = 0; cc < CMAX; ++cc) acc[cc] = 0.0;
   for (int64_t j0 = jbeg; j0 < jend; j0 += kChunk) {
     const int jn = (int)srtt_dev::min64(kChunk, jend - j0);
     __syncthreads();
@@ -90,7 +94,7 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
     // (column-major gaussian_matrix fill, sampling.hpp:74-75).
     for (int idx = tid; idx < jn * c; idx += kThreads) {
       const int jl = idx / c, cc = idx - jl * c;
-      const uint64_t t = (uint64_t)(j0 + jl) + (uint64_t)cc * (uint64_t)T.w;
+      const uint64_t t = (uint64_t)(j0 + jl) + (uint64_t)(cc + c0) * (uint64_t)T.w;
       om[jl * c + cc] = T.omega ? T.omega[t] : srtt_dev::normal_at(T.state0, T.draw_offset, t, T.flags);
     }
     // Fibre base offsets: decode the sampled column over the complement
@@ -162,10 +166,11 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
     double s = 0.0;
     for (int g = 0; g < JS; ++g) s += red[(g * RT + rl) * c + cc];
     if (T.fsplit > 1)
-      T.zpart[((int64_t)fchunk * c + cc) * T.rows + row] = s;
+      T.zpart[((int64_t)fchunk * ctot + cc + c0) * T.rows + row] = s;
     else
-      T.z[row + (int64_t)cc * ldz] = s;
+      T.z[row + (int64_t)(cc + c0) * ldz] = s;
   }
+  }  // column windows
 }
 
 // ---------------------------------------------------------------------------
@@ -484,7 +489,7 @@ int srtt_sketch_threads() { return kThreads; }
 cudaError_t srtt_launch_sketch(const SketchTarget* d_targets, int ntargets, int64_t total_ctas,
                                int cmax, cudaStream_t stream) {
   if (total_ctas <= 0) return cudaSuccess;
-  const size_t smem = srtt_sketch_smem_bytes(cmax);
+  const size_t smem = srtt_sketch_smem_bytes(cmax < 64 ? cmax : 64);
   if (cmax <= 16) {
     SRTT_ENSURE_SMEM((sketch_kernel<16>), smem);
     sketch_kernel<16><<<(unsigned)total_ctas, kThreads, smem, stream>>>(d_targets, ntargets);

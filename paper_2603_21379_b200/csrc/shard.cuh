@@ -466,7 +466,9 @@ struct HtShard {
     }
     for (int i = 1; i < nn; ++i)
       if (ranks[i] + p > SRTT_MAX_SKETCH_COLS)
-        invalid("sub_r_rtl_ht: rank + oversampling above 64 is not supported by the B200 basis kernel");
+        invalid("sub_r_rtl_ht: rank + oversampling above 256 is not supported by the B200 basis kernels");
+  for (int i = 1; i < nn; ++i)
+    if (ranks[i] > 64) invalid("sub_r_rtl_ht: node ranks above 64 are not supported by the B200 transfer kernel");
     {
       const int64_t rr[2] = {ranks[tr.left[0]], ranks[tr.right[0]]};
       check_core_ranks(2, rr, "sub_r_rtl_ht");

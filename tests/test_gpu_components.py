@@ -46,7 +46,8 @@ def test_fiber_gathers_bitwise(handle, dims):
 @pytest.mark.parametrize("dims,modes,w,c", [((128, 128, 128), [0], 52, 13), ((128, 128, 128), [2], 52, 13),
                                             ((40,) * 5, [3], 44, 11), ((12,) * 6, [0, 1, 2], 60, 15),
                                             ((12,) * 6, [3, 4], 60, 15), ((9, 8, 7, 6), [1, 3], 25, 20),
-                                            ((30, 20, 10), [1], 200, 42),
+                                            ((30, 20, 10), [1], 200, 42), ((30, 20, 10), [1], 250, 100),
+                                            ((64, 80, 90), [0], 3000, 80),
                                             # many fibres: split over CTAs (fixed-order partial sums)
                                             ((64, 80, 90), [0], 6000, 42), ((64, 80, 90), [1], 5000, 13),
                                             ((63, 81, 90), [0], 6000, 21), ((7, 9, 5, 2000), [0, 1, 2], 1500, 15),
@@ -69,7 +70,8 @@ def test_fused_sketch_matches_oracle(handle, dims, modes, w, c):
 
 @pytest.mark.parametrize("n,c,r,decay", [(40, 11, 6, 6), (128, 13, 8, 8), (200, 20, 12, 12), (12, 15, 10, 15),
                                          (144, 15, 10, 10), (2048, 42, 32, 32), (5000, 42, 32, 14),
-                                         (20736, 15, 10, 10), (3, 5, 2, 3)])
+                                         (20736, 15, 10, 10), (3, 5, 2, 3), (1000, 24, 16, 24), (700, 32, 30, 20),
+                                         (300, 80, 70, 40), (60, 100, 50, 60)])
 def test_basis_matches_oracle(handle, n, c, r, decay):
     """K2 (sketch.hpp:74-93): same numerical rank, same leading subspace,
     orthonormal to 1e-12 (test_sketch.cpp:198-204); covers the warp path,

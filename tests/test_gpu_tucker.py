@@ -184,7 +184,7 @@ def test_exec_policy_validated_like_the_reference(handle):
 def test_ranks_above_32_match_oracle(handle):
     """Ranks above the core kernel's 32-wide DMMA tiles (modes 0/1) run as
     rank blocks scattered into the core; parity with the oracle as usual.
-    r + p above 64 (the basis kernels) is refused up front."""
+    r + p above 256 is refused up front."""
     dims, ranks, p, s = (64, 56, 40), [48, 40, 20], 10, [70, 60, 40]
     x, _, _ = planted_tucker(dims, (48, 40, 20), 9)
     x = x + 1e-10 * np.random.default_rng(3).standard_normal(dims)
@@ -204,6 +204,28 @@ def test_ranks_above_32_match_oracle(handle):
           enumerate(zip(dims, (40, 36, 5)))]
     g = P.multi_ttm_core(x, fs, handle=handle)
     assert np.abs(g - O.core_from_factors(x, fs)).max() <= 1e-12 * np.abs(x).max() * 64
-    with pytest.raises(P.InvalidArgument, match="rank \\+ oversampling above 64"):
-        P.sub_r_hosvd(np.random.default_rng(1).standard_normal((40, 40, 8)), [8, 8, 8], 60, [120] * 3, 0,
+    with pytest.raises(P.InvalidArgument, match="rank \\+ oversampling above 256"):
+        P.sub_r_hosvd(np.random.default_rng(1).standard_normal((300, 300, 2)), [8, 8, 2], 250, [400, 400, 90000], 0,
                       handle=handle)
+
+
+def test_wide_sketches_above_64_columns_match_oracle(handle):
+    """r + p above 64 (the register basis kernels' width): the reference bounds
+    ranks only by the extents (tucker.hpp:184-197), so the sketch takes
+    several 64-column passes and the basis the generic global-memory kernel;
+    parity with the oracle as for every other decomposition."""
+    dims, ranks, p, s = (96, 90, 20), [70, 66, 12], 8, [100, 90, 30]
+    x, _, _ = planted_tucker(dims, (70, 66, 12), 5)
+    x = x + 1e-10 * np.random.default_rng(4).standard_normal(dims)
+    rep = P.SubsampleReport()
+    t = P.sub_r_hosvd(x, ranks, p, s, 7, report=rep, handle=handle)
+    orep = O.SubsampleReport()
+    to = O.sub_r_hosvd(x, ranks, p, s, 7, report=orep)
+    assert rep.achieved_ranks == orep.achieved_ranks
+    for k in range(3):
+        q = rep.achieved_ranks[k]
+        assert O.orthonormality_defect(t.factors[k]) <= 1e-12
+        assert projector_gap(t.factors[k][:, :q], to.factors[k][:, :q]) <= 1e-9
+    assert aligned_core_error(t.core, t.factors, to.core, to.factors) <= 1e-9
+    eg, ec = tucker_rel_error(x, t.core, t.factors), tucker_rel_error(x, to.core, to.factors)
+    assert abs(eg - ec) <= 1e-10 * max(ec, 1.0)
