@@ -1612,6 +1612,33 @@ __device__ void wtree_apply(const WTree& tr, int c, int q, const double* v0, int
   constexpr int RT = WTile<CP>::RT, CHUNK = WTile<CP>::CHUNK;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double* wsm = wscr_all + (size_t)warp * WTile<CP>::WSCR;
+  // one level-0 block per warp (the usual case): every warp copies its block's
+  // reflectors into its staging area now, while the upper levels (fewer
+  // warps) run; otherwise each block is staged right before it is applied
+  const bool prestaged = stage0 != nullptr && tr.nblk[0] <= nw;
+  auto stage_block = [&](int b) {
+    const int r0 = b * CHUNK;
+    const int nr = min(CHUNK, tr.rows[0] - r0);
+    const int kb = min(nr, c);
+    const double* vb = v0 + r0;
+    double* st = stage0 + (size_t)warp * (CHUNK + 1) * c;
+    const int tot = kb * nr;
+    for (int i0 = lane; i0 < tot; i0 += 32 * 8) {  // batches of 8 loads in flight per lane
+      double tmp[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = i0 + 32 * u;
+        tmp[u] = idx < tot ? vb[idx % nr + (int64_t)(idx / nr) * ldv0] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = i0 + 32 * u;
+        if (idx < tot) st[idx % nr + (idx / nr) * (CHUNK + 1)] = tmp[u];
+      }
+    }
+    __syncwarp();
+  };
+  if (prestaged && warp < tr.nblk[0]) stage_block(warp);
   for (int l = tr.L - 1; l >= 0; --l) {
     const int rows = tr.rows[l];
     const double* vsrc = l == 0 ? v0 : arena + tr.soff[l];
@@ -1627,24 +1654,8 @@ __device__ void wtree_apply(const WTree& tr, int c, int q, const double* v0, int
       const double* vb = vsrc + r0;
       int64_t ldvb = ldv;
       if (l == 0 && stage0) {
-        double* st = stage0 + (size_t)warp * (CHUNK + 1) * c;
-        // batches of 8 loads in flight per lane (the block sits in L2)
-        const int tot = kb * nr;
-        for (int i0 = lane; i0 < tot; i0 += 32 * 8) {
-          double tmp[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int idx = i0 + 32 * u;
-            tmp[u] = idx < tot ? vb[idx % nr + (int64_t)(idx / nr) * ldv] : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int idx = i0 + 32 * u;
-            if (idx < tot) st[idx % nr + (idx / nr) * (CHUNK + 1)] = tmp[u];
-          }
-        }
-        __syncwarp();
-        vb = st;
+        if (!prestaged) stage_block(b);
+        vb = stage0 + (size_t)warp * (CHUNK + 1) * c;
         ldvb = CHUNK + 1;
       }
       double y[RT][CP];
@@ -1737,8 +1748,9 @@ __global__ void __launch_bounds__(kThreads) basis_wtree_kernel(const BasisTarget
     wqr_factor<CP, false>(a, c, k, nullptr, 0, nullptr, s.B, LDB, 1, s.wscr);
     __syncwarp();
     PROF_MARK(2);
-    if (CP == 16) sweeps = jacobi_rows_nov<4, 4>(s.B, LDB, k);
-    else sweeps = jacobi_rows_nov<2, 16>(s.B, LDB, k);
+    if (CP == 16) sweeps = k <= 12 ? jacobi_rows_nov<4, 3>(s.B, LDB, k) : jacobi_rows_nov<4, 4>(s.B, LDB, k);
+    else sweeps = k <= 20 ? jacobi_rows_nov<2, 10>(s.B, LDB, k)
+                          : (k <= 24 ? jacobi_rows_nov<2, 12>(s.B, LDB, k) : jacobi_rows_nov<2, 16>(s.B, LDB, k));
   }
   __syncthreads();
   PROF_MARK_CTA(3);
@@ -2115,7 +2127,8 @@ __global__ void __launch_bounds__(kThreads) basis_wide_top_kernel(const BasisTar
     __syncthreads();
     tqr_factor<false>(a, c, k, nullptr, 0, nullptr, s.rb, ldr, 1, ts);  // R_1(j, col) at rb[j * ldr + col]
   }
-  const int sweeps = jacobi_rows_cta<16>(s.rb, ldr, k, pairs);
+  const int sweeps = k <= 32 ? jacobi_rows_cta<8>(s.rb, ldr, k, pairs)
+                     : (k <= 48 ? jacobi_rows_cta<12>(s.rb, ldr, k, pairs) : jacobi_rows_cta<16>(s.rb, ldr, k, pairs));
   PROF_MARK_CTA(10);
   const int lane = tid & 31, warp = tid >> 5;
   for (int i = warp; i < k; i += kWarps) {
