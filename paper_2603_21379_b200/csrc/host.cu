@@ -47,7 +47,7 @@ size_t srtt_wtree_top_smem(int n0, int c, bool pad);
 int64_t srtt_wtree_persist_doubles(int rows, int c);
 size_t srtt_wtree_factor_smem(int rows, int c);
 size_t srtt_wtree_apply_smem(int rows, int c);
-cudaError_t srtt_launch_wtree_top(int, const BasisTarget*, const int*, int, size_t, cudaStream_t);
+cudaError_t srtt_launch_wtree_top(int, int, const BasisTarget*, const int*, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_wtree_factor(int, const BasisTarget*, const int2*, int, size_t, cudaStream_t);
 cudaError_t srtt_launch_wtree_apply(int, const BasisTarget*, const int2*, int, size_t, cudaStream_t);
 int srtt_wide_block_rows();
@@ -604,8 +604,9 @@ struct BasisLists {
   size_t off_map[SRTT_MAX_QR_LEVELS] = {};  // per TSQR level: CTA -> (target, block)
   // register-tree targets by column padding (16 / 32): single-CTA ones, the
   // tops of tall ones, and the (target, CTA) map of the tall ones
-  std::vector<int> w_small[2], w_tall[2];
-  size_t off_w_small[2] = {}, off_w_tall[2] = {}, off_w_map[2] = {};
+  // (single-CTA ones split again: at most one warp block / taller)
+  std::vector<int> w_small[4], w_tall[2];
+  size_t off_w_small[4] = {}, off_w_tall[2] = {}, off_w_map[2] = {};
   int w_ctas[2] = {};
   // wide register path (kind 2): single-block targets, tall ones, and the
   // per-level (target, block) maps of the tall ones
@@ -626,13 +627,14 @@ BasisLists make_basis_lists(const std::vector<BasisTarget>& targets, Blob& blob)
       const BasisTarget& t = targets[i];
       if (t.kind != 1 || srtt_wtree_cp(t.c) != (v ? 32 : 16)) continue;
       if (t.nlevels == 0) {
-        L.w_small[v].push_back(i);
+        L.w_small[2 * v + (t.n > srtt_wtree_chunk(v ? 32 : 16) ? 1 : 0)].push_back(i);
       } else {
         L.w_tall[v].push_back(i);
         for (int b = 0; b < t.lv[0].nblk; ++b) map.push_back(make_int2(i, b));
       }
     }
-    if (!L.w_small[v].empty()) L.off_w_small[v] = blob.add(L.w_small[v].data(), sizeof(int) * L.w_small[v].size());
+    for (int u = 2 * v; u < 2 * v + 2; ++u)
+      if (!L.w_small[u].empty()) L.off_w_small[u] = blob.add(L.w_small[u].data(), sizeof(int) * L.w_small[u].size());
     if (!L.w_tall[v].empty()) {
       L.off_w_tall[v] = blob.add(L.w_tall[v].data(), sizeof(int) * L.w_tall[v].size());
       L.off_w_map[v] = blob.add(map.data(), sizeof(int2) * map.size());
@@ -694,13 +696,13 @@ int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const 
   const int nt = (int)targets.size();
   // register-tree targets: single-CTA ones on the side stream, tall ones as
   // factor -> top -> apply on the main stream
-  for (int v = 0; v < 2; ++v) {
-    const int cp = v ? 32 : 16;
-    if (!lists.w_small[v].empty()) {
+  for (int u = 0; u < 4; ++u) {
+    const int cp = u >= 2 ? 32 : 16;
+    if (!lists.w_small[u].empty()) {
       size_t smem = 0;
-      for (int i : lists.w_small[v]) smem = std::max(smem, srtt_wtree_top_smem((int)targets[i].n, targets[i].c, true));
-      CK(srtt_launch_wtree_top(cp, dT, reinterpret_cast<const int*>(dblob + lists.off_w_small[v]),
-                               (int)lists.w_small[v].size(), smem, small_stream ? small_stream : h->stream));
+      for (int i : lists.w_small[u]) smem = std::max(smem, srtt_wtree_top_smem((int)targets[i].n, targets[i].c, true));
+      CK(srtt_launch_wtree_top(cp, u & 1, dT, reinterpret_cast<const int*>(dblob + lists.off_w_small[u]),
+                               (int)lists.w_small[u].size(), smem, small_stream ? small_stream : h->stream));
       ++launches;
     }
   }
@@ -716,7 +718,7 @@ int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const 
     }
     const int2* map = reinterpret_cast<const int2*>(dblob + lists.off_w_map[v]);
     CK(srtt_launch_wtree_factor(cp, dT, map, lists.w_ctas[v], sf, h->stream));
-    CK(srtt_launch_wtree_top(cp, dT, reinterpret_cast<const int*>(dblob + lists.off_w_tall[v]),
+    CK(srtt_launch_wtree_top(cp, 1, dT, reinterpret_cast<const int*>(dblob + lists.off_w_tall[v]),
                              (int)lists.w_tall[v].size(), st, h->stream));
     CK(srtt_launch_wtree_apply(cp, dT, map, lists.w_ctas[v], sa, h->stream));
     launches += 3;

@@ -1551,14 +1551,196 @@ __device__ int jacobi_rows_nov(double* B, int ldb, int k) {
   return sweep;
 }
 
-// Factor levels lo..L-1 of a CTA's tree. Level 0 reads in0 (ld ld0) and
-// writes its reflectors to v0 (ld ldv0; may alias in0); upper levels live in
-// the arena. All warps of the CTA take row blocks round-robin.
+// ---- row-split teams ---------------------------------------------------------
+// A block taller than one warp's 32 RT rows is factored by several warps
+// TOGETHER instead of warp by warp plus another tree level: warp w holds rows
+// [w rpw, (w + 1) rpw) of the block (rpw a multiple of 32, all columns), the
+// per-warp column totals of a step meet in shared memory (double-buffered,
+// ONE named barrier per step), every warp derives the same reflector scalars
+// and updates its own rows. The pivot rows 0..c-1 all live in warp 0
+// (c <= 32 <= rpw). One level of c steps replaces two.
+template <int CP> struct TeamRows {
+  static constexpr int SCR = 2 * 8 * CP + 2 * 2 * CP;  // CTA-shared doubles: warp totals + pivot row (+ dump), x2
+};
+
+__device__ __forceinline__ void team_bar(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// rows per warp and active warps for a block of nr rows on nw warps: one
+// warp when the block fits its registers, else an even split
+__device__ __forceinline__ void team_split(int nr, int nw, int chunk, int* nwa, int* rpw) {
+  if (nr <= chunk) {
+    *nwa = 1;
+    *rpw = chunk;
+    return;
+  }
+  const int a = min(nw, (nr + chunk - 1) / chunk);
+  int r = ((nr + a - 1) / a + 31) & ~31;
+  if (r > chunk) r = chunk;
+  *rpw = r;
+  *nwa = (nr + r - 1) / r;
+}
+
 template <int CP>
+__device__ void trows_factor(double (&a)[WTile<CP>::RT][CP], int w, int nwa, int rpw, int nr, int c, double* vout, int ldv,
+                             double* gout, double* rout, int rs, int cs, double* wsm, double* tscr) {
+  constexpr int RT = WTile<CP>::RT, LPC = 32 / CP;
+  const int lane = threadIdx.x & 31;
+  const int mycol = lane / LPC;
+  double* red = wsm;
+  double* csm = wsm + WTile<CP>::RED + CP;
+  const int row0 = w * rpw;
+  const int kb = nr < c ? nr : c;
+  uint32_t va = smem_addr(vout) + 8u * (uint32_t)(row0 + lane);
+  const uint32_t ga = smem_addr(gout);
+  uint32_t ra = smem_addr(rout) + 8u * (uint32_t)(mycol * cs);
+  const uint32_t vstep = 8u * (uint32_t)ldv, rstep = 8u * (uint32_t)(rs + cs);
+  for (int j = 0; j < kb; ++j) {
+    double* xsb = tscr + (j & 1) * 8 * CP;
+    double* prb = tscr + 2 * 8 * CP + (j & 1) * 2 * CP;
+    if (w == 0) {
+      double2* pdst = reinterpret_cast<double2*>(lane == j ? prb : prb + CP);
+#pragma unroll
+      for (int p = 0; p < CP; p += 2) pdst[p / 2] = make_double2(a[0][p], a[0][p + 1]);
+    }
+    double xm[RT];
+#pragma unroll
+    for (int t = 0; t < RT; ++t) xm[t] = (row0 + t * 32 + lane > j) ? a[t][0] : 0.0;
+    double D[CP];
+#pragma unroll
+    for (int p = 0; p < CP; ++p) {
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) s = fma(xm[t], a[t][p], s);
+      D[p] = s;
+    }
+    const double dw = reduce_scatter_sm<CP>(D, red, lane);
+    if (lane % LPC == 0) xsb[w * CP + mycol] = dw;
+    team_bar(nwa * 32);
+    // all 8 warp slots, fixed order (the slots of inactive warps are zero)
+    double d0 = 0.0, d1 = 0.0, s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int v = 0; v < 8; v += 2) {
+      d0 += xsb[v * CP + mycol];
+      d1 += xsb[(v + 1) * CP + mycol];
+      s0 += xsb[v * CP];
+      s1 += xsb[(v + 1) * CP];
+    }
+    const double dtot = d0 + d1, ss = s0 + s1;
+    const double alpha = prb[0];
+    double beta = alpha, ujj = 0.0, g = 0.0;
+    if (ss != 0.0) {
+      const double n2 = fma(alpha, alpha, ss);
+      const double rn = rsqrt(n2);
+      const double nrm = n2 * rn;
+      beta = -copysign(nrm, alpha);
+      ujj = alpha - beta;
+      g = rn * __drcp_rn(fabs(ujj));
+    }
+    const double arow = prb[mycol];
+    const double cl = g * fma(ujj, arow, dtot);
+    if (lane % LPC == 0) {
+      csm[mycol] = cl;
+      if (w == 0 && j + mycol < c) sts_f64(ra, mycol == 0 ? beta : arow - cl * ujj);
+    }
+    ra += rstep;
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+      const int row = row0 + t * 32 + lane;
+      if (t * 32 < rpw && row < nr) sts_f64(va + 256u * t, row > j ? xm[t] : (row == j ? ujj : 0.0));
+    }
+    if (w == 0 && lane == 0) sts_f64(ga + 8u * j, g);
+    va += vstep;
+    __syncwarp();
+#pragma unroll
+    for (int p = 0; p < CP; p += 2) {
+      const double2 e = reinterpret_cast<const double2*>(csm)[p / 2];
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        if (p > 0) a[t][p - 1] = fma(-e.x, xm[t], a[t][p]);
+        a[t][p] = fma(-e.y, xm[t], a[t][p + 1 < CP ? p + 1 : p]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < RT; ++t) a[t][CP - 1] = 0.0;
+    __syncwarp();
+  }
+}
+
+template <int CP>
+__device__ void trows_apply(double (&y)[WTile<CP>::RT][CP], int w, int nwa, int rpw, int nr, int kb, const double* v, int ldv,
+                            const double* g, double* wsm, double* tscr) {
+  constexpr int RT = WTile<CP>::RT, LPC = 32 / CP;
+  const int lane = threadIdx.x & 31;
+  const int mycol = lane / LPC;
+  double* red = wsm;
+  double* esm = wsm + WTile<CP>::RED;
+  const int row0 = w * rpw;
+  const uint32_t vstep = 8u * (uint32_t)ldv;
+  uint32_t va = smem_addr(v) + 8u * (uint32_t)(row0 + lane) + vstep * (uint32_t)(kb > 0 ? kb - 1 : 0);
+  const uint32_t ga = smem_addr(g);
+  double vt[RT];
+#pragma unroll
+  for (int t = 0; t < RT; ++t)
+    vt[t] = (kb > 0 && t * 32 < rpw && row0 + t * 32 + lane < nr) ? lds_f64(va + 256u * t) : 0.0;
+  for (int j = kb - 1; j >= 0; --j) {
+    double* xsb = tscr + (j & 1) * 8 * CP;
+    va -= vstep;
+    double vn[RT];
+#pragma unroll
+    for (int t = 0; t < RT; ++t)
+      vn[t] = (j > 0 && t * 32 < rpw && row0 + t * 32 + lane < nr) ? lds_f64(va + 256u * t) : 0.0;
+    const double gj = lds_f64(ga + 8u * j);
+    double D[CP];
+#pragma unroll
+    for (int p = 0; p < CP; ++p) {
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) s = fma(vt[t], y[t][p], s);
+      D[p] = s;
+    }
+    const double dw = reduce_scatter_sm<CP>(D, red, lane);
+    if (lane % LPC == 0) xsb[w * CP + mycol] = dw;
+    team_bar(nwa * 32);
+    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; u += 2) {
+      d0 += xsb[u * CP + mycol];
+      d1 += xsb[(u + 1) * CP + mycol];
+    }
+    const double dtot = d0 + d1;
+    if (lane % LPC == 0) esm[mycol] = gj * dtot;
+    __syncwarp();
+#pragma unroll
+    for (int p = 0; p < CP; p += 2) {
+      const double2 e = reinterpret_cast<const double2*>(esm)[p / 2];
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        y[t][p] = fma(-e.x, vt[t], y[t][p]);
+        y[t][p + 1] = fma(-e.y, vt[t], y[t][p + 1]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < RT; ++t) vt[t] = vn[t];
+  }
+}
+
+// Factor the levels of a CTA's tree: every level cuts its rows into team
+// blocks of (warps x 32 RT) rows taken one after the other by the whole CTA
+// (normally there is exactly one). Level 0 reads in0 (ld ld0) and writes its
+// reflectors to v0 (ld ldv0; may alias in0); with stage0 set (v0 is global
+// memory) a block's reflectors are staged in shared memory during the step
+// loop -- a global store there would make every barrier of the step wait for
+// its acknowledgement -- and copied out afterwards. Upper levels live in the
+// arena.
+template <int CP, bool TEAM = true>
 __device__ void wtree_factor(const WTree& tr, int c, const double* in0, int64_t ld0, double* v0, int64_t ldv0,
-                             double* arena, double* wscr_all, double* stage0 = nullptr) {
+                             double* arena, double* wscr_all, double* tscr, double* stage0 = nullptr) {
   constexpr int RT = WTile<CP>::RT, CHUNK = WTile<CP>::CHUNK;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int TB = nw * CHUNK;
   double* wsm = wscr_all + (size_t)warp * WTile<CP>::WSCR;
   for (int l = 0; l < tr.L; ++l) {
     const int rows = tr.rows[l];
@@ -1567,78 +1749,70 @@ __device__ void wtree_factor(const WTree& tr, int c, const double* in0, int64_t 
     double* vdst = l == 0 ? v0 : arena + tr.soff[l];
     const int64_t ldv = l == 0 ? ldv0 : (rows | 1);
     double* rnext = arena + tr.soff[l + 1];
-    const int64_t ldr = tr.rows[l + 1] | 1;
-    for (int b = warp; b < tr.nblk[l]; b += nw) {
-      const int r0 = b * CHUNK;
-      const int nr = min(CHUNK, rows - r0);
-      double a[RT][CP];
-#pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        const int row = t * 32 + lane;
-#pragma unroll
-        for (int p = 0; p < CP; ++p) a[t][p] = (row < nr && p < c) ? src[r0 + row + (int64_t)p * lds] : 0.0;
+    const int ldr = tr.rows[l + 1] | 1;
+    for (int b = 0; b < tr.nblk[l]; ++b) {
+      const int r0 = b * TB;
+      const int nr = min(TB, rows - r0);
+      int nwa, rpw;
+      team_split(nr, nw, CHUNK, &nwa, &rpw);
+      const bool staged = l == 0 && stage0 != nullptr;
+      double* vb = staged ? stage0 : vdst + r0;
+      const int ldvb = staged ? TB + 1 : (int)ldv;
+      if (TEAM && nwa > 1) {  // warp-total slots of the inactive warps must read zero
+        for (int i = threadIdx.x; i < 2 * 8 * CP; i += blockDim.x) tscr[i] = 0.0;
+        __syncthreads();
       }
-      __syncwarp();
-      if (l == 0 && stage0) {
-        // v0 is global memory: a store there inside the step loop would make
-        // every warp barrier of the step wait for its acknowledgement, so
-        // the reflectors are staged in shared memory and copied out after
-        double* st = stage0 + (size_t)warp * (CHUNK + 1) * c;
-        wqr_factor<CP, true>(a, nr, c, st, CHUNK + 1, arena + tr.goff[l] + b * c, rnext + b * c, 1, ldr, wsm);
-        __syncwarp();
-        const int kb = min(nr, c);
-        for (int j = 0; j < kb; ++j)
+      if (warp < nwa) {
+        double a[RT][CP];
 #pragma unroll
-          for (int t = 0; t < RT; ++t) {
-            const int row = t * 32 + lane;
-            if (row < nr) vdst[r0 + row + (int64_t)j * ldv] = st[row + j * (CHUNK + 1)];
-          }
+        for (int t = 0; t < RT; ++t) {
+          const int row = warp * rpw + t * 32 + lane;
+#pragma unroll
+          for (int p = 0; p < CP; ++p)
+            a[t][p] = (t * 32 < rpw && row < nr && p < c) ? src[r0 + row + (int64_t)p * lds] : 0.0;
+        }
         __syncwarp();
-      } else {
-        wqr_factor<CP, true>(a, nr, c, vdst + r0, ldv, arena + tr.goff[l] + b * c, rnext + b * c, 1, ldr, wsm);
+        if (!TEAM || nwa == 1)
+          wqr_factor<CP, true>(a, nr, c, vb, ldvb, arena + tr.goff[l] + b * c, rnext + b * c, 1, ldr, wsm);
+        else
+          trows_factor<CP>(a, warp, nwa, rpw, nr, c, vb, ldvb, arena + tr.goff[l] + b * c, rnext + b * c, 1, ldr, wsm,
+                           tscr);
+      }
+      __syncthreads();
+      if (staged) {
+        const int kb = min(nr, c);
+        for (int idx = threadIdx.x; idx < nr * kb; idx += blockDim.x) {
+          const int i = idx % nr, j = idx / nr;
+          vdst[r0 + i + (int64_t)j * ldv] = stage0[i + j * (TB + 1)];
+        }
+        __syncthreads();
       }
     }
-    __syncthreads();
   }
 }
 
 // Back-application through levels L-1..0: Y_L (arena) holds the kb_top x q
-// input; the level-0 result goes to out0 (ld ldo). v0 as in wtree_factor;
-// when stage0 is set the level-0 reflector block is first copied into the
-// warp's staging area (it lives in global memory).
-template <int CP>
+// input; the level-0 result goes to out0 (ld ldo). With stage0 set the
+// level-0 reflectors (global memory) are copied to shared memory first.
+template <int CP, bool TEAM = true>
 __device__ void wtree_apply(const WTree& tr, int c, int q, const double* v0, int64_t ldv0, double* arena,
-                            double* wscr_all, double* out0, int64_t ldo, double* stage0) {
+                            double* wscr_all, double* tscr, double* out0, int64_t ldo, double* stage0) {
   constexpr int RT = WTile<CP>::RT, CHUNK = WTile<CP>::CHUNK;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int TB = nw * CHUNK;
   double* wsm = wscr_all + (size_t)warp * WTile<CP>::WSCR;
-  // one level-0 block per warp (the usual case): every warp copies its block's
-  // reflectors into its staging area now, while the upper levels (fewer
-  // warps) run; otherwise each block is staged right before it is applied
-  const bool prestaged = stage0 != nullptr && tr.nblk[0] <= nw;
-  auto stage_block = [&](int b) {
-    const int r0 = b * CHUNK;
-    const int nr = min(CHUNK, tr.rows[0] - r0);
+  auto stage_block = [&](int b) {  // cooperative, coalesced; ends with a CTA barrier
+    const int r0 = b * TB;
+    const int nr = min(TB, tr.rows[0] - r0);
     const int kb = min(nr, c);
-    const double* vb = v0 + r0;
-    double* st = stage0 + (size_t)warp * (CHUNK + 1) * c;
-    const int tot = kb * nr;
-    for (int i0 = lane; i0 < tot; i0 += 32 * 8) {  // batches of 8 loads in flight per lane
-      double tmp[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = i0 + 32 * u;
-        tmp[u] = idx < tot ? vb[idx % nr + (int64_t)(idx / nr) * ldv0] : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = i0 + 32 * u;
-        if (idx < tot) st[idx % nr + (idx / nr) * (CHUNK + 1)] = tmp[u];
-      }
+    for (int idx = threadIdx.x; idx < nr * kb; idx += blockDim.x) {
+      const int i = idx % nr, j = idx / nr;
+      stage0[i + j * (TB + 1)] = v0[r0 + i + (int64_t)j * ldv0];
     }
-    __syncwarp();
+    __syncthreads();
   };
-  if (prestaged && warp < tr.nblk[0]) stage_block(warp);
+  const bool prestaged = stage0 != nullptr && tr.nblk[0] == 1;
+  if (prestaged) stage_block(0);
   for (int l = tr.L - 1; l >= 0; --l) {
     const int rows = tr.rows[l];
     const double* vsrc = l == 0 ? v0 : arena + tr.soff[l];
@@ -1647,34 +1821,43 @@ __device__ void wtree_apply(const WTree& tr, int c, int q, const double* v0, int
     const int64_t ldyi = tr.rows[l + 1] | 1;
     double* yout = l == 0 ? out0 : arena + tr.yoff[l];
     const int64_t ldyo = l == 0 ? ldo : (rows | 1);
-    for (int b = warp; b < tr.nblk[l]; b += nw) {
-      const int r0 = b * CHUNK;
-      const int nr = min(CHUNK, rows - r0);
+    for (int b = 0; b < tr.nblk[l]; ++b) {
+      const int r0 = b * TB;
+      const int nr = min(TB, rows - r0);
       const int kb = min(nr, c);
-      const double* vb = vsrc + r0;
-      int64_t ldvb = ldv;
-      if (l == 0 && stage0) {
-        if (!prestaged) stage_block(b);
-        vb = stage0 + (size_t)warp * (CHUNK + 1) * c;
-        ldvb = CHUNK + 1;
+      int nwa, rpw;
+      team_split(nr, nw, CHUNK, &nwa, &rpw);
+      const bool staged = l == 0 && stage0 != nullptr;
+      if (staged && !prestaged) stage_block(b);
+      const double* vb = staged ? stage0 : vsrc + r0;
+      const int ldvb = staged ? TB + 1 : (int)ldv;
+      if (TEAM && nwa > 1) {
+        for (int i = threadIdx.x; i < 2 * 8 * CP; i += blockDim.x) tscr[i] = 0.0;
+        __syncthreads();
       }
-      double y[RT][CP];
+      if (warp < nwa) {
+        double y[RT][CP];
 #pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        const int row = t * 32 + lane;
+        for (int t = 0; t < RT; ++t) {
+          const int row = warp * rpw + t * 32 + lane;
 #pragma unroll
-        for (int p = 0; p < CP; ++p) y[t][p] = (row < kb && p < q) ? yin[b * c + row + (int64_t)p * ldyi] : 0.0;
+          for (int p = 0; p < CP; ++p)
+            y[t][p] = (t * 32 < rpw && row < kb && p < q) ? yin[b * c + row + (int64_t)p * ldyi] : 0.0;
+        }
+        if (!TEAM || nwa == 1)
+          wqr_apply<CP>(y, nr, kb, vb, ldvb, arena + tr.goff[l] + b * c, wsm);
+        else
+          trows_apply<CP>(y, warp, nwa, rpw, nr, kb, vb, ldvb, arena + tr.goff[l] + b * c, wsm, tscr);
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+          const int row = warp * rpw + t * 32 + lane;
+#pragma unroll
+          for (int p = 0; p < CP; ++p)
+            if (t * 32 < rpw && row < nr && p < q) yout[r0 + row + (int64_t)p * ldyo] = y[t][p];
+        }
       }
-      wqr_apply<CP>(y, nr, kb, vb, ldvb, arena + tr.goff[l] + b * c, wsm);
-#pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        const int row = t * 32 + lane;
-#pragma unroll
-        for (int p = 0; p < CP; ++p)
-          if (row < nr && p < q) yout[r0 + row + (int64_t)p * ldyo] = y[t][p];
-      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
@@ -1682,6 +1865,7 @@ struct WTopSmem {
   double* v0;     // (n0 | 1) x c level-0 reflectors
   double* arena;  // tree arena
   double* wscr;   // per-warp scratch
+  double* tscr;   // row-team scratch
   double* B;      // CP x (CP + 1) Jacobi rows
   double* sig;
   double* dots;
@@ -1692,14 +1876,18 @@ struct WTopSmem {
 
 __host__ __device__ inline size_t wtop_doubles(int n0, int c, int CP, int nwarps, int chunk, bool pad) {
   const WTree tr = wtree_plan(n0, c, chunk);
-  return (size_t)(n0 | 1) * c + tr.total + 4 + (size_t)nwarps * (CP == 16 ? WTile<16>::WSCR : WTile<32>::WSCR) + (size_t)CP * (CP + 1) + CP + CP +
+  return (size_t)(n0 | 1) * c + tr.total + 4 + (size_t)nwarps * (CP == 16 ? WTile<16>::WSCR : WTile<32>::WSCR) + 20 * CP +
+         (size_t)CP * (CP + 1) + CP + CP +
          64 + (pad ? n0 : 0) + CP / 2 + 2;
 }
 
 // Whole basis of a single-CTA target (nlevels == 0), or the top of a tall
 // one (nlevels == 1: input = the stacked R of the factor kernel, output =
 // the stacked Y for the apply kernel).
-template <int CP>
+// TEAM = false: targets of at most one warp block (every block of the tree is
+// a single warp's): the row-team code is left out of the kernel, whose
+// once-executed straight-line parts are instruction-fetch bound.
+template <int CP, bool TEAM>
 __global__ void __launch_bounds__(kThreads) basis_wtree_kernel(const BasisTarget* __restrict__ targets,
                                                               const int* __restrict__ list) {
   constexpr int RT = WTile<CP>::RT, CHUNK = WTile<CP>::CHUNK;
@@ -1712,13 +1900,14 @@ __global__ void __launch_bounds__(kThreads) basis_wtree_kernel(const BasisTarget
   const bool tall = T.nlevels > 0;
   const QrLevel L = T.lv[T.nlevels];
   const int n0 = (int)L.n, c = T.c, r = T.r;
-  const WTree tr = wtree_plan(n0, c, CHUNK);
+  const WTree tr = wtree_plan(n0, c, kWarps * CHUNK);
   WTopSmem s;
   {
     double* p = reinterpret_cast<double*>(smem_raw);
     s.v0 = p; p += ((size_t)(n0 | 1) * c + 1) & ~(size_t)1;
     s.arena = p; p += (tr.total + 1) & ~1;
     s.wscr = p; p += (size_t)kWarps * WTile<CP>::WSCR;  // 16-byte aligned (vector accesses)
+    s.tscr = p; p += TeamRows<CP>::SCR;
     s.B = p; p += CP * LDB;
     s.sig = p; p += CP;
     s.dots = p; p += CP;
@@ -1730,7 +1919,7 @@ __global__ void __launch_bounds__(kThreads) basis_wtree_kernel(const BasisTarget
   for (int i = tid; i < tr.persist; i += blockDim.x) s.arena[i] = 0.0;
   for (int i = tid; i < CP * LDB; i += blockDim.x) s.B[i] = 0.0;
   __syncthreads();
-  wtree_factor<CP>(tr, c, L.a, L.n, s.v0, n0 | 1, s.arena, s.wscr);
+  wtree_factor<CP, TEAM>(tr, c, L.a, L.n, s.v0, n0 | 1, s.arena, s.wscr, s.tscr);
   PROF_MARK_CTA(1);
   // R^T = Q_1 R_1, then Jacobi on the rows of R_1 (warp 0)
   const int k = tr.rows[tr.L];
@@ -1789,7 +1978,7 @@ __global__ void __launch_bounds__(kThreads) basis_wtree_kernel(const BasisTarget
   }
   __syncthreads();
   PROF_MARK_CTA(4);
-  wtree_apply<CP>(tr, c, q, s.v0, n0 | 1, s.arena, s.wscr, tall ? L.y : T.u, tall ? L.n : T.n, nullptr);
+  wtree_apply<CP, TEAM>(tr, c, q, s.v0, n0 | 1, s.arena, s.wscr, s.tscr, tall ? L.y : T.u, tall ? L.n : T.n, nullptr);
   PROF_MARK_CTA(5);
   if (!tall && q < r)
     pad_columns(T.u, n0, n0, q, r, T.state0, T.draw_offset, (uint64_t)T.normal_base, s.vpad, s.dots, s.red);
@@ -2340,13 +2529,14 @@ __global__ void __launch_bounds__(kWfThreads) basis_wfactor_kernel(const BasisTa
   const int c = T.c;
   const int64_t r0 = (int64_t)tb.y * L.blk_rows;
   const int nrows = (int)srtt_dev::min64(L.blk_rows, L.n - r0);
-  const WTree tr = wtree_plan(nrows, c, CHUNK);
+  const WTree tr = wtree_plan(nrows, c, (kWfThreads / 32) * CHUNK);
   double* arena = reinterpret_cast<double*>(smem_raw);
   double* wscr = arena + ((tr.persist + 1) & ~1);
-  double* stage = wscr + (size_t)(kWfThreads / 32) * WTile<CP>::WSCR;
+  double* tscr = wscr + (size_t)(kWfThreads / 32) * WTile<CP>::WSCR;
+  double* stage = tscr + TeamRows<CP>::SCR;
   for (int i = threadIdx.x; i < tr.persist; i += blockDim.x) arena[i] = 0.0;
   __syncthreads();
-  wtree_factor<CP>(tr, c, L.a + r0, L.n, L.a + r0, L.n, arena, wscr, stage);
+  wtree_factor<CP>(tr, c, L.a + r0, L.n, L.a + r0, L.n, arena, wscr, tscr, stage);
   const int k = tr.rows[tr.L];
   const double* Rf = arena + tr.soff[tr.L];
   for (int idx = threadIdx.x; idx < k * c; idx += blockDim.x) {
@@ -2372,10 +2562,11 @@ __global__ void __launch_bounds__(kWfThreads) basis_wapply_kernel(const BasisTar
   const int q = T.info[0];
   const int64_t r0 = (int64_t)tb.y * L.blk_rows;
   const int nrows = (int)srtt_dev::min64(L.blk_rows, L.n - r0);
-  const WTree tr = wtree_plan(nrows, c, CHUNK);
+  const WTree tr = wtree_plan(nrows, c, (kWfThreads / 32) * CHUNK);
   double* arena = reinterpret_cast<double*>(smem_raw);
   double* wscr = arena + ((tr.total + 1) & ~1);
-  double* stage = wscr + (size_t)(kWfThreads / 32) * WTile<CP>::WSCR;
+  double* tscr = wscr + (size_t)(kWfThreads / 32) * WTile<CP>::WSCR;
+  double* stage = tscr + TeamRows<CP>::SCR;
   const double* up = T.vup + (int64_t)tb.y * T.vup_stride;
   for (int i = threadIdx.x; i < tr.persist; i += blockDim.x) arena[i] = up[i];
   const int k = tr.rows[tr.L];
@@ -2385,7 +2576,7 @@ __global__ void __launch_bounds__(kWfThreads) basis_wapply_kernel(const BasisTar
     yt[i + (size_t)col * (k | 1)] = P.y[(int64_t)col * P.n + (int64_t)tb.y * c + i];
   }
   __syncthreads();
-  wtree_apply<CP>(tr, c, q, L.a + r0, L.n, arena, wscr, L.y + r0, L.n, stage);
+  wtree_apply<CP>(tr, c, q, L.a + r0, L.n, arena, wscr, tscr, L.y + r0, L.n, stage);
 }
 
 }  // namespace
@@ -2500,38 +2691,45 @@ int srtt_wtree_factor_threads() { return kWfThreads; }
 
 size_t srtt_wtree_top_smem(int n0, int c, bool pad) {
   const int cp = srtt_wtree_cp(c);
-  return wtop_doubles(n0, c, cp, kWarps, srtt_wtree_chunk(cp), pad) * sizeof(double) + 64;
+  return wtop_doubles(n0, c, cp, kWarps, kWarps * srtt_wtree_chunk(cp), pad) * sizeof(double) + 64;
 }
 
 int64_t srtt_wtree_persist_doubles(int rows, int c) {
   const int cp = srtt_wtree_cp(c);
-  return wtree_plan(rows, c, srtt_wtree_chunk(cp)).persist;
+  return wtree_plan(rows, c, (kWfThreads / 32) * srtt_wtree_chunk(cp)).persist;
 }
 
 size_t srtt_wtree_factor_smem(int rows, int c) {
   const int cp = srtt_wtree_cp(c);
-  const WTree tr = wtree_plan(rows, c, srtt_wtree_chunk(cp));
-  return ((size_t)tr.persist + 2 + (size_t)(kWfThreads / 32) * ((cp == 16 ? WTile<16>::WSCR : WTile<32>::WSCR) + (size_t)(srtt_wtree_chunk(cp) + 1) * c)) * sizeof(double);
+  const int tb = (kWfThreads / 32) * srtt_wtree_chunk(cp);
+  const WTree tr = wtree_plan(rows, c, tb);
+  return ((size_t)tr.persist + 2 + (size_t)(kWfThreads / 32) * (cp == 16 ? WTile<16>::WSCR : WTile<32>::WSCR) + 20 * cp +
+          (size_t)(tb + 1) * c) * sizeof(double);
 }
 
 size_t srtt_wtree_apply_smem(int rows, int c) {
   const int cp = srtt_wtree_cp(c);
   const int chunk = srtt_wtree_chunk(cp);
-  const WTree tr = wtree_plan(rows, c, chunk);
-  return ((size_t)tr.total + 2 + (size_t)(kWfThreads / 32) * ((cp == 16 ? WTile<16>::WSCR : WTile<32>::WSCR) + (size_t)(chunk + 1) * c)) *
-         sizeof(double);
+  const int tb = (kWfThreads / 32) * chunk;
+  const WTree tr = wtree_plan(rows, c, tb);
+  return ((size_t)tr.total + 2 + (size_t)(kWfThreads / 32) * (cp == 16 ? WTile<16>::WSCR : WTile<32>::WSCR) + 20 * cp +
+          (size_t)(tb + 1) * c) * sizeof(double);
 }
 
-cudaError_t srtt_launch_wtree_top(int cp, const BasisTarget* d_targets, const int* d_list, int n, size_t smem,
+cudaError_t srtt_launch_wtree_top(int cp, int team, const BasisTarget* d_targets, const int* d_list, int n, size_t smem,
                                   cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
+#define SRTT_WTOP(CPV, TV)                                                                   \
+  do {                                                                                       \
+    SRTT_ENSURE_SMEM((basis_wtree_kernel<CPV, TV>), smem);                                   \
+    basis_wtree_kernel<CPV, TV><<<n, kThreads, smem, stream>>>(d_targets, d_list);           \
+  } while (0)
   if (cp == 16) {
-    SRTT_ENSURE_SMEM((basis_wtree_kernel<16>), smem);
-    basis_wtree_kernel<16><<<n, kThreads, smem, stream>>>(d_targets, d_list);
+    if (team) SRTT_WTOP(16, true); else SRTT_WTOP(16, false);
   } else {
-    SRTT_ENSURE_SMEM((basis_wtree_kernel<32>), smem);
-    basis_wtree_kernel<32><<<n, kThreads, smem, stream>>>(d_targets, d_list);
+    if (team) SRTT_WTOP(32, true); else SRTT_WTOP(32, false);
   }
+#undef SRTT_WTOP
   return cudaGetLastError();
 }
 
