@@ -1920,6 +1920,23 @@ extern "C" {
 const char* srtt_last_error(void) { return g_last_error.c_str(); }
 int srtt_version(void) { return 100; }
 
+// Development / test aid (no GPU needed): the K2 plan of an n x c sketch with
+// target rank r. out[0] = kernel family (0 shared-memory QR, 1 register
+// tree, 2 wide register teams, 3 generic), out[1] = levels below the top,
+// out[2] = CTAs at level 0, out[3] = rows per level-0 CTA, out[4] = rows of
+// the top block.
+int srtt_debug_basis_plan(int64_t n, int32_t c, int32_t r, int64_t* out) {
+  return guarded([&] {
+    if (!out || n < 1 || c < 1 || r < 1 || r > c) invalid("srtt_debug_basis_plan: bad arguments");
+    const BasisPlan b = plan_basis(n, c, r);
+    out[0] = b.kind;
+    out[1] = b.nlevels;
+    out[2] = b.lv_nblk[0];
+    out[3] = b.lv_blk[0];
+    out[4] = b.lv_n[b.nlevels];
+  });
+}
+
 int srtt_create(const srtt_options* opts, srtt_handle** out) {
   return guarded([&] {
     if (!out) invalid("srtt_create: null output");
