@@ -427,8 +427,12 @@ def run_product(args):
     def kernel_samples(n):
         # the core kernel's own duration (CUDA events around that launch
         # inside the library), from report-carrying calls outside the timed loop
+        # (a stream-ordered call is enqueued right before each one, so the
+        # measured launch starts on a busy GPU at load clocks, as inside the
+        # timed loop, not on one that idled during the previous read-back)
         core_t = []
         for _ in range(n):
+            _run_product(P, cfg, x, dims, 0, h)
             r = P.SubsampleReport()
             _run_product(P, cfg, x, dims, 0, h, report=r)
             core_t.append(r.kernel_seconds.get("core", 0.0))
