@@ -125,7 +125,23 @@ __global__ void __launch_bounds__(kThreads) sketch_kernel(const SketchTarget* __
       }
     } else if (active) {
       int jl = js;
-      // 4 independent loads in flight per thread before the FMAs.
+      // 8, then 4, independent loads in flight per thread before the FMAs
+      // (strided targets pay one DRAM burst per element: latency-bound).
+      for (; jl + 7 * JS < jn; jl += 8 * JS) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t bu = base[jl + u * JS];
+          v[u] = bu >= 0 ? __ldg(x + bu + roff) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double* ou = om + (jl + u * JS) * c;
+#pragma unroll
+          for (int cc = 0; cc < CMAX; ++cc)
+            if (cc < c) acc[cc] += v[u] * ou[cc];
+        }
+      }
       for (; jl + 3 * JS < jn; jl += 4 * JS) {
         const int64_t b0 = base[jl], b1 = base[jl + JS], b2 = base[jl + 2 * JS], b3 = base[jl + 3 * JS];
         const double v0 = b0 >= 0 ? __ldg(x + b0 + roff) : 0.0;
