@@ -6,7 +6,14 @@ import srtt_oracle as O
 
 
 def projector_gap(a, b):
-    """||A A^T - B B^T||_F for orthonormal A, B (test_htucker.cpp:216-217)."""
+    """||A A^T - B B^T||_F for orthonormal A, B (test_htucker.cpp:216-217).
+    Tall bases (the n x n projectors would not fit) use the equivalent
+    sqrt(||(I - B B^T) A||_F^2 + ||(I - A A^T) B||_F^2), exact for orthonormal
+    columns and free of cancellation."""
+    if a.shape[0] > 25000:
+        ra = a - b @ (b.T @ a)
+        rb = b - a @ (a.T @ b)
+        return float(np.sqrt(np.linalg.norm(ra) ** 2 + np.linalg.norm(rb) ** 2))
     return float(np.linalg.norm(a @ a.T - b @ b.T))
 
 
