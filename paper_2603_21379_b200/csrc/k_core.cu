@@ -822,10 +822,21 @@ __global__ void ttm_split_kernel(const TtmParams T) {
       } else {
         // lanes split the flattened (i, part) space: lane sub takes every
         // S-th (i, q) pair in i-major order (fixed order per lane)
+        // (four loads in flight, the sum in the same order)
         const int64_t np = T.nparts, total_iq = T.n * np;
-        for (int64_t e = sub; e < total_iq; e += S) {
-          const int64_t i = e / np, q = e - i * np;
-          s0 = fma(in[T.g * i + q * T.part_stride], cf[cs * i], s0);
+        for (int64_t e = sub; e < total_iq; e += 4 * S) {
+          double v[4], w[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int64_t ee = e + (int64_t)u * S;
+            const bool in_range = ee < total_iq;
+            const int64_t i = in_range ? ee / np : 0, q = in_range ? ee - i * np : 0;
+            v[u] = in_range ? in[T.g * i + q * T.part_stride] : 0.0;
+            w[u] = in_range ? cf[cs * i] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (e + (int64_t)u * S < total_iq) s0 = fma(v[u], w[u], s0);
         }
       }
     }
