@@ -960,6 +960,10 @@ __global__ void __launch_bounds__(256) ttm_block_kernel(const TtmParams T) {
 template <int RR>
 __global__ void __launch_bounds__(256) ttm_splitk_kernel(const TtmParams T, int64_t chunk, double* partial) {
   __shared__ double red[2][RR][64];
+  // the factor rows of one 64-row tile of the mode (read by every thread);
+  // overlays red, which is only used after the accumulation (barrier between)
+  double (*us)[RR + 1] = reinterpret_cast<double (*)[RR + 1]>(&red[0][0][0]);
+  static_assert(64 * (RR + 1) <= 2 * RR * 64, "tile overlay");
   const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
   const int64_t gi = (int64_t)blockIdx.x * 64 + tx;
   const int64_t i_lo = (int64_t)blockIdx.y * chunk, i_hi = min64(T.n, i_lo + chunk);
@@ -968,30 +972,40 @@ __global__ void __launch_bounds__(256) ttm_splitk_kernel(const TtmParams T, int6
     double acc[RR];
 #pragma unroll
     for (int b = 0; b < RR; ++b) acc[b] = 0.0;
-    if (gi < T.g) {
-      const double* in = T.in + gi + T.g * T.n * pi;
-      constexpr int kB = 4;
-      for (int64_t i0 = i_lo + ty; i0 < i_hi; i0 += 4 * kB) {
-        double v[kB];
+    const double* in = T.in + gi + T.g * T.n * pi;
+    constexpr int kB = 4;
+    for (int64_t t0 = i_lo; t0 < i_hi; t0 += 64) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < 64 * RR; e += 256) {
+        const int ii = T.transpose ? e % 64 : e / RR, b = T.transpose ? e / 64 : e % RR;
+        const int64_t i = t0 + ii;
+        us[ii][b] = (i < i_hi && b < T.rr) ? __ldg(T.u + ci * i + cs * b) : 0.0;
+      }
+      __syncthreads();
+      if (gi < T.g) {
+        const int64_t t1 = min64(i_hi, t0 + 64);
+        for (int64_t i0 = t0 + ty; i0 < t1; i0 += 4 * kB) {
+          double v[kB];
 #pragma unroll
-        for (int u = 0; u < kB; ++u) {
-          const int64_t i = i0 + 4 * u;
-          v[u] = 0.0;
-          if (i < i_hi) {
-            const double* pp = in + T.g * i;
-            double s0 = pp[0];
-            for (int q = 1; q < T.nparts; ++q) s0 += pp[q * T.part_stride];
-            v[u] = s0;
+          for (int u = 0; u < kB; ++u) {
+            const int64_t i = i0 + 4 * u;
+            v[u] = 0.0;
+            if (i < t1) {
+              const double* pp = in + T.g * i;
+              double s0 = pp[0];
+              for (int q = 1; q < T.nparts; ++q) s0 += pp[q * T.part_stride];
+              v[u] = s0;
+            }
           }
-        }
 #pragma unroll
-        for (int u = 0; u < kB; ++u) {
-          const int64_t i = i0 + 4 * u;
-          if (i < i_hi) {
-            const double* cf = T.u + ci * i;
+          for (int u = 0; u < kB; ++u) {
+            const int64_t i = i0 + 4 * u;
+            if (i < t1) {
+              const double* cf = us[(int)(i - t0)];
 #pragma unroll
-            for (int b = 0; b < RR; ++b)
-              if (b < T.rr) acc[b] = fma(v[u], __ldg(cf + cs * b), acc[b]);
+              for (int b = 0; b < RR; ++b)
+                if (b < T.rr) acc[b] = fma(v[u], cf[b], acc[b]);
+            }
           }
         }
       }
