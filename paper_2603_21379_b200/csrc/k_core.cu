@@ -991,9 +991,17 @@ __global__ void __launch_bounds__(256) ttm_splitk_kernel(const TtmParams T, int6
             const int64_t i = i0 + 4 * u;
             v[u] = 0.0;
             if (i < t1) {
+              // the parts four at a time: independent loads, the same left-to-right sum
               const double* pp = in + T.g * i;
-              double s0 = pp[0];
-              for (int q = 1; q < T.nparts; ++q) s0 += pp[q * T.part_stride];
+              double s0 = 0.0;
+              for (int q0 = 0; q0 < T.nparts; q0 += 4) {
+                double pv[4];
+#pragma unroll
+                for (int w = 0; w < 4; ++w) pv[w] = q0 + w < T.nparts ? pp[(int64_t)(q0 + w) * T.part_stride] : 0.0;
+#pragma unroll
+                for (int w = 0; w < 4; ++w)
+                  if (q0 + w < T.nparts) s0 = (q0 + w == 0) ? pv[w] : s0 + pv[w];
+              }
               v[u] = s0;
             }
           }
