@@ -635,7 +635,58 @@ struct HtShard {
     return launch_sketch_group(reinterpret_cast<const SketchTarget*>(dp + off_sk), sk, ctas, cmax, h->stream);
   }
   // Phase 2: bases of every node (K2) and the internal transfers (K4).
-  int enqueue_bases(srtt_handle* h) {
+  // fork (the fused sharded path): as in the single-GPU decomposition the
+  // single-CTA bases and the transfers run on the side stream and overlap
+  // the tall bases and the root pass, which only needs the root children
+  // (htucker.hpp:203-209); enqueue_join() closes the fork after the root.
+  bool forked = false;
+  int enqueue_bases(srtt_handle* h, bool fork = false) {
+    forked = false;
+    if (fork && replicated && !bt.empty()) {
+      // replicated: the factor pack is complete only when both streams'
+      // bases are; after its allreduce the transfers go to the side stream
+      int n = 0;
+      CK(cudaEventRecord(h->fj[0], h->stream));
+      CK(cudaStreamWaitEvent(h->side, h->fj[0], 0));
+      n += launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt), lists, dp,
+                              reinterpret_cast<double*>(ws + off_pad), max_n, h->side);
+      CK(cudaEventRecord(h->fj[1], h->side));
+      CK(cudaStreamWaitEvent(h->stream, h->fj[1], 0));
+      allreduce_sum(h, reinterpret_cast<double*>(ws + off_upack), (size_t)upack_n);
+      allreduce_sum_i32(h, dinfo, 4 * (size_t)(nt + 1));
+      CK(cudaEventRecord(h->fj[2], h->stream));
+      CK(cudaStreamWaitEvent(h->side, h->fj[2], 0));
+      if (!tt.empty()) {
+        CK(srtt_launch_transfer(reinterpret_cast<const TransferTarget*>(dp + off_tt), (int)tt.size(), tctas, max_rl,
+                                max_rr, h->side));
+        ++n;
+      }
+      CK(cudaEventRecord(h->fj[3], h->side));
+      forked = true;
+      return n;
+    }
+    if (fork && !replicated && !bt.empty()) {
+      int n = 0;
+      CK(cudaEventRecord(h->fj[0], h->stream));
+      CK(cudaStreamWaitEvent(h->side, h->fj[0], 0));
+      n += launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt), lists, dp,
+                              reinterpret_cast<double*>(ws + off_pad), max_n, h->side);
+      CK(cudaEventRecord(h->fj[1], h->side));    // single-CTA bases done
+      CK(cudaEventRecord(h->fj[2], h->stream));  // tall bases done
+      CK(cudaStreamWaitEvent(h->side, h->fj[2], 0));
+      if (!tt.empty()) {
+        CK(srtt_launch_transfer(reinterpret_cast<const TransferTarget*>(dp + off_tt), (int)tt.size(), tctas, max_rl,
+                                max_rr, h->side));
+        ++n;
+      }
+      CK(cudaEventRecord(h->fj[3], h->side));
+      bool root_needs_small = false;
+      for (int t : lists.small)
+        if (t + 1 == tr.left[0] || t + 1 == tr.right[0]) root_needs_small = true;  // target t is node t + 1
+      if (root_needs_small) CK(cudaStreamWaitEvent(h->stream, h->fj[1], 0));
+      forked = true;
+      return n;
+    }
     int n = bt.empty() ? 0
                        : launch_basis_group(h, bt, reinterpret_cast<const BasisTarget*>(dp + off_bt), lists, dp,
                                             reinterpret_cast<double*>(ws + off_pad), max_n);
@@ -649,6 +700,10 @@ struct HtShard {
       ++n;
     }
     return n;
+  }
+  void enqueue_join(srtt_handle* h) {
+    if (forked) CK(cudaStreamWaitEvent(h->stream, h->fj[3], 0));
+    forked = false;
   }
   // Phase 3: this range's partial root transfer U_l^T M_w U_r[c_lo:c_hi].
   int enqueue_root(srtt_handle* h, const double* x, const double* ul, const double* ur_full, double* out) {
@@ -742,9 +797,10 @@ void run_sub_r_rtl_ht_sharded(srtt_handle* h, const double* x_in, int x_on_devic
     tm.mark();  // 3
     if (!replicated) allreduce_sum(h, S.zsum(), (size_t)S.zn);
     tm.mark();  // 4
-    h->launches += S.enqueue_bases(h);
+    h->launches += S.enqueue_bases(h, true);
     tm.mark();  // 5
     h->launches += S.enqueue_root(h, xroot, S.ubasis(il), S.ubasis(ir), d_root);
+    S.enqueue_join(h);
     tm.mark();  // 6
     allreduce_sum(h, d_root, (size_t)rl0 * rr0);
     tm.mark();  // 7
