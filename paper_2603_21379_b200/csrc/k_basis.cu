@@ -1319,7 +1319,9 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
 // beyond nr and columns beyond c are zero). Reflector j goes to
 // vout[row + j * ldv] (STOREV), g_j to gout[j], row j of R to
 // rout[j * rs + col * cs] (entries on and right of the diagonal only).
-template <int CP, bool STOREV>
+// RTL: row groups that can hold rows (compile time; the second QR of the small
+// SVD has at most 32 rows: one group, a quarter of the FMA work)
+template <int CP, bool STOREV, int RTL = WTile<CP>::RT>
 __device__ void wqr_factor(double (&a)[WTile<CP>::RT][CP], int nr, int c, double* vout, int ldv, double* gout,
                            double* rout, int rs, int cs, double* wsm) {
   constexpr int RT = WTile<CP>::RT, LPC = 32 / CP;
@@ -1357,7 +1359,7 @@ __device__ void wqr_factor(double (&a)[WTile<CP>::RT][CP], int nr, int c, double
     for (int p = 0; p < CP; ++p) {
       double s = 0.0;
 #pragma unroll
-      for (int t = 0; t < RT; ++t) s = fma(xm[t], a[t][p], s);
+      for (int t = 0; t < RTL; ++t) s = fma(xm[t], a[t][p], s);
       D[p] = s;
     }
     WQR_CLK(1);
@@ -1399,13 +1401,13 @@ __device__ void wqr_factor(double (&a)[WTile<CP>::RT][CP], int nr, int c, double
     for (int p = 0; p < CP; p += 2) {
       const double2 e = reinterpret_cast<const double2*>(csm)[p / 2];
 #pragma unroll
-      for (int t = 0; t < RT; ++t) {
+      for (int t = 0; t < RTL; ++t) {
         if (p > 0) a[t][p - 1] = fma(-e.x, xm[t], a[t][p]);
         a[t][p] = fma(-e.y, xm[t], a[t][p + 1 < CP ? p + 1 : p]);
       }
     }
 #pragma unroll
-    for (int t = 0; t < RT; ++t) a[t][CP - 1] = 0.0;
+    for (int t = 0; t < RTL; ++t) a[t][CP - 1] = 0.0;
     __syncwarp();
     WQR_CLK(5);
   }
@@ -1934,7 +1936,7 @@ __global__ void __launch_bounds__(kThreads) basis_wtree_kernel(const BasisTarget
 #pragma unroll
       for (int p = 0; p < CP; ++p) a[t][p] = (row < c && p < k) ? Rf[p + (size_t)row * ldr] : 0.0;
     }
-    wqr_factor<CP, false>(a, c, k, nullptr, 0, nullptr, s.B, LDB, 1, s.wscr);
+    wqr_factor<CP, false, 1>(a, c, k, nullptr, 0, nullptr, s.B, LDB, 1, s.wscr);  // c <= 32 rows: one row group
     __syncwarp();
     PROF_MARK(2);
     if (CP == 16) sweeps = k <= 12 ? jacobi_rows_nov<4, 3>(s.B, LDB, k) : jacobi_rows_nov<4, 4>(s.B, LDB, k);
