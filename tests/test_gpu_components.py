@@ -72,7 +72,10 @@ def test_fused_sketch_matches_oracle(handle, dims, modes, w, c):
                                          (144, 15, 10, 10), (2048, 42, 32, 32), (5000, 42, 32, 14),
                                          (20736, 15, 10, 10), (3, 5, 2, 3), (1000, 24, 16, 24), (700, 32, 30, 20),
                                          (300, 80, 70, 40), (60, 100, 50, 60), (100000, 15, 10, 10),
-                                         (9000, 30, 20, 12), (1500, 16, 16, 16)])
+                                         (9000, 30, 20, 12), (1500, 16, 16, 16),
+                                         # edges of the kernel families
+                                         (1, 1, 1, 1), (5, 1, 1, 1), (2, 2, 2, 2), (33, 32, 32, 32), (65, 33, 20, 33),
+                                         (256, 64, 50, 64), (257, 64, 64, 30), (129, 16, 9, 16), (64, 17, 17, 5)])
 def test_basis_matches_oracle(handle, n, c, r, decay):
     """K2 (sketch.hpp:74-93): same numerical rank, same leading subspace,
     orthonormal to 1e-12 (test_sketch.cpp:198-204); covers the warp path,
