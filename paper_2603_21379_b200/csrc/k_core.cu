@@ -916,7 +916,7 @@ __global__ void __launch_bounds__(256) ttm_block_kernel(const TtmParams T) {
   for (int b = 0; b < RR; ++b) acc[b] = 0.0;
   if (gi < T.g) {
     const double* in = T.in + gi + T.g * T.n * pi;
-    constexpr int kB = 4;
+    constexpr int kB = 8;  // loads in flight per thread
     for (int64_t i0 = ty; i0 < T.n; i0 += 4 * kB) {
       double v[kB];
 #pragma unroll
