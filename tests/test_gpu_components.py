@@ -75,7 +75,9 @@ def test_fused_sketch_matches_oracle(handle, dims, modes, w, c):
                                          (9000, 30, 20, 12), (1500, 16, 16, 16),
                                          # edges of the kernel families
                                          (1, 1, 1, 1), (5, 1, 1, 1), (2, 2, 2, 2), (33, 32, 32, 32), (65, 33, 20, 33),
-                                         (256, 64, 50, 64), (257, 64, 64, 30), (129, 16, 9, 16), (64, 17, 17, 5)])
+                                         (256, 64, 50, 64), (257, 64, 64, 30), (129, 16, 9, 16), (64, 17, 17, 5),
+                                         # so tall that the stacked top no longer fits one CTA: shared-memory TSQR levels
+                                         (1200000, 15, 10, 10)])
 def test_basis_matches_oracle(handle, n, c, r, decay):
     """K2 (sketch.hpp:74-93): same numerical rank, same leading subspace,
     orthonormal to 1e-12 (test_sketch.cpp:198-204); covers the warp path,
