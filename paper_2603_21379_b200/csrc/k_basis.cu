@@ -1807,9 +1807,21 @@ __device__ void wtree_apply(const WTree& tr, int c, int q, const double* v0, int
     const int r0 = b * TB;
     const int nr = min(TB, tr.rows[0] - r0);
     const int kb = min(nr, c);
-    for (int idx = threadIdx.x; idx < nr * kb; idx += blockDim.x) {
-      const int i = idx % nr, j = idx / nr;
-      stage0[i + j * (TB + 1)] = v0[r0 + i + (int64_t)j * ldv0];
+    // batches of 16 independent loads per thread: the block comes from L2 /
+    // HBM, and a load-store-load-store loop would pay the latency per element
+    const int tot = nr * kb, nth = blockDim.x;
+    for (int i0 = threadIdx.x; i0 < tot; i0 += nth * 16) {
+      double tmp[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int idx = i0 + u * nth;
+        tmp[u] = idx < tot ? v0[r0 + idx % nr + (int64_t)(idx / nr) * ldv0] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int idx = i0 + u * nth;
+        if (idx < tot) stage0[idx % nr + (idx / nr) * (TB + 1)] = tmp[u];
+      }
     }
     __syncthreads();
   };
@@ -2570,7 +2582,14 @@ __global__ void __launch_bounds__(kWfThreads) basis_wapply_kernel(const BasisTar
   double* tscr = wscr + (size_t)(kWfThreads / 32) * WTile<CP>::WSCR;
   double* stage = tscr + TeamRows<CP>::SCR;
   const double* up = T.vup + (int64_t)tb.y * T.vup_stride;
-  for (int i = threadIdx.x; i < tr.persist; i += blockDim.x) arena[i] = up[i];
+  for (int i0 = threadIdx.x; i0 < tr.persist; i0 += blockDim.x * 8) {  // 8 loads in flight per thread
+    double tmp[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) tmp[u] = i0 + u * (int)blockDim.x < tr.persist ? up[i0 + u * blockDim.x] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 + u * (int)blockDim.x < tr.persist) arena[i0 + u * blockDim.x] = tmp[u];
+  }
   const int k = tr.rows[tr.L];
   double* yt = arena + tr.yoff[tr.L];
   for (int idx = threadIdx.x; idx < k * q; idx += blockDim.x) {
