@@ -2438,9 +2438,21 @@ __global__ void __launch_bounds__(kThreads) basis_wide_apply_kernel(const BasisT
   double* gst = p; p += (c + 2) & ~1;
   p += ((size_t)c * (c | 1) + 1) & ~(size_t)1;
   const TeamScratch ts = team_scratch(p);
-  for (int idx = threadIdx.x; idx < mb * kb; idx += blockDim.x) {
-    const int i = idx % mb, j = idx / mb;
-    vst[i + (size_t)j * ldv] = L.a[(int64_t)j * L.n + r0 + i];
+  {  // 8 independent loads per thread and pass (the block comes from L2 / HBM)
+    const int tot = mb * kb, nth = blockDim.x;
+    for (int i0 = threadIdx.x; i0 < tot; i0 += nth * 8) {
+      double tmp[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = i0 + u * nth;
+        tmp[u] = idx < tot ? L.a[(int64_t)(idx / mb) * L.n + r0 + idx % mb] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = i0 + u * nth;
+        if (idx < tot) vst[idx % mb + (size_t)(idx / mb) * ldv] = tmp[u];
+      }
+    }
   }
   for (int j = threadIdx.x; j < c; j += blockDim.x) gst[j] = L.tau[(int64_t)b * c + j];
   __syncthreads();
