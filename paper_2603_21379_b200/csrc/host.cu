@@ -605,8 +605,10 @@ struct BasisLists {
   // register-tree targets by column padding (16 / 32): single-CTA ones, the
   // tops of tall ones, and the (target, CTA) map of the tall ones
   // (single-CTA ones split again: at most one warp block / taller)
-  std::vector<int> w_small[4], w_tall[2];
-  size_t off_w_small[4] = {}, off_w_tall[2] = {}, off_w_map[2] = {};
+  // w_small[4 cp + slot]: slot 0 = taller than one warp block (row teams),
+  // slots 1..3 = at most 32 / 64 / 128 rows (1 / 2 / 4 row groups)
+  std::vector<int> w_small[8], w_tall[2];
+  size_t off_w_small[8] = {}, off_w_tall[2] = {}, off_w_map[2] = {};
   int w_ctas[2] = {};
   // wide register path (kind 2): single-block targets, tall ones, and the
   // per-level (target, block) maps of the tall ones
@@ -627,13 +629,15 @@ BasisLists make_basis_lists(const std::vector<BasisTarget>& targets, Blob& blob)
       const BasisTarget& t = targets[i];
       if (t.kind != 1 || srtt_wtree_cp(t.c) != (v ? 32 : 16)) continue;
       if (t.nlevels == 0) {
-        L.w_small[2 * v + (t.n > srtt_wtree_chunk(v ? 32 : 16) ? 1 : 0)].push_back(i);
+        const int64_t groups = (t.n + 31) / 32;
+        const int slot = t.n > srtt_wtree_chunk(v ? 32 : 16) ? 0 : (groups <= 1 ? 1 : (groups <= 2 ? 2 : 3));
+        L.w_small[4 * v + slot].push_back(i);
       } else {
         L.w_tall[v].push_back(i);
         for (int b = 0; b < t.lv[0].nblk; ++b) map.push_back(make_int2(i, b));
       }
     }
-    for (int u = 2 * v; u < 2 * v + 2; ++u)
+    for (int u = 4 * v; u < 4 * v + 4; ++u)
       if (!L.w_small[u].empty()) L.off_w_small[u] = blob.add(L.w_small[u].data(), sizeof(int) * L.w_small[u].size());
     if (!L.w_tall[v].empty()) {
       L.off_w_tall[v] = blob.add(L.w_tall[v].data(), sizeof(int) * L.w_tall[v].size());
@@ -696,12 +700,13 @@ int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const 
   const int nt = (int)targets.size();
   // register-tree targets: single-CTA ones on the side stream, tall ones as
   // factor -> top -> apply on the main stream
-  for (int u = 0; u < 4; ++u) {
-    const int cp = u >= 2 ? 32 : 16;
+  for (int u = 0; u < 8; ++u) {
+    const int cp = u >= 4 ? 32 : 16;
+    static const int kMode[4] = {0, 1, 2, 4};  // slot -> row groups (0: row teams)
     if (!lists.w_small[u].empty()) {
       size_t smem = 0;
       for (int i : lists.w_small[u]) smem = std::max(smem, srtt_wtree_top_smem((int)targets[i].n, targets[i].c, true));
-      CK(srtt_launch_wtree_top(cp, u & 1, dT, reinterpret_cast<const int*>(dblob + lists.off_w_small[u]),
+      CK(srtt_launch_wtree_top(cp, kMode[u & 3], dT, reinterpret_cast<const int*>(dblob + lists.off_w_small[u]),
                                (int)lists.w_small[u].size(), smem, small_stream ? small_stream : h->stream));
       ++launches;
     }
@@ -718,7 +723,7 @@ int launch_basis_group(srtt_handle* h, std::vector<BasisTarget>& targets, const 
     }
     const int2* map = reinterpret_cast<const int2*>(dblob + lists.off_w_map[v]);
     CK(srtt_launch_wtree_factor(cp, dT, map, lists.w_ctas[v], sf, h->stream));
-    CK(srtt_launch_wtree_top(cp, 1, dT, reinterpret_cast<const int*>(dblob + lists.off_w_tall[v]),
+    CK(srtt_launch_wtree_top(cp, 0, dT, reinterpret_cast<const int*>(dblob + lists.off_w_tall[v]),
                              (int)lists.w_tall[v].size(), st, h->stream));
     CK(srtt_launch_wtree_apply(cp, dT, map, lists.w_ctas[v], sa, h->stream));
     launches += 3;

@@ -1415,7 +1415,7 @@ __device__ void wqr_factor(double (&a)[WTile<CP>::RT][CP], int nr, int c, double
 }
 
 // y <- H_0 ... H_{kb-1} y for the warp's register block y (nr rows).
-template <int CP>
+template <int CP, int RTL = WTile<CP>::RT>
 __device__ void wqr_apply(double (&y)[WTile<CP>::RT][CP], int nr, int kb, const double* v, int ldv, const double* g,
                           double* wsm) {
   constexpr int RT = WTile<CP>::RT, LPC = 32 / CP;
@@ -1441,7 +1441,7 @@ __device__ void wqr_apply(double (&y)[WTile<CP>::RT][CP], int nr, int kb, const 
     for (int p = 0; p < CP; ++p) {
       double s = 0.0;
 #pragma unroll
-      for (int t = 0; t < RT; ++t) s = fma(vt[t], y[t][p], s);
+      for (int t = 0; t < RTL; ++t) s = fma(vt[t], y[t][p], s);
       D[p] = s;
     }
     const double dtot = reduce_scatter_sm<CP>(D, red, lane);
@@ -1451,7 +1451,7 @@ __device__ void wqr_apply(double (&y)[WTile<CP>::RT][CP], int nr, int kb, const 
     for (int p = 0; p < CP; p += 2) {
       const double2 e = reinterpret_cast<const double2*>(esm)[p / 2];
 #pragma unroll
-      for (int t = 0; t < RT; ++t) {
+      for (int t = 0; t < RTL; ++t) {
         y[t][p] = fma(-e.x, vt[t], y[t][p]);
         y[t][p + 1] = fma(-e.y, vt[t], y[t][p + 1]);
       }
@@ -1737,10 +1737,15 @@ __device__ void trows_apply(double (&y)[WTile<CP>::RT][CP], int w, int nwa, int 
 // loop -- a global store there would make every barrier of the step wait for
 // its acknowledgement -- and copied out afterwards. Upper levels live in the
 // arena.
-template <int CP, bool TEAM = true>
+// RTLM = 0: blocks taller than one warp's run as row teams; RTLM = r > 0: the
+// target has at most 32 r rows (one warp block), the team code is left out
+// and the FMA loops touch r row groups only (compile time).
+template <int CP, int RTLM = 0>
 __device__ void wtree_factor(const WTree& tr, int c, const double* in0, int64_t ld0, double* v0, int64_t ldv0,
                              double* arena, double* wscr_all, double* tscr, double* stage0 = nullptr) {
   constexpr int RT = WTile<CP>::RT, CHUNK = WTile<CP>::CHUNK;
+  constexpr bool TEAM = RTLM == 0;
+  constexpr int RTL = TEAM ? RT : RTLM;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int TB = nw * CHUNK;
   double* wsm = wscr_all + (size_t)warp * WTile<CP>::WSCR;
@@ -1775,7 +1780,7 @@ __device__ void wtree_factor(const WTree& tr, int c, const double* in0, int64_t 
         }
         __syncwarp();
         if (!TEAM || nwa == 1)
-          wqr_factor<CP, true>(a, nr, c, vb, ldvb, arena + tr.goff[l] + b * c, rnext + b * c, 1, ldr, wsm);
+          wqr_factor<CP, true, RTL>(a, nr, c, vb, ldvb, arena + tr.goff[l] + b * c, rnext + b * c, 1, ldr, wsm);
         else
           trows_factor<CP>(a, warp, nwa, rpw, nr, c, vb, ldvb, arena + tr.goff[l] + b * c, rnext + b * c, 1, ldr, wsm,
                            tscr);
@@ -1796,10 +1801,12 @@ __device__ void wtree_factor(const WTree& tr, int c, const double* in0, int64_t 
 // Back-application through levels L-1..0: Y_L (arena) holds the kb_top x q
 // input; the level-0 result goes to out0 (ld ldo). With stage0 set the
 // level-0 reflectors (global memory) are copied to shared memory first.
-template <int CP, bool TEAM = true>
+template <int CP, int RTLM = 0>
 __device__ void wtree_apply(const WTree& tr, int c, int q, const double* v0, int64_t ldv0, double* arena,
                             double* wscr_all, double* tscr, double* out0, int64_t ldo, double* stage0) {
   constexpr int RT = WTile<CP>::RT, CHUNK = WTile<CP>::CHUNK;
+  constexpr bool TEAM = RTLM == 0;
+  constexpr int RTL = TEAM ? RT : RTLM;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int TB = nw * CHUNK;
   double* wsm = wscr_all + (size_t)warp * WTile<CP>::WSCR;
@@ -1859,7 +1866,7 @@ __device__ void wtree_apply(const WTree& tr, int c, int q, const double* v0, int
             y[t][p] = (t * 32 < rpw && row < kb && p < q) ? yin[b * c + row + (int64_t)p * ldyi] : 0.0;
         }
         if (!TEAM || nwa == 1)
-          wqr_apply<CP>(y, nr, kb, vb, ldvb, arena + tr.goff[l] + b * c, wsm);
+          wqr_apply<CP, RTL>(y, nr, kb, vb, ldvb, arena + tr.goff[l] + b * c, wsm);
         else
           trows_apply<CP>(y, warp, nwa, rpw, nr, kb, vb, ldvb, arena + tr.goff[l] + b * c, wsm, tscr);
 #pragma unroll
@@ -1901,7 +1908,7 @@ __host__ __device__ inline size_t wtop_doubles(int n0, int c, int CP, int nwarps
 // TEAM = false: targets of at most one warp block (every block of the tree is
 // a single warp's): the row-team code is left out of the kernel, whose
 // once-executed straight-line parts are instruction-fetch bound.
-template <int CP, bool TEAM>
+template <int CP, int RTLM>
 __global__ void __launch_bounds__(kThreads) basis_wtree_kernel(const BasisTarget* __restrict__ targets,
                                                               const int* __restrict__ list) {
   constexpr int RT = WTile<CP>::RT, CHUNK = WTile<CP>::CHUNK;
@@ -1933,7 +1940,7 @@ __global__ void __launch_bounds__(kThreads) basis_wtree_kernel(const BasisTarget
   for (int i = tid; i < tr.persist; i += blockDim.x) s.arena[i] = 0.0;
   for (int i = tid; i < CP * LDB; i += blockDim.x) s.B[i] = 0.0;
   __syncthreads();
-  wtree_factor<CP, TEAM>(tr, c, L.a, L.n, s.v0, n0 | 1, s.arena, s.wscr, s.tscr);
+  wtree_factor<CP, RTLM>(tr, c, L.a, L.n, s.v0, n0 | 1, s.arena, s.wscr, s.tscr);
   PROF_MARK_CTA(1);
   // R^T = Q_1 R_1, then Jacobi on the rows of R_1 (warp 0)
   const int k = tr.rows[tr.L];
@@ -1992,7 +1999,7 @@ __global__ void __launch_bounds__(kThreads) basis_wtree_kernel(const BasisTarget
   }
   __syncthreads();
   PROF_MARK_CTA(4);
-  wtree_apply<CP, TEAM>(tr, c, q, s.v0, n0 | 1, s.arena, s.wscr, s.tscr, tall ? L.y : T.u, tall ? L.n : T.n, nullptr);
+  wtree_apply<CP, RTLM>(tr, c, q, s.v0, n0 | 1, s.arena, s.wscr, s.tscr, tall ? L.y : T.u, tall ? L.n : T.n, nullptr);
   PROF_MARK_CTA(5);
   if (!tall && q < r)
     pad_columns(T.u, n0, n0, q, r, T.state0, T.draw_offset, (uint64_t)T.normal_base, s.vpad, s.dots, s.red);
@@ -2749,18 +2756,29 @@ size_t srtt_wtree_apply_smem(int rows, int c) {
           (size_t)(tb + 1) * c) * sizeof(double);
 }
 
-cudaError_t srtt_launch_wtree_top(int cp, int team, const BasisTarget* d_targets, const int* d_list, int n, size_t smem,
+// mode 0: row teams (blocks taller than one warp's); r > 0: a single-warp-block
+// target of at most 32 r rows (r = 1, 2, 4 for c <= 16; 1, 2 for c <= 32)
+cudaError_t srtt_launch_wtree_top(int cp, int mode, const BasisTarget* d_targets, const int* d_list, int n, size_t smem,
                                   cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
-#define SRTT_WTOP(CPV, TV)                                                                   \
+#define SRTT_WTOP(CPV, MV)                                                                   \
   do {                                                                                       \
-    SRTT_ENSURE_SMEM((basis_wtree_kernel<CPV, TV>), smem);                                   \
-    basis_wtree_kernel<CPV, TV><<<n, kThreads, smem, stream>>>(d_targets, d_list);           \
+    SRTT_ENSURE_SMEM((basis_wtree_kernel<CPV, MV>), smem);                                   \
+    basis_wtree_kernel<CPV, MV><<<n, kThreads, smem, stream>>>(d_targets, d_list);           \
   } while (0)
   if (cp == 16) {
-    if (team) SRTT_WTOP(16, true); else SRTT_WTOP(16, false);
+    switch (mode) {
+      case 0: SRTT_WTOP(16, 0); break;
+      case 1: SRTT_WTOP(16, 1); break;
+      case 2: SRTT_WTOP(16, 2); break;
+      default: SRTT_WTOP(16, 4); break;
+    }
   } else {
-    if (team) SRTT_WTOP(32, true); else SRTT_WTOP(32, false);
+    switch (mode) {
+      case 0: SRTT_WTOP(32, 0); break;
+      case 1: SRTT_WTOP(32, 1); break;
+      default: SRTT_WTOP(32, 2); break;
+    }
   }
 #undef SRTT_WTOP
   return cudaGetLastError();
