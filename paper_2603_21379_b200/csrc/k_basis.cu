@@ -1905,9 +1905,10 @@ __host__ __device__ inline size_t wtop_doubles(int n0, int c, int CP, int nwarps
 // Whole basis of a single-CTA target (nlevels == 0), or the top of a tall
 // one (nlevels == 1: input = the stacked R of the factor kernel, output =
 // the stacked Y for the apply kernel).
-// TEAM = false: targets of at most one warp block (every block of the tree is
-// a single warp's): the row-team code is left out of the kernel, whose
-// once-executed straight-line parts are instruction-fetch bound.
+// RTLM > 0: targets of at most one warp block with 32 RTLM rows (every block of
+// the tree is a single warp's): the row-team code is left out of the kernel,
+// whose once-executed straight-line parts are instruction-fetch bound, and
+// the FMA loops cover RTLM row groups. RTLM = 0: row teams, all row groups.
 template <int CP, int RTLM>
 __global__ void __launch_bounds__(kThreads) basis_wtree_kernel(const BasisTarget* __restrict__ targets,
                                                               const int* __restrict__ list) {
